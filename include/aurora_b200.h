@@ -1,0 +1,164 @@
+/*
+ * aurora_b200.h -- C ABI of the B200-native Aurora MoE-layer hot path.
+ *
+ * One shared library (paper_2410_17043_b200/libaurora_b200.so, built for
+ * sm_100a) exports these entry points. Plain pointers and sizes only; every
+ * pointer named d_* / "device" is a CUDA device pointer, `stream` is a
+ * cudaStream_t passed as void*. Calls are asynchronous on `stream`; results
+ * that the reference returns synchronously (status words, phase counts) are
+ * written to device memory and read by the host shim only on the drop-in /
+ * debug path -- the MoE layer itself never synchronises with the host.
+ *
+ * The reference (arxiv 2410.17043, package `moeplan`) is pure Python with
+ * no FFI; each entry point below names the reference function it replaces
+ * (file:line under pkg/src/moeplan/). The Python binding a maintainer would
+ * add on the reference side is in INTEGRATION.md.
+ */
+#ifndef AURORA_B200_H
+#define AURORA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return / status codes. Map to the reference's exception types:
+ *   AURORA_EINVAL    -> ValueError           (core.py:88-94, commsched.py:213-216, 252-258)
+ *   AURORA_EOVERFLOW -> DecompositionError   (commsched.py:417-421, phase bound n^2-2n+2)
+ *   AURORA_ENOMATCH  -> DecompositionError   (commsched.py:424-429, no perfect matching)   */
+#define AURORA_OK 0
+#define AURORA_EINVAL 1
+#define AURORA_EOVERFLOW 2
+#define AURORA_ENOMATCH 3
+#define AURORA_ECUDA 10
+#define AURORA_EUNSUPPORTED 11
+#define AURORA_ETIMEOUT 12
+
+#define AURORA_MAX_RANKS 32
+
+int aurora_version(void);
+
+/* Table capacities: raw permutation phases (commsched.py:410, n^2-2n+2) and
+ * stripped phases (each of the <= n(n-1) real pairs can split one raw phase:
+ * 2n^2-3n+2). */
+int aurora_raw_phase_cap(int n);
+int aurora_phase_cap(int n);
+
+/* ---------------------------------------------------------------- K2 ----
+ * aurora_schedule_f64: replaces moeplan.commsched.build_schedule
+ * (commsched.py:448-481) including decompose's raw permutations
+ * (commsched.py:394-435). Bit-exact with the reference for n <= 32.
+ *   d[n*n]   traffic matrix, row-major, float64 (TrafficMatrix.entries, core.py:75-97)
+ *   bw[n]    ClusterSpec.bandwidths (core.py:179-181); NULL == all 1.0
+ *   raw_perm[(n^2-2n+2)*n], raw_dur[n^2-2n+2], n_raw[1]       (decompose output)
+ *   phase_recv[(2n^2-3n+2)*n]  receiver of sender i in phase k, or -1
+ *   phase_dur[2n^2-3n+2], n_phases[1], b_max[1] (bmax_heterogeneous)
+ *   status[1] AURORA_OK / EINVAL / EOVERFLOW / ENOMATCH
+ * The makespan is math.fsum(phase_dur) (commsched.py:480), done by the shim. */
+int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_perm,
+                        double* raw_dur, int32_t* n_raw, int32_t* phase_recv, double* phase_dur,
+                        int32_t* n_phases, double* b_max, int32_t* status, void* stream);
+
+/* aurora_schedule_counts: the in-layer variant. Same schedule, computed from
+ * the router's int32 GPU x GPU token counts (diagonal = local tokens,
+ * ignored by the schedule like TrafficMatrix does, core.py:95), plus the
+ * engine tables:
+ *   chunks[P][n][4]   per phase k and sender i: {receiver, first token of the
+ *                     pair's send list, token count, arrival index at receiver}
+ *   rchunks[P][n][4]  the same chunks indexed by receiver j: {sender, first,
+ *                     count, index in the sender's send order} (the combine
+ *                     runs CommSchedule.reversed(), commsched.py:310-319)
+ *   n_in[n], n_out[n] chunks arriving at / leaving each rank
+ *   soff[n][n]        start of list(i,j) inside sender i's send list (row prefix)
+ *   roff[n][n]        start of list(i,j) inside receiver j's buffer (column prefix)
+ * Heterogeneous durations (time units, commsched.py:338-347) are converted to
+ * whole tokens per chunk by rounding each pair's cumulative time x
+ * min(B_i,B_j); the last chunk absorbs the rounding so per-pair totals are exact. */
+int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32_t* phase_recv,
+                           double* phase_dur, int32_t* n_phases, int32_t* chunks,
+                           int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* soff,
+                           int32_t* roff, int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- K1 ----
+ * aurora_route: top-k gating + GPU x GPU traffic matrix. No reference
+ * function: the reference models the gate as LayerProfile.gate_work
+ * (core.py:194-221) and consumes its output as TrafficMatrix (core.py:75-117)
+ * relabelled by deploy_to_gpus (core.py:337-345).
+ *   x[T][H] bf16, w_gate[E][H] bf16, bias[E] f32; H % 256 == 0, E <= 64, k <= 8
+ *   gpu_of_expert[E]  rank hosting expert e (DeploymentPlan.assignment_a, core.py:253-304)
+ *   tokens are grouped by rank: token t (local index) lives on rank
+ *   rank_base + t / tokens_per_rank (workload.py:59-61)
+ * Outputs: topk_idx[T][k], topk_w[T][k] (softmax over the selected logits),
+ *   slot_dst[T][k] (destination rank of the slot, -1 when an earlier slot of
+ *   the same token already goes there: a token crosses the network once per
+ *   destination), blk_cnt[T/64][n] per-64-token-block destination histogram,
+ *   counts[n][n] += this call's rows (must be zeroed by the caller). */
+int aurora_route(const void* x, const void* w_gate, const float* bias, int T, int H, int E,
+                 int k, const int32_t* gpu_of_expert, int n, int rank_base, int tokens_per_rank,
+                 int32_t* topk_idx, float* topk_w, int32_t* slot_dst, int32_t* blk_cnt,
+                 int32_t* counts, void* stream);
+
+/* ---------------------------------------------------------------- K3 ----
+ * aurora_pack: the token permutation. For each local source rank i and
+ * destination j, list(i,j) = the rank's tokens routed to j in ascending token
+ * order; send_list[i_local][soff[i][j] + p] = local token index of the p-th
+ * entry; pos[t][s] = p for the slot's destination (same p for deduplicated
+ * slots). Needs counts complete for the local rows. */
+int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T,
+                int k, int n, int rank_base, int tokens_per_rank, int32_t* send_list,
+                int32_t* pos, void* stream);
+
+/* ------------------------------------------------------------ K4 / K6 ----
+ * aurora_engine: executes the schedule as in-kernel stores into peer
+ * memory, self-timed per chunk (a chunk i->j starts once every earlier chunk
+ * into j has landed), replacing a single NCCL alltoallv. mode 0 = dispatch
+ * (CommSchedule phases, commsched.py:112-132), mode 1 = combine (the
+ * reversed schedule, commsched.py:310-319: same phases, directions flipped).
+ *   tables from aurora_schedule_counts; n_local ranks [rank_base, rank_base+n_local)
+ *   dispatch: src rows = x_local[i_local] gathered through send_list,
+ *             dst = recv_buf[j] rows roff[i][j] + first ...
+ *   combine:  src rows = out_buf[j_local] rows roff[i][j] + first ...,
+ *             dst = ret_buf[i] rows soff[i][j] + first ...
+ *   src_bufs[n_local], dst_bufs[n] (peer-mapped), ctrs[n] (peer-mapped int32
+ *   arrival counters, zero on entry, left zero on exit), all device arrays.
+ *   ctas_per_rank copy CTAs per local rank; all must be co-resident.
+ *   spin_limit bounds every flag wait (0 = unbounded); on expiry status = ETIMEOUT. */
+int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* chunks,
+                  const int32_t* rchunks, const int32_t* n_phases, const int32_t* n_in,
+                  const int32_t* n_out, const int32_t* soff, const int32_t* roff,
+                  const int32_t* send_list, int send_list_stride, const void* const* src_bufs,
+                  void* const* dst_bufs, int64_t src_rank_stride_rows, int row_bytes,
+                  int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
+                  int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------- K7 ----
+ * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret[soff[i][dst_s] + pos[t][s]]
+ * in fp32, bf16 out. The reference's LayerProfile.agg_work (core.py:194-221). */
+int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const int32_t* soff,
+                     const int32_t* pos, const int32_t* slot_dst, const float* topk_w, int T,
+                     int k, int H, int n, int rank_base, int tokens_per_rank, void* out,
+                     void* stream);
+
+/* ---------------------------------------------------------------- K5 ----
+ * aurora_expert_ffn: SwiGLU experts as tcgen05/TMEM grouped GEMMs fed by TMA
+ * (the reference's ffn_work_per_token, core.py:194-221 / sim.py:71-89).
+ *   groups G (one per local expert); rows of group g start at row g*cap of
+ *   a_buf [G*cap][H] bf16; m_rows[g] (device) rows are valid.
+ *   w13[G][2F][H] bf16: rows interleaved in 128-row blocks (gate block b at
+ *   rows 256b..256b+127, up block at 256b+128..256b+255) -- see DESIGN.md
+ *   w2[G][H][F] bf16; h_buf [G*cap][F] bf16 scratch; y_buf [G*cap][H] bf16 out.
+ *   y = (silu(x W1^T) * (x W3^T)) W2^T, fp32 accumulate. */
+int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
+                      void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
+                      int num_sms, void* stream);
+
+/* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
+ * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */
+int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_rows, int G,
+                        int64_t cap, int N, int K, int epilogue, int num_sms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AURORA_B200_H */

@@ -1,0 +1,481 @@
+// K2: Aurora's contention-free all-to-all schedule, computed on the device.
+//
+// Bit-exact restatement of moeplan.build_schedule (reference
+// pkg/src/moeplan/commsched.py:448-481) for n <= 32 GPUs, run by ONE warp:
+//   time_normalize        commsched.py:338-347   lane i divides row i
+//   bmax_heterogeneous    commsched.py:350-352   numpy pairwise row sums / sequential col sums
+//   augment               commsched.py:355-391   greedy fill, lane 0 (sequential by definition)
+//   AugmentedMatrix check commsched.py:247-262
+//   decompose             commsched.py:394-435   lane-parallel snap/min/update
+//   perfect_matching      matching.py:75-112     lane 0, bitmask rows, explicit DFS stacks
+//   hopcroft_karp         matching.py:20-72      level-synchronous bitmask BFS (distances are
+//                                                order-independent), exact-order DFS
+//   strip/_coalesce       commsched.py:463-479   interleaved with decompose (it only needs the
+//                                                raw phases produced so far)
+// Compiled with -fmad=false so every double operation rounds exactly like numpy.
+//
+// The same kernel also turns the schedule into the dispatch engine's chunk
+// table (per phase, per sender: receiver, first token, token count, position
+// in the receiver's arrival order) plus the send/receive buffer layout, so
+// the MoE layer never synchronises with the host between router and engine.
+#include "common.cuh"
+
+namespace {
+
+constexpr int HK_INF = -1;  // matching.py:17
+
+struct SchedParams {
+  const double* d64;      // n*n doubles, or
+  const int32_t* d32;     // n*n int32 token counts (in-layer path)
+  const double* bw;       // n bandwidths, nullptr == all 1.0 (ClusterSpec.uniform)
+  int n;
+  int32_t* raw_perm;      // [R_MAX][n]      (nullable)
+  double* raw_dur;        // [R_MAX]         (nullable)
+  int32_t* n_raw;         // [1]             (nullable)
+  int32_t* phase_recv;    // [P_MAX][n]
+  double* phase_dur;      // [P_MAX]
+  int32_t* n_phases;      // [1]
+  double* b_max;          // [1]             (nullable)
+  int32_t* status;        // [1]
+  int4* chunks;           // [P_MAX][n]      (nullable) {recv, start, ntok, rseq}
+  int4* rchunks;          // [P_MAX][n]      by receiver: {send, start, ntok, sseq}
+  int32_t* n_in;          // [n]             (nullable) chunks arriving at each receiver
+  int32_t* n_out;         // [n]             chunks leaving each sender
+  int32_t* soff;          // [n][n]          (nullable) start of list(i,j) in sender i's send list
+  int32_t* roff;          // [n][n]          (nullable) start of list(i,j) in receiver j's buffer
+};
+
+// numpy pairwise_sum (n <= 128 branch, and n < 8 sequential), row-major row of t
+__device__ double np_pairwise_row(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; i++) r += a[i];
+    return r;
+  }
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+    r0 += a[i]; r1 += a[i + 1]; r2 += a[i + 2]; r3 += a[i + 3];
+    r4 += a[i + 4]; r5 += a[i + 5]; r6 += a[i + 6]; r7 += a[i + 7];
+  }
+  double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; i++) res += a[i];
+  return res;
+}
+
+struct MatchState {
+  int ml[AUR_MAXN];
+  int mr[AUR_MAXN];
+  int dist[AUR_MAXN];
+  uint32_t sup[AUR_MAXN];
+  uint32_t pref[AUR_MAXN];
+  int ok;
+};
+
+// hopcroft_karp DFS from free root u, matching.py:57-65, with an explicit stack.
+// Candidates are visited in ascending v; the acceptance test is evaluated at
+// visit time against the current state, exactly like the recursive loop.
+// Returns the free right vertex the augmenting path ended on, or -1.
+__device__ int hk_dfs(MatchState& s, int root) {
+  int us[AUR_MAXN + 1], vs[AUR_MAXN + 1];
+  uint32_t left[AUR_MAXN + 1];
+  int top = 0;
+  us[0] = root;
+  left[0] = s.pref[root];
+  while (top >= 0) {
+    int u = us[top];
+    uint32_t m = left[top];
+    if (m == 0) {  // exhausted: dfs(u) returns False
+      s.dist[u] = HK_INF;
+      top--;
+      continue;
+    }
+    int v = __ffs(m) - 1;
+    left[top] = m & (m - 1);
+    int w = s.mr[v];
+    if (w < 0) {  // free right vertex: augment along the stack
+      vs[top] = v;
+      for (int l = top; l >= 0; l--) {
+        s.ml[us[l]] = vs[l];
+        s.mr[vs[l]] = us[l];
+      }
+      return v;
+    }
+    if (s.dist[w] == s.dist[u] + 1) {
+      vs[top] = v;
+      top++;
+      us[top] = w;
+      left[top] = s.pref[w];
+    }
+  }
+  return -1;
+}
+
+// perfect_matching's Kuhn extension, matching.py:96-106 (shared `seen` per root).
+__device__ bool kuhn_aug(MatchState& s, int root) {
+  int us[AUR_MAXN + 1], vs[AUR_MAXN + 1];
+  uint32_t left[AUR_MAXN + 1];
+  uint32_t seen = 0;
+  int top = 0;
+  us[0] = root;
+  left[0] = s.sup[root];
+  while (top >= 0) {
+    int u = us[top];
+    uint32_t m = left[top] & ~seen;  // "if seen[v]: continue" evaluated at visit time
+    if (m == 0) {
+      top--;
+      continue;
+    }
+    int v = __ffs(m) - 1;
+    left[top] = m & (m - 1);
+    seen |= 1u << v;
+    int w = s.mr[v];
+    if (w < 0) {
+      vs[top] = v;
+      for (int l = top; l >= 0; l--) {
+        s.ml[us[l]] = vs[l];
+        s.mr[vs[l]] = us[l];
+      }
+      return true;
+    }
+    vs[top] = v;
+    top++;
+    us[top] = w;
+    left[top] = s.sup[w];
+  }
+  return false;
+}
+
+// perfect_matching(support, preferred): matching.py:75-112. Lane 0 only.
+__device__ bool perfect_matching(MatchState& s, int n) {
+  uint32_t all = (n == 32) ? 0xffffffffu : ((1u << n) - 1);
+  for (int u = 0; u < n; u++) { s.ml[u] = -1; s.mr[u] = -1; }
+  uint32_t free_right = all;  // right vertices with mr < 0
+  for (;;) {
+    // --- bfs(): matching.py:37-55. Level-synchronous; dist = BFS level, which
+    // is independent of queue order, and `found` depends only on the reached set.
+    uint32_t frontier = 0;
+    for (int u = 0; u < n; u++) {
+      if (s.ml[u] < 0) { s.dist[u] = 0; frontier |= 1u << u; }
+      else s.dist[u] = HK_INF;
+    }
+    bool found = false;
+    int level = 0;
+    while (frontier) {
+      uint32_t reach = 0;
+      for (uint32_t f = frontier; f; f &= f - 1) reach |= s.pref[__ffs(f) - 1];
+      if (reach & free_right) found = true;
+      uint32_t next = 0;
+      for (uint32_t r = reach & ~free_right; r; r &= r - 1) {
+        int w = s.mr[__ffs(r) - 1];
+        if (s.dist[w] == HK_INF) { s.dist[w] = level + 1; next |= 1u << w; }
+      }
+      frontier = next;
+      level++;
+    }
+    if (!found) break;
+    for (int u = 0; u < n; u++) {
+      if (s.ml[u] < 0) {
+        int v = hk_dfs(s, u);
+        if (v >= 0) free_right &= ~(1u << v);
+      }
+    }
+  }
+  for (int u = 0; u < n; u++) {
+    if (s.ml[u] < 0) {
+      if (!kuhn_aug(s, u)) return false;
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
+  __shared__ double t_s[AUR_MAXN][AUR_MAXN + 1];     // time matrix; later "remaining" of strip
+  __shared__ double rem_s[AUR_MAXN][AUR_MAXN + 1];   // decompose remaining (d')
+  __shared__ double real_s[AUR_MAXN][AUR_MAXN + 1];  // decompose real
+  __shared__ double rr_s[AUR_MAXN], cr_s[AUR_MAXN];
+  __shared__ MatchState ms;
+  __shared__ int rcnt_s[AUR_MAXN];
+
+  const int lane = threadIdx.x;
+  const int n = p.n;
+  const bool on = lane < n;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  int status = AURORA_OK;
+
+  // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
+  double bw_i = (on && p.bw) ? p.bw[lane] : 1.0;
+  bool bad = false;
+  if (on) {
+    for (int j = 0; j < n; j++) {
+      double dij = p.d64 ? p.d64[lane * n + j] : (double)p.d32[lane * n + j];
+      double bw_j = p.bw ? p.bw[j] : 1.0;
+      double m = bw_j < bw_i ? bw_j : bw_i;
+      double v = dij / m;
+      if (v != v || v < 0) bad = true;
+      t_s[lane][j] = (lane == j) ? 0.0 : v;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) status = AURORA_EINVAL;
+  __syncwarp();
+
+  // ---- bmax_heterogeneous (commsched.py:350-352): numpy-order row/col sums
+  double row = on ? np_pairwise_row(&t_s[lane][0], n) : -INF;
+  double col = -INF;
+  if (on) {
+    col = 0.0;
+    for (int i = 0; i < n; i++) col += t_s[i][lane];
+  }
+  const double rmax = warp_max_d(row), cmax = warp_max_d(col);
+  const double b_max = cmax > rmax ? cmax : rmax;
+  const double eps = 1e-12 * (b_max > 1.0 ? b_max : 1.0);  // _snap_eps, commsched.py:43-45
+  if (lane == 0 && p.b_max) *p.b_max = b_max;
+
+  int nr = 0, np_ = 0;
+  const int R_MAX = n * n - 2 * n + 2;
+  const int P_MAX = 2 * n * n - 3 * n + 2;
+
+  if (status == AURORA_OK && b_max > 0) {
+    // ---- augment (commsched.py:367-391): greedy transportation fill on lane 0
+    if (on) { rr_s[lane] = b_max - row; cr_s[lane] = b_max - col; }
+    if (on) for (int j = 0; j < n; j++) real_s[lane][j] = 0.0;  // x
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < n; i++) {
+        if (rr_s[i] <= 0) continue;
+        for (int j = 0; j < n; j++) {
+          if (i == j || cr_s[j] <= 0) continue;
+          double fill = cr_s[j] < rr_s[i] ? cr_s[j] : rr_s[i];
+          real_s[i][j] = fill;
+          rr_s[i] -= fill;
+          cr_s[j] -= fill;
+          if (rr_s[i] <= 0) break;
+        }
+      }
+    }
+    __syncwarp();
+    if (on) {
+      if (rr_s[lane] > eps) real_s[lane][lane] = rr_s[lane];
+      for (int j = 0; j < n; j++) {
+        double x = real_s[lane][j];
+        if (x < 0) x = 0.0;
+        double dp = t_s[lane][j] + x;
+        rem_s[lane][j] = dp;
+        double r = dp - x;  // np.clip(a.d_prime - a.x, 0, None)
+        real_s[lane][j] = r < 0.0 ? 0.0 : r;
+      }
+    }
+    __syncwarp();
+    // AugmentedMatrix.__post_init__ balance check (commsched.py:252-258)
+    {
+      const double tol = 1e-9 * (b_max > 1.0 ? b_max : 1.0);
+      bool unbal = false;
+      if (on) {
+        double rs = np_pairwise_row(&rem_s[lane][0], n), cs = 0.0;
+        for (int i = 0; i < n; i++) cs += rem_s[i][lane];
+        unbal = fabs(rs - b_max) > tol || fabs(cs - b_max) > tol;
+      }
+      if (__any_sync(0xffffffffu, unbal)) status = AURORA_EINVAL;
+    }
+
+    // ---- decompose (commsched.py:406-435) interleaved with the strip (463-479)
+    int last_recv = -2;  // receiver of this lane in the last kept phase
+    double cur_dur = 0.0;
+    while (status == AURORA_OK) {
+      bool anyrow = false;
+      uint32_t sup = 0, pref = 0;
+      if (on) {
+        for (int j = 0; j < n; j++) {
+          double r = rem_s[lane][j];
+          if (r <= eps) { r = 0.0; rem_s[lane][j] = 0.0; }
+          double re = real_s[lane][j];
+          if (r < re) { re = r; real_s[lane][j] = r; }
+          anyrow |= r != 0.0;
+          if (r > 0) sup |= 1u << j;
+          if (re > eps) pref |= 1u << j;
+        }
+      }
+      if (!__any_sync(0xffffffffu, anyrow)) break;
+      if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
+      if (on) { ms.sup[lane] = sup; ms.pref[lane] = pref; }
+      __syncwarp();
+      if (lane == 0) ms.ok = perfect_matching(ms, n);
+      __syncwarp();
+      if (!ms.ok) { status = AURORA_ENOMATCH; break; }
+      const int pj = on ? ms.ml[lane] : 0;
+      const double dur = warp_min_d(on ? rem_s[lane][pj] : INF);
+      if (on) {
+        rem_s[lane][pj] -= dur;
+        double re = real_s[lane][pj] - dur;
+        real_s[lane][pj] = re < 0.0 ? 0.0 : re;
+        if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
+      }
+      if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
+      nr++;
+
+      // strip this raw phase against the real demand still undelivered (t_s)
+      double left = dur;
+      while (left > eps) {
+        double lv = on ? t_s[lane][pj] : 0.0;
+        bool act = on && lv > eps;
+        unsigned amask = __ballot_sync(0xffffffffu, act);
+        double step;
+        if (amask == 0) {
+          step = left;  // idle Phase((), left)
+        } else {
+          double m = warp_min_d(act ? lv : INF);
+          step = m < left ? m : left;
+        }
+        const int recv = act ? pj : -1;
+        if (step > eps) {  // drop <= eps phases, then _coalesce identical neighbours
+          bool same = np_ > 0 && __all_sync(0xffffffffu, !on || recv == last_recv);
+          if (same) {
+            cur_dur = cur_dur + step;
+          } else {
+            if (np_ >= P_MAX) { status = AURORA_EOVERFLOW; break; }
+            np_++;
+            cur_dur = step;
+            last_recv = recv;
+            if (on) p.phase_recv[(np_ - 1) * n + lane] = recv;
+          }
+          if (lane == 0) p.phase_dur[np_ - 1] = cur_dur;
+        }
+        if (amask == 0) break;
+        if (act) t_s[lane][pj] = lv - step;
+        left -= step;
+      }
+    }
+  }
+  if (lane == 0) {
+    *p.status = status;
+    *p.n_phases = status == AURORA_OK ? np_ : 0;
+    if (p.n_raw) *p.n_raw = nr;
+  }
+  if (status != AURORA_OK) np_ = 0;
+
+  // ---- engine tables: buffer layout + chunk list (CommSchedule.per_pair_totals
+  // order, commsched.py:291-297, split per phase)
+  if (p.soff && on) {
+    int acc = 0;
+    for (int j = 0; j < n; j++) {  // row prefix: list(i,j) inside sender i's send list
+      p.soff[lane * n + j] = acc;
+      acc += p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
+    }
+    acc = 0;
+    for (int i = 0; i < n; i++) {  // column prefix: list(i,j) inside receiver j's buffer
+      p.roff[i * n + lane] = acc;
+      acc += p.d32 ? p.d32[i * n + lane] : (int)p.d64[i * n + lane];
+    }
+  }
+  if (p.chunks) {
+    // rem_s: cumulative delivered time per pair; real_s (as int): tokens issued so far
+    int* tok = reinterpret_cast<int*>(&real_s[0][0]);
+    int* lastc = reinterpret_cast<int*>(&real_s[0][0]) + AUR_MAXN * AUR_MAXN;
+    if (on) {
+      for (int j = 0; j < n; j++) {
+        rem_s[lane][j] = 0.0;
+        tok[lane * AUR_MAXN + j] = 0;
+        lastc[lane * AUR_MAXN + j] = -1;
+      }
+      rcnt_s[lane] = 0;
+    }
+    int sseq = 0;  // this sender's chunk count so far
+    __syncwarp();
+    for (int k = 0; k < np_; k++) {
+      if (on) p.rchunks[k * n + lane] = make_int4(-1, 0, 0, 0);
+      __syncwarp();
+      const double dk = p.phase_dur[k];
+      const int j = on ? p.phase_recv[k * n + lane] : -1;
+      int4 c = make_int4(-1, 0, 0, 0);
+      if (j >= 0) {
+        double cum = rem_s[lane][j] + dk;
+        rem_s[lane][j] = cum;
+        double bw_j = p.bw ? p.bw[j] : 1.0;
+        double scale = bw_j < bw_i ? bw_j : bw_i;
+        int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
+        int tk = (int)rint(cum * scale);
+        if (tk > want) tk = want;
+        int start = tok[lane * AUR_MAXN + j];
+        if (tk < start) tk = start;
+        tok[lane * AUR_MAXN + j] = tk;
+        c = make_int4(j, start, tk - start, rcnt_s[j]);
+        lastc[lane * AUR_MAXN + j] = k;
+        p.rchunks[k * n + j] = make_int4(lane, start, tk - start, sseq);
+        sseq++;
+      }
+      __syncwarp();
+      if (j >= 0) rcnt_s[j] += 1;  // receivers are distinct within a phase
+      if (on) p.chunks[k * n + lane] = c;
+      __syncwarp();
+    }
+    // fractional (heterogeneous) durations: make every pair's chunk total exact
+    if (on) {
+      for (int j = 0; j < n; j++) {
+        int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
+        int got = tok[lane * AUR_MAXN + j];
+        int kl = lastc[lane * AUR_MAXN + j];
+        if (kl >= 0 && got != want) {
+          p.chunks[kl * n + lane].z += want - got;
+          p.rchunks[kl * n + j].z += want - got;
+        }
+      }
+      p.n_in[lane] = rcnt_s[lane];
+      p.n_out[lane] = sseq;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_perm,
+                                   double* raw_dur, int32_t* n_raw, int32_t* phase_recv,
+                                   double* phase_dur, int32_t* n_phases, double* b_max,
+                                   int32_t* status, void* stream) {
+  if (n < 1 || n > AUR_MAXN || !d || !phase_recv || !phase_dur || !n_phases || !status)
+    return AURORA_EINVAL;
+  SchedParams p{};
+  p.d64 = d;
+  p.bw = bw;
+  p.n = n;
+  p.raw_perm = raw_perm;
+  p.raw_dur = raw_dur;
+  p.n_raw = n_raw;
+  p.phase_recv = phase_recv;
+  p.phase_dur = phase_dur;
+  p.n_phases = n_phases;
+  p.b_max = b_max;
+  p.status = status;
+  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, int n,
+                                      int32_t* phase_recv, double* phase_dur, int32_t* n_phases,
+                                      int32_t* chunks, int32_t* rchunks, int32_t* n_in,
+                                      int32_t* n_out, int32_t* soff, int32_t* roff,
+                                      int32_t* status, void* stream) {
+  if (n < 1 || n > AUR_MAXN || !counts || !phase_recv || !phase_dur || !n_phases || !status ||
+      !chunks || !rchunks || !n_in || !n_out || !soff || !roff)
+    return AURORA_EINVAL;
+  SchedParams p{};
+  p.d32 = counts;
+  p.bw = bw;
+  p.n = n;
+  p.phase_recv = phase_recv;
+  p.phase_dur = phase_dur;
+  p.n_phases = n_phases;
+  p.status = status;
+  p.chunks = reinterpret_cast<int4*>(chunks);
+  p.rchunks = reinterpret_cast<int4*>(rchunks);
+  p.n_in = n_in;
+  p.n_out = n_out;
+  p.soff = soff;
+  p.roff = roff;
+  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_raw_phase_cap(int n) { return n * n - 2 * n + 2; }
+extern "C" int aurora_phase_cap(int n) { return n <= 1 ? 1 : 2 * n * n - 3 * n + 2; }

@@ -1,0 +1,103 @@
+"""Host side of the drop-in: boundary types, placement, reversal and the
+validator, checked against the reference's golden outputs."""
+import numpy as np
+import pytest
+
+import paper_2410_17043_b200 as A
+from golden_io import placement_cases, schedule_cases, spec_examples
+
+
+def test_traffic_matrix_validation_mirrors_reference():
+    with pytest.raises(ValueError):
+        A.TrafficMatrix([[0, 1]])
+    with pytest.raises(ValueError):
+        A.TrafficMatrix([[0, np.nan], [0, 0]])
+    with pytest.raises(ValueError, match=r"negative entry at \(0, 1\)"):
+        A.TrafficMatrix([[0, -1], [0, 0]])
+    m = A.TrafficMatrix([[5, 2], [3, 7]])
+    assert m.entries.tolist() == [[0, 2], [3, 0]]
+    assert not m.entries.flags.writeable
+    src = np.array([[0.0, 1.0], [2.0, 0.0]])
+    m = A.TrafficMatrix(src)
+    src[0, 1] = 9
+    assert m.entries[0, 1] == 1.0  # never aliases caller memory
+    assert A.reverse_all_to_all(A.TrafficMatrix([[0, 2], [3, 0]])).entries.tolist() == \
+        spec_examples()["reverse_0_2_3_0"]
+
+
+def test_cluster_and_plan_validation():
+    with pytest.raises(ValueError):
+        A.GpuSpec(0.0)
+    with pytest.raises(ValueError):
+        A.ClusterSpec((A.GpuSpec(1.0, 2.0), A.GpuSpec(2.0, 1.0)))
+    with pytest.raises(ValueError):
+        A.ClusterSpec(())
+    with pytest.raises(ValueError):
+        A.DeploymentPlan((0, 0))
+    p = A.DeploymentPlan.from_pairing([1, 0])
+    assert p.assignment_b == (1, 0) and p.pairing == (1, 0)
+    comb = A.combine_colocated(A.TrafficMatrix([[0, 1], [0, 0]]), A.TrafficMatrix([[0, 0], [2, 0]]), p)
+    assert comb.entries.tolist() == spec_examples()["combine_swapped"]
+
+
+def test_placement_matches_reference_goldens():
+    g = placement_cases()
+    for c in g["assign_exclusive_hetero"]:
+        cl = A.ClusterSpec(tuple(A.GpuSpec(b, s) for b, s in zip(c["bw"], c["scales"])))
+        assert list(A.assign_exclusive_hetero(c["loads"], cl).assignment_a) == c["assignment"]
+    for c in g["pair_case1"]:
+        pairing, h = A.pair_case1(c["a"], c["b"])
+        assert list(pairing) == c["pairing"] and h.tolist() == c["h"]
+    for c in g["bottleneck_matching"]:
+        m = A.bottleneck_matching(c["w"])
+        assert list(m.pairs) == c["pairs"] and m.bottleneck_value == c["value"]
+    for c in g["hopcroft_karp"]:
+        size, ml = A.hopcroft_karp(c["adj"], n_right=len(c["adj"]))
+        assert size == c["size"] and [(-1 if v is None else v) for v in ml] == c["match_left"]
+
+    def prof(p):
+        return A.LayerProfile(p["gate_work"], p["agg_work"], p["ffn_work_per_token"], p["ffn_base_work"],
+                              A.TrafficMatrix(p["d"]))
+
+    for c in g["colocate_homogeneous"]:
+        pl = A.colocate_homogeneous(prof(c["a"]), prof(c["b"]))
+        assert list(pl.assignment_a) == c["assignment_a"] and list(pl.assignment_b) == c["assignment_b"]
+        assert list(pl.pairing) == c["pairing"]
+    for c in g["colocate_heterogeneous"]:
+        cl = A.ClusterSpec(tuple(A.GpuSpec(b, s) for b, s in zip(c["bw"], c["scales"])))
+        pl = A.colocate_heterogeneous(prof(c["a"]), prof(c["b"]), cl)
+        assert list(pl.assignment_a) == c["assignment_a"] and list(pl.assignment_b) == c["assignment_b"]
+    for c in g["deploy_to_gpus"]:
+        assert A.deploy_to_gpus(A.TrafficMatrix(c["d"]), c["assignment"]).entries.tolist() == c["out"]
+    for c in g["combine_colocated"]:
+        pl = A.DeploymentPlan(tuple(c["assignment_a"]), tuple(c["assignment_b"]))
+        out = A.combine_colocated(A.TrafficMatrix(c["a"]), A.TrafficMatrix(c["b"]), pl)
+        assert out.entries.tolist() == c["out"]
+    for c in g["expert_loads"]:
+        lp = A.LayerProfile(0, 0, 0, 0, A.TrafficMatrix(c["d"]))
+        assert A.expert_loads(lp).tolist() == c["loads"]
+
+
+def test_spec_placement_examples():
+    ex = spec_examples()
+    cl = A.ClusterSpec((A.GpuSpec(1, 1), A.GpuSpec(2, 2), A.GpuSpec(4, 4)))
+    assert list(A.assign_exclusive_hetero([9, 4, 1], cl).assignment_a) == ex["assign_9_4_1"]
+    assert float(max(A.pair_case1([1, 3, 5], [2, 4, 6])[1])) == ex["pair_case1_135_246_hmax"]
+    assert A.bottleneck_matching([[5, 4], [5, 4]]).bottleneck_value == ex["bottleneck_5454"]
+    with pytest.raises(A.CaseOnePreconditionError):
+        A.pair_case1(np.array([[1, 2]]), np.array([[1, 1]]))
+
+
+def test_reversed_and_validator_on_golden_schedules():
+    for c in schedule_cases()[:200]:
+        phases = tuple(A.Phase(tuple(tuple(t) for t in tr), d) for tr, d in c["phases"])
+        s = A.CommSchedule(c["n"], phases, c["makespan"])
+        rev = s.reversed()
+        assert [[[list(t) for t in p.transfers], p.duration] for p in rev.phases] == c["reversed"]
+        assert s.completion_times().tolist() == c["completion_times"]
+        cl = A.ClusterSpec(tuple(A.GpuSpec(b) for b in c["bw"]))
+        assert A.validate_schedule(s, A.TrafficMatrix(c["d"]), cl).ok == c["valid"]
+    # a contended schedule is reported
+    bad = A.CommSchedule(3, (A.Phase(((0, 2), (1, 2)), 1.0),), 1.0)
+    rep = A.validate_schedule(bad, A.TrafficMatrix([[0, 0, 1], [0, 0, 1], [0, 0, 0]]), A.ClusterSpec.uniform(3))
+    assert not rep.contention_ok and not rep.optimal
