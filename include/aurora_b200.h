@@ -72,13 +72,14 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  *   n_in[n], n_out[n] chunks arriving at / leaving each rank
  *   soff[n][n]        start of list(i,j) inside sender i's send list (row prefix)
  *   roff[n][n]        start of list(i,j) inside receiver j's buffer (column prefix)
+ *   rtot[n]           rows each receiver holds (column sums incl. the diagonal)
  * Heterogeneous durations (time units, commsched.py:338-347) are converted to
  * whole tokens per chunk by rounding each pair's cumulative time x
  * min(B_i,B_j); the last chunk absorbs the rounding so per-pair totals are exact. */
 int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32_t* phase_recv,
                            double* phase_dur, int32_t* n_phases, int32_t* chunks,
                            int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* soff,
-                           int32_t* roff, int32_t* status, void* stream);
+                           int32_t* roff, int32_t* rtot, int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------- K1 ----
  * aurora_route: top-k gating + GPU x GPU traffic matrix. No reference
@@ -90,9 +91,9 @@ int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32
  *   tokens are grouped by rank: token t (local index) lives on rank
  *   rank_base + t / tokens_per_rank (workload.py:59-61)
  * Outputs: topk_idx[T][k], topk_w[T][k] (softmax over the selected logits),
- *   slot_dst[T][k] (destination rank of the slot, -1 when an earlier slot of
- *   the same token already goes there: a token crosses the network once per
- *   destination), blk_cnt[T/64][n] per-64-token-block destination histogram,
+ *   slot_dst[T][k] (destination rank g of the slot, or -(g+1) when an earlier
+ *   slot of the same token already goes to g: a token crosses the network
+ *   once per destination), blk_cnt[T/64][n] per-64-token-block histogram,
  *   counts[n][n] += this call's rows (must be zeroed by the caller). */
 int aurora_route(const void* x, const void* w_gate, const float* bias, int T, int H, int E,
                  int k, const int32_t* gpu_of_expert, int n, int rank_base, int tokens_per_rank,
@@ -115,7 +116,8 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * into j has landed), replacing a single NCCL alltoallv. mode 0 = dispatch
  * (CommSchedule phases, commsched.py:112-132), mode 1 = combine (the
  * reversed schedule, commsched.py:310-319: same phases, directions flipped).
- *   tables from aurora_schedule_counts; n_local ranks [rank_base, rank_base+n_local)
+ *   tables from aurora_schedule_counts; counts[n][n] from aurora_route;
+ *   n_local ranks [rank_base, rank_base+n_local) are served by this call
  *   dispatch: src rows = x_local[i_local] gathered through send_list,
  *             dst = recv_buf[j] rows roff[i][j] + first ...
  *   combine:  src rows = out_buf[j_local] rows roff[i][j] + first ...,
@@ -124,21 +126,25 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  *   arrival counters, zero on entry, left zero on exit), all device arrays.
  *   ctas_per_rank copy CTAs per local rank; all must be co-resident.
  *   spin_limit bounds every flag wait (0 = unbounded); on expiry status = ETIMEOUT. */
-int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* chunks,
-                  const int32_t* rchunks, const int32_t* n_phases, const int32_t* n_in,
-                  const int32_t* n_out, const int32_t* soff, const int32_t* roff,
-                  const int32_t* send_list, int send_list_stride, const void* const* src_bufs,
-                  void* const* dst_bufs, int64_t src_rank_stride_rows, int row_bytes,
+int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,
+                  const int32_t* chunks, const int32_t* rchunks, const int32_t* n_phases,
+                  const int32_t* n_in, const int32_t* n_out, const int32_t* soff,
+                  const int32_t* roff, const int32_t* send_list, int send_list_stride,
+                  const void* const* src_bufs, void* const* dst_bufs, int row_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
                   int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------- K7 ----
- * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret[soff[i][dst_s] + pos[t][s]]
- * in fp32, bf16 out. The reference's LayerProfile.agg_work (core.py:194-221). */
+ * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret_i[soff[i][dst_s] + pos[t][s]]
+ * in fp32, bf16 out (pre_weighted = 0; every slot must have its own destination),
+ * or the plain sum of the rows of the non-duplicate slots when the expert side
+ * already applied the gate weights and pre-reduced its local experts
+ * (pre_weighted = 1). ret_i = ret_buf + i_local * ret_rank_stride_rows rows.
+ * The reference's LayerProfile.agg_work (core.py:194-221). */
 int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const int32_t* soff,
                      const int32_t* pos, const int32_t* slot_dst, const float* topk_w, int T,
-                     int k, int H, int n, int rank_base, int tokens_per_rank, void* out,
-                     void* stream);
+                     int k, int H, int n, int rank_base, int tokens_per_rank, int pre_weighted,
+                     void* out, void* stream);
 
 /* ---------------------------------------------------------------- K5 ----
  * aurora_expert_ffn: SwiGLU experts as tcgen05/TMEM grouped GEMMs fed by TMA

@@ -1,0 +1,255 @@
+// K4 dispatch / K6 combine: the Aurora schedule executed as in-kernel stores
+// into peer memory (NVSwitch is the paper's big switch).
+//
+// Schedule semantics (reference pkg/src/moeplan/commsched.py:112-162): in
+// phase k sender i transmits `duration` tokens of its pair (i, j) while no
+// other sender targets j and i targets nobody else. Instead of a global
+// barrier per phase, every copy CTA runs its sender's chunk list in phase
+// order and starts a chunk once ALL earlier chunks into the same receiver
+// have landed (per-receiver arrival counter, release/acquire at system
+// scope). Each GPU's send order and receive order are exactly the
+// schedule's, so the execution stays contention-free while never waiting
+// longer than the phase-aligned timeline would. Correctness does not depend
+// on pacing: every chunk owns a disjoint, precomputed region of the peer
+// buffer.
+//
+// Combine (mode 1) replays the same phases with directions flipped -- the
+// reference's CommSchedule.reversed() (commsched.py:310-319) -- from the
+// rchunks table, sending expert outputs back to the token owners.
+#include "common.cuh"
+
+namespace {
+
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+
+struct EngineParams {
+  int mode, n, n_local, rank_base;
+  const int32_t* counts;
+  const int4* chunks;
+  const int4* rchunks;
+  const int32_t* n_phases;
+  const int32_t* n_in;
+  const int32_t* n_out;
+  const int32_t* soff;
+  const int32_t* roff;
+  const int32_t* send_list;
+  int send_list_stride;
+  const char* const* src_bufs;
+  char* const* dst_bufs;
+  int row_bytes;
+  int32_t* const* ctrs;
+  int C;
+  int max_phases;
+  long long spin_limit;
+  int32_t* status;
+};
+
+// wait until *ctr >= target (thread 0), bounded
+__device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long long limit) {
+  long long spins = 0;
+  while (ld_acquire_sys(ctr) < target) {
+    if (limit && ++spins > limit) return false;
+    __nanosleep(32);
+  }
+  return true;
+}
+
+// copy rows [r0, r1) of one chunk: warp per row, 16-byte vectors, 4 in flight per lane
+template <bool GATHER>
+__device__ __forceinline__ void copy_rows(const EngineParams& p, const char* src_base,
+                                          const int32_t* gather, int src_row0, char* dst_base,
+                                          int dst_row0, int r0, int r1) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = p.row_bytes >> 4;
+  for (int r = r0 + warp; r < r1; r += WARPS) {
+    const long long srow = GATHER ? (long long)gather[src_row0 + r] : (long long)(src_row0 + r);
+    const int4* s = reinterpret_cast<const int4*>(src_base + srow * p.row_bytes);
+    int4* d = reinterpret_cast<int4*>(dst_base + (long long)(dst_row0 + r) * p.row_bytes);
+    int u = lane;
+    for (; u + 96 < vec; u += 128) {
+      int4 a = ld_nc_v4(s + u), b = ld_nc_v4(s + u + 32), c = ld_nc_v4(s + u + 64),
+           e = ld_nc_v4(s + u + 96);
+      st_na_v4(d + u, a);
+      st_na_v4(d + u + 32, b);
+      st_na_v4(d + u + 64, c);
+      st_na_v4(d + u + 96, e);
+    }
+    for (; u < vec; u += 32) st_na_v4(d + u, ld_nc_v4(s + u));
+  }
+}
+
+__device__ __forceinline__ void signal(int32_t* ctr) {
+  __syncthreads();  // every thread's stores of this slice are done
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    red_release_sys_add(ctr, 1);
+  }
+}
+
+__global__ void __launch_bounds__(THREADS) engine_kernel(EngineParams p) {
+  const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
+  const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
+  const int n = p.n;
+  const int nph = min(*p.n_phases, p.max_phases);
+  const bool dispatch = p.mode == 0;
+  const char* src = p.src_bufs[r_local];
+  const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
+  __shared__ int abort_s;
+  if (threadIdx.x == 0) abort_s = 0;
+  __syncthreads();
+
+  for (int k = 0; k < nph; k++) {
+    // dispatch: chunk of sender g; combine: chunk of the reversed schedule where g sends back
+    const int4 ch = dispatch ? p.chunks[k * n + g] : p.rchunks[k * n + g];
+    const int peer = ch.x;  // dispatch: receiver j; combine: original sender i (now receiver)
+    if (peer < 0) continue;
+    const int first = ch.y, ntok = ch.z, seq = ch.w;
+    if (threadIdx.x == 0) {
+      if (!wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit)) {
+        abort_s = 1;
+        atomicExch(p.status, AURORA_ETIMEOUT);
+      }
+    }
+    __syncthreads();
+    if (abort_s) return;
+    const int per = (ntok + p.C - 1) / p.C;
+    const int r0 = min(ntok, c * per), r1 = min(ntok, r0 + per);
+    if (dispatch) {
+      // x rows of list(g, peer) -> recv_buf[peer] rows roff[g][peer] + first ...
+      copy_rows<true>(p, src, list, p.soff[g * n + peer] + first, p.dst_bufs[peer],
+                      p.roff[g * n + peer] + first, r0, r1);
+    } else {
+      // y rows of pair (peer, g) at roff[peer][g] -> ret_buf[peer] rows soff[peer][g] ...
+      copy_rows<false>(p, src, nullptr, p.roff[peer * n + g] + first, p.dst_bufs[peer],
+                       p.soff[peer * n + g] + first, r0, r1);
+    }
+    signal(p.ctrs[peer]);
+  }
+
+  // local (diagonal) rows never cross the network (TrafficMatrix zeroes them, core.py:95)
+  {
+    const int nloc = p.counts[g * n + g];
+    const int per = (nloc + p.C - 1) / p.C;
+    const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
+    if (dispatch)
+      copy_rows<true>(p, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g], r0, r1);
+    else
+      copy_rows<false>(p, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0,
+                       r1);
+  }
+
+  // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
+  if (c == 0 && threadIdx.x == 0) {
+    const int expect = (dispatch ? p.n_in[g] : p.n_out[g]) * p.C;
+    if (!wait_ge(p.ctrs[g], expect, p.spin_limit)) {
+      atomicExch(p.status, AURORA_ETIMEOUT);
+    } else {
+      *(volatile int32_t*)p.ctrs[g] = 0;
+      __threadfence_system();
+    }
+  }
+}
+
+// K7: out[t] = sum over slots of (w *) returned rows, fp32 accumulate, bf16 out. Warp per token.
+__global__ void __launch_bounds__(THREADS) aggregate_kernel(
+    const __nv_bfloat16* __restrict__ ret, long long ret_stride_rows, const int32_t* __restrict__ soff,
+    const int32_t* __restrict__ pos, const int32_t* __restrict__ slot_dst,
+    const float* __restrict__ topk_w, int T, int k, int H, int n, int rank_base,
+    int tokens_per_rank, int pre_weighted, __nv_bfloat16* __restrict__ out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * WARPS + warp;
+  if (t >= T) return;
+  const int i_local = t / tokens_per_rank, i = rank_base + i_local;
+  const __nv_bfloat16* base = ret + (size_t)i_local * ret_stride_rows * H;
+  const int4* rows[8];
+  float w[8];
+  int ns = 0;
+  for (int s = 0; s < k; s++) {
+    const int v = slot_dst[(size_t)t * k + s];
+    if (pre_weighted && v < 0) continue;  // duplicate slot: row already pre-reduced
+    const int j = v >= 0 ? v : -(v + 1);
+    rows[ns] = reinterpret_cast<const int4*>(base + (size_t)(soff[i * n + j] + pos[(size_t)t * k + s]) * H);
+    w[ns] = pre_weighted ? 1.0f : topk_w[(size_t)t * k + s];
+    ns++;
+  }
+  int4* o = reinterpret_cast<int4*>(out + (size_t)t * H);
+  for (int u = lane; u < H / 8; u += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < ns; q++) {
+      int4 v = ld_nc_v4(rows[q] + u);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        float2 f = __bfloat1622float2(b[e]);
+        acc[2 * e] = fmaf(w[q], f.x, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(w[q], f.y, acc[2 * e + 1]);
+      }
+    }
+    int4 r;
+    __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    o[u] = r;
+  }
+}
+
+}  // namespace
+
+extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,
+                             const int32_t* chunks, const int32_t* rchunks,
+                             const int32_t* n_phases, const int32_t* n_in, const int32_t* n_out,
+                             const int32_t* soff, const int32_t* roff, const int32_t* send_list,
+                             int send_list_stride, const void* const* src_bufs,
+                             void* const* dst_bufs, int row_bytes, int32_t* const* ctrs,
+                             int ctas_per_rank, int max_phases, int64_t spin_limit,
+                             int32_t* status, void* stream) {
+  if ((mode != 0 && mode != 1) || n < 1 || n > AUR_MAXN || n_local < 1 || rank_base < 0 ||
+      rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
+      !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
+      (mode == 0 && !send_list))
+    return AURORA_EINVAL;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (n_local * ctas_per_rank > 2 * sms) return AURORA_EINVAL;  // must be co-resident
+  EngineParams p;
+  p.mode = mode;
+  p.n = n;
+  p.n_local = n_local;
+  p.rank_base = rank_base;
+  p.counts = counts;
+  p.chunks = reinterpret_cast<const int4*>(chunks);
+  p.rchunks = reinterpret_cast<const int4*>(rchunks);
+  p.n_phases = n_phases;
+  p.n_in = n_in;
+  p.n_out = n_out;
+  p.soff = soff;
+  p.roff = roff;
+  p.send_list = send_list;
+  p.send_list_stride = send_list_stride;
+  p.src_bufs = reinterpret_cast<const char* const*>(src_bufs);
+  p.dst_bufs = reinterpret_cast<char* const*>(dst_bufs);
+  p.row_bytes = row_bytes;
+  p.ctrs = ctrs;
+  p.C = ctas_per_rank;
+  p.max_phases = max_phases;
+  p.spin_limit = spin_limit;
+  p.status = status;
+  engine_kernel<<<n_local * ctas_per_rank, THREADS, 0, (cudaStream_t)stream>>>(p);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows,
+                                const int32_t* soff, const int32_t* pos, const int32_t* slot_dst,
+                                const float* topk_w, int T, int k, int H, int n, int rank_base,
+                                int tokens_per_rank, int pre_weighted, void* out, void* stream) {
+  if (T <= 0 || k < 1 || k > 8 || H % 8 || n < 1 || n > AUR_MAXN || tokens_per_rank < 1)
+    return AURORA_EINVAL;
+  aggregate_kernel<<<(T + WARPS - 1) / WARPS, THREADS, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)ret_buf, ret_rank_stride_rows, soff, pos, slot_dst, topk_w, T, k, H,
+      n, rank_base, tokens_per_rank, pre_weighted, (__nv_bfloat16*)out);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}

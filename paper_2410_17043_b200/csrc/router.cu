@@ -1,0 +1,257 @@
+// K1 router (top-k gating + GPU x GPU traffic histogram) and K3 pack (token
+// permutation into per-destination send lists).
+//
+// The reference has no router: it models the gate as LayerProfile.gate_work
+// (pkg/src/moeplan/core.py:194-221) and consumes its output as a
+// TrafficMatrix (core.py:75-117) of one batch shard per GPU (workload.py:55-87).
+// The arithmetic below DEFINES the router (oracle/router_oracle.c restates
+// it bit-for-bit):
+//   raw(t,e) = xor-tree over 32 lanes (offsets 16,8,4,2,1) of
+//              p_l = sequential fmaf over h = 256 i + 8 l + jj  (i asc, jj asc)
+//   logit    = raw + bias[e];  top-k with lowest index on ties;
+//   weights  = softmax over the k selected logits.
+// The tree is evaluated as a reduce-scatter (lane q ends with pair q), which
+// has the same tree shape, hence the same bits, as the butterfly.
+//
+// HBM-bound: x is streamed once with 16-byte non-allocating loads; w_gate
+// (E*H*2 bytes) stays L1/L2-resident.
+#include "common.cuh"
+
+namespace {
+
+constexpr int TILE = 64;      // tokens per CTA (blk_cnt granularity)
+constexpr int WARPS = 8;      // 256 threads
+constexpr int MAXK = 8;
+constexpr int MAXE = 64;
+
+__device__ __forceinline__ void bf16x8_to_f32(const int4& v, float* f) {
+  const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    f[2 * q] = __uint_as_float(w[q] << 16);
+    f[2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
+  }
+}
+
+// One warp computes the logits of TG tokens x EP experts (TG*EP == 32) and
+// leaves pair q = lane (token q / EP, expert q % EP) in its return value.
+template <int TG, int EP>
+__device__ __forceinline__ float warp_logits(const int4* __restrict__ xrow[TG],
+                                             const int4* __restrict__ wrow, int h_chunks, int lane,
+                                             int hv) {
+  static_assert(TG * EP == 32, "tile");
+  float acc[TG][EP];
+#pragma unroll
+  for (int t = 0; t < TG; t++)
+#pragma unroll
+    for (int e = 0; e < EP; e++) acc[t][e] = 0.0f;
+  for (int i = 0; i < h_chunks; i++) {
+    const int c = 32 * i + lane;  // 16-byte chunk index within the row
+    float xf[TG][8];
+#pragma unroll
+    for (int t = 0; t < TG; t++) {
+      int4 v = ld_nc_v4(xrow[t] + c);
+      bf16x8_to_f32(v, xf[t]);
+    }
+#pragma unroll
+    for (int e = 0; e < EP; e++) {
+      int4 wv = __ldg(wrow + (size_t)e * hv + c);
+      float wf[8];
+      bf16x8_to_f32(wv, wf);
+#pragma unroll
+      for (int t = 0; t < TG; t++)
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) acc[t][e] = fmaf(xf[t][jj], wf[jj], acc[t][e]);
+    }
+  }
+  // reduce-scatter: 32 values per lane -> 1, keeping the upper half when (lane & o)
+  float v[32];
+#pragma unroll
+  for (int q = 0; q < 32; q++) v[q] = acc[q / EP][q % EP];
+#pragma unroll
+  for (int o = 16, s = 32; o >= 1; o >>= 1, s >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int q = 0; q < s / 2; q++) {
+      float mine = upper ? v[q + s / 2] : v[q];
+      float send = upper ? v[q] : v[q + s / 2];
+      float got = __shfl_xor_sync(0xffffffffu, send, o);
+      v[q] = mine + got;
+    }
+  }
+  return v[0];
+}
+
+template <int TG, int EP>
+__global__ void __launch_bounds__(WARPS * 32) route_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int T, int H, int E, int k,
+    const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
+    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
+    int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  __shared__ float logit_s[TILE][MAXE + 1];
+  __shared__ int hist_s[AUR_MAXN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * TILE;
+  const int hv = H / 8;         // int4 per row
+  const int h_chunks = H / 256;
+  if (threadIdx.x < AUR_MAXN) hist_s[threadIdx.x] = 0;
+
+  // ---- logits: warp w owns tokens [t0 + 8w, t0 + 8w + 8)
+  for (int tg = 0; tg < 8; tg += TG) {
+    const int tb = t0 + warp * 8 + tg;
+    const int4* xrow[TG];
+#pragma unroll
+    for (int t = 0; t < TG; t++) {
+      int tt = min(tb + t, T - 1);
+      xrow[t] = reinterpret_cast<const int4*>(x + (size_t)tt * H);
+    }
+    for (int e0 = 0; e0 < E; e0 += EP) {
+      const int4* wrow = reinterpret_cast<const int4*>(wg + (size_t)e0 * H);
+      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv);
+      const int tq = lane / EP, eq = e0 + lane % EP;
+      logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
+    }
+  }
+  __syncthreads();
+
+  // ---- top-k + softmax + destinations: thread per token (first 64 threads)
+  if (threadIdx.x < TILE) {
+    const int tl = threadIdx.x, t = t0 + tl;
+    const bool valid = t < T;
+    int dst[MAXK];
+    if (valid) {
+      uint64_t taken = 0;
+      int sel[MAXK];
+      float sv[MAXK];
+      for (int s = 0; s < k; s++) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < E; e++) {
+          if ((taken >> e) & 1) continue;
+          float l = logit_s[tl][e];
+          if (best < 0 || l > bv) { best = e; bv = l; }
+        }
+        taken |= 1ull << best;
+        sel[s] = best;
+        sv[s] = bv;
+      }
+      float z = 0.0f, ex[MAXK];
+      for (int s = 0; s < k; s++) { ex[s] = expf(sv[s] - sv[0]); z += ex[s]; }
+      for (int s = 0; s < k; s++) {
+        topk_idx[(size_t)t * k + s] = sel[s];
+        topk_w[(size_t)t * k + s] = ex[s] / z;
+        int g = gpu_of_expert[sel[s]];
+        bool dup = false;
+        for (int q = 0; q < s; q++) dup |= (gpu_of_expert[sel[q]] == g);
+        dst[s] = dup ? -1 : g;
+        slot_dst[(size_t)t * k + s] = dup ? -(g + 1) : g;  // duplicates encoded as -(rank+1)
+      }
+    }
+    // warp-aggregated histogram: one shared atomic per distinct destination per warp
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    for (int s = 0; s < k; s++) {
+      int dd = valid ? dst[s] : -1;
+      unsigned peers = __match_any_sync(0xffffffffu, dd);
+      if (valid && dd >= 0 && (__ffs(peers & active) - 1) == lane) atomicAdd(&hist_s[dd], __popc(peers));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < n) {
+    const int c = hist_s[threadIdx.x];
+    blk_cnt[(size_t)blockIdx.x * n + threadIdx.x] = c;
+    const int src = rank_base + t0 / tokens_per_rank;
+    if (c) atomicAdd(&counts[src * n + threadIdx.x], c);
+  }
+}
+
+// K3: token permutation. CTA = 64 threads = the 64 tokens of one route tile.
+// list(i, j) = rank i's tokens bound for j in ascending order; the entry for
+// token t lands at soff[i][j] + (entries of earlier tiles of rank i, from
+// blk_cnt) + (entries of earlier tokens in this tile, from warp ballots).
+__global__ void __launch_bounds__(TILE) pack_kernel(
+    const int32_t* __restrict__ slot_dst, const int32_t* __restrict__ blk_cnt,
+    const int32_t* __restrict__ counts, int T, int k, int n, int rank_base, int tokens_per_rank,
+    int32_t* __restrict__ send_list, int32_t* __restrict__ pos) {
+  __shared__ int base_s[AUR_MAXN];   // entries of earlier tiles of rank i, per destination
+  __shared__ int soff_s[AUR_MAXN];   // start of list(i, j) in rank i's send list
+  __shared__ int warp0_s[AUR_MAXN];  // entries of warp 0 per destination
+  const int tl = threadIdx.x, warp = tl >> 5, lane = tl & 31;
+  const int t0 = blockIdx.x * TILE, t = t0 + tl;
+  const int i_local = t0 / tokens_per_rank, i = rank_base + i_local;
+  const int b_first = i_local * (tokens_per_rank / TILE);
+  if (tl < n) {
+    int so = 0, acc = 0;
+    for (int jj = 0; jj < tl; jj++) so += counts[i * n + jj];
+    for (int b = b_first; b < (int)blockIdx.x; b++) acc += blk_cnt[(size_t)b * n + tl];
+    base_s[tl] = acc;
+    soff_s[tl] = so;
+  }
+  const bool valid = t < T;
+  int full[MAXK];  // destination rank of every slot (duplicates decoded)
+  uint32_t mine = 0;
+  for (int s = 0; s < k; s++) {
+    int v = valid ? slot_dst[(size_t)t * k + s] : 0;
+    full[s] = v >= 0 ? v : -(v + 1);
+    if (valid) mine |= 1u << full[s];
+  }
+  int* list = send_list + (size_t)i_local * ((size_t)tokens_per_rank * k);
+  const unsigned lt = (1u << lane) - 1;
+  unsigned bal[AUR_MAXN];
+  for (int j = 0; j < n; j++) {
+    bal[j] = __ballot_sync(0xffffffffu, (mine >> j) & 1);
+    if (warp == 0 && lane == 0) warp0_s[j] = __popc(bal[j]);
+  }
+  __syncthreads();
+  if (valid) {
+    for (int s = 0; s < k; s++) {
+      const int j = full[s];
+      const int p = base_s[j] + (warp ? warp0_s[j] : 0) + __popc(bal[j] & lt);
+      pos[(size_t)t * k + s] = p;
+      if (slot_dst[(size_t)t * k + s] >= 0) list[soff_s[j] + p] = t - i_local * tokens_per_rank;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias, int T, int H,
+                            int E, int k, const int32_t* gpu_of_expert, int n, int rank_base,
+                            int tokens_per_rank, int32_t* topk_idx, float* topk_w,
+                            int32_t* slot_dst, int32_t* blk_cnt, int32_t* counts, void* stream) {
+  if (T <= 0 || H % 256 || k < 1 || k > MAXK || k > E || n < 1 || n > AUR_MAXN ||
+      tokens_per_rank % TILE || T % tokens_per_rank)
+    return AURORA_EINVAL;
+  const int blocks = (T + TILE - 1) / TILE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const __nv_bfloat16* xb = (const __nv_bfloat16*)x;
+  const __nv_bfloat16* wb = (const __nv_bfloat16*)w_gate;
+#define LAUNCH(TG, EP)                                                                          \
+  route_kernel<TG, EP><<<blocks, WARPS * 32, 0, s>>>(xb, wb, bias, T, H, E, k, gpu_of_expert, n, \
+                                                    rank_base, tokens_per_rank, topk_idx,        \
+                                                    topk_w, slot_dst, blk_cnt, counts)
+  switch (E) {
+    case 4: LAUNCH(8, 4); break;
+    case 8: LAUNCH(4, 8); break;
+    case 16: LAUNCH(2, 16); break;
+    case 32: LAUNCH(1, 32); break;
+    case 64: LAUNCH(1, 32); break;
+    default: return AURORA_EUNSUPPORTED;
+  }
+#undef LAUNCH
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts,
+                           int T, int k, int n, int rank_base, int tokens_per_rank,
+                           int32_t* send_list, int32_t* pos, void* stream) {
+  if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
+      T % tokens_per_rank)
+    return AURORA_EINVAL;
+  pack_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(slot_dst, blk_cnt, counts, T, k, n,
+                                                           rank_base, tokens_per_rank, send_list,
+                                                           pos);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}

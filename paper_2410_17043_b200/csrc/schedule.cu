@@ -43,6 +43,7 @@ struct SchedParams {
   int32_t* n_out;         // [n]             chunks leaving each sender
   int32_t* soff;          // [n][n]          (nullable) start of list(i,j) in sender i's send list
   int32_t* roff;          // [n][n]          (nullable) start of list(i,j) in receiver j's buffer
+  int32_t* rtot;          // [n]             (nullable) rows held by each receiver
 };
 
 // numpy pairwise_sum (n <= 128 branch, and n < 8 sequential), row-major row of t
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       p.roff[i * n + lane] = acc;
       acc += p.d32 ? p.d32[i * n + lane] : (int)p.d64[i * n + lane];
     }
+    if (p.rtot) p.rtot[lane] = acc;
   }
   if (p.chunks) {
     // rem_s: cumulative delivered time per pair; real_s (as int): tokens issued so far
@@ -454,7 +456,7 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
                                       int32_t* phase_recv, double* phase_dur, int32_t* n_phases,
                                       int32_t* chunks, int32_t* rchunks, int32_t* n_in,
                                       int32_t* n_out, int32_t* soff, int32_t* roff,
-                                      int32_t* status, void* stream) {
+                                      int32_t* rtot, int32_t* status, void* stream) {
   if (n < 1 || n > AUR_MAXN || !counts || !phase_recv || !phase_dur || !n_phases || !status ||
       !chunks || !rchunks || !n_in || !n_out || !soff || !roff)
     return AURORA_EINVAL;
@@ -472,6 +474,7 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
   p.n_out = n_out;
   p.soff = soff;
   p.roff = roff;
+  p.rtot = rtot;
   aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

@@ -92,7 +92,7 @@ def test_pack_oracle_small():
     topk = np.array([[0, 1], [1, 0], [2, 3], [3, 3 - 1], [0, 2], [1, 1 + 2]], dtype=np.int32)
     counts, lists, pos = pack_oracle(topk, [0, 0, 1, 1], 2)  # 4 experts on 2 GPUs, 3 tokens per rank
     # rank 0 has tokens 0,1,2; token 0 -> experts 0,1 both on GPU 0 (dedupe)
-    assert counts.tolist() == [[2, 1], [2, 2]]
+    assert counts.tolist() == [[2, 1], [2, 3]]
     assert lists[0][0] == [0, 1] and lists[0][1] == [2]
     assert lists[1][0] == [4, 5] and lists[1][1] == [3, 4, 5]
     assert pos[0].tolist() == [0, 0] and pos[4].tolist() == [0, 1] and pos[5].tolist() == [1, 2]
