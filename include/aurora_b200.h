@@ -164,6 +164,12 @@ int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* 
 int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_rows, int G,
                         int64_t cap, int N, int K, int epilogue, int num_sms, void* stream);
 
+/* Diagnostics: one K2 run with per-section cycle counters
+ * prof[5] = {snap+masks, matching, update, strip, decompose total};
+ * scratch >= (n^2-2n+2)*n + 3 + (2n^2-3n+2)*n int32, dscratch >= 3n^2 doubles. */
+int aurora_debug_schedule_cycles(const double* d, int n, long long* prof, int32_t* scratch,
+                                 double* dscratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,7 @@ _SIGNATURES = {
                          _c_int, _vp, _vp],
     "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],
     "aurora_grouped_gemm": [_vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _c_int, _vp],
+    "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
 }
 
 _lib = None

@@ -44,6 +44,7 @@ struct SchedParams {
   int32_t* soff;          // [n][n]          (nullable) start of list(i,j) in sender i's send list
   int32_t* roff;          // [n][n]          (nullable) start of list(i,j) in receiver j's buffer
   int32_t* rtot;          // [n]             (nullable) rows held by each receiver
+  long long* prof;        // [8]             (nullable) diagnostics: cycles per section
 };
 
 // numpy pairwise_sum (n <= 128 branch, and n < 8 sequential), row-major row of t
@@ -282,7 +283,9 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     // ---- decompose (commsched.py:406-435) interleaved with the strip (463-479)
     int last_recv = -2;  // receiver of this lane in the last kept phase
     double cur_dur = 0.0;
+    long long cyc[5] = {0, 0, 0, 0, clock64()};
     while (status == AURORA_OK) {
+      long long c0 = clock64();
       bool anyrow = false;
       uint32_t sup = 0, pref = 0;
       if (on) {
@@ -300,8 +303,12 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
       if (on) { ms.sup[lane] = sup; ms.pref[lane] = pref; }
       __syncwarp();
+      long long c1 = clock64();
       if (lane == 0) ms.ok = perfect_matching(ms, n);
       __syncwarp();
+      long long c2 = clock64();
+      cyc[0] += c1 - c0;
+      cyc[1] += c2 - c1;
       if (!ms.ok) { status = AURORA_ENOMATCH; break; }
       const int pj = on ? ms.ml[lane] : 0;
       const double dur = warp_min_d(on ? rem_s[lane][pj] : INF);
@@ -313,6 +320,8 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       }
       if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
       nr++;
+      long long c3 = clock64();
+      cyc[2] += c3 - c2;
 
       // strip this raw phase against the real demand still undelivered (t_s)
       double left = dur;
@@ -345,6 +354,11 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
         if (act) t_s[lane][pj] = lv - step;
         left -= step;
       }
+      cyc[3] += clock64() - c3;
+    }
+    if (p.prof && lane == 0) {
+      for (int q = 0; q < 4; q++) p.prof[q] = cyc[q];
+      p.prof[4] = clock64() - cyc[4];
     }
   }
   if (lane == 0) {
@@ -475,6 +489,28 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
   p.soff = soff;
   p.roff = roff;
   p.rtot = rtot;
+  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+// Diagnostics: cycles spent in [snap+masks, matching, update, strip, decompose total].
+extern "C" int aurora_debug_schedule_cycles(const double* d, int n, long long* prof,
+                                            int32_t* scratch, double* dscratch, void* stream) {
+  if (n < 1 || n > AUR_MAXN) return AURORA_EINVAL;
+  const int R = n * n - 2 * n + 2, P = 2 * n * n - 3 * n + 2;
+  SchedParams p{};
+  p.d64 = d;
+  p.n = n;
+  p.raw_perm = scratch;
+  p.n_raw = scratch + R * n;
+  p.n_phases = scratch + R * n + 1;
+  p.status = scratch + R * n + 2;
+  p.phase_recv = scratch + R * n + 3;
+  p.raw_dur = dscratch;
+  p.phase_dur = dscratch + R;
+  p.prof = prof;
+  (void)P;
   aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
