@@ -1,0 +1,309 @@
+"""The Aurora MoE layer on B200: router -> on-device schedule -> scheduled
+NVSwitch dispatch -> tcgen05 experts -> reversed-schedule combine -> aggregate.
+
+This is the execution the reference only simulates: ``simulate_exclusive``
+(reference ``pkg/src/moeplan/sim.py:130-154``) models a layer as gate ->
+all-to-all (``build_schedule``) -> FFN -> reversed all-to-all -> aggregation
+behind barriers. Here every stage is a CUDA kernel from libaurora_b200.so and
+the host never waits on the device inside :meth:`AuroraMoELayer.forward`.
+
+Ranks and devices. The layer has ``n`` expert-parallel ranks (one expert per
+rank, experts placed by a ``DeploymentPlan``: ``assignment_a[e]`` = rank of
+expert e, reference core.py:253-304). A process drives ``n_local`` of them on
+its GPU; with one process per GPU and ``n_local == 1`` the peer buffers are
+CUDA-IPC mappings of the other GPUs' HBM and the engine's stores cross
+NVSwitch. With fewer GPUs than ranks the remaining ranks share a GPU
+("loopback"): identical kernels, identical tables, peer pointers that
+happen to be local.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import DeploymentPlan
+
+__all__ = ["MoEConfig", "AuroraMoELayer", "zipf_bias", "interleave_gate_up"]
+
+
+@dataclass(frozen=True)
+class MoEConfig:
+    """Shapes of one MoE layer."""
+
+    hidden: int
+    ffn: int
+    experts: int
+    top_k: int
+    tokens: int          # global tokens T per layer call (T / ranks per rank)
+    ranks: int           # expert-parallel ranks n
+    skew: float = 1.0    # Zipf exponent of the router bias
+    seed: int = 0
+
+    @property
+    def tokens_per_rank(self) -> int:
+        return self.tokens // self.ranks
+
+    def validate(self) -> None:
+        if self.tokens % self.ranks or self.tokens_per_rank % 64:
+            raise ValueError("tokens per rank must be a multiple of 64")
+        if self.hidden % 256 or self.ffn % 128 or (2 * self.ffn) % 256:
+            raise ValueError("hidden must be a multiple of 256 and ffn of 128")
+        if self.experts != self.ranks:
+            raise ValueError("this build hosts one expert per rank (experts == ranks), as the reference's "
+                             "DeploymentPlan does (core.py:246-273)")
+        if not (1 <= self.top_k <= min(8, self.experts)):
+            raise ValueError("top_k out of range")
+
+
+def zipf_bias(experts: int, skew: float, gen: torch.Generator) -> torch.Tensor:
+    """Router bias b_e = -s ln(rank_e + 1), rank = random permutation: the
+    popularity law of workload.py:49-52 (1/(rank+1)^s) in logit space."""
+    rank = torch.randperm(experts, generator=gen)
+    return (-skew * torch.log(rank.double() + 1.0)).float()
+
+
+def interleave_gate_up(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """[G,F,H] gate and up projections -> [G,2F,H] in 128-row blocks
+    (gate block b, up block b, ...), the layout the SwiGLU epilogue reads."""
+    G, F, H = w1.shape
+    return torch.stack([w1.view(G, F // 128, 128, H), w3.view(G, F // 128, 128, H)], dim=2).reshape(G, 2 * F, H)
+
+
+class AuroraMoELayer:
+    """One MoE layer, expert-parallel over ``cfg.ranks`` ranks.
+
+    ``rank_base``/``n_local`` select the ranks this process drives
+    (default: all of them, on the current device). ``peer_bufs`` is filled
+    by :mod:`paper_2410_17043_b200.dist` for multi-GPU runs.
+    """
+
+    def __init__(self, cfg: MoEConfig, plan: Optional[DeploymentPlan] = None, *, rank_base: int = 0,
+                 n_local: Optional[int] = None, bandwidths=None, device=None, ctas_per_rank: Optional[int] = None,
+                 weights: Optional[dict] = None, spin_limit: int = 1 << 26):
+        cfg.validate()
+        self.cfg = cfg
+        self.L = _lib.load()
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        n = cfg.ranks
+        self.n = n
+        self.rank_base = rank_base
+        self.n_local = n if n_local is None else n_local
+        self.plan = plan if plan is not None else DeploymentPlan.identity(n)
+        if self.plan.n != cfg.experts:
+            raise ValueError("plan must cover every expert")
+        sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        self.num_sms = sms
+        self.C = ctas_per_rank or max(1, min(32, (sms // self.n_local)))
+        self.spin_limit = spin_limit
+        H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
+        Tr = cfg.tokens_per_rank
+        self.T_local = Tr * self.n_local
+        dev = self.dev
+        i32 = dict(dtype=torch.int32, device=dev)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+
+        # ---- parameters (synthetic, seeded; experts hosted here only)
+        if weights is None:
+            weights = self.synthetic_weights(cfg, dev, [self.expert_of_rank(r) for r in self.local_ranks])
+        self.w_gate = weights["w_gate"].to(dev, torch.bfloat16).contiguous()
+        self.bias = weights["bias"].to(dev, torch.float32).contiguous()
+        self.w13 = weights["w13"].to(dev, torch.bfloat16).contiguous()   # [n_local, 2F, H] interleaved
+        self.w2 = weights["w2"].to(dev, torch.bfloat16).contiguous()     # [n_local, H, F]
+        self.gpu_of_expert = torch.tensor(self.plan.assignment_a, **i32)
+        self.bw = None if bandwidths is None else torch.tensor(np.asarray(bandwidths, float), dtype=torch.float64,
+                                                               device=dev)
+
+        # ---- routing / permutation state
+        self.topk_idx = torch.empty(self.T_local, k, **i32)
+        self.topk_w = torch.empty(self.T_local, k, dtype=torch.float32, device=dev)
+        self.slot_dst = torch.empty(self.T_local, k, **i32)
+        self.blk_cnt = torch.empty(self.T_local // 64, n, **i32)
+        self.counts = torch.zeros(n, n, **i32)
+        self.send_list = torch.empty(self.n_local, Tr * k, **i32)
+        self.pos = torch.empty(self.T_local, k, **i32)
+
+        # ---- schedule tables (written by K2 on the device)
+        P = self.L.aurora_phase_cap(n)
+        self.P = P
+        self.phase_recv = torch.empty(P, n, **i32)
+        self.phase_dur = torch.empty(P, dtype=torch.float64, device=dev)
+        self.sched_i = torch.zeros(2, **i32)          # n_phases, status
+        self.chunks = torch.empty(P, n, 4, **i32)
+        self.rchunks = torch.empty(P, n, 4, **i32)
+        self.n_in = torch.empty(n, **i32)
+        self.n_out = torch.empty(n, **i32)
+        self.soff = torch.empty(n, n, **i32)
+        self.roff = torch.empty(n, n, **i32)
+        self.rtot = torch.empty(n, **i32)
+        self.engine_status = torch.zeros(1, **i32)
+
+        # ---- data buffers. A rank can receive at most every token once.
+        self.cap = cfg.tokens
+        self.recv = torch.empty(self.n_local * self.cap, H, **bf)
+        self.hbuf = torch.empty(self.n_local * self.cap, F, **bf)
+        self.ybuf = torch.empty(self.n_local * self.cap, H, **bf)
+        self.ret_stride = Tr * k
+        self.ret = torch.empty(self.n_local * self.ret_stride, H, **bf)
+        self.out = torch.empty(self.T_local, H, **bf)
+        self.ctr_d = torch.zeros(n, **i32)
+        self.ctr_c = torch.zeros(n, **i32)
+        self.x = None
+        self._tables_for(None)
+
+    # ------------------------------------------------------------ helpers
+    @property
+    def local_ranks(self):
+        return list(range(self.rank_base, self.rank_base + self.n_local))
+
+    def expert_of_rank(self, r: int) -> int:
+        return self.plan.assignment_a.index(r)
+
+    @staticmethod
+    def synthetic_weights(cfg: MoEConfig, dev, experts) -> dict:
+        """Seeded random-init parameters: W_g ~ N(0, 1/H), Zipf bias, expert
+        weights N(0, 1/fan_in); generated per expert so any
+        rank subset reproduces the same model."""
+        H, F, E = cfg.hidden, cfg.ffn, cfg.experts
+        g = torch.Generator(device="cpu").manual_seed(cfg.seed)
+        w_gate = (torch.randn(E, H, generator=g) / math.sqrt(H)).to(torch.bfloat16)
+        bias = zipf_bias(E, cfg.skew, g)
+        w13, w2 = [], []
+        for e in experts:
+            ge = torch.Generator(device=dev).manual_seed(cfg.seed * 1000003 + 17 * e + 1)
+            w1 = (torch.randn(1, F, H, generator=ge, device=dev) / math.sqrt(H)).to(torch.bfloat16)
+            w3 = (torch.randn(1, F, H, generator=ge, device=dev) / math.sqrt(H)).to(torch.bfloat16)
+            w13.append(interleave_gate_up(w1, w3)[0])
+            w2.append((torch.randn(H, F, generator=ge, device=dev) / math.sqrt(F)).to(torch.bfloat16))
+        return {"w_gate": w_gate, "bias": bias, "w13": torch.stack(w13), "w2": torch.stack(w2)}
+
+    def _ptr_table(self, ptrs) -> torch.Tensor:
+        return torch.tensor([int(p) for p in ptrs], dtype=torch.int64, device=self.dev)
+
+    def _tables_for(self, x: Optional[torch.Tensor], peers: Optional[dict] = None) -> None:
+        """Device pointer tables for the engine. ``peers`` (multi-GPU) maps
+        buffer name -> list of n peer addresses; loopback uses local slices."""
+        H = self.cfg.hidden
+        esz = 2
+        Tr = self.cfg.tokens_per_rank
+        if peers is None:
+            recv_p = [self.recv.data_ptr() + r * self.cap * H * esz for r in range(self.n)]
+            ret_p = [self.ret.data_ptr() + r * self.ret_stride * H * esz for r in range(self.n)]
+            ctr_d = [self.ctr_d.data_ptr() + 4 * r for r in range(self.n)]
+            ctr_c = [self.ctr_c.data_ptr() + 4 * r for r in range(self.n)]
+        else:
+            recv_p, ret_p, ctr_d, ctr_c = peers["recv"], peers["ret"], peers["ctr_d"], peers["ctr_c"]
+        self.t_dst_d = self._ptr_table(recv_p)
+        self.t_dst_c = self._ptr_table(ret_p)
+        self.t_ctr_d = self._ptr_table(ctr_d)
+        self.t_ctr_c = self._ptr_table(ctr_c)
+        self.t_src_c = self._ptr_table([self.ybuf.data_ptr() + r * self.cap * H * esz for r in range(self.n_local)])
+        if x is not None:
+            self.t_src_d = self._ptr_table([x.data_ptr() + r * Tr * H * esz for r in range(self.n_local)])
+            self.x = x
+
+    # ------------------------------------------------------------ stages
+    def route(self, x: torch.Tensor, stream: int) -> None:
+        cfg = self.cfg
+        self.counts.zero_()
+        _lib.check(self.L.aurora_route(x.data_ptr(), self.w_gate.data_ptr(), self.bias.data_ptr(), self.T_local,
+                                       cfg.hidden, cfg.experts, cfg.top_k, self.gpu_of_expert.data_ptr(), self.n,
+                                       self.rank_base, cfg.tokens_per_rank, self.topk_idx.data_ptr(),
+                                       self.topk_w.data_ptr(), self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
+                                       self.counts.data_ptr(), stream), "aurora_route")
+
+    def exchange_counts(self) -> None:
+        """Multi-GPU: complete the traffic matrix (each process owns its rows).
+        Loopback: nothing to do, every row was produced here."""
+        if self.n_local != self.n:
+            import torch.distributed as dist
+            dist.all_reduce(self.counts)
+
+    def schedule(self, stream: int) -> None:
+        _lib.check(self.L.aurora_schedule_counts(
+            self.counts.data_ptr(), None if self.bw is None else self.bw.data_ptr(), self.n,
+            self.phase_recv.data_ptr(), self.phase_dur.data_ptr(), self.sched_i.data_ptr(),
+            self.chunks.data_ptr(), self.rchunks.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
+            self.soff.data_ptr(), self.roff.data_ptr(), self.rtot.data_ptr(), self.sched_i[1:].data_ptr(),
+            stream), "aurora_schedule_counts")
+
+    def pack(self, stream: int) -> None:
+        cfg = self.cfg
+        _lib.check(self.L.aurora_pack(self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(), self.counts.data_ptr(),
+                                      self.T_local, cfg.top_k, self.n, self.rank_base, cfg.tokens_per_rank,
+                                      self.send_list.data_ptr(), self.pos.data_ptr(), stream), "aurora_pack")
+
+    def _engine(self, mode: int, stream: int) -> None:
+        cfg = self.cfg
+        src = self.t_src_d if mode == 0 else self.t_src_c
+        dst = self.t_dst_d if mode == 0 else self.t_dst_c
+        ctr = self.t_ctr_d if mode == 0 else self.t_ctr_c
+        _lib.check(self.L.aurora_engine(
+            mode, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            self.rchunks.data_ptr(), self.sched_i.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
+            self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
+            src.data_ptr(), dst.data_ptr(), cfg.hidden * 2, ctr.data_ptr(), self.C, self.P, self.spin_limit,
+            self.engine_status.data_ptr(), stream), "aurora_engine")
+
+    def dispatch(self, stream: int) -> None:
+        self._engine(0, stream)
+
+    def experts(self, stream: int) -> None:
+        cfg = self.cfg
+        m_rows = self.rtot[self.rank_base:]
+        _lib.check(self.L.aurora_expert_ffn(self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+                                            self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_rows.data_ptr(),
+                                            self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
+                   "aurora_expert_ffn")
+
+    def combine(self, stream: int) -> None:
+        self._engine(1, stream)
+
+    def aggregate(self, stream: int) -> None:
+        cfg = self.cfg
+        _lib.check(self.L.aurora_aggregate(self.ret.data_ptr(), self.ret_stride, self.soff.data_ptr(),
+                                           self.pos.data_ptr(), self.slot_dst.data_ptr(), self.topk_w.data_ptr(),
+                                           self.T_local, cfg.top_k, cfg.hidden, self.n, self.rank_base,
+                                           cfg.tokens_per_rank, 0, self.out.data_ptr(), stream), "aurora_aggregate")
+
+    # ------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape."""
+        if x.dtype != torch.bfloat16 or x.shape != (self.T_local, self.cfg.hidden) or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous bf16 [{self.T_local}, {self.cfg.hidden}]")
+        if self.x is None or x.data_ptr() != self.x.data_ptr():
+            self._tables_for(x, getattr(self, "_peers", None))
+        s = _lib.stream_ptr()
+        self.route(x, s)
+        self.exchange_counts()
+        self.schedule(s)
+        self.pack(s)
+        self.dispatch(s)
+        self.experts(s)
+        self.combine(s)
+        self.aggregate(s)
+        return self.out
+
+    __call__ = forward
+
+    def check_status(self) -> None:
+        """Debug path: raise if the device scheduler or engine reported an error."""
+        st, es = int(self.sched_i[1].item()), int(self.engine_status.item())
+        if st != 0:
+            raise RuntimeError(f"device scheduler status {st}")
+        if es != 0:
+            raise RuntimeError(f"engine status {es} (timeout)")
+
+    def schedule_objects(self):
+        """The current batch's schedule as reference-shaped CommSchedule (debug / drop-in parity)."""
+        from .commsched import CommSchedule, Phase
+        nph = int(self.sched_i[0].item())
+        pr = self.phase_recv[:nph].cpu().numpy()
+        pd = self.phase_dur[:nph].cpu().numpy()
+        phases = tuple(Phase(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(d))
+                       for row, d in zip(pr, pd))
+        return CommSchedule(self.n, phases, math.fsum(p.duration for p in phases))
