@@ -1,0 +1,372 @@
+"""Benchmark of the Aurora MoE-layer hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--skew S]
+
+Workload (BASELINE.json configs[1], "C2"): Mixtral-8x7B-shaped MoE layer,
+hidden 4096, FFN 14336, 8 experts top-2, bf16, 16384 tokens, expert-parallel
+over 8 ranks, synthetic Zipf-skewed routing (s = 1.0), random-init weights.
+A step is one layer forward over the 16384 tokens: router + traffic matrix,
+on-device Aurora schedule, token pack, scheduled dispatch, tcgen05 SwiGLU
+experts, reversed-schedule combine, aggregation. With N GPUs each GPU drives
+8/N ranks (N = 1: all eight ranks on one B200, the engine's peer stores land
+in local HBM; N = 8: one rank per GPU over NVSwitch). Total work is fixed:
+"scaling": "strong".
+
+``--impl reference`` times the reference's CPU path: the oracle port
+(oracle/, a restatement of the reference's build_schedule plus the CPU
+restatement of router / SwiGLU experts / aggregation) on a bounded token
+sample of the same workload, with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer all-to-all µs vs send/recv lower bound; layer tokens/s at 1/2/4/8 B200"
+NVLINK_GBS = 900.0  # nominal per direction per GPU (the paper's big-switch B)
+NVLINK_MEASURED_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skew", type=float, default=1.0)
+    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--ffn", type=int, default=14336)
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--topk", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    return {"workload": "C2 Mixtral-8x7B MoE layer (EP over 8 ranks)", "hidden": args.hidden, "ffn": args.ffn,
+            "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.experts,
+            "skew": args.skew, "seed": args.seed, "gpus": args.gpus,
+            "l2": "inputs larger than L2 (x 128 MiB, expert weights 2.6 GiB read every step)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self, device_index=0):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+            rows = [r for r in rows if len(r) >= 9 and r[0].strip() == str(device_index)]
+            if not rows:
+                return out
+            sm = sorted(int(float(r[1])) for r in rows)
+            out["sm_mhz"] = sm[len(sm) // 2]
+            out["sm_max_mhz"] = int(float(rows[0][2]))
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = set()
+            for r in rows:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            out["reasons"] = sorted(reasons)
+            out["samples"] = len(rows)
+        except Exception:
+            pass
+        return out
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline
+def cpu_reference_step(x_bits, w_gate_bits, bias, w1, w3, w2, k, n, gpu_of_expert):
+    """One pass of the oracle port over a token sample: router (C), traffic
+    matrix + permutation, build_schedule restatement (C), fp32 SwiGLU experts
+    (numpy BLAS, all threads), gate-weighted aggregation."""
+    from oracle.oracle import build_schedule_oracle, moe_layer_oracle, pack_oracle, router_oracle
+    import numpy as np
+    import torch
+    _, idx, wts = router_oracle(x_bits, w_gate_bits, bias, k)
+    counts, _, _ = pack_oracle(idx, gpu_of_expert, n)
+    d = counts.astype(float)
+    np.fill_diagonal(d, 0)
+    build_schedule_oracle(d)
+    x = torch.from_numpy(x_bits.astype(np.int32) << 16).view(torch.float32).numpy()
+    return moe_layer_oracle(x, idx, wts, w1, w3, w2)
+
+
+def run_cpu(args, sample_tokens, reps, seed=0):
+    """Times the oracle port on `sample_tokens` tokens of the workload. Returns
+    (tokens/s, schedule ms on the full C2-size traffic matrix, seconds per rep)."""
+    import numpy as np
+    import torch
+    from oracle.oracle import build_schedule_oracle
+    torch.set_num_threads(os.cpu_count() or 1)
+    H, F, E, k, n = args.hidden, args.ffn, args.experts, args.topk, args.experts
+    g = torch.Generator().manual_seed(seed)
+    from paper_2410_17043_b200.layer import zipf_bias
+    w_gate = (torch.randn(E, H, generator=g) / math.sqrt(H)).to(torch.bfloat16)
+    bias = zipf_bias(E, args.skew, g).numpy()
+    gx = torch.Generator().manual_seed(seed + 5)
+    x = torch.randn(sample_tokens, H, generator=gx).to(torch.bfloat16)
+    ge = torch.Generator().manual_seed(seed + 7)
+    # bf16 on the host (2.6 GiB at C2); the oracle widens one expert at a time
+    w1 = [(torch.randn(F, H, generator=ge) / math.sqrt(H)).to(torch.bfloat16) for _ in range(E)]
+    w3 = [(torch.randn(F, H, generator=ge) / math.sqrt(H)).to(torch.bfloat16) for _ in range(E)]
+    w2 = [(torch.randn(H, F, generator=ge) / math.sqrt(F)).to(torch.bfloat16) for _ in range(E)]
+    xb = x.view(torch.int16).numpy().view(np.uint16)
+    wb = w_gate.view(torch.int16).numpy().view(np.uint16)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        cpu_reference_step(xb, wb, bias, w1, w3, w2, k, n, list(range(E)))
+        times.append(time.perf_counter() - t0)
+    med = sorted(times)[len(times) // 2]
+    # the schedule on a full-size (16384-token) traffic matrix: the reference's own hot path
+    rng = np.random.default_rng(seed)
+    pop = 1.0 / (rng.permutation(n) + 1.0) ** args.skew
+    d = np.round(np.outer(np.full(n, args.tokens * k / n), pop / pop.sum()))
+    np.fill_diagonal(d, 0)
+    st = []
+    for _ in range(30):
+        t0 = time.perf_counter()
+        build_schedule_oracle(d)
+        st.append(time.perf_counter() - t0)
+    return sample_tokens / med, 1e3 * sorted(st)[len(st) // 2], med
+
+
+def reference_arm(args):
+    import torch.distributed as dist  # noqa: F401
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sample = 256
+    reps = max(1, args.steps)
+    for _ in range(min(args.warmup, 1)):
+        run_cpu(args, sample, 1)
+    tps, sched_ms, sec = run_cpu(args, sample, reps)
+    cores = os.cpu_count() or 1
+    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": reps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload(args),
+            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"{sample} tokens of the C2 layer per step (router + traffic matrix + "
+                                       f"build_schedule restatement + fp32 SwiGLU experts + aggregation)",
+                             "build_schedule_ms_n8": sched_ms},
+            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2410_17043_b200 import _lib
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n = args.experts
+    if n % world:
+        raise SystemExit(f"{n} ranks do not split over {world} GPUs")
+    n_local = n // world
+    cfg = MoEConfig(hidden=args.hidden, ffn=args.ffn, experts=args.experts, top_k=args.topk, tokens=args.tokens,
+                    ranks=n, skew=args.skew, seed=args.seed)
+    layer = AuroraMoELayer(cfg, rank_base=rank * n_local, n_local=n_local)
+    if world > 1:
+        from paper_2410_17043_b200 import dist as adist
+        adist.connect_peers(layer)
+    dev = layer.dev
+    g = torch.Generator(device=dev).manual_seed(args.seed + 101 + rank)
+    x = torch.randn(layer.T_local, cfg.hidden, device=dev, generator=g).to(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    sp = _lib.stream_ptr(stream)
+
+    stages = ["route", "schedule", "pack", "dispatch", "experts", "combine", "aggregate"]
+
+    def step(ev=None):
+        layer._tables_for(x, getattr(layer, "_peers", None)) if layer.x is None else None
+        if ev is not None:
+            ev[0].record(stream)
+        layer.route(x, sp)
+        layer.exchange_counts()
+        if ev is not None:
+            ev[1].record(stream)
+        layer.schedule(sp)
+        if ev is not None:
+            ev[2].record(stream)
+        layer.pack(sp)
+        if ev is not None:
+            ev[3].record(stream)
+        layer.dispatch(sp)
+        if ev is not None:
+            ev[4].record(stream)
+        layer.experts(sp)
+        if ev is not None:
+            ev[5].record(stream)
+        layer.combine(sp)
+        if ev is not None:
+            ev[6].record(stream)
+        layer.aggregate(sp)
+        if ev is not None:
+            ev[7].record(stream)
+
+    layer._tables_for(x, getattr(layer, "_peers", None))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    layer.check_status()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", f"clocks_r{rank}.csv")
+                          if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_r{rank}.csv")
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with clocks:
+        time.sleep(0.3)
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for s_ in range(args.steps):
+            step(evs[s_])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    layer.check_status()
+    stage_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
+    ms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms.item()) / args.steps
+
+    # ---- end to end through the public API with host buffers (pinned), copies timed
+    xh = x.cpu().pin_memory()
+    outh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True)
+        layer(xd)
+        outh.copy_(layer.out, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        layer(xd)
+        outh.copy_(layer.out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    layer.check_status()
+
+    # ---- roofline of the dominant kernel (the tcgen05 expert GEMMs) and the all-to-all bound
+    counts = layer.counts.cpu().numpy().astype(np.int64)
+    m_local = counts.sum(axis=0)[layer.rank_base:layer.rank_base + n_local]
+    gemm_flops = float(m_local.sum()) * 2 * 3 * cfg.hidden * cfg.ffn
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak_tf = peaks.get("bf16_tflops_sustained")
+    peak_src = "measured (MEASURED_PEAKS.json bf16_tflops_sustained)"
+    if peak_tf is None:
+        peak_tf, peak_src = 1400.0, "fallback (B200_PROFILING.md sustained)"
+    achieved_tf = gemm_flops / (stage_ms["experts"] * 1e-3) / 1e12
+    off = counts.copy()
+    np.fill_diagonal(off, 0)
+    bmax_tokens = int(max(off.sum(axis=1).max(), off.sum(axis=0).max()))
+    row_bytes = cfg.hidden * 2
+    bound_us = bmax_tokens * row_bytes / (NVLINK_GBS * 1e9) * 1e6
+    nph = int(layer.sched_i[0].item())
+    line = {
+        "metric": METRIC, "value": cfg.tokens / (ms_per_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload(args),
+        "stage_ms": stage_ms,
+        "all_to_all": {
+            "dispatch_us": stage_ms["dispatch"] * 1e3, "combine_us": stage_ms["combine"] * 1e3,
+            "schedule_us": stage_ms["schedule"] * 1e3,
+            "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
+            "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
+            "bound_basis": "b_max x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
+            "transport": "NVSwitch peer stores" if world > 1 else
+                         "loopback: all 8 ranks on one GPU, peer stores land in local HBM (not NVLink)",
+        },
+        "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved_tf / peak_tf, "traffic": None, "kernel": "aurora grouped_gemm_kernel "
+                     "(GEMM1 SwiGLU + GEMM2), FLOPs = sum_e m_e * 2 * 3 * H * F", "peak_source": peak_src,
+                     "flops_per_step": gemm_flops},
+        "gpu_launches": 8 * args.steps,
+        "e2e": {"value": cfg.tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(outh.numel() * 2),
+                "ms_per_step": e2e_ms, "path": "AuroraMoELayer.__call__ on pinned host buffers"},
+        "clocks": clocks.summary(local_rank),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tps, sched_ms, sec = run_cpu(args, 256, 3)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
+                                "sample": "256 tokens of the C2 layer per rep, median of 3 (oracle router + "
+                                          "build_schedule restatement + fp32 numpy experts + aggregation)",
+                                "build_schedule_ms_n8": sched_ms}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -174,20 +174,27 @@ def pack_oracle(topk_idx: np.ndarray, gpu_of_expert, n: int):
     return counts, lists, pos
 
 
+def _f32(w):
+    if hasattr(w, "detach"):  # torch tensor (e.g. bf16 weights kept compact on the host)
+        return w.detach().float().numpy()
+    return np.asarray(w, dtype=np.float32)
+
+
 def moe_layer_oracle(x: np.ndarray, topk_idx, topk_w, w1, w3, w2) -> np.ndarray:
     """fp32 SwiGLU MoE: out[t] = sum_s w[t,s] * W2_e (silu(W1_e x) * W3_e x).
-    x [T,H], w1/w3 [E,F,H], w2 [E,H,F] as float32 numpy arrays."""
+    x [T,H] float32; w1/w3 [E][F,H], w2 [E][H,F]: arrays or per-expert
+    sequences (numpy or torch, converted to fp32 one expert at a time)."""
     T, H = x.shape
-    E = w1.shape[0]
+    E = len(w1)
     out = np.zeros((T, H), dtype=np.float32)
     for e in range(E):
         rows, slots = np.nonzero(topk_idx == e)
         if rows.size == 0:
             continue
         xe = x[rows]
-        g = xe @ w1[e].T
-        u = xe @ w3[e].T
+        g = xe @ _f32(w1[e]).T
+        u = xe @ _f32(w3[e]).T
         h = (g / (1.0 + np.exp(-g))) * u
-        y = h @ w2[e].T
+        y = h @ _f32(w2[e]).T
         out[rows] += topk_w[rows, slots][:, None] * y
     return out
