@@ -55,27 +55,34 @@ __device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long lon
   return true;
 }
 
-// copy rows [r0, r1) of one chunk: warp per row, 16-byte vectors, 4 in flight per lane
+// copy rows [r0, r1) of one chunk: warp per row, 16-byte vectors, up to 16
+// loads in flight per lane (one 8 KiB row per warp per batch at hidden 4096,
+// 64 KiB per CTA) so a pair's CTAs keep enough bytes in flight to cover
+// HBM / NVLink latency.
 template <bool GATHER>
 __device__ __forceinline__ void copy_rows(const EngineParams& p, const char* src_base,
                                           const int32_t* gather, int src_row0, char* dst_base,
                                           int dst_row0, int r0, int r1) {
+  constexpr int U = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int vec = p.row_bytes >> 4;
   for (int r = r0 + warp; r < r1; r += WARPS) {
     const long long srow = GATHER ? (long long)gather[src_row0 + r] : (long long)(src_row0 + r);
     const int4* s = reinterpret_cast<const int4*>(src_base + srow * p.row_bytes);
     int4* d = reinterpret_cast<int4*>(dst_base + (long long)(dst_row0 + r) * p.row_bytes);
-    int u = lane;
-    for (; u + 96 < vec; u += 128) {
-      int4 a = ld_nc_v4(s + u), b = ld_nc_v4(s + u + 32), c = ld_nc_v4(s + u + 64),
-           e = ld_nc_v4(s + u + 96);
-      st_na_v4(d + u, a);
-      st_na_v4(d + u + 32, b);
-      st_na_v4(d + u + 64, c);
-      st_na_v4(d + u + 96, e);
+    for (int u0 = 0; u0 < vec; u0 += 32 * U) {
+      int4 v[U];
+#pragma unroll
+      for (int q = 0; q < U; q++) {
+        const int u = u0 + q * 32 + lane;
+        if (u < vec) v[q] = ld_nc_v4(s + u);
+      }
+#pragma unroll
+      for (int q = 0; q < U; q++) {
+        const int u = u0 + q * 32 + lane;
+        if (u < vec) st_na_v4(d + u, v[q]);
+      }
     }
-    for (; u < vec; u += 32) st_na_v4(d + u, ld_nc_v4(s + u));
   }
 }
 

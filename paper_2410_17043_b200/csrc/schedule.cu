@@ -191,6 +191,283 @@ __device__ bool perfect_matching(MatchState& s, int n) {
   return true;
 }
 
+// ============================================================================
+// Register-resident fast path for n <= 16 (the shapes the layer uses).
+// Same algorithm, same visiting order; every piece of matching state lives in
+// packed registers (bit fields selected with compile-time-unrolled code) and
+// every lane keeps its matrix row in registers, so a DFS step is a handful of
+// ALU ops instead of a chain of shared/local memory round trips.
+// ============================================================================
+
+// W 64-bit words holding fields of BITS bits (BITS divides 64)
+template <int BITS, int W>
+struct Pk {
+  uint64_t w[W];
+  static constexpr int PER = 64 / BITS;
+  static constexpr uint64_t FM = (BITS == 64) ? ~0ull : ((1ull << BITS) - 1);
+  __device__ __forceinline__ void fill(uint64_t v) {
+#pragma unroll
+    for (int k = 0; k < W; k++) w[k] = v;
+  }
+  __device__ __forceinline__ uint64_t get(int idx) const {
+    const int wi = idx / PER, sh = (idx % PER) * BITS;
+    uint64_t r = w[0];
+#pragma unroll
+    for (int k = 1; k < W; k++)
+      if (wi == k) r = w[k];
+    return (r >> sh) & FM;
+  }
+  __device__ __forceinline__ void set(int idx, uint64_t v) {
+    const int wi = idx / PER, sh = (idx % PER) * BITS;
+    const uint64_t m = FM << sh, nv = (v & FM) << sh;
+#pragma unroll
+    for (int k = 0; k < W; k++)
+      if (wi == k) w[k] = (w[k] & ~m) | nv;
+  }
+};
+
+template <int NB>
+struct FastMatch {
+  static constexpr int MW = (NB * NB + 63) / 64;  // words of NB-bit masks
+  static constexpr int DW = (NB * 8 + 63) / 64;   // words of byte distances
+  Pk<NB, MW> pref, sup;   // adjacency masks per left vertex
+  Pk<4, 1> ml, mr;        // matches (valid where the free bit is clear)
+  uint32_t freeL, freeR;
+  Pk<8, DW> dist;         // BFS level, 0xFF = _INF
+  Pk<4, 1> us, vs;        // DFS stack: vertex and chosen right vertex per depth
+  Pk<NB, MW> left;        // DFS stack: candidates still to try per depth
+
+  __device__ __forceinline__ void augment_path(int top, int v) {
+    vs.set(top, v);
+    for (int l = top; l >= 0; l--) {
+      const int uu = (int)us.get(l), vv = (int)vs.get(l);
+      ml.set(uu, vv);
+      mr.set(vv, uu);
+    }
+    freeL &= ~(1u << (int)us.get(0));
+    freeR &= ~(1u << v);
+  }
+
+  // hopcroft_karp dfs(root), matching.py:57-65. A vertex on the stack at depth
+  // d has BFS distance d (roots are free, dist 0; children need dist[u] + 1),
+  // so dist[u] + 1 == depth + 1.
+  __device__ __forceinline__ bool hk_dfs(int root) {
+    int top = 0;
+    us.set(0, root);
+    left.set(0, pref.get(root));
+    while (top >= 0) {
+      const uint32_t m = (uint32_t)left.get(top);
+      if (m == 0) {
+        dist.set((int)us.get(top), 0xFF);
+        top--;
+        continue;
+      }
+      const int v = __ffs(m) - 1;
+      left.set(top, m & (m - 1));
+      if ((freeR >> v) & 1) {
+        augment_path(top, v);
+        return true;
+      }
+      const int w = (int)mr.get(v);
+      if ((int)dist.get(w) == top + 1) {
+        vs.set(top, v);
+        top++;
+        us.set(top, w);
+        left.set(top, pref.get(w));
+      }
+    }
+    return false;
+  }
+
+  // perfect_matching's augment(u, seen), matching.py:96-106
+  __device__ __forceinline__ bool kuhn(int root) {
+    uint32_t seen = 0;
+    int top = 0;
+    us.set(0, root);
+    left.set(0, sup.get(root));
+    while (top >= 0) {
+      const uint32_t m = (uint32_t)left.get(top) & ~seen;
+      if (m == 0) {
+        top--;
+        continue;
+      }
+      const int v = __ffs(m) - 1;
+      left.set(top, m & (m - 1));
+      seen |= 1u << v;
+      if ((freeR >> v) & 1) {
+        augment_path(top, v);
+        return true;
+      }
+      vs.set(top, v);
+      top++;
+      us.set(top, (int)mr.get(v));
+      left.set(top, sup.get((int)mr.get(v)));
+    }
+    return false;
+  }
+
+  __device__ bool run(int n) {
+    const uint32_t all = (1u << n) - 1;
+    freeL = all;
+    freeR = all;
+    ml.fill(0);
+    mr.fill(0);
+    for (;;) {  // hopcroft_karp main loop, matching.py:67-72
+      uint32_t frontier = freeL;
+#pragma unroll
+      for (int u = 0; u < NB; u++)
+        if (u < n) dist.set(u, ((freeL >> u) & 1) ? 0 : 0xFF);
+      bool found = false;
+      int level = 0;
+      while (frontier) {
+        uint32_t reach = 0;
+        for (uint32_t f = frontier; f; f &= f - 1) reach |= (uint32_t)pref.get(__ffs(f) - 1);
+        if (reach & freeR) found = true;
+        uint32_t next = 0;
+        for (uint32_t r = reach & ~freeR; r; r &= r - 1) {
+          const int w = (int)mr.get(__ffs(r) - 1);
+          if (dist.get(w) == 0xFF) {
+            dist.set(w, level + 1);
+            next |= 1u << w;
+          }
+        }
+        frontier = next;
+        level++;
+      }
+      if (!found) break;
+      for (int u = 0; u < n; u++)
+        if ((freeL >> u) & 1) hk_dfs(u);
+    }
+    for (int u = 0; u < n; u++)
+      if (((freeL >> u) & 1) && !kuhn(u)) return false;
+    return true;
+  }
+};
+
+// min over lanes of a non-negative double (+inf allowed): IEEE order of
+// non-negative doubles is the order of their bit patterns
+__device__ __forceinline__ double warp_min_nonneg(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | mlo));
+}
+
+template <int NB>
+__device__ __forceinline__ double row_pick(const double (&a)[NB], int j) {
+  double r = a[0];
+#pragma unroll
+  for (int q = 1; q < NB; q++)
+    if (q == j) r = a[q];
+  return r;
+}
+template <int NB>
+__device__ __forceinline__ void row_put(double (&a)[NB], int j, double v) {
+#pragma unroll
+  for (int q = 0; q < NB; q++)
+    if (q == j) a[q] = v;
+}
+
+// decompose (commsched.py:406-435) + strip/_coalesce (463-479), n <= NB <= 16.
+template <int NB>
+__device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_MAXN + 1],
+                               const double (*real_in)[AUR_MAXN + 1],
+                               const double (*t_in)[AUR_MAXN + 1], uint32_t* pref_s,
+                               uint32_t* sup_s, int* perm_s, double eps, int& nr_out,
+                               int& np_out, int& status) {
+  const int lane = threadIdx.x, n = p.n;
+  const bool on = lane < n;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const int R_MAX = n * n - 2 * n + 2, P_MAX = 2 * n * n - 3 * n + 2;
+  double rem[NB], real[NB], lr[NB];
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    rem[j] = (on && j < n) ? rem_in[lane][j] : 0.0;
+    real[j] = (on && j < n) ? real_in[lane][j] : 0.0;
+    lr[j] = (on && j < n) ? t_in[lane][j] : 0.0;
+  }
+  int nr = 0, np_ = 0, last_recv = -2;
+  double cur_dur = 0.0;
+  FastMatch<NB> fm;
+  while (true) {
+    bool anyrow = false;
+    uint32_t sup = 0, pref = 0;
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+      double r = rem[j];
+      if (r <= eps) r = 0.0;  // remaining[remaining <= eps] = 0
+      rem[j] = r;
+      if (r < real[j]) real[j] = r;  // np.minimum(real, remaining)
+      anyrow |= r != 0.0;
+      if (r > 0) sup |= 1u << j;
+      if (real[j] > eps) pref |= 1u << j;
+    }
+    if (!__any_sync(0xffffffffu, on && anyrow)) break;
+    if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
+    if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < NB; u++) {
+        fm.pref.set(u, u < n ? pref_s[u] : 0);
+        fm.sup.set(u, u < n ? sup_s[u] : 0);
+      }
+      const bool ok = fm.run(n);
+      uint32_t mlw = (uint32_t)(fm.ml.w[0] & 0xffffffffull);
+      perm_s[0] = ok ? 1 : 0;
+#pragma unroll
+      for (int u = 0; u < NB; u++) perm_s[1 + u] = (int)fm.ml.get(u);
+      (void)mlw;
+    }
+    __syncwarp();
+    if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
+    const int pj = on ? perm_s[1 + lane] : 0;
+    const double dur = warp_min_nonneg(on ? row_pick<NB>(rem, pj) : INF);
+    if (on) {
+      row_put<NB>(rem, pj, row_pick<NB>(rem, pj) - dur);
+      const double re = row_pick<NB>(real, pj) - dur;
+      row_put<NB>(real, pj, re < 0.0 ? 0.0 : re);
+      if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
+    }
+    if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
+    nr++;
+    double left = dur;
+    while (left > eps) {
+      const double lv = on ? row_pick<NB>(lr, pj) : 0.0;
+      const bool act = on && lv > eps;
+      const unsigned amask = __ballot_sync(0xffffffffu, act);
+      double step;
+      if (amask == 0) {
+        step = left;
+      } else {
+        const double m = warp_min_nonneg(act ? lv : INF);
+        step = m < left ? m : left;
+      }
+      const int recv = act ? pj : -1;
+      if (step > eps) {
+        const bool same = np_ > 0 && __all_sync(0xffffffffu, !on || recv == last_recv);
+        if (same) {
+          cur_dur = cur_dur + step;
+        } else {
+          if (np_ >= P_MAX) { status = AURORA_EOVERFLOW; break; }
+          np_++;
+          cur_dur = step;
+          last_recv = recv;
+          if (on) p.phase_recv[(np_ - 1) * n + lane] = recv;
+        }
+        if (lane == 0) p.phase_dur[np_ - 1] = cur_dur;
+      }
+      if (amask == 0) break;
+      if (act) row_put<NB>(lr, pj, lv - step);
+      left -= step;
+    }
+    if (status != AURORA_OK) break;
+  }
+  nr_out = nr;
+  np_out = np_;
+}
+
 __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
   __shared__ double t_s[AUR_MAXN][AUR_MAXN + 1];     // time matrix; later "remaining" of strip
   __shared__ double rem_s[AUR_MAXN][AUR_MAXN + 1];   // decompose remaining (d')
@@ -284,7 +561,14 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     int last_recv = -2;  // receiver of this lane in the last kept phase
     double cur_dur = 0.0;
     long long cyc[5] = {0, 0, 0, 0, clock64()};
-    while (status == AURORA_OK) {
+    if (status == AURORA_OK && n <= 16) {
+      if (n <= 8)
+        decompose_fast<8>(p, rem_s, real_s, t_s, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
+      else
+        decompose_fast<16>(p, rem_s, real_s, t_s, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
+      if (p.prof && lane == 0) p.prof[4] = clock64() - cyc[4];
+    }
+    while (status == AURORA_OK && n > 16) {
       long long c0 = clock64();
       bool anyrow = false;
       uint32_t sup = 0, pref = 0;

@@ -98,7 +98,8 @@ class AuroraMoELayer:
             raise ValueError("plan must cover every expert")
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
-        self.C = ctas_per_rank or max(1, min(32, (sms // self.n_local)))
+        # copy CTAs per rank: two 256-thread CTAs fit per SM, all must be co-resident
+        self.C = ctas_per_rank or max(1, min(32, (2 * sms) // self.n_local))
         self.spin_limit = spin_limit
         H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
         Tr = cfg.tokens_per_rank
