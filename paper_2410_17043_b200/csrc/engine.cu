@@ -94,7 +94,7 @@ __device__ __forceinline__ void signal(int32_t* ctr) {
   }
 }
 
-__global__ void __launch_bounds__(THREADS) engine_kernel(EngineParams p) {
+__global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
   const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
   const int n = p.n;
@@ -216,10 +216,16 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
       !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
       (mode == 0 && !send_list))
     return AURORA_EINVAL;
-  int dev = 0, sms = 0;
+  int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (n_local * ctas_per_rank > 2 * sms) return AURORA_EINVAL;  // must be co-resident
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0) != cudaSuccess ||
+      occ < 1)
+    return AURORA_ECUDA;
+  // every copy CTA spins on flags written by others: all of them must be
+  // co-resident. Clamp deterministically (every process computes the same C).
+  ctas_per_rank = min(ctas_per_rank, (occ * sms) / n_local);
+  if (ctas_per_rank < 1) return AURORA_EINVAL;
   EngineParams p;
   p.mode = mode;
   p.n = n;

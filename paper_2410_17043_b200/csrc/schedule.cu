@@ -306,7 +306,7 @@ struct FastMatch {
     return false;
   }
 
-  __device__ bool run(int n) {
+  __device__ __forceinline__ bool run(int n) {
     const uint32_t all = (1u << n) - 1;
     freeL = all;
     freeR = all;
@@ -390,7 +390,9 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
   int nr = 0, np_ = 0, last_recv = -2;
   double cur_dur = 0.0;
   FastMatch<NB> fm;
+  long long cy[4] = {0, 0, 0, 0}, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
   while (true) {
+    t0 = clock64();
     bool anyrow = false;
     uint32_t sup = 0, pref = 0;
 #pragma unroll
@@ -407,6 +409,7 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
     if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
     if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
     __syncwarp();
+    t1 = clock64();
     if (lane == 0) {
 #pragma unroll
       for (int u = 0; u < NB; u++) {
@@ -422,6 +425,7 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
     }
     __syncwarp();
     if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
+    t2 = clock64();
     const int pj = on ? perm_s[1 + lane] : 0;
     const double dur = warp_min_nonneg(on ? row_pick<NB>(rem, pj) : INF);
     if (on) {
@@ -432,6 +436,7 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
     }
     if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
     nr++;
+    t3 = clock64();
     double left = dur;
     while (left > eps) {
       const double lv = on ? row_pick<NB>(lr, pj) : 0.0;
@@ -463,7 +468,14 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
       left -= step;
     }
     if (status != AURORA_OK) break;
+    const long long t4 = clock64();
+    cy[0] += t1 - t0;
+    cy[1] += t2 - t1;
+    cy[2] += t3 - t2;
+    cy[3] += t4 - t3;
   }
+  if (p.prof && lane == 0)
+    for (int q = 0; q < 4; q++) p.prof[q] = cy[q];
   nr_out = nr;
   np_out = np_;
 }
