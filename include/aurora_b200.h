@@ -113,9 +113,13 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
 /* ------------------------------------------------------------ K4 / K6 ----
  * aurora_engine: executes the schedule as in-kernel stores into peer
  * memory, self-timed per chunk (a chunk i->j starts once every earlier chunk
- * into j has landed), replacing a single NCCL alltoallv. mode 0 = dispatch
- * (CommSchedule phases, commsched.py:112-132), mode 1 = combine (the
- * reversed schedule, commsched.py:310-319: same phases, directions flipped).
+ * into j has landed), replacing a single NCCL alltoallv. mode bit 0: 0 =
+ * dispatch (CommSchedule phases, commsched.py:112-132), 1 = combine (the
+ * reversed schedule, commsched.py:310-319: same phases, directions flipped);
+ * mode bit 1: peers live on other GPUs (system-scope flag ordering) -- clear
+ * when every rank of the call shares this GPU (gpu scope suffices).
+ * Consecutive phases of one pair are one chunk (aurora_schedule_counts merges
+ * them), so a handshake only happens where the schedule changes partners.
  *   tables from aurora_schedule_counts; counts[n][n] from aurora_route;
  *   n_local ranks [rank_base, rank_base+n_local) are served by this call
  *   dispatch: src rows = x_local[i_local] gathered through send_list,

@@ -47,6 +47,9 @@ __device__ __forceinline__ void st_release_sys(int* p, int v) {
 __device__ __forceinline__ void red_release_sys_add(int* p, int v) {
   asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // 16-byte global accesses that bypass L1 allocation (streaming copies)
 __device__ __forceinline__ int4 ld_nc_v4(const int4* p) {

@@ -45,12 +45,13 @@ struct EngineParams {
   int32_t* status;
 };
 
-// wait until *ctr >= target (thread 0), bounded
-__device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long long limit) {
+// wait until *ctr >= target (thread 0), bounded. `sys`: the counter is written
+// by other GPUs (system scope); otherwise every rank lives on this GPU.
+__device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long long limit, bool sys) {
   long long spins = 0;
-  while (ld_acquire_sys(ctr) < target) {
+  while ((sys ? ld_acquire_sys(ctr) : ld_acquire_gpu(ctr)) < target) {
     if (limit && ++spins > limit) return false;
-    __nanosleep(32);
+    if (spins > 64) __nanosleep(20);
   }
   return true;
 }
@@ -86,11 +87,16 @@ __device__ __forceinline__ void copy_rows(const EngineParams& p, const char* src
   }
 }
 
-__device__ __forceinline__ void signal(int32_t* ctr) {
-  __syncthreads();  // every thread's stores of this slice are done
+__device__ __forceinline__ void signal(int32_t* ctr, bool sys) {
+  __syncthreads();  // every thread's stores of this slice are issued
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    red_release_sys_add(ctr, 1);
+    if (sys) {
+      __threadfence_system();  // cumulative: orders the CTA's stores (observed via bar.sync)
+      red_release_sys_add(ctr, 1);
+    } else {
+      __threadfence();
+      red_release_gpu_add(ctr, 1);
+    }
   }
 }
 
@@ -99,7 +105,8 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
   const int n = p.n;
   const int nph = min(*p.n_phases, p.max_phases);
-  const bool dispatch = p.mode == 0;
+  const bool dispatch = (p.mode & 1) == 0;
+  const bool sys = (p.mode & 2) != 0;  // peers on other GPUs: system-scope ordering
   const char* src = p.src_bufs[r_local];
   const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
   __shared__ int abort_s;
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     if (peer < 0) continue;
     const int first = ch.y, ntok = ch.z, seq = ch.w;
     if (threadIdx.x == 0) {
-      if (!wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit)) {
+      if (!wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit, sys)) {
         abort_s = 1;
         atomicExch(p.status, AURORA_ETIMEOUT);
       }
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
       copy_rows<false>(p, src, nullptr, p.roff[peer * n + g] + first, p.dst_bufs[peer],
                        p.soff[peer * n + g] + first, r0, r1);
     }
-    signal(p.ctrs[peer]);
+    signal(p.ctrs[peer], sys);
   }
 
   // local (diagonal) rows never cross the network (TrafficMatrix zeroes them, core.py:95)
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
   if (c == 0 && threadIdx.x == 0) {
     const int expect = (dispatch ? p.n_in[g] : p.n_out[g]) * p.C;
-    if (!wait_ge(p.ctrs[g], expect, p.spin_limit)) {
+    if (!wait_ge(p.ctrs[g], expect, p.spin_limit, sys)) {
       atomicExch(p.status, AURORA_ETIMEOUT);
     } else {
       *(volatile int32_t*)p.ctrs[g] = 0;
@@ -211,10 +218,10 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst_bufs, int row_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
-  if ((mode != 0 && mode != 1) || n < 1 || n > AUR_MAXN || n_local < 1 || rank_base < 0 ||
+  if (mode < 0 || mode > 3 || n < 1 || n > AUR_MAXN || n_local < 1 || rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
-      (mode == 0 && !send_list))
+      ((mode & 1) == 0 && !send_list))
     return AURORA_EINVAL;
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);

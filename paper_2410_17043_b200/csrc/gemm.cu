@@ -121,13 +121,20 @@ struct TileIter {
   int mt[MAX_GROUPS];  // m-tiles per group
 };
 
-__device__ __forceinline__ void tile_coords(const TileIter& it, int G, int t, int& g, int& mt,
-                                            int& nt) {
+// Tile t -> (group, m-tile, n-tile). Inside a group, tiles walk blocks of
+// `gm` m-tiles: within a block the m-tile varies fastest (CTAs running
+// together share one weight tile), and the block's A rows (gm x 128 x K)
+// stay L2-resident while every n-tile passes over them.
+__device__ __forceinline__ void tile_coords(const TileIter& it, int G, int gm, int t, int& g,
+                                            int& mt, int& nt) {
   g = 0;
   while (g + 1 < G && it.prefix[g + 1] <= t) g++;
   const int local = t - it.prefix[g];
-  nt = local / it.mt[g];
-  mt = local % it.mt[g];
+  const int per_block = gm * it.n_tiles_n;
+  const int sb = local / per_block, rem = local - sb * per_block;
+  const int rows = min(gm, it.mt[g] - sb * gm);
+  mt = sb * gm + rem % rows;
+  nt = rem / rows;
 }
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
@@ -136,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ c,
                         const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
-                        int epilogue) {
+                        int epilogue, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < it.total; t += gridDim.x) {
         int g, mt, nt;
-        tile_coords(it, G, t, g, mt, nt);
+        tile_coords(it, G, group_m, t, g, mt, nt);
         const int a_row = (int)(g * cap) + mt * BM;
         const int b_row = g * N + nt * BN;
         for (int kb = 0; kb < k_blocks; kb++) {
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int local = 0;
     for (int t = blockIdx.x; t < it.total; t += gridDim.x, local++) {
       int g, mt, nt;
-      tile_coords(it, G, t, g, mt, nt);
+      tile_coords(it, G, group_m, t, g, mt, nt);
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc_fence_after();
@@ -341,13 +348,15 @@ int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_rows,
       return AURORA_ECUDA;
     attr_set = true;
   }
+  // m-tile block: ~32 MiB of A rows, re-read from L2 by every n-tile
+  const int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BM * K * 2)));
   if (num_sms <= 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   grouped_gemm_kernel<<<num_sms, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_rows, G, (long long)cap, N, K, epilogue);
+      ma, mb, (__nv_bfloat16*)c, m_rows, G, (long long)cap, N, K, epilogue, group_m);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       }
       cyc[3] += clock64() - c3;
     }
-    if (p.prof && lane == 0) {
+    if (p.prof && lane == 0 && n > 16) {
       for (int q = 0; q < 4; q++) p.prof[q] = cyc[q];
       p.prof[4] = clock64() - cyc[4];
     }
@@ -691,7 +691,14 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       }
       rcnt_s[lane] = 0;
     }
-    int sseq = 0;  // this sender's chunk count so far
+    // A pair that stays matched across consecutive phases of BOTH its sender
+    // and its receiver (typical: a raw phase split because another pair ran
+    // out) is one continuous transfer; it becomes one chunk, so the engine
+    // never pays a handshake inside it. Send and receive orders are unchanged.
+    int sseq = 0;                    // this sender's chunk count so far
+    int my_last_j = -1, my_last_k = -1;
+    __shared__ int lastfrom_s[AUR_MAXN];
+    if (on) lastfrom_s[lane] = -1;
     __syncwarp();
     for (int k = 0; k < np_; k++) {
       if (on) p.rchunks[k * n + lane] = make_int4(-1, 0, 0, 0);
@@ -699,6 +706,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       const double dk = p.phase_dur[k];
       const int j = on ? p.phase_recv[k * n + lane] : -1;
       int4 c = make_int4(-1, 0, 0, 0);
+      bool merged = false;
       if (j >= 0) {
         double cum = rem_s[lane][j] + dk;
         rem_s[lane][j] = cum;
@@ -710,13 +718,24 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
         int start = tok[lane * AUR_MAXN + j];
         if (tk < start) tk = start;
         tok[lane * AUR_MAXN + j] = tk;
-        c = make_int4(j, start, tk - start, rcnt_s[j]);
-        lastc[lane * AUR_MAXN + j] = k;
-        p.rchunks[k * n + j] = make_int4(lane, start, tk - start, sseq);
-        sseq++;
+        if (my_last_j == j && lastfrom_s[j] == lane) {
+          merged = true;
+          p.chunks[my_last_k * n + lane].z += tk - start;
+          p.rchunks[my_last_k * n + j].z += tk - start;
+        } else {
+          c = make_int4(j, start, tk - start, rcnt_s[j]);
+          p.rchunks[k * n + j] = make_int4(lane, start, tk - start, sseq);
+          sseq++;
+          my_last_j = j;
+          my_last_k = k;
+        }
+        lastc[lane * AUR_MAXN + j] = my_last_k;
       }
       __syncwarp();
-      if (j >= 0) rcnt_s[j] += 1;  // receivers are distinct within a phase
+      if (j >= 0) {  // receivers are distinct within a phase
+        if (!merged) rcnt_s[j] += 1;
+        lastfrom_s[j] = lane;
+      }
       if (on) p.chunks[k * n + lane] = c;
       __syncwarp();
     }

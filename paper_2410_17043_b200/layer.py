@@ -243,8 +243,9 @@ class AuroraMoELayer:
         src = self.t_src_d if mode == 0 else self.t_src_c
         dst = self.t_dst_d if mode == 0 else self.t_dst_c
         ctr = self.t_ctr_d if mode == 0 else self.t_ctr_c
+        sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
         _lib.check(self.L.aurora_engine(
-            mode, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            mode | sys_scope, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.sched_i.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2, ctr.data_ptr(), self.C, self.P, self.spin_limit,
