@@ -199,42 +199,46 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 // ALU ops instead of a chain of shared/local memory round trips.
 // ============================================================================
 
-// W 64-bit words holding fields of BITS bits (BITS divides 64)
+// W 32-bit words holding fields of BITS bits (BITS divides 32). 32-bit words
+// keep every get/set to a shift, a mask and (W > 1) a short select chain.
 template <int BITS, int W>
 struct Pk {
-  uint64_t w[W];
-  static constexpr int PER = 64 / BITS;
-  static constexpr uint64_t FM = (BITS == 64) ? ~0ull : ((1ull << BITS) - 1);
-  __device__ __forceinline__ void fill(uint64_t v) {
+  uint32_t w[W];
+  static constexpr unsigned PER = 32 / BITS;
+  static constexpr uint32_t FM = (BITS == 32) ? ~0u : ((1u << BITS) - 1);
+  __device__ __forceinline__ void fill(uint32_t v) {
 #pragma unroll
     for (int k = 0; k < W; k++) w[k] = v;
   }
-  __device__ __forceinline__ uint64_t get(int idx) const {
-    const int wi = idx / PER, sh = (idx % PER) * BITS;
-    uint64_t r = w[0];
+  __device__ __forceinline__ uint32_t get(unsigned idx) const {
+    const unsigned wi = idx / PER, sh = (idx % PER) * BITS;
+    uint32_t r = w[0];
 #pragma unroll
-    for (int k = 1; k < W; k++)
+    for (unsigned k = 1; k < W; k++)
       if (wi == k) r = w[k];
     return (r >> sh) & FM;
   }
-  __device__ __forceinline__ void set(int idx, uint64_t v) {
-    const int wi = idx / PER, sh = (idx % PER) * BITS;
-    const uint64_t m = FM << sh, nv = (v & FM) << sh;
+  __device__ __forceinline__ void set(unsigned idx, uint32_t v) {
+    const unsigned wi = idx / PER, sh = (idx % PER) * BITS;
+    const uint32_t m = FM << sh, nv = (v & FM) << sh;
 #pragma unroll
-    for (int k = 0; k < W; k++)
+    for (unsigned k = 0; k < W; k++)
       if (wi == k) w[k] = (w[k] & ~m) | nv;
   }
 };
 
 template <int NB>
 struct FastMatch {
-  static constexpr int MW = (NB * NB + 63) / 64;  // words of NB-bit masks
-  static constexpr int DW = (NB * 8 + 63) / 64;   // words of byte distances
+  static constexpr int MW = NB * NB / 32;        // words of NB-bit masks
+  static constexpr int NW = NB * 4 / 32;         // words of nibble arrays
+  static constexpr int DB = NB <= 8 ? 4 : 8;     // bits per BFS distance
+  static constexpr int DW = NB * DB / 32;
+  static constexpr uint32_t DINF = (1u << DB) - 1;  // _INF
   Pk<NB, MW> pref, sup;   // adjacency masks per left vertex
-  Pk<4, 1> ml, mr;        // matches (valid where the free bit is clear)
+  Pk<4, NW> ml, mr;       // matches (valid where the free bit is clear)
   uint32_t freeL, freeR;
-  Pk<8, DW> dist;         // BFS level, 0xFF = _INF
-  Pk<4, 1> us, vs;        // DFS stack: vertex and chosen right vertex per depth
+  Pk<DB, DW> dist;        // BFS level, DINF = _INF
+  Pk<4, NW> us, vs;       // DFS stack: vertex and chosen right vertex per depth
   Pk<NB, MW> left;        // DFS stack: candidates still to try per depth
 
   __device__ __forceinline__ void augment_path(int top, int v) {
@@ -258,7 +262,7 @@ struct FastMatch {
     while (top >= 0) {
       const uint32_t m = (uint32_t)left.get(top);
       if (m == 0) {
-        dist.set((int)us.get(top), 0xFF);
+        dist.set(us.get(top), DINF);
         top--;
         continue;
       }
@@ -316,7 +320,7 @@ struct FastMatch {
       uint32_t frontier = freeL;
 #pragma unroll
       for (int u = 0; u < NB; u++)
-        if (u < n) dist.set(u, ((freeL >> u) & 1) ? 0 : 0xFF);
+        if (u < n) dist.set(u, ((freeL >> u) & 1) ? 0 : DINF);
       bool found = false;
       int level = 0;
       while (frontier) {
@@ -326,7 +330,7 @@ struct FastMatch {
         uint32_t next = 0;
         for (uint32_t r = reach & ~freeR; r; r &= r - 1) {
           const int w = (int)mr.get(__ffs(r) - 1);
-          if (dist.get(w) == 0xFF) {
+          if (dist.get(w) == DINF) {
             dist.set(w, level + 1);
             next |= 1u << w;
           }
@@ -417,11 +421,9 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
         fm.sup.set(u, u < n ? sup_s[u] : 0);
       }
       const bool ok = fm.run(n);
-      uint32_t mlw = (uint32_t)(fm.ml.w[0] & 0xffffffffull);
       perm_s[0] = ok ? 1 : 0;
 #pragma unroll
       for (int u = 0; u < NB; u++) perm_s[1 + u] = (int)fm.ml.get(u);
-      (void)mlw;
     }
     __syncwarp();
     if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
