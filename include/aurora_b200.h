@@ -168,6 +168,16 @@ int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* 
 int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_rows, int G,
                         int64_t cap, int N, int K, int epilogue, int num_sms, void* stream);
 
+/* ------------------------------------------------------- peer memory ----
+ * CUDA IPC for the multi-GPU layer (one process per GPU). aurora_ipc_get
+ * returns the handle of the allocation containing `ptr` (handle buffer of
+ * aurora_ipc_handle_bytes() bytes) and ptr's offset inside it; a peer process
+ * maps it with aurora_ipc_open(handle, offset, &peer_ptr). */
+int aurora_ipc_handle_bytes(void);
+int aurora_ipc_get(const void* ptr, void* handle, int64_t* offset);
+int aurora_ipc_open(const void* handle, int64_t offset, void** out);
+int aurora_ipc_close(void* base);
+
 /* Diagnostics: one K2 run with per-section cycle counters
  * prof[5] = {snap+masks, matching, update, strip, decompose total};
  * scratch >= (n^2-2n+2)*n + 3 + (2n^2-3n+2)*n int32, dscratch >= 3n^2 doubles. */
