@@ -199,154 +199,7 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 // ALU ops instead of a chain of shared/local memory round trips.
 // ============================================================================
 
-// W 32-bit words holding fields of BITS bits (BITS divides 32). 32-bit words
-// keep every get/set to a shift, a mask and (W > 1) a short select chain.
-template <int BITS, int W>
-struct Pk {
-  uint32_t w[W];
-  static constexpr unsigned PER = 32 / BITS;
-  static constexpr uint32_t FM = (BITS == 32) ? ~0u : ((1u << BITS) - 1);
-  __device__ __forceinline__ void fill(uint32_t v) {
-#pragma unroll
-    for (int k = 0; k < W; k++) w[k] = v;
-  }
-  __device__ __forceinline__ uint32_t get(unsigned idx) const {
-    const unsigned wi = idx / PER, sh = (idx % PER) * BITS;
-    uint32_t r = w[0];
-#pragma unroll
-    for (unsigned k = 1; k < W; k++)
-      if (wi == k) r = w[k];
-    return (r >> sh) & FM;
-  }
-  __device__ __forceinline__ void set(unsigned idx, uint32_t v) {
-    const unsigned wi = idx / PER, sh = (idx % PER) * BITS;
-    const uint32_t m = FM << sh, nv = (v & FM) << sh;
-#pragma unroll
-    for (unsigned k = 0; k < W; k++)
-      if (wi == k) w[k] = (w[k] & ~m) | nv;
-  }
-};
-
-template <int NB>
-struct FastMatch {
-  static constexpr int MW = NB * NB / 32;        // words of NB-bit masks
-  static constexpr int NW = NB * 4 / 32;         // words of nibble arrays
-  static constexpr int DB = NB <= 8 ? 4 : 8;     // bits per BFS distance
-  static constexpr int DW = NB * DB / 32;
-  static constexpr uint32_t DINF = (1u << DB) - 1;  // _INF
-  Pk<NB, MW> pref, sup;   // adjacency masks per left vertex
-  Pk<4, NW> ml, mr;       // matches (valid where the free bit is clear)
-  uint32_t freeL, freeR;
-  Pk<DB, DW> dist;        // BFS level, DINF = _INF
-  Pk<4, NW> us, vs;       // DFS stack: vertex and chosen right vertex per depth
-  Pk<NB, MW> left;        // DFS stack: candidates still to try per depth
-
-  __device__ __forceinline__ void augment_path(int top, int v) {
-    vs.set(top, v);
-    for (int l = top; l >= 0; l--) {
-      const int uu = (int)us.get(l), vv = (int)vs.get(l);
-      ml.set(uu, vv);
-      mr.set(vv, uu);
-    }
-    freeL &= ~(1u << (int)us.get(0));
-    freeR &= ~(1u << v);
-  }
-
-  // hopcroft_karp dfs(root), matching.py:57-65. A vertex on the stack at depth
-  // d has BFS distance d (roots are free, dist 0; children need dist[u] + 1),
-  // so dist[u] + 1 == depth + 1.
-  __device__ __forceinline__ bool hk_dfs(int root) {
-    int top = 0;
-    us.set(0, root);
-    left.set(0, pref.get(root));
-    while (top >= 0) {
-      const uint32_t m = (uint32_t)left.get(top);
-      if (m == 0) {
-        dist.set(us.get(top), DINF);
-        top--;
-        continue;
-      }
-      const int v = __ffs(m) - 1;
-      left.set(top, m & (m - 1));
-      if ((freeR >> v) & 1) {
-        augment_path(top, v);
-        return true;
-      }
-      const int w = (int)mr.get(v);
-      if ((int)dist.get(w) == top + 1) {
-        vs.set(top, v);
-        top++;
-        us.set(top, w);
-        left.set(top, pref.get(w));
-      }
-    }
-    return false;
-  }
-
-  // perfect_matching's augment(u, seen), matching.py:96-106
-  __device__ __forceinline__ bool kuhn(int root) {
-    uint32_t seen = 0;
-    int top = 0;
-    us.set(0, root);
-    left.set(0, sup.get(root));
-    while (top >= 0) {
-      const uint32_t m = (uint32_t)left.get(top) & ~seen;
-      if (m == 0) {
-        top--;
-        continue;
-      }
-      const int v = __ffs(m) - 1;
-      left.set(top, m & (m - 1));
-      seen |= 1u << v;
-      if ((freeR >> v) & 1) {
-        augment_path(top, v);
-        return true;
-      }
-      vs.set(top, v);
-      top++;
-      us.set(top, (int)mr.get(v));
-      left.set(top, sup.get((int)mr.get(v)));
-    }
-    return false;
-  }
-
-  __device__ __forceinline__ bool run(int n) {
-    const uint32_t all = (1u << n) - 1;
-    freeL = all;
-    freeR = all;
-    ml.fill(0);
-    mr.fill(0);
-    for (;;) {  // hopcroft_karp main loop, matching.py:67-72
-      uint32_t frontier = freeL;
-#pragma unroll
-      for (int u = 0; u < NB; u++)
-        if (u < n) dist.set(u, ((freeL >> u) & 1) ? 0 : DINF);
-      bool found = false;
-      int level = 0;
-      while (frontier) {
-        uint32_t reach = 0;
-        for (uint32_t f = frontier; f; f &= f - 1) reach |= (uint32_t)pref.get(__ffs(f) - 1);
-        if (reach & freeR) found = true;
-        uint32_t next = 0;
-        for (uint32_t r = reach & ~freeR; r; r &= r - 1) {
-          const int w = (int)mr.get(__ffs(r) - 1);
-          if (dist.get(w) == DINF) {
-            dist.set(w, level + 1);
-            next |= 1u << w;
-          }
-        }
-        frontier = next;
-        level++;
-      }
-      if (!found) break;
-      for (int u = 0; u < n; u++)
-        if ((freeL >> u) & 1) hk_dfs(u);
-    }
-    for (int u = 0; u < n; u++)
-      if (((freeL >> u) & 1) && !kuhn(u)) return false;
-    return true;
-  }
-};
+#include "fastmatch.cuh"
 
 // min over lanes of a non-negative double (+inf allowed): IEEE order of
 // non-negative doubles is the order of their bit patterns

@@ -1,0 +1,52 @@
+// Host check of the K2 fast-path matcher (paper_2410_17043_b200/csrc/fastmatch.cuh)
+// against the oracle's perfect_matching restatement, on random bitmask graphs.
+#include <cstdint>
+#include <cstdio>
+#include <random>
+
+#include "../../paper_2410_17043_b200/csrc/fastmatch.cuh"
+
+extern "C" int oracle_perfect_matching_masks(int n, const uint32_t* sup, const uint32_t* pref, int* perm);
+
+template <int NB>
+static int check(std::mt19937& rng, int iters) {
+  int bad = 0;
+  for (int it = 0; it < iters; it++) {
+    const int n = 1 + (int)(rng() % NB);
+    uint32_t sup[32], pref[32];
+    const double ps = 0.2 + 0.8 * (rng() % 1000) / 1000.0, pp = (rng() % 1000) / 1000.0;
+    for (int i = 0; i < n; i++) {
+      sup[i] = pref[i] = 0;
+      for (int j = 0; j < n; j++) {
+        if ((rng() % 1000) / 1000.0 < ps) {
+          sup[i] |= 1u << j;
+          if ((rng() % 1000) / 1000.0 < pp) pref[i] |= 1u << j;
+        }
+      }
+    }
+    if (it % 3 == 0)  // balanced-matrix-like supports always have a perfect matching
+      for (int i = 0; i < n; i++) sup[i] |= 1u << ((i + it) % n);
+    int ref[32];
+    const int ok_ref = oracle_perfect_matching_masks(n, sup, pref, ref);
+    FastMatch<NB> fm;
+    for (int u = 0; u < NB; u++) {
+      fm.pref.set(u, u < n ? pref[u] : 0);
+      fm.sup.set(u, u < n ? sup[u] : 0);
+    }
+    const bool ok = fm.run(n);
+    bool same = ok == (bool)ok_ref;
+    if (same && ok)
+      for (int u = 0; u < n; u++) same &= (int)fm.ml.get(u) == ref[u];
+    if (!same && bad++ < 5) {
+      std::printf("mismatch NB=%d n=%d ok=%d/%d\n", NB, n, (int)ok, ok_ref);
+    }
+  }
+  return bad;
+}
+
+int main() {
+  std::mt19937 rng(12345);
+  int bad = check<8>(rng, 200000) + check<16>(rng, 100000);
+  std::printf("fastmatch mismatches: %d\n", bad);
+  return bad != 0;
+}
