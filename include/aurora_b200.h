@@ -70,16 +70,14 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  *                     count, index in the sender's send order} (the combine
  *                     runs CommSchedule.reversed(), commsched.py:310-319)
  *   n_in[n], n_out[n] chunks arriving at / leaving each rank
- *   soff[n][n]        start of list(i,j) inside sender i's send list (row prefix)
- *   roff[n][n]        start of list(i,j) inside receiver j's buffer (column prefix)
- *   rtot[n]           rows each receiver holds (column sums incl. the diagonal)
+ * (the buffer layout soff / roff the chunk offsets refer to comes from aurora_pack)
  * Heterogeneous durations (time units, commsched.py:338-347) are converted to
  * whole tokens per chunk by rounding each pair's cumulative time x
  * min(B_i,B_j); the last chunk absorbs the rounding so per-pair totals are exact. */
 int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32_t* phase_recv,
                            double* phase_dur, int32_t* n_phases, int32_t* chunks,
-                           int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* soff,
-                           int32_t* roff, int32_t* rtot, int32_t* status, void* stream);
+                           int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* status,
+                           void* stream);
 
 /* ---------------------------------------------------------------- K1 ----
  * aurora_route: top-k gating + GPU x GPU traffic matrix. No reference
@@ -105,10 +103,17 @@ int aurora_route(const void* x, const void* w_gate, const float* bias, int T, in
  * destination j, list(i,j) = the rank's tokens routed to j in ascending token
  * order; send_list[i_local][soff[i][j] + p] = local token index of the p-th
  * entry; pos[t][s] = p for the slot's destination (same p for deduplicated
- * slots). Needs counts complete for the local rows. */
+ * slots). Needs counts complete (every row, for the layout).
+ * Buffer layout (all [n] / [n][n] int32, written for every rank):
+ *   soff[i][j]  start of list(i,j) in sender i's send list / return buffer (row prefix)
+ *   roff[i][j]  start of list(i,j) in receiver j's buffer: the local rows
+ *               list(j,j) first (roff[j][j] = 0), then the other senders in
+ *               index order, so the local expert work can start before the schedule
+ *   rtot[j]     rows receiver j holds; rloc[j] = counts[j][j]; rrem[j] = rtot - rloc */
 int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T,
                 int k, int n, int rank_base, int tokens_per_rank, int32_t* send_list,
-                int32_t* pos, void* stream);
+                int32_t* pos, int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc,
+                int32_t* rrem, void* stream);
 
 /* ------------------------------------------------------------ K4 / K6 ----
  * aurora_engine: executes the schedule as in-kernel stores into peer
@@ -117,7 +122,9 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * dispatch (CommSchedule phases, commsched.py:112-132), 1 = combine (the
  * reversed schedule, commsched.py:310-319: same phases, directions flipped);
  * mode bit 1: peers live on other GPUs (system-scope flag ordering) -- clear
- * when every rank of the call shares this GPU (gpu scope suffices).
+ * when every rank of the call shares this GPU (gpu scope suffices);
+ * mode bit 2: local (diagonal) rows only -- no schedule needed, so it can run
+ * while K2 is still computing; mode bit 3: scheduled remote chunks only.
  * Consecutive phases of one pair are one chunk (aurora_schedule_counts merges
  * them), so a handshake only happens where the schedule changes partners.
  *   tables from aurora_schedule_counts; counts[n][n] from aurora_route;
@@ -153,20 +160,23 @@ int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const in
 /* ---------------------------------------------------------------- K5 ----
  * aurora_expert_ffn: SwiGLU experts as tcgen05/TMEM grouped GEMMs fed by TMA
  * (the reference's ffn_work_per_token, core.py:194-221 / sim.py:71-89).
- *   groups G (one per local expert); rows of group g start at row g*cap of
- *   a_buf [G*cap][H] bf16; m_rows[g] (device) rows are valid.
+ *   groups G (one per local expert); group g owns rows g*cap .. g*cap+cap-1 of
+ *   a_buf [G*cap][H] bf16 and processes rows g*cap + m_start[g] + [0, m_rows[g])
+ *   (device arrays; m_start may be NULL = 0) -- so the local rows and the
+ *   network rows of one receive buffer can run as two launches.
  *   w13[G][2F][H] bf16: rows interleaved in 128-row blocks (gate block b at
  *   rows 256b..256b+127, up block at 256b+128..256b+255) -- see DESIGN.md
  *   w2[G][H][F] bf16; h_buf [G*cap][F] bf16 scratch; y_buf [G*cap][H] bf16 out.
  *   y = (silu(x W1^T) * (x W3^T)) W2^T, fp32 accumulate. */
 int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
-                      void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
-                      int num_sms, void* stream);
+                      void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
+                      int64_t cap, int H, int F, int num_sms, void* stream);
 
 /* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
  * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */
-int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_rows, int G,
-                        int64_t cap, int N, int K, int epilogue, int num_sms, void* stream);
+int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_start,
+                        const int32_t* m_rows, int G, int64_t cap, int N, int K, int epilogue,
+                        int num_sms, void* stream);
 
 /* ------------------------------------------------------- peer memory ----
  * CUDA IPC for the multi-GPU layer (one process per GPU). aurora_ipc_get

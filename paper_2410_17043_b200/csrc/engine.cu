@@ -104,16 +104,19 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
   const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
   const int n = p.n;
-  const int nph = min(*p.n_phases, p.max_phases);
+  // the schedule may still be running when a local-only copy starts: read it only when used
+  const int nph = (p.mode & 4) ? 0 : min(*p.n_phases, p.max_phases);
   const bool dispatch = (p.mode & 1) == 0;
-  const bool sys = (p.mode & 2) != 0;  // peers on other GPUs: system-scope ordering
+  const bool sys = (p.mode & 2) != 0;          // peers on other GPUs: system-scope ordering
+  const bool do_remote = (p.mode & 4) == 0;    // bit 2: local rows only
+  const bool do_local = (p.mode & 8) == 0;     // bit 3: scheduled (remote) chunks only
   const char* src = p.src_bufs[r_local];
   const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
   __shared__ int abort_s;
   if (threadIdx.x == 0) abort_s = 0;
   __syncthreads();
 
-  for (int k = 0; k < nph; k++) {
+  for (int k = 0; k < (do_remote ? nph : 0); k++) {
     // dispatch: chunk of sender g; combine: chunk of the reversed schedule where g sends back
     const int4 ch = dispatch ? p.chunks[k * n + g] : p.rchunks[k * n + g];
     const int peer = ch.x;  // dispatch: receiver j; combine: original sender i (now receiver)
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   }
 
   // local (diagonal) rows never cross the network (TrafficMatrix zeroes them, core.py:95)
-  {
+  if (do_local) {
     const int nloc = p.counts[g * n + g];
     const int per = (nloc + p.C - 1) / p.C;
     const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   }
 
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
-  if (c == 0 && threadIdx.x == 0) {
+  if (do_remote && c == 0 && threadIdx.x == 0) {
     const int expect = (dispatch ? p.n_in[g] : p.n_out[g]) * p.C;
     if (!wait_ge(p.ctrs[g], expect, p.spin_limit, sys)) {
       atomicExch(p.status, AURORA_ETIMEOUT);
@@ -218,7 +221,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst_bufs, int row_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
-  if (mode < 0 || mode > 3 || n < 1 || n > AUR_MAXN || n_local < 1 || rank_base < 0 ||
+  if (mode < 0 || mode > 15 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+      rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
       ((mode & 1) == 0 && !send_list))

@@ -119,6 +119,7 @@ struct TileIter {
   int total;           // total tiles
   int prefix[MAX_GROUPS + 1];
   int mt[MAX_GROUPS];  // m-tiles per group
+  int ms[MAX_GROUPS];  // first row of the group's range (m_start)
 };
 
 // Tile t -> (group, m-tile, n-tile). Inside a group, tiles walk blocks of
@@ -142,7 +143,8 @@ __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f +
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, __nv_bfloat16* __restrict__ c,
-                        const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
+                        const int32_t* __restrict__ m_start, const int32_t* __restrict__ m_rows,
+                        int G, long long cap, int N, int K,
                         int epilogue, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     for (int g = 0; g < G; g++) {
       const int m = m_rows[g];
+      it.ms[g] = m_start ? m_start[g] : 0;
       it.mt[g] = (m + BM - 1) / BM;
       it.prefix[g] = acc;
       acc += it.mt[g] * it.n_tiles_n;
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int t = blockIdx.x; t < it.total; t += gridDim.x) {
         int g, mt, nt;
         tile_coords(it, G, group_m, t, g, mt, nt);
-        const int a_row = (int)(g * cap) + mt * BM;
+        const int a_row = (int)(g * cap) + it.ms[g] + mt * BM;
         const int b_row = g * N + nt * BN;
         for (int kb = 0; kb < k_blocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       const int row_in_group = mt * BM + quarter * 32 + lane;
       const bool live = row_in_group < m_rows[g];
-      const long long row = g * cap + row_in_group;
+      const long long row = g * cap + it.ms[g] + row_in_group;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (epilogue == 1) {
         __nv_bfloat16* out = c + row * (long long)(N / 2) + nt * (BN / 2);
@@ -332,7 +335,8 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_rows, int G,
+int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start,
+                   const int32_t* m_rows, int G,
                    int64_t cap, int N, int K, int epilogue, int num_sms, cudaStream_t stream) {
   if (G < 1 || G > MAX_GROUPS || cap < 1 || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
@@ -356,26 +360,30 @@ int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_rows,
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   grouped_gemm_kernel<<<num_sms, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_rows, G, (long long)cap, N, K, epilogue, group_m);
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
 
 }  // namespace
 
-extern "C" int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_rows,
+extern "C" int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_start,
+                                   const int32_t* m_rows,
                                    int G, int64_t cap, int N, int K, int epilogue, int num_sms,
                                    void* stream) {
-  return launch_grouped(a, b, c, m_rows, G, cap, N, K, epilogue, num_sms, (cudaStream_t)stream);
+  return launch_grouped(a, b, c, m_start, m_rows, G, cap, N, K, epilogue, num_sms,
+                        (cudaStream_t)stream);
 }
 
 extern "C" int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
-                                 void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H,
+                                 void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
+                                 int64_t cap, int H,
                                  int F, int num_sms, void* stream) {
   // h = silu(x W1^T) * (x W3^T): N = 2F interleaved, K = H
-  int rc = launch_grouped(a_buf, w13, h_buf, m_rows, G, cap, 2 * F, H, 1, num_sms,
+  int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 2 * F, H, 1, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
   // y = h W2^T: N = H, K = F
-  return launch_grouped(h_buf, w2, y_buf, m_rows, G, cap, H, F, 0, num_sms, (cudaStream_t)stream);
+  return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, H, F, 0, num_sms,
+                        (cudaStream_t)stream);
 }

@@ -172,12 +172,32 @@ __global__ void __launch_bounds__(WARPS * 32) route_kernel(
 __global__ void __launch_bounds__(TILE) pack_kernel(
     const int32_t* __restrict__ slot_dst, const int32_t* __restrict__ blk_cnt,
     const int32_t* __restrict__ counts, int T, int k, int n, int rank_base, int tokens_per_rank,
-    int32_t* __restrict__ send_list, int32_t* __restrict__ pos) {
+    int32_t* __restrict__ send_list, int32_t* __restrict__ pos, int32_t* __restrict__ soff,
+    int32_t* __restrict__ roff, int32_t* __restrict__ rtot, int32_t* __restrict__ rloc,
+    int32_t* __restrict__ rrem) {
   __shared__ int base_s[AUR_MAXN];   // entries of earlier tiles of rank i, per destination
   __shared__ int soff_s[AUR_MAXN];   // start of list(i, j) in rank i's send list
   __shared__ int warp0_s[AUR_MAXN];  // entries of warp 0 per destination
   const int tl = threadIdx.x, warp = tl >> 5, lane = tl & 31;
   const int t0 = blockIdx.x * TILE, t = t0 + tl;
+  if (blockIdx.x == 0 && tl < n) {  // buffer layout of every rank (thread tl: sender row / receiver column tl)
+    int acc = 0;
+    for (int j = 0; j < n; j++) {
+      soff[tl * n + j] = acc;
+      acc += counts[tl * n + j];
+    }
+    const int loc = counts[tl * n + tl];
+    roff[tl * n + tl] = 0;  // local rows first
+    acc = loc;
+    for (int i = 0; i < n; i++) {
+      if (i == tl) continue;
+      roff[i * n + tl] = acc;
+      acc += counts[i * n + tl];
+    }
+    rtot[tl] = acc;
+    rloc[tl] = loc;
+    rrem[tl] = acc - loc;
+  }
   const int i_local = t0 / tokens_per_rank, i = rank_base + i_local;
   const int b_first = i_local * (tokens_per_rank / TILE);
   if (tl < n) {
@@ -245,13 +265,14 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
 
 extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts,
                            int T, int k, int n, int rank_base, int tokens_per_rank,
-                           int32_t* send_list, int32_t* pos, void* stream) {
+                           int32_t* send_list, int32_t* pos, int32_t* soff, int32_t* roff,
+                           int32_t* rtot, int32_t* rloc, int32_t* rrem, void* stream) {
   if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
-      T % tokens_per_rank)
+      T % tokens_per_rank || !soff || !roff || !rtot || !rloc || !rrem)
     return AURORA_EINVAL;
-  pack_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(slot_dst, blk_cnt, counts, T, k, n,
-                                                           rank_base, tokens_per_rank, send_list,
-                                                           pos);
+  pack_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
+      slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
+      rtot, rloc, rrem);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -41,9 +41,6 @@ struct SchedParams {
   int4* rchunks;          // [P_MAX][n]      by receiver: {send, start, ntok, sseq}
   int32_t* n_in;          // [n]             (nullable) chunks arriving at each receiver
   int32_t* n_out;         // [n]             chunks leaving each sender
-  int32_t* soff;          // [n][n]          (nullable) start of list(i,j) in sender i's send list
-  int32_t* roff;          // [n][n]          (nullable) start of list(i,j) in receiver j's buffer
-  int32_t* rtot;          // [n]             (nullable) rows held by each receiver
   long long* prof;        // [8]             (nullable) diagnostics: cycles per section
 };
 
@@ -228,9 +225,8 @@ __device__ __forceinline__ void row_put(double (&a)[NB], int j, double v) {
 
 // decompose (commsched.py:406-435) + strip/_coalesce (463-479), n <= NB <= 16.
 template <int NB>
-__device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_MAXN + 1],
-                               const double (*real_in)[AUR_MAXN + 1],
-                               const double (*t_in)[AUR_MAXN + 1], uint32_t* pref_s,
+__device__ void decompose_fast(const SchedParams& p, const double* rem_in, const double* real_in,
+                               const double* t_in, int ld, uint32_t* pref_s,
                                uint32_t* sup_s, int* perm_s, double eps, int& nr_out,
                                int& np_out, int& status) {
   const int lane = threadIdx.x, n = p.n;
@@ -240,9 +236,9 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
   double rem[NB], real[NB], lr[NB];
 #pragma unroll
   for (int j = 0; j < NB; j++) {
-    rem[j] = (on && j < n) ? rem_in[lane][j] : 0.0;
-    real[j] = (on && j < n) ? real_in[lane][j] : 0.0;
-    lr[j] = (on && j < n) ? t_in[lane][j] : 0.0;
+    rem[j] = (on && j < n) ? rem_in[lane * ld + j] : 0.0;
+    real[j] = (on && j < n) ? real_in[lane * ld + j] : 0.0;
+    lr[j] = (on && j < n) ? t_in[lane * ld + j] : 0.0;
   }
   int nr = 0, np_ = 0, last_recv = -2;
   double cur_dur = 0.0;
@@ -335,13 +331,16 @@ __device__ void decompose_fast(const SchedParams& p, const double (*rem_in)[AUR_
   np_out = np_;
 }
 
+// MAXN = 16 or 32: shared memory sized for the launch (a 16-rank schedule
+// needs 7 KB, so it co-resides with a persistent GEMM CTA on the same SM).
+template <int MAXN>
 __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
-  __shared__ double t_s[AUR_MAXN][AUR_MAXN + 1];     // time matrix; later "remaining" of strip
-  __shared__ double rem_s[AUR_MAXN][AUR_MAXN + 1];   // decompose remaining (d')
-  __shared__ double real_s[AUR_MAXN][AUR_MAXN + 1];  // decompose real
-  __shared__ double rr_s[AUR_MAXN], cr_s[AUR_MAXN];
+  __shared__ double t_s[MAXN][MAXN + 1];     // time matrix; later "remaining" of strip
+  __shared__ double rem_s[MAXN][MAXN + 1];   // decompose remaining (d')
+  __shared__ double real_s[MAXN][MAXN + 1];  // decompose real
+  __shared__ double rr_s[MAXN], cr_s[MAXN];
   __shared__ MatchState ms;
-  __shared__ int rcnt_s[AUR_MAXN];
+  __shared__ int rcnt_s[MAXN];
 
   const int lane = threadIdx.x;
   const int n = p.n;
@@ -430,9 +429,9 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     long long cyc[5] = {0, 0, 0, 0, clock64()};
     if (status == AURORA_OK && n <= 16) {
       if (n <= 8)
-        decompose_fast<8>(p, rem_s, real_s, t_s, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
+        decompose_fast<8>(p, &rem_s[0][0], &real_s[0][0], &t_s[0][0], MAXN + 1, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
       else
-        decompose_fast<16>(p, rem_s, real_s, t_s, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
+        decompose_fast<16>(p, &rem_s[0][0], &real_s[0][0], &t_s[0][0], MAXN + 1, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
       if (p.prof && lane == 0) p.prof[4] = clock64() - cyc[4];
     }
     while (status == AURORA_OK && n > 16) {
@@ -519,30 +518,17 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
   }
   if (status != AURORA_OK) np_ = 0;
 
-  // ---- engine tables: buffer layout + chunk list (CommSchedule.per_pair_totals
-  // order, commsched.py:291-297, split per phase)
-  if (p.soff && on) {
-    int acc = 0;
-    for (int j = 0; j < n; j++) {  // row prefix: list(i,j) inside sender i's send list
-      p.soff[lane * n + j] = acc;
-      acc += p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
-    }
-    acc = 0;
-    for (int i = 0; i < n; i++) {  // column prefix: list(i,j) inside receiver j's buffer
-      p.roff[i * n + lane] = acc;
-      acc += p.d32 ? p.d32[i * n + lane] : (int)p.d64[i * n + lane];
-    }
-    if (p.rtot) p.rtot[lane] = acc;
-  }
+  // ---- engine chunk list (CommSchedule.per_pair_totals order, commsched.py:291-297,
+  // split per phase); the buffer layout itself comes from aurora_pack
   if (p.chunks) {
     // rem_s: cumulative delivered time per pair; real_s (as int): tokens issued so far
     int* tok = reinterpret_cast<int*>(&real_s[0][0]);
-    int* lastc = reinterpret_cast<int*>(&real_s[0][0]) + AUR_MAXN * AUR_MAXN;
+    int* lastc = reinterpret_cast<int*>(&real_s[0][0]) + MAXN * MAXN;
     if (on) {
       for (int j = 0; j < n; j++) {
         rem_s[lane][j] = 0.0;
-        tok[lane * AUR_MAXN + j] = 0;
-        lastc[lane * AUR_MAXN + j] = -1;
+        tok[lane * MAXN + j] = 0;
+        lastc[lane * MAXN + j] = -1;
       }
       rcnt_s[lane] = 0;
     }
@@ -552,7 +538,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     // never pays a handshake inside it. Send and receive orders are unchanged.
     int sseq = 0;                    // this sender's chunk count so far
     int my_last_j = -1, my_last_k = -1;
-    __shared__ int lastfrom_s[AUR_MAXN];
+    __shared__ int lastfrom_s[MAXN];
     if (on) lastfrom_s[lane] = -1;
     __syncwarp();
     for (int k = 0; k < np_; k++) {
@@ -570,9 +556,9 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
         int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
         int tk = (int)rint(cum * scale);
         if (tk > want) tk = want;
-        int start = tok[lane * AUR_MAXN + j];
+        int start = tok[lane * MAXN + j];
         if (tk < start) tk = start;
-        tok[lane * AUR_MAXN + j] = tk;
+        tok[lane * MAXN + j] = tk;
         if (my_last_j == j && lastfrom_s[j] == lane) {
           merged = true;
           p.chunks[my_last_k * n + lane].z += tk - start;
@@ -584,7 +570,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
           my_last_j = j;
           my_last_k = k;
         }
-        lastc[lane * AUR_MAXN + j] = my_last_k;
+        lastc[lane * MAXN + j] = my_last_k;
       }
       __syncwarp();
       if (j >= 0) {  // receivers are distinct within a phase
@@ -598,8 +584,8 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     if (on) {
       for (int j = 0; j < n; j++) {
         int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
-        int got = tok[lane * AUR_MAXN + j];
-        int kl = lastc[lane * AUR_MAXN + j];
+        int got = tok[lane * MAXN + j];
+        int kl = lastc[lane * MAXN + j];
         if (kl >= 0 && got != want) {
           p.chunks[kl * n + lane].z += want - got;
           p.rchunks[kl * n + j].z += want - got;
@@ -609,6 +595,13 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       p.n_out[lane] = sseq;
     }
   }
+}
+
+void launch_schedule(const SchedParams& p, cudaStream_t s) {
+  if (p.n <= 16)
+    aurora_schedule_kernel<16><<<1, 32, 0, s>>>(p);
+  else
+    aurora_schedule_kernel<32><<<1, 32, 0, s>>>(p);
 }
 
 }  // namespace
@@ -631,7 +624,7 @@ extern "C" int aurora_schedule_f64(const double* d, const double* bw, int n, int
   p.n_phases = n_phases;
   p.b_max = b_max;
   p.status = status;
-  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  launch_schedule(p, (cudaStream_t)stream);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
@@ -639,10 +632,9 @@ extern "C" int aurora_schedule_f64(const double* d, const double* bw, int n, int
 extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, int n,
                                       int32_t* phase_recv, double* phase_dur, int32_t* n_phases,
                                       int32_t* chunks, int32_t* rchunks, int32_t* n_in,
-                                      int32_t* n_out, int32_t* soff, int32_t* roff,
-                                      int32_t* rtot, int32_t* status, void* stream) {
+                                      int32_t* n_out, int32_t* status, void* stream) {
   if (n < 1 || n > AUR_MAXN || !counts || !phase_recv || !phase_dur || !n_phases || !status ||
-      !chunks || !rchunks || !n_in || !n_out || !soff || !roff)
+      !chunks || !rchunks || !n_in || !n_out)
     return AURORA_EINVAL;
   SchedParams p{};
   p.d32 = counts;
@@ -656,10 +648,7 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
   p.rchunks = reinterpret_cast<int4*>(rchunks);
   p.n_in = n_in;
   p.n_out = n_out;
-  p.soff = soff;
-  p.roff = roff;
-  p.rtot = rtot;
-  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  launch_schedule(p, (cudaStream_t)stream);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
@@ -681,7 +670,7 @@ extern "C" int aurora_debug_schedule_cycles(const double* d, int n, long long* p
   p.phase_dur = dscratch + R;
   p.prof = prof;
   (void)P;
-  aurora_schedule_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(p);
+  launch_schedule(p, (cudaStream_t)stream);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -98,8 +98,9 @@ class AuroraMoELayer:
             raise ValueError("plan must cover every expert")
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
-        # copy CTAs per rank: two 256-thread CTAs fit per SM, all must be co-resident
-        self.C = ctas_per_rank or max(1, min(32, (2 * sms) // self.n_local))
+        # copy CTAs per rank: one per SM, so they stay co-resident next to the
+        # persistent expert GEMM that overlaps them (the engine clamps to occupancy too)
+        self.C = ctas_per_rank or max(1, min(32, sms // self.n_local))
         self.spin_limit = spin_limit
         H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
         Tr = cfg.tokens_per_rank
@@ -138,10 +139,19 @@ class AuroraMoELayer:
         self.rchunks = torch.empty(P, n, 4, **i32)
         self.n_in = torch.empty(n, **i32)
         self.n_out = torch.empty(n, **i32)
+        # buffer layout (written by K3 from the counts): local rows first in every receive buffer
         self.soff = torch.empty(n, n, **i32)
         self.roff = torch.empty(n, n, **i32)
         self.rtot = torch.empty(n, **i32)
+        self.rloc = torch.empty(n, **i32)
+        self.rrem = torch.empty(n, **i32)
         self.engine_status = torch.zeros(1, **i32)
+        # overlap: the local rows' copy + expert GEMM run on a side stream while
+        # K2 computes the schedule and the engine moves the network rows
+        self.overlap = True
+        self.side = torch.cuda.Stream(device=dev)
+        self._ev_pack = torch.cuda.Event()
+        self._ev_local = torch.cuda.Event()
 
         # ---- data buffers. A rank can receive at most every token once.
         self.cap = cfg.tokens
@@ -229,20 +239,23 @@ class AuroraMoELayer:
             self.counts.data_ptr(), None if self.bw is None else self.bw.data_ptr(), self.n,
             self.phase_recv.data_ptr(), self.phase_dur.data_ptr(), self.sched_i.data_ptr(),
             self.chunks.data_ptr(), self.rchunks.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
-            self.soff.data_ptr(), self.roff.data_ptr(), self.rtot.data_ptr(), self.sched_i[1:].data_ptr(),
-            stream), "aurora_schedule_counts")
+            self.sched_i[1:].data_ptr(), stream), "aurora_schedule_counts")
 
     def pack(self, stream: int) -> None:
         cfg = self.cfg
         _lib.check(self.L.aurora_pack(self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(), self.counts.data_ptr(),
                                       self.T_local, cfg.top_k, self.n, self.rank_base, cfg.tokens_per_rank,
-                                      self.send_list.data_ptr(), self.pos.data_ptr(), stream), "aurora_pack")
+                                      self.send_list.data_ptr(), self.pos.data_ptr(), self.soff.data_ptr(),
+                                      self.roff.data_ptr(), self.rtot.data_ptr(), self.rloc.data_ptr(),
+                                      self.rrem.data_ptr(), stream), "aurora_pack")
 
+    # engine mode bits (include/aurora_b200.h): 1 combine, 2 system scope, 4 local only, 8 remote only
     def _engine(self, mode: int, stream: int) -> None:
         cfg = self.cfg
-        src = self.t_src_d if mode == 0 else self.t_src_c
-        dst = self.t_dst_d if mode == 0 else self.t_dst_c
-        ctr = self.t_ctr_d if mode == 0 else self.t_ctr_c
+        combine = mode & 1
+        src = self.t_src_c if combine else self.t_src_d
+        dst = self.t_dst_c if combine else self.t_dst_d
+        ctr = self.t_ctr_c if combine else self.t_ctr_d
         sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
         _lib.check(self.L.aurora_engine(
             mode | sys_scope, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
@@ -251,14 +264,22 @@ class AuroraMoELayer:
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2, ctr.data_ptr(), self.C, self.P, self.spin_limit,
             self.engine_status.data_ptr(), stream), "aurora_engine")
 
-    def dispatch(self, stream: int) -> None:
-        self._engine(0, stream)
+    def dispatch(self, stream: int, part: str = "all") -> None:
+        self._engine({"all": 0, "local": 4, "remote": 8}[part], stream)
 
-    def experts(self, stream: int) -> None:
+    def experts(self, stream: int, part: str = "all") -> None:
+        """SwiGLU experts over this process's receive buffers: all rows, the
+        local rows only (they need no schedule), or the network rows only."""
         cfg = self.cfg
-        m_rows = self.rtot[self.rank_base:]
+        rb = self.rank_base
+        if part == "all":
+            m_start, m_rows = 0, self.rtot[rb:].data_ptr()
+        elif part == "local":
+            m_start, m_rows = 0, self.rloc[rb:].data_ptr()
+        else:
+            m_start, m_rows = self.rloc[rb:].data_ptr(), self.rrem[rb:].data_ptr()
         _lib.check(self.L.aurora_expert_ffn(self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
-                                            self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_rows.data_ptr(),
+                                            self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_start or None, m_rows,
                                             self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
                    "aurora_expert_ffn")
 
@@ -274,18 +295,37 @@ class AuroraMoELayer:
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor) -> torch.Tensor:
-        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape."""
+        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape.
+
+        Stream plan (no host synchronisation anywhere):
+          main: route -> (counts exchange) -> pack -+-> schedule -> dispatch(network rows) --+
+          side:                                     +-> copy local rows -> experts(local) ---+
+          main: experts(network rows) -> combine (reversed schedule) -> aggregate
+        """
         if x.dtype != torch.bfloat16 or x.shape != (self.T_local, self.cfg.hidden) or not x.is_contiguous():
             raise ValueError(f"x must be contiguous bf16 [{self.T_local}, {self.cfg.hidden}]")
         if self.x is None or x.data_ptr() != self.x.data_ptr():
             self._tables_for(x, getattr(self, "_peers", None))
-        s = _lib.stream_ptr()
+        main = torch.cuda.current_stream(self.dev)
+        s = int(main.cuda_stream)
         self.route(x, s)
         self.exchange_counts()
-        self.schedule(s)
         self.pack(s)
-        self.dispatch(s)
-        self.experts(s)
+        if not self.overlap:
+            self.schedule(s)
+            self.dispatch(s)
+            self.experts(s)
+        else:
+            self._ev_pack.record(main)
+            self.side.wait_event(self._ev_pack)
+            ss = int(self.side.cuda_stream)
+            self.dispatch(ss, "local")
+            self.experts(ss, "local")
+            self._ev_local.record(self.side)
+            self.schedule(s)
+            self.dispatch(s, "remote")
+            main.wait_event(self._ev_local)
+            self.experts(s, "remote")
         self.combine(s)
         self.aggregate(s)
         return self.out

@@ -20,7 +20,7 @@ def _run(torch, L, _lib, G, cap, m_rows, N, K, epilogue, seed=0):
     out_cols = N // 2 if epilogue else N
     c = torch.full((G * cap, out_cols), float("nan"), device="cuda", dtype=torch.bfloat16)
     m = torch.tensor(m_rows, dtype=torch.int32, device="cuda")
-    rc = L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), m.data_ptr(), G, cap, N, K, epilogue,
+    rc = L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, m.data_ptr(), G, cap, N, K, epilogue,
                                0, _lib.stream_ptr())
     assert rc == 0
     torch.cuda.synchronize()
@@ -70,7 +70,7 @@ def test_expert_ffn_matches_fp32(env):
     m_rows = [cap, 100]
     m = torch.tensor(m_rows, dtype=torch.int32, device="cuda")
     rc = L.aurora_expert_ffn(x.data_ptr(), w13.contiguous().data_ptr(), w2.data_ptr(), h.data_ptr(), y.data_ptr(),
-                             m.data_ptr(), G, cap, H, F, 0, _lib.stream_ptr())
+                             None, m.data_ptr(), G, cap, H, F, 0, _lib.stream_ptr())
     assert rc == 0
     torch.cuda.synchronize()
     for gi in range(G):

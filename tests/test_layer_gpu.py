@@ -50,11 +50,12 @@ def _check_layer(torch, cfg, plan=None, out_tol=3e-2):
     o = build_schedule_oracle(d)
     got = layer.schedule_objects()
     assert [(p.transfers, p.duration) for p in got.phases] == o["phases"]
-    # dispatched rows: receiver j holds x rows of list(0,j), list(1,j), ... bit-exact
+    # dispatched rows: receiver j holds its local rows list(j,j) first, then
+    # list(i,j) for the other senders in index order -- bit-exact copies of x
     xb = x.view(torch.int16)
     recv = layer.recv.view(torch.int16)
     for j in range(n):
-        rows = [t for i in range(n) for t in lists[i][j]]
+        rows = list(lists[j][j]) + [t for i in range(n) if i != j for t in lists[i][j]]
         if rows:
             assert torch.equal(recv[j * layer.cap: j * layer.cap + len(rows)], xb[rows])
     # combined output vs fp32 oracle
@@ -82,6 +83,20 @@ def test_layer_n8_skewed_permuted_plan(torch):
     from paper_2410_17043_b200.layer import MoEConfig
     cfg = MoEConfig(hidden=1024, ffn=512, experts=8, top_k=2, tokens=4096, ranks=8, skew=2.0, seed=1)
     _check_layer(torch, cfg, DeploymentPlan((3, 0, 7, 1, 6, 2, 5, 4)))
+
+
+def test_layer_serial_and_overlapped_agree(torch):
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=8, top_k=2, tokens=2048, ranks=8, skew=1.0, seed=4)
+    layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    layer.overlap = False
+    serial = layer(x).clone()
+    layer.overlap = True
+    over = layer(x)
+    torch.cuda.synchronize()
+    layer.check_status()
+    assert torch.equal(serial, over)
 
 
 def test_layer_repeated_calls_rearm_counters(torch):
