@@ -354,6 +354,7 @@ def main():
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(outh.numel() * 2),
                 "ms_per_step": e2e_ms, "path": "AuroraMoELayer.__call__ on pinned host buffers"},
         "clocks": clocks.summary(local_rank),
+        "timeline_ms": layer.timeline(x),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, sched_ms, sec = run_cpu(args, 256, 3)

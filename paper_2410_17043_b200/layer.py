@@ -19,6 +19,7 @@ happen to be local.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -148,7 +149,11 @@ class AuroraMoELayer:
         self.engine_status = torch.zeros(1, **i32)
         # overlap: the local rows' copy + expert GEMM run on a side stream while
         # K2 computes the schedule and the engine moves the network rows
-        self.overlap = True
+        self.overlap = os.environ.get("AURORA_OVERLAP", "schedule")  # "none" | "schedule" | "full"
+        if self.overlap == "none":
+            self.overlap = False
+        self.C_overlap = int(os.environ.get("AURORA_C_OVERLAP", "0"))  # copy CTAs/rank beside the GEMM
+        self.trace = None
         self.side = torch.cuda.Stream(device=dev)
         self._ev_pack = torch.cuda.Event()
         self._ev_local = torch.cuda.Event()
@@ -308,9 +313,13 @@ class AuroraMoELayer:
             self._tables_for(x, getattr(self, "_peers", None))
         main = torch.cuda.current_stream(self.dev)
         s = int(main.cuda_stream)
+        tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
+        mark = (lambda k, st: tr[k].record(st)) if tr else (lambda k, st: None)
+        mark("start", main)
         self.route(x, s)
         self.exchange_counts()
         self.pack(s)
+        mark("packed", main)
         if not self.overlap:
             self.schedule(s)
             self.dispatch(s)
@@ -320,15 +329,51 @@ class AuroraMoELayer:
             self.side.wait_event(self._ev_pack)
             ss = int(self.side.cuda_stream)
             self.dispatch(ss, "local")
+            mark("local_copied", self.side)
             self.experts(ss, "local")
+            mark("local_gemm_done", self.side)
             self._ev_local.record(self.side)
             self.schedule(s)
-            self.dispatch(s, "remote")
-            main.wait_event(self._ev_local)
+            mark("scheduled", main)
+            if self.overlap == "schedule":
+                # only the (latency-bound) scheduler hides under the local GEMM;
+                # the bandwidth-bound dispatch runs after it
+                main.wait_event(self._ev_local)
+                mark("joined", main)
+                self.dispatch(s, "remote")
+                mark("dispatched", main)
+            else:
+                c_full = self.C
+                self.C = self.C_overlap or self.C
+                try:
+                    self.dispatch(s, "remote")
+                finally:
+                    self.C = c_full
+                mark("dispatched", main)
+                main.wait_event(self._ev_local)
+                mark("joined", main)
             self.experts(s, "remote")
+        mark("experts_done", main)
         self.combine(s)
+        mark("combined", main)
         self.aggregate(s)
+        mark("end", main)
         return self.out
+
+    TRACE_POINTS = ("start", "packed", "local_copied", "local_gemm_done", "scheduled", "dispatched", "joined",
+                    "experts_done", "combined", "end")
+
+    def timeline(self, x: torch.Tensor) -> dict:
+        """One traced forward: ms from start to each point (diagnostics)."""
+        self.trace = {k: torch.cuda.Event(enable_timing=True) for k in self.TRACE_POINTS}
+        try:
+            self.forward(x)
+            torch.cuda.synchronize(self.dev)
+            t0 = self.trace["start"]
+            return {k: round(t0.elapsed_time(e), 4) for k, e in self.trace.items()
+                    if k == "start" or e.query()}
+        finally:
+            self.trace = None
 
     __call__ = forward
 
