@@ -99,9 +99,9 @@ class AuroraMoELayer:
             raise ValueError("plan must cover every expert")
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
-        # copy CTAs per rank: one per SM, so they stay co-resident next to the
-        # persistent expert GEMM that overlaps them (the engine clamps to occupancy too)
-        self.C = ctas_per_rank or max(1, min(32, sms // self.n_local))
+        # copy CTAs per rank (two 256-thread CTAs fit per SM; all must be
+        # co-resident -- the engine clamps to the occupancy limit too)
+        self.C = ctas_per_rank or max(1, min(32, (2 * sms) // self.n_local))
         self.spin_limit = spin_limit
         H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
         Tr = cfg.tokens_per_rank
@@ -149,7 +149,11 @@ class AuroraMoELayer:
         self.engine_status = torch.zeros(1, **i32)
         # overlap: the local rows' copy + expert GEMM run on a side stream while
         # K2 computes the schedule and the engine moves the network rows
-        self.overlap = os.environ.get("AURORA_OVERLAP", "schedule")  # "none" | "schedule" | "full"
+        # Measured on B200 (profiles/r01_overlap_sweep.json): the expert GEMM runs
+        # at the 1 kW power cap, so overlapping the copies only slows it, and
+        # splitting it into local/network launches re-reads every expert's
+        # weights. Serial is the default; the overlapped plans stay selectable.
+        self.overlap = os.environ.get("AURORA_OVERLAP", "none")  # "none" | "schedule" | "full"
         if self.overlap == "none":
             self.overlap = False
         self.C_overlap = int(os.environ.get("AURORA_C_OVERLAP", "0"))  # copy CTAs/rank beside the GEMM
@@ -314,7 +318,11 @@ class AuroraMoELayer:
         main = torch.cuda.current_stream(self.dev)
         s = int(main.cuda_stream)
         tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
-        mark = (lambda k, st: tr[k].record(st)) if tr else (lambda k, st: None)
+        def mark(k, st):
+            if tr:
+                tr[k].record(st)
+                self._marked.add(k)
+        self._marked = set()
         mark("start", main)
         self.route(x, s)
         self.exchange_counts()
@@ -370,8 +378,7 @@ class AuroraMoELayer:
             self.forward(x)
             torch.cuda.synchronize(self.dev)
             t0 = self.trace["start"]
-            return {k: round(t0.elapsed_time(e), 4) for k, e in self.trace.items()
-                    if k == "start" or e.query()}
+            return {k: round(t0.elapsed_time(e), 4) for k, e in self.trace.items() if k in self._marked}
         finally:
             self.trace = None
 
