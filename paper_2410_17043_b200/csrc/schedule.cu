@@ -198,50 +198,71 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 
 #include "fastmatch.cuh"
 
-// min over lanes of a non-negative double (+inf allowed): IEEE order of
-// non-negative doubles is the order of their bit patterns
-__device__ __forceinline__ double warp_min_nonneg(double v) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
-  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
-  const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | mlo));
-}
+// Value domain of the fast path. Homogeneous integer traffic (the in-layer
+// path: int32 token counts, B = 1) is exact in int32, where every eps test of
+// the reference (x > 1e-12 max(1, b_max), b_max < 2^31) is x > 0; general
+// inputs use IEEE double with the reference's eps.
+template <typename V>
+struct Dom;
+template <>
+struct Dom<double> {
+  double eps;
+  __device__ __forceinline__ bool pos(double x) const { return x > eps; }
+  __device__ __forceinline__ static double inf() { return __longlong_as_double(0x7ff0000000000000ll); }
+  // min over lanes of a non-negative double: IEEE order of non-negative
+  // doubles is the order of their bit patterns
+  __device__ __forceinline__ static double warp_min(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t mlo = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return __longlong_as_double((long long)(((unsigned long long)mh << 32) | mlo));
+  }
+};
+template <>
+struct Dom<int> {
+  __device__ __forceinline__ bool pos(int x) const { return x > 0; }
+  __device__ __forceinline__ static int inf() { return 0x7fffffff; }
+  __device__ __forceinline__ static int warp_min(int v) {
+    return (int)__reduce_min_sync(0xffffffffu, (unsigned)v);
+  }
+};
 
-template <int NB>
-__device__ __forceinline__ double row_pick(const double (&a)[NB], int j) {
-  double r = a[0];
+template <int NB, typename V>
+__device__ __forceinline__ V row_pick(const V (&a)[NB], int j) {
+  V r = a[0];
 #pragma unroll
   for (int q = 1; q < NB; q++)
     if (q == j) r = a[q];
   return r;
 }
-template <int NB>
-__device__ __forceinline__ void row_put(double (&a)[NB], int j, double v) {
+template <int NB, typename V>
+__device__ __forceinline__ void row_put(V (&a)[NB], int j, V v) {
 #pragma unroll
   for (int q = 0; q < NB; q++)
     if (q == j) a[q] = v;
 }
 
-// decompose (commsched.py:406-435) + strip/_coalesce (463-479), n <= NB <= 16.
-template <int NB>
+// decompose (commsched.py:406-435) + strip/_coalesce (463-479), n <= NB <= 16,
+// every lane holding its row of remaining / real / undelivered in registers.
+template <int NB, typename V>
 __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const double* real_in,
                                const double* t_in, int ld, uint32_t* pref_s,
-                               uint32_t* sup_s, int* perm_s, double eps, int& nr_out,
-                               int& np_out, int& status) {
+                               uint32_t* sup_s, int* perm_s, Dom<V> dom, signed char* precv_s,
+                               double* pdur_s, int& nr_out, int& np_out, int& status) {
   const int lane = threadIdx.x, n = p.n;
   const bool on = lane < n;
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const V INF = Dom<V>::inf();
   const int R_MAX = n * n - 2 * n + 2, P_MAX = 2 * n * n - 3 * n + 2;
-  double rem[NB], real[NB], lr[NB];
+  V rem[NB], real[NB], lr[NB];
 #pragma unroll
   for (int j = 0; j < NB; j++) {
-    rem[j] = (on && j < n) ? rem_in[lane * ld + j] : 0.0;
-    real[j] = (on && j < n) ? real_in[lane * ld + j] : 0.0;
-    lr[j] = (on && j < n) ? t_in[lane * ld + j] : 0.0;
+    rem[j] = (on && j < n) ? (V)rem_in[lane * ld + j] : (V)0;
+    real[j] = (on && j < n) ? (V)real_in[lane * ld + j] : (V)0;
+    lr[j] = (on && j < n) ? (V)t_in[lane * ld + j] : (V)0;
   }
   int nr = 0, np_ = 0, last_recv = -2;
-  double cur_dur = 0.0;
+  V cur_dur = 0;
   FastMatch<NB> fm;
   long long cy[4] = {0, 0, 0, 0}, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
   while (true) {
@@ -250,13 +271,13 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
     uint32_t sup = 0, pref = 0;
 #pragma unroll
     for (int j = 0; j < NB; j++) {
-      double r = rem[j];
-      if (r <= eps) r = 0.0;  // remaining[remaining <= eps] = 0
+      V r = rem[j];
+      if (!dom.pos(r)) r = 0;  // remaining[remaining <= eps] = 0
       rem[j] = r;
       if (r < real[j]) real[j] = r;  // np.minimum(real, remaining)
-      anyrow |= r != 0.0;
+      anyrow |= r != 0;
       if (r > 0) sup |= 1u << j;
-      if (real[j] > eps) pref |= 1u << j;
+      if (dom.pos(real[j])) pref |= 1u << j;
     }
     if (!__any_sync(0xffffffffu, on && anyrow)) break;
     if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
@@ -278,30 +299,30 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
     if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
     t2 = clock64();
     const int pj = on ? perm_s[1 + lane] : 0;
-    const double dur = warp_min_nonneg(on ? row_pick<NB>(rem, pj) : INF);
+    const V dur = Dom<V>::warp_min(on ? row_pick<NB, V>(rem, pj) : INF);
     if (on) {
-      row_put<NB>(rem, pj, row_pick<NB>(rem, pj) - dur);
-      const double re = row_pick<NB>(real, pj) - dur;
-      row_put<NB>(real, pj, re < 0.0 ? 0.0 : re);
+      row_put<NB, V>(rem, pj, row_pick<NB, V>(rem, pj) - dur);
+      const V re = row_pick<NB, V>(real, pj) - dur;
+      row_put<NB, V>(real, pj, re < 0 ? (V)0 : re);
       if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
     }
-    if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
+    if (lane == 0 && p.raw_dur) p.raw_dur[nr] = (double)dur;
     nr++;
     t3 = clock64();
-    double left = dur;
-    while (left > eps) {
-      const double lv = on ? row_pick<NB>(lr, pj) : 0.0;
-      const bool act = on && lv > eps;
+    V left = dur;
+    while (dom.pos(left)) {
+      const V lv = on ? row_pick<NB, V>(lr, pj) : (V)0;
+      const bool act = on && dom.pos(lv);
       const unsigned amask = __ballot_sync(0xffffffffu, act);
-      double step;
+      V step;
       if (amask == 0) {
         step = left;
       } else {
-        const double m = warp_min_nonneg(act ? lv : INF);
+        const V m = Dom<V>::warp_min(act ? lv : INF);
         step = m < left ? m : left;
       }
       const int recv = act ? pj : -1;
-      if (step > eps) {
+      if (dom.pos(step)) {
         const bool same = np_ > 0 && __all_sync(0xffffffffu, !on || recv == last_recv);
         if (same) {
           cur_dur = cur_dur + step;
@@ -310,12 +331,18 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
           np_++;
           cur_dur = step;
           last_recv = recv;
-          if (on) p.phase_recv[(np_ - 1) * n + lane] = recv;
+          if (on) {
+            p.phase_recv[(np_ - 1) * n + lane] = recv;
+            precv_s[(np_ - 1) * n + lane] = (signed char)recv;
+          }
         }
-        if (lane == 0) p.phase_dur[np_ - 1] = cur_dur;
+        if (lane == 0) {
+          p.phase_dur[np_ - 1] = (double)cur_dur;
+          pdur_s[np_ - 1] = (double)cur_dur;
+        }
       }
       if (amask == 0) break;
-      if (act) row_put<NB>(lr, pj, lv - step);
+      if (act) row_put<NB, V>(lr, pj, lv - step);
       left -= step;
     }
     if (status != AURORA_OK) break;
@@ -335,6 +362,10 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
 // needs 7 KB, so it co-resides with a persistent GEMM CTA on the same SM).
 template <int MAXN>
 __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
+  // phase tables staged in shared memory for the chunk pass (fast path only)
+  constexpr int PST = MAXN <= 16 ? 2 * MAXN * MAXN - 3 * MAXN + 2 : 1;
+  __shared__ signed char precv_s[PST * MAXN];
+  __shared__ double pdur_s[PST];
   __shared__ double t_s[MAXN][MAXN + 1];     // time matrix; later "remaining" of strip
   __shared__ double rem_s[MAXN][MAXN + 1];   // decompose remaining (d')
   __shared__ double real_s[MAXN][MAXN + 1];  // decompose real
@@ -356,7 +387,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       double dij = p.d64 ? p.d64[lane * n + j] : (double)p.d32[lane * n + j];
       double bw_j = p.bw ? p.bw[j] : 1.0;
       double m = bw_j < bw_i ? bw_j : bw_i;
-      double v = dij / m;
+      double v = p.bw ? dij / m : dij;  // x / 1.0 == x exactly
       if (v != v || v < 0) bad = true;
       t_s[lane][j] = (lane == j) ? 0.0 : v;
     }
@@ -428,10 +459,22 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     double cur_dur = 0.0;
     long long cyc[5] = {0, 0, 0, 0, clock64()};
     if (status == AURORA_OK && n <= 16) {
-      if (n <= 8)
-        decompose_fast<8>(p, &rem_s[0][0], &real_s[0][0], &t_s[0][0], MAXN + 1, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
-      else
-        decompose_fast<16>(p, &rem_s[0][0], &real_s[0][0], &t_s[0][0], MAXN + 1, ms.pref, ms.sup, ms.ml, eps, nr, np_, status);
+      // integer domain: int32 counts on a uniform cluster (every value an integer < 2^31)
+      const bool int_dom = p.d32 && !p.bw;
+      const double* R = &rem_s[0][0];
+      const double* Q = &real_s[0][0];
+      const double* Tt = &t_s[0][0];
+      if (n <= 8) {
+        if (int_dom)
+          decompose_fast<8, int>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<int>{}, precv_s, pdur_s, nr, np_, status);
+        else
+          decompose_fast<8, double>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<double>{eps}, precv_s, pdur_s, nr, np_, status);
+      } else {
+        if (int_dom)
+          decompose_fast<16, int>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<int>{}, precv_s, pdur_s, nr, np_, status);
+        else
+          decompose_fast<16, double>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<double>{eps}, precv_s, pdur_s, nr, np_, status);
+      }
       if (p.prof && lane == 0) p.prof[4] = clock64() - cyc[4];
     }
     while (status == AURORA_OK && n > 16) {
@@ -538,48 +581,58 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     // never pays a handshake inside it. Send and receive orders are unchanged.
     int sseq = 0;                    // this sender's chunk count so far
     int my_last_j = -1, my_last_k = -1;
+    int4 pend_c = make_int4(-1, 0, 0, 0), pend_rc = make_int4(-1, 0, 0, 0);  // open chunk
+    const bool staged = n <= 16;     // phase tables also in shared memory
     __shared__ int lastfrom_s[MAXN];
     if (on) lastfrom_s[lane] = -1;
     __syncwarp();
     for (int k = 0; k < np_; k++) {
       if (on) p.rchunks[k * n + lane] = make_int4(-1, 0, 0, 0);
       __syncwarp();
-      const double dk = p.phase_dur[k];
-      const int j = on ? p.phase_recv[k * n + lane] : -1;
-      int4 c = make_int4(-1, 0, 0, 0);
-      bool merged = false;
+      const double dk = staged ? pdur_s[k] : p.phase_dur[k];
+      const int j = on ? (staged ? (int)precv_s[k * n + lane] : p.phase_recv[k * n + lane]) : -1;
+      bool opened = false;
       if (j >= 0) {
         double cum = rem_s[lane][j] + dk;
         rem_s[lane][j] = cum;
-        double bw_j = p.bw ? p.bw[j] : 1.0;
-        double scale = bw_j < bw_i ? bw_j : bw_i;
-        int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
+        const double bw_j = p.bw ? p.bw[j] : 1.0;
+        const double scale = bw_j < bw_i ? bw_j : bw_i;
+        const int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
         int tk = (int)rint(cum * scale);
         if (tk > want) tk = want;
-        int start = tok[lane * MAXN + j];
+        const int start = tok[lane * MAXN + j];
         if (tk < start) tk = start;
         tok[lane * MAXN + j] = tk;
-        if (my_last_j == j && lastfrom_s[j] == lane) {
-          merged = true;
-          p.chunks[my_last_k * n + lane].z += tk - start;
-          p.rchunks[my_last_k * n + j].z += tk - start;
+        if (my_last_j == j && lastfrom_s[j] == lane) {  // continues the open chunk
+          pend_c.z += tk - start;
+          pend_rc.z += tk - start;
         } else {
-          c = make_int4(j, start, tk - start, rcnt_s[j]);
-          p.rchunks[k * n + j] = make_int4(lane, start, tk - start, sseq);
+          if (my_last_k >= 0) {  // close the previous chunk of this sender
+            p.chunks[my_last_k * n + lane] = pend_c;
+            p.rchunks[my_last_k * n + my_last_j] = pend_rc;
+          }
+          pend_c = make_int4(j, start, tk - start, rcnt_s[j]);
+          pend_rc = make_int4(lane, start, tk - start, sseq);
           sseq++;
           my_last_j = j;
           my_last_k = k;
+          opened = true;
         }
         lastc[lane * MAXN + j] = my_last_k;
       }
       __syncwarp();
       if (j >= 0) {  // receivers are distinct within a phase
-        if (!merged) rcnt_s[j] += 1;
+        if (opened) rcnt_s[j] += 1;
         lastfrom_s[j] = lane;
       }
-      if (on) p.chunks[k * n + lane] = c;
+      if (on && !opened) p.chunks[k * n + lane] = make_int4(-1, 0, 0, 0);
       __syncwarp();
     }
+    if (on && my_last_k >= 0) {
+      p.chunks[my_last_k * n + lane] = pend_c;
+      p.rchunks[my_last_k * n + my_last_j] = pend_rc;
+    }
+    __syncwarp();
     // fractional (heterogeneous) durations: make every pair's chunk total exact
     if (on) {
       for (int j = 0; j < n; j++) {

@@ -79,3 +79,82 @@ def test_device_schedule_errors(A):
         A.build_schedule(A.TrafficMatrix(np.ones((33, 33))), A.ClusterSpec.uniform(33))
     with pytest.raises(ValueError):
         A.build_schedule(A.TrafficMatrix(np.ones((3, 3))), A.ClusterSpec.uniform(2))
+
+
+def _expected_chunks(phases, counts, n):
+    """Host restatement of the engine tables: per phase and sender the
+    (receiver, first, count, arrival index); same-pair runs that are
+    consecutive for both sender and receiver are one chunk."""
+    P = len(phases)
+    ch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
+    rch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
+    issued = np.zeros((n, n), dtype=np.int64)
+    rcnt = [0] * n
+    sseq = [0] * n
+    last_j = [-1] * n
+    last_k = [-1] * n
+    last_from = [-1] * n
+    for k, (transfers, dur) in enumerate(phases):
+        tok = int(round(dur))
+        opened = []
+        for i, j in transfers:
+            start = int(issued[i, j])
+            issued[i, j] += tok
+            if last_j[i] == j and last_from[j] == i:
+                kk = last_k[i]
+                a = ch[kk][i]
+                ch[kk][i] = (a[0], a[1], a[2] + tok, a[3])
+                b = rch[kk][j]
+                rch[kk][j] = (b[0], b[1], b[2] + tok, b[3])
+            else:
+                ch[k][i] = (j, start, tok, rcnt[j])
+                rch[k][j] = (i, start, tok, sseq[i])
+                sseq[i] += 1
+                last_j[i], last_k[i] = j, k
+                opened.append(j)
+        for i, j in transfers:
+            last_from[j] = i
+        for j in opened:
+            rcnt[j] += 1
+    return ch, rch, rcnt, sseq
+
+
+def test_counts_path_int_domain_and_chunk_tables(A):
+    """aurora_schedule_counts (int32 counts, uniform cluster: the int32 fast
+    path) vs the oracle, plus its chunk tables vs a host restatement."""
+    import torch
+    from oracle.oracle import build_schedule_oracle
+    from paper_2410_17043_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(77)
+    for it in range(200):
+        n = int(rng.choice([2, 3, 4, 6, 8, 8, 8, 12, 16]))
+        c = _fuzz_matrix(rng, n, it % 2).astype(np.int32)
+        dev = torch.device("cuda")
+        counts = torch.tensor(c, dtype=torch.int32, device=dev)
+        P = L.aurora_phase_cap(n)
+        i32 = dict(dtype=torch.int32, device=dev)
+        pr = torch.empty(P, n, **i32)
+        pd = torch.empty(P, dtype=torch.float64, device=dev)
+        si = torch.zeros(2, **i32)
+        chunks = torch.empty(P, n, 4, **i32)
+        rchunks = torch.empty(P, n, 4, **i32)
+        n_in = torch.empty(n, **i32)
+        n_out = torch.empty(n, **i32)
+        rc = L.aurora_schedule_counts(counts.data_ptr(), None, n, pr.data_ptr(), pd.data_ptr(), si.data_ptr(),
+                                      chunks.data_ptr(), rchunks.data_ptr(), n_in.data_ptr(), n_out.data_ptr(),
+                                      si[1:].data_ptr(), _lib.stream_ptr())
+        assert rc == 0
+        torch.cuda.synchronize()
+        nph, status = si.tolist()
+        assert status == 0
+        d = c.astype(float)
+        np.fill_diagonal(d, 0)
+        o = build_schedule_oracle(d)
+        got = [(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(t))
+               for row, t in zip(pr[:nph].tolist(), pd[:nph].tolist())]
+        assert got == o["phases"], (n, it)
+        ch, rch, rcnt, sseq = _expected_chunks(o["phases"], d, n)
+        assert [[tuple(x) for x in row] for row in chunks[:nph].tolist()] == ch
+        assert [[tuple(x) for x in row] for row in rchunks[:nph].tolist()] == rch
+        assert n_in.tolist() == rcnt and n_out.tolist() == sseq
