@@ -193,6 +193,10 @@ int aurora_ipc_close(void* base);
  * scratch >= (n^2-2n+2)*n + 3 + (2n^2-3n+2)*n int32, dscratch >= 3n^2 doubles. */
 int aurora_debug_schedule_cycles(const double* d, int n, long long* prof, int32_t* scratch,
                                  double* dscratch, void* stream);
+/* Diagnostics: every later K2 launch (any entry point) writes its section
+ * cycles to the device array prof[8] = {snap+masks, matching, update, strip,
+ * decompose, prologue, whole kernel, chunk pass}; NULL turns it off. */
+int aurora_debug_set_schedule_profile(long long* prof);
 
 #ifdef __cplusplus
 }

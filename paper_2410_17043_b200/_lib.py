@@ -35,6 +35,7 @@ _SIGNATURES = {
     "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],
     "aurora_grouped_gemm": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _c_int, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
+    "aurora_debug_set_schedule_profile": [_vp],
     "aurora_ipc_handle_bytes": [],
     "aurora_ipc_get": [_vp, _vp, _vp],
     "aurora_ipc_open": [_vp, _c_i64, _vp],

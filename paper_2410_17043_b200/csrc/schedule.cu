@@ -358,6 +358,8 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
   np_out = np_;
 }
 
+__device__ long long* g_sched_prof = nullptr;
+
 // MAXN = 16 or 32: shared memory sized for the launch (a 16-rank schedule
 // needs 7 KB, so it co-resides with a persistent GEMM CTA on the same SM).
 template <int MAXN>
@@ -378,6 +380,8 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
   const bool on = lane < n;
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   int status = AURORA_OK;
+  const long long k_start = clock64();
+  if (!p.prof) p.prof = g_sched_prof;  // diagnostics hook (aurora_debug_set_schedule_profile)
 
   // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
   double bw_i = (on && p.bw) ? p.bw[lane] : 1.0;
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
     int last_recv = -2;  // receiver of this lane in the last kept phase
     double cur_dur = 0.0;
     long long cyc[5] = {0, 0, 0, 0, clock64()};
+    if (p.prof && lane == 0) p.prof[5] = cyc[4] - k_start;  // prologue: normalise, bmax, augment
     if (status == AURORA_OK && n <= 16) {
       // integer domain: int32 counts on a uniform cluster (every value an integer < 2^31)
       const bool int_dom = p.d32 && !p.bw;
@@ -563,6 +568,7 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
 
   // ---- engine chunk list (CommSchedule.per_pair_totals order, commsched.py:291-297,
   // split per phase); the buffer layout itself comes from aurora_pack
+  const long long c_start = clock64();
   if (p.chunks) {
     // rem_s: cumulative delivered time per pair; real_s (as int): tokens issued so far
     int* tok = reinterpret_cast<int*>(&real_s[0][0]);
@@ -648,7 +654,23 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       p.n_out[lane] = sseq;
     }
   }
+  if (p.prof && lane == 0) {
+    const long long now = clock64();
+    p.prof[6] = now - k_start;  // whole kernel
+    p.prof[7] = now - c_start;  // chunk pass
+  }
 }
+
+}  // namespace
+
+// Diagnostics: make every subsequent K2 launch record its section cycles in
+// prof[8] (NULL switches it off).
+extern "C" int aurora_debug_set_schedule_profile(long long* prof) {
+  return cudaMemcpyToSymbol(g_sched_prof, &prof, sizeof(prof)) == cudaSuccess ? AURORA_OK
+                                                                                : AURORA_ECUDA;
+}
+
+namespace {
 
 void launch_schedule(const SchedParams& p, cudaStream_t s) {
   if (p.n <= 16)
