@@ -111,3 +111,49 @@ def test_layer_repeated_calls_rearm_counters(torch):
     layer.check_status()
     assert torch.equal(first, again)
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
+
+
+def test_layer_c2_full_size(torch):
+    """The bench workload itself (C2: 16384 tokens, hidden 4096, FFN 14336, 8
+    experts top-2, 8 ranks): bit-exact routing / traffic matrix / token
+    permutation / schedule / dispatched rows vs the oracle, and the output of
+    256 sampled tokens vs a plain PyTorch fp32 reference of the same layer."""
+    from oracle.oracle import bf16_bits, build_schedule_oracle, pack_oracle, router_oracle
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=4096, ffn=14336, experts=8, top_k=2, tokens=16384, ranks=8, skew=1.0, seed=0)
+    layer = AuroraMoELayer(cfg)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda", generator=g).to(torch.bfloat16)
+    out = layer(x).clone()
+    torch.cuda.synchronize()
+    layer.check_status()
+    n, k = cfg.ranks, cfg.top_k
+    _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), k)
+    assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
+    counts, lists, pos = pack_oracle(idx, layer.plan.assignment_a, n)
+    assert np.array_equal(layer.counts.cpu().numpy(), counts)
+    assert np.array_equal(layer.pos.cpu().numpy(), pos)
+    d = counts.astype(float)
+    np.fill_diagonal(d, 0)
+    assert [(p.transfers, p.duration) for p in layer.schedule_objects().phases] == build_schedule_oracle(d)["phases"]
+    xb, recv = x.view(torch.int16), layer.recv.view(torch.int16)
+    for j in range(n):
+        rows = torch.tensor(list(lists[j][j]) + [t for i in range(n) if i != j for t in lists[i][j]], device="cuda")
+        assert torch.equal(recv[j * layer.cap: j * layer.cap + len(rows)], xb[rows])
+    # fp32 reference for a token sample
+    sample = torch.randperm(cfg.tokens, generator=torch.Generator().manual_seed(1))[:256].cuda()
+    F = cfg.ffn
+    v = layer.w13.view(n, F // 128, 2, 128, cfg.hidden)
+    ref = torch.zeros(len(sample), cfg.hidden, device="cuda")
+    xs = x[sample].float()
+    ti = layer.topk_idx[sample].long()
+    tw = layer.topk_w[sample]
+    for r in range(n):
+        e = layer.expert_of_rank(r)
+        w1 = v[r, :, 0].reshape(F, cfg.hidden).float()
+        w3 = v[r, :, 1].reshape(F, cfg.hidden).float()
+        y = (torch.nn.functional.silu(xs @ w1.T) * (xs @ w3.T)) @ layer.w2[r].float().T
+        wsel = ((ti == e).float() * tw).sum(1, keepdim=True)
+        ref += wsel * y
+    err = (out[sample].float() - ref).abs().max().item()
+    assert err <= 3e-2 * ref.abs().max().item(), err
