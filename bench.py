@@ -283,6 +283,14 @@ def main():
     layer.check_status()
     stage_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
     serial_ms = sum(stage_ms.values())
+    # ablation: the same engine with the schedule's pacing switched off
+    layer.unpaced = 16
+    for s_ in range(args.steps):
+        staged_step(evs[s_])
+    torch.cuda.synchronize()
+    layer.check_status()
+    layer.unpaced = 0
+    unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
 
     # ---- end to end through the public API with host buffers (pinned), copies timed
     xh = x.cpu().pin_memory()
@@ -339,6 +347,8 @@ def main():
         "all_to_all": {
             "dispatch_us": stage_ms["dispatch"] * 1e3, "combine_us": stage_ms["combine"] * 1e3,
             "schedule_us": stage_ms["schedule"] * 1e3,
+            "unscheduled_dispatch_us": unpaced_ms["dispatch"] * 1e3,
+            "unscheduled_combine_us": unpaced_ms["combine"] * 1e3,
             "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
             "bound_basis": "b_max x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",

@@ -124,7 +124,9 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * mode bit 1: peers live on other GPUs (system-scope flag ordering) -- clear
  * when every rank of the call shares this GPU (gpu scope suffices);
  * mode bit 2: local (diagonal) rows only -- no schedule needed, so it can run
- * while K2 is still computing; mode bit 3: scheduled remote chunks only.
+ * while K2 is still computing; mode bit 3: scheduled remote chunks only;
+ * mode bit 4: ablation -- no pacing, every sender pushes all of its chunks at
+ * once (the unscheduled all-pairs-concurrent all-to-all).
  * Consecutive phases of one pair are one chunk (aurora_schedule_counts merges
  * them), so a handshake only happens where the schedule changes partners.
  *   tables from aurora_schedule_counts; counts[n][n] from aurora_route;

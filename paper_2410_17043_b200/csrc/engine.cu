@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const bool sys = (p.mode & 2) != 0;          // peers on other GPUs: system-scope ordering
   const bool do_remote = (p.mode & 4) == 0;    // bit 2: local rows only
   const bool do_local = (p.mode & 8) == 0;     // bit 3: scheduled (remote) chunks only
+  const bool paced = (p.mode & 16) == 0;       // bit 4: ablation, every pair at once (no schedule)
   const char* src = p.src_bufs[r_local];
   const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
   __shared__ int abort_s;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     if (peer < 0) continue;
     const int first = ch.y, ntok = ch.z, seq = ch.w;
     if (threadIdx.x == 0) {
-      if (!wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit, sys)) {
+      if (paced && !wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit, sys)) {
         abort_s = 1;
         atomicExch(p.status, AURORA_ETIMEOUT);
       }
@@ -221,7 +222,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst_bufs, int row_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
-  if (mode < 0 || mode > 15 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+  if (mode < 0 || mode > 31 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||

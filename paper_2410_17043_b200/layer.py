@@ -157,6 +157,7 @@ class AuroraMoELayer:
         if self.overlap == "none":
             self.overlap = False
         self.C_overlap = int(os.environ.get("AURORA_C_OVERLAP", "0"))  # copy CTAs/rank beside the GEMM
+        self.unpaced = 0  # 16: ablation -- run the all-to-all without the schedule's pacing
         self.trace = None
         self.side = torch.cuda.Stream(device=dev)
         self._ev_pack = torch.cuda.Event()
@@ -274,7 +275,7 @@ class AuroraMoELayer:
             self.engine_status.data_ptr(), stream), "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all") -> None:
-        self._engine({"all": 0, "local": 4, "remote": 8}[part], stream)
+        self._engine({"all": 0, "local": 4, "remote": 8}[part] | self.unpaced, stream)
 
     def experts(self, stream: int, part: str = "all") -> None:
         """SwiGLU experts over this process's receive buffers: all rows, the
@@ -293,7 +294,7 @@ class AuroraMoELayer:
                    "aurora_expert_ffn")
 
     def combine(self, stream: int) -> None:
-        self._engine(1, stream)
+        self._engine(1 | self.unpaced, stream)
 
     def aggregate(self, stream: int) -> None:
         cfg = self.cfg

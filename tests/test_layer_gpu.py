@@ -157,3 +157,45 @@ def test_layer_c2_full_size(torch):
         ref += wsel * y
     err = (out[sample].float() - ref).abs().max().item()
     assert err <= 3e-2 * ref.abs().max().item(), err
+
+
+def test_layer_heterogeneous_cluster(torch):
+    """C4 (heterogeneous emulation): placement by assign_exclusive_hetero
+    (placement.py:46-60) from a calibration pass, schedule on the fp64
+    time-normalised matrix (commsched.py:338-347) bit-exact with the oracle,
+    fractional durations turned into whole-token chunks whose per-pair totals
+    equal the traffic matrix, and a correct layer output."""
+    import paper_2410_17043_b200 as A
+    from oracle.oracle import build_schedule_oracle
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    bw = [1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4]
+    cluster = A.ClusterSpec(tuple(A.GpuSpec(b, b) for b in bw))
+    cfg = MoEConfig(hidden=512, ffn=256, experts=8, top_k=2, tokens=4096, ranks=8, skew=1.5, seed=9)
+    calib = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    calib(x)
+    torch.cuda.synchronize()
+    loads = calib.counts.cpu().numpy().sum(axis=0)  # tokens per expert (identity plan)
+    plan = A.assign_exclusive_hetero(loads, cluster)
+    layer = AuroraMoELayer(cfg, plan, bandwidths=bw)
+    out = layer(x)
+    torch.cuda.synchronize()
+    layer.check_status()
+    counts = layer.counts.cpu().numpy().astype(float)
+    np.fill_diagonal(counts, 0)
+    o = build_schedule_oracle(counts, bw)
+    got = layer.schedule_objects()
+    assert [(p.transfers, p.duration) for p in got.phases] == o["phases"]
+    nph = int(layer.sched_i[0])
+    ch = layer.chunks[:nph].cpu().numpy()
+    tot = np.zeros((8, 8))
+    for row in ch:
+        for i, (j, first, cnt, _) in enumerate(row):
+            if j >= 0:
+                tot[i, j] += cnt
+    assert np.array_equal(tot, counts)
+    # output identical to the homogeneous-cluster run of the same plan (schedule only changes pacing)
+    ref_layer = AuroraMoELayer(cfg, plan)
+    ref = ref_layer(x)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
