@@ -19,8 +19,14 @@
 // (gate block, up block): the 256-column tile holds matching gate / up
 // columns and emits silu(gate) * up for 128 output columns.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
+
+// the CTA-pair variant (gemm2sm.cu)
+int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
+                              const int32_t* m_rows, int G, int64_t cap, int N, int K,
+                              int epilogue, int num_sms, cudaStream_t stream);
 
 namespace {
 
@@ -335,9 +341,22 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// kernel choice: "2sm" = CTA-pair tcgen05 (gemm2sm.cu), "1sm" = this file's kernel
+bool use_pair_kernel() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("AURORA_GEMM");
+    mode = (e && e[0] == '1') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
 int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start,
                    const int32_t* m_rows, int G,
                    int64_t cap, int N, int K, int epilogue, int num_sms, cudaStream_t stream) {
+  if (use_pair_kernel())
+    return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, N, K, epilogue, num_sms,
+                                     stream);
   if (G < 1 || G > MAX_GROUPS || cap < 1 || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
     return AURORA_EINVAL;

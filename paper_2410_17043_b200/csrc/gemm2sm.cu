@@ -1,0 +1,277 @@
+// K5, CTA-pair variant: the expert grouped GEMM on tcgen05.mma.cta_group::2.
+//
+// A cluster of two CTAs (one TPC) computes a 256 x 256 output tile: CTA r
+// stages A rows [m0 + 128 r, +128) and weight rows [n0 + 128 r, +128) (the
+// instruction reads A's M halves and B's N halves from the two CTAs' shared
+// memory at the same offsets) and keeps output rows m0 + 128 r .. +127, all
+// 256 columns, in its own TMEM. Per CTA a pipeline stage is 32 KB instead of
+// 48 KB, so six stages fit, and each SM reads half as many B bytes per FLOP.
+//
+// Roles per CTA: warp 0 TMA producer (both CTAs; bytes land on the leader's
+// full barrier), warp 1 TMEM allocator (both, cta_group::2) and MMA issuer
+// (leader only), warps 2-5 epilogue (both; arrive on the leader's tmem_empty).
+// Same grouped tiling, rasterisation, epilogues and C ABI as gemm.cu.
+#include "tc_helpers.cuh"
+
+namespace {
+
+constexpr int BMP = 256, BN = 256, BK = 64, STAGES = 6, UMMA_K = 16;
+constexpr int HALF = 128;                        // rows per CTA of A and of B
+constexpr int THREADS = 192;
+constexpr int A_BYTES = HALF * BK * 2;           // 16 KB
+constexpr int B_BYTES = HALF * BK * 2;           // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB per CTA
+constexpr int TMEM_COLS = 512;                   // 2 accumulators x 256 columns
+constexpr int MAX_GROUPS = 64;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t IDESC = tc::idesc_bf16(BMP, BN);
+
+struct TileIter2 {
+  int n_tiles_n, total;
+  int prefix[MAX_GROUPS + 1];
+  int mt[MAX_GROUPS];
+  int ms[MAX_GROUPS];
+};
+
+__device__ __forceinline__ void tile_coords2(const TileIter2& it, int G, int gm, int t, int& g,
+                                             int& mt, int& nt) {
+  g = 0;
+  while (g + 1 < G && it.prefix[g + 1] <= t) g++;
+  const int local = t - it.prefix[g];
+  const int per_block = gm * it.n_tiles_n;
+  const int sb = local / per_block, rem = local - sb * per_block;
+  const int rows = min(gm, it.mt[g] - sb * gm);
+  mt = sb * gm + rem % rows;
+  nt = rem / rows;
+}
+
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap map_a,
+                            const __grid_constant__ CUtensorMap map_b,
+                            __nv_bfloat16* __restrict__ c, const int32_t* __restrict__ m_start,
+                            const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
+                            int epilogue, int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + 2);
+  __shared__ TileIter2 it;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    it.n_tiles_n = N / BN;
+    int acc = 0;
+    for (int g = 0; g < G; g++) {
+      const int m = m_rows[g];
+      it.mt[g] = (m + BMP - 1) / BMP;
+      it.ms[g] = m_start ? m_start[g] : 0;
+      it.prefix[g] = acc;
+      acc += it.mt[g] * it.n_tiles_n;
+    }
+    it.prefix[G] = acc;
+    it.total = acc;
+    for (int s = 0; s < STAGES; s++) {
+      tc::mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
+      tc::mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+    }
+    for (int a = 0; a < 2; a++) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 2 * 128);  // every epilogue thread of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(tmem_base_s)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_base_s;
+  const int k_blocks = K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t full0 = tc::mapa(tc::smem_u32(&full[0]), 0);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = cluster_id; t < it.total; t += n_clusters) {
+        int g, mt, nt;
+        tile_coords2(it, G, group_m, t, g, mt, nt);
+        const int a_row = (int)(g * cap) + it.ms[g] + mt * BMP + (int)rank * HALF;
+        const int b_row = g * N + nt * BN + (int)rank * HALF;
+        for (int kb = 0; kb < k_blocks; kb++) {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          if (leader) tc::mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t fb = full0 + s * 8;
+          tc::tma_load_2d_pair(sa, &map_a, fb, kb * BK, a_row);
+          tc::tma_load_2d_pair(sa + A_BYTES, &map_b, fb, kb * BK, b_row);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      for (int t = cluster_id; t < it.total; t += n_clusters, local++) {
+        const int acc = local & 1;
+        tc::mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < k_blocks; kb++) {
+          tc::mbar_wait(&full[s], ph);
+          tc::fence_after();
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          const uint64_t ad = tc::sw128_desc(sa), bd = tc::sw128_desc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; k++)
+            tc::umma_bf16_pair(d, ad + 2 * k, bd + 2 * k, IDESC, (kb | k) != 0);
+          tc::umma_commit_pair(&empty[s], 0x3);  // frees the stage in both CTAs
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc::umma_commit_pair(&tfull[acc], 0x3);
+      }
+    }
+  } else {  // ---------------- epilogue warps 2..5 (both CTAs)
+    const int quarter = warp & 3;
+    const uint32_t tempty0 = tc::mapa(tc::smem_u32(&tempty[0]), 0);
+    int local = 0;
+    for (int t = cluster_id; t < it.total; t += n_clusters, local++) {
+      int g, mt, nt;
+      tile_coords2(it, G, group_m, t, g, mt, nt);
+      const int acc = local & 1;
+      tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc::fence_after();
+      const int row_in_group = mt * BMP + (int)rank * HALF + quarter * 32 + lane;
+      const bool live = row_in_group < m_rows[g];
+      const long long row = g * cap + it.ms[g] + row_in_group;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      if (epilogue == 1) {
+        __nv_bfloat16* out = c + row * (long long)(N / 2) + nt * (BN / 2);
+        for (int c0 = 0; c0 < BN / 2; c0 += 32) {
+          uint32_t gr[32], ur[32];
+          TC_TMEM_LD32(tbase + c0, gr);
+          TC_TMEM_LD32(tbase + BN / 2 + c0, ur);
+          tc::tmem_ld_wait();
+          if (live) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+              float a0 = silu_mul(__uint_as_float(gr[2 * q]), __uint_as_float(ur[2 * q]));
+              float a1 = silu_mul(__uint_as_float(gr[2 * q + 1]), __uint_as_float(ur[2 * q + 1]));
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
+              packed[q] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            int4* o = reinterpret_cast<int4*>(out + c0);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              o[q] = make_int4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          }
+        }
+      } else {
+        __nv_bfloat16* out = c + row * (long long)N + nt * BN;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          TC_TMEM_LD32(tbase + c0, r);
+          tc::tmem_ld_wait();
+          if (live) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+              packed[q] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            int4* o = reinterpret_cast<int4*>(out + c0);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              o[q] = make_int4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          }
+        }
+      }
+      tc::fence_before();
+      tc::mbar_arrive_cluster(tempty0 + acc * 8);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync();
+  if (warp == 1) {
+    __syncwarp();
+    tc::fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
+int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
+                              const int32_t* m_rows, int G, int64_t cap, int N, int K,
+                              int epilogue, int num_sms, cudaStream_t stream) {
+  if (G < 1 || G > MAX_GROUPS || cap < 1 || N % BN || K % BK || N <= 0 || K <= 0 ||
+      (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
+    return AURORA_EINVAL;
+  CUtensorMap ma, mb;
+  if (!make_map_2d(&ma, a, (uint64_t)G * cap, K, HALF) ||
+      !make_map_2d(&mb, b, (uint64_t)G * N, K, HALF))
+    return AURORA_ECUDA;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_BYTES) != cudaSuccess)
+      return AURORA_ECUDA;
+    attr_set = true;
+  }
+  const int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BMP * K * 2)));
+  if (num_sms <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = num_sms & ~1;
+  grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
