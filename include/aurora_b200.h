@@ -109,11 +109,16 @@ int aurora_route(const void* x, const void* w_gate, const float* bias, int T, in
  *   roff[i][j]  start of list(i,j) in receiver j's buffer: the local rows
  *               list(j,j) first (roff[j][j] = 0), then the other senders in
  *               index order, so the local expert work can start before the schedule
- *   rtot[j]     rows receiver j holds; rloc[j] = counts[j][j]; rrem[j] = rtot - rloc */
+ *   rtot[j]     rows receiver j holds; rloc[j] = counts[j][j]; rrem[j] = rtot - rloc
+ * meta (nullable; needed when a rank hosts several experts): per send-list row
+ * a record of k {int32 local expert on the destination or -1, float gate
+ * weight}, padded to a multiple of 16 bytes (meta_bytes = roundup(8k, 16));
+ * [n_local][T/n * k] records. local_of_expert[E] = expert index within its rank. */
 int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T,
                 int k, int n, int rank_base, int tokens_per_rank, int32_t* send_list,
                 int32_t* pos, int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc,
-                int32_t* rrem, void* stream);
+                int32_t* rrem, const int32_t* topk_idx, const float* topk_w,
+                const int32_t* local_of_expert, void* meta, void* stream);
 
 /* ------------------------------------------------------------ K4 / K6 ----
  * aurora_engine: executes the schedule as in-kernel stores into peer
@@ -135,6 +140,9 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  *             dst = recv_buf[j] rows roff[i][j] + first ...
  *   combine:  src rows = out_buf[j_local] rows roff[i][j] + first ...,
  *             dst = ret_buf[i] rows soff[i][j] + first ...
+ *   optional second plane (dispatch only; NULL to skip): src2_bufs[n_local] rows
+ *   of row2_bytes in send-list order (aurora_pack's meta), landing beside the
+ *   token rows in dst2_bufs[n] at the same row index;
  *   src_bufs[n_local], dst_bufs[n] (peer-mapped), ctrs[n] (peer-mapped int32
  *   arrival counters, zero on entry, left zero on exit), all device arrays.
  *   ctas_per_rank copy CTAs per local rank; all must be co-resident.
@@ -144,6 +152,7 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
                   const int32_t* n_in, const int32_t* n_out, const int32_t* soff,
                   const int32_t* roff, const int32_t* send_list, int send_list_stride,
                   const void* const* src_bufs, void* const* dst_bufs, int row_bytes,
+                  const void* const* src2_bufs, void* const* dst2_bufs, int row2_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
                   int32_t* status, void* stream);
 
@@ -173,6 +182,33 @@ int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const in
 int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                       void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
                       int64_t cap, int H, int F, int num_sms, void* stream);
+
+/* Same FFN with the groups packed back to back (a rank hosting several
+ * experts): group g's rows are a_buf rows [g_off[g], g_off[g] + g_rows[g]);
+ * a_rows = rows allocated in a_buf / h_buf / y_buf. */
+int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2, void* h_buf,
+                             void* y_buf, const int32_t* g_off, const int32_t* g_rows, int G,
+                             int64_t a_rows, int H, int F, int num_sms, void* stream);
+
+/* Several experts per rank (E > n). After the dispatch, receiver rows of the
+ * local ranks (rank r_local: rows r_local*cap + [0, rtot[rank_base+r_local]))
+ * carry aurora_pack's meta records (copied by the engine's second plane).
+ *   aurora_expert_sort: group g = r_local*G + local expert; g_rows[g], packed
+ *     offsets g_off[0..n_local*G] (g_off[n_local*G] = total), g_src[p] = the
+ *     received row of grouped position p, inv[row][slot] = p or -1.
+ *     scratch >= ceil(n_local*cap/256) * n_local*G ints.
+ *   aurora_gather_rows: dst[p] = src[idx[p]] for p < *count (device count).
+ *   aurora_expert_reduce: ybuf[row] = sum_slots w * yg[inv[row][slot]] (fp32 -> bf16),
+ *     the pre-reduction that returns one row per (token, rank) to the combine. */
+int aurora_expert_sort(const void* meta, int64_t cap, int meta_bytes, const int32_t* rtot,
+                       int n_local, int rank_base, int k, int G, int32_t* g_off, int32_t* g_rows,
+                       int32_t* g_src, int32_t* inv, int32_t* scratch, int scratch_ints,
+                       void* stream);
+int aurora_gather_rows(const void* src, void* dst, const int32_t* idx, const int32_t* count,
+                       int64_t max_rows, int row_bytes, void* stream);
+int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap,
+                         int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k,
+                         int H, void* ybuf, void* stream);
 
 /* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
  * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */

@@ -27,13 +27,18 @@ _SIGNATURES = {
     "aurora_route": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
                      _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                    _vp],
+                    _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
-                      _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _vp],
+                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _vp],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp],
     "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],
     "aurora_grouped_gemm": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _c_int, _vp],
+    "aurora_expert_ffn_packed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],
+    "aurora_expert_sort": [_vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
+                           _vp, _c_int, _vp],
+    "aurora_gather_rows": [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp],
+    "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "aurora_debug_set_schedule_profile": [_vp],
     "aurora_ipc_handle_bytes": [],

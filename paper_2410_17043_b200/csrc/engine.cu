@@ -38,6 +38,9 @@ struct EngineParams {
   const char* const* src_bufs;
   char* const* dst_bufs;
   int row_bytes;
+  const char* const* src2_bufs;  // optional second plane (dispatch): per-row expert metadata
+  char* const* dst2_bufs;
+  int row2_bytes;
   int32_t* const* ctrs;
   int C;
   int max_phases;
@@ -61,16 +64,16 @@ __device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long lon
 // 64 KiB per CTA) so a pair's CTAs keep enough bytes in flight to cover
 // HBM / NVLink latency.
 template <bool GATHER>
-__device__ __forceinline__ void copy_rows(const EngineParams& p, const char* src_base,
+__device__ __forceinline__ void copy_rows(int row_bytes, const char* src_base,
                                           const int32_t* gather, int src_row0, char* dst_base,
                                           int dst_row0, int r0, int r1) {
   constexpr int U = 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int vec = p.row_bytes >> 4;
+  const int vec = row_bytes >> 4;
   for (int r = r0 + warp; r < r1; r += WARPS) {
     const long long srow = GATHER ? (long long)gather[src_row0 + r] : (long long)(src_row0 + r);
-    const int4* s = reinterpret_cast<const int4*>(src_base + srow * p.row_bytes);
-    int4* d = reinterpret_cast<int4*>(dst_base + (long long)(dst_row0 + r) * p.row_bytes);
+    const int4* s = reinterpret_cast<const int4*>(src_base + srow * row_bytes);
+    int4* d = reinterpret_cast<int4*>(dst_base + (long long)(dst_row0 + r) * row_bytes);
     for (int u0 = 0; u0 < vec; u0 += 32 * U) {
       int4 v[U];
 #pragma unroll
@@ -135,11 +138,14 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     const int r0 = min(ntok, c * per), r1 = min(ntok, r0 + per);
     if (dispatch) {
       // x rows of list(g, peer) -> recv_buf[peer] rows roff[g][peer] + first ...
-      copy_rows<true>(p, src, list, p.soff[g * n + peer] + first, p.dst_bufs[peer],
+      copy_rows<true>(p.row_bytes, src, list, p.soff[g * n + peer] + first, p.dst_bufs[peer],
                       p.roff[g * n + peer] + first, r0, r1);
+      if (p.src2_bufs)
+        copy_rows<false>(p.row2_bytes, p.src2_bufs[r_local], nullptr, p.soff[g * n + peer] + first,
+                         p.dst2_bufs[peer], p.roff[g * n + peer] + first, r0, r1);
     } else {
       // y rows of pair (peer, g) at roff[peer][g] -> ret_buf[peer] rows soff[peer][g] ...
-      copy_rows<false>(p, src, nullptr, p.roff[peer * n + g] + first, p.dst_bufs[peer],
+      copy_rows<false>(p.row_bytes, src, nullptr, p.roff[peer * n + g] + first, p.dst_bufs[peer],
                        p.soff[peer * n + g] + first, r0, r1);
     }
     signal(p.ctrs[peer], sys);
@@ -151,9 +157,15 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     const int per = (nloc + p.C - 1) / p.C;
     const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
     if (dispatch)
-      copy_rows<true>(p, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g], r0, r1);
+    {
+      copy_rows<true>(p.row_bytes, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g],
+                      r0, r1);
+      if (p.src2_bufs)
+        copy_rows<false>(p.row2_bytes, p.src2_bufs[r_local], nullptr, p.soff[g * n + g],
+                         p.dst2_bufs[g], p.roff[g * n + g], r0, r1);
+    }
     else
-      copy_rows<false>(p, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0,
+      copy_rows<false>(p.row_bytes, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0,
                        r1);
   }
 
@@ -219,7 +231,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              const int32_t* n_phases, const int32_t* n_in, const int32_t* n_out,
                              const int32_t* soff, const int32_t* roff, const int32_t* send_list,
                              int send_list_stride, const void* const* src_bufs,
-                             void* const* dst_bufs, int row_bytes, int32_t* const* ctrs,
+                             void* const* dst_bufs, int row_bytes, const void* const* src2_bufs,
+                             void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
   if (mode < 0 || mode > 31 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
@@ -256,6 +269,10 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.src_bufs = reinterpret_cast<const char* const*>(src_bufs);
   p.dst_bufs = reinterpret_cast<char* const*>(dst_bufs);
   p.row_bytes = row_bytes;
+  p.src2_bufs = reinterpret_cast<const char* const*>(src2_bufs);
+  p.dst2_bufs = reinterpret_cast<char* const*>(dst2_bufs);
+  p.row2_bytes = row2_bytes;
+  if (src2_bufs && (!dst2_bufs || row2_bytes <= 0 || row2_bytes % 16)) return AURORA_EINVAL;
   p.ctrs = ctrs;
   p.C = ctas_per_rank;
   p.max_phases = max_phases;

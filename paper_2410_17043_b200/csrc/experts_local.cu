@@ -1,0 +1,219 @@
+// Several experts per rank (E > n, config C5; two models' experts on one GPU,
+// config C3): after the dispatch a received row may belong to up to k of the
+// rank's local experts (a token crosses the network once per destination).
+//   aurora_expert_sort    group the received rows by local expert (counting sort)
+//   aurora_gather_rows    materialise each expert's rows contiguously for the GEMM
+//   aurora_expert_reduce  pre-reduce: y_row = sum over its local experts of w * FFN_e(row),
+//                         so the combine returns ONE row per (token, rank) and the
+//                         reversed traffic matrix stays the dispatch transpose
+//                         (LayerProfile.d_second, reference core.py:219-221).
+#include "common.cuh"
+
+namespace {
+
+constexpr int ROWS_PER_BLOCK = 256;
+constexpr int MAX_SLOTS = 8;
+
+__device__ __forceinline__ bool row_valid(long long row, long long cap, const int32_t* rtot,
+                                          int rank_base, int& r_local, int& i) {
+  r_local = (int)(row / cap);
+  i = (int)(row - (long long)r_local * cap);
+  return i < rtot[rank_base + r_local];
+}
+
+// pass 1: per-block histogram of (local rank, local expert) groups
+__global__ void sort_count_kernel(const uint8_t* __restrict__ meta, long long cap, int meta_bytes,
+                                  const int32_t* __restrict__ rtot, int n_local, int rank_base,
+                                  int k, int G, int32_t* __restrict__ blk_hist) {
+  extern __shared__ int hist[];
+  const int Gt = n_local * G;
+  for (int g = threadIdx.x; g < Gt; g += blockDim.x) hist[g] = 0;
+  __syncthreads();
+  const long long row = (long long)blockIdx.x * ROWS_PER_BLOCK + threadIdx.x;
+  int r, i;
+  if (row < (long long)n_local * cap && row_valid(row, cap, rtot, rank_base, r, i)) {
+    const int2* m = reinterpret_cast<const int2*>(meta + row * meta_bytes);
+    for (int s = 0; s < k; s++) {
+      const int e = m[s].x;
+      if (e >= 0) atomicAdd(&hist[r * G + e], 1);
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < Gt; g += blockDim.x) blk_hist[(size_t)blockIdx.x * Gt + g] = hist[g];
+}
+
+// pass 2 (one CTA): group sizes, packed offsets, and every block's base per group
+__global__ void sort_scan_kernel(int32_t* __restrict__ blk_hist, int blocks, int Gt,
+                                 int32_t* __restrict__ g_off, int32_t* __restrict__ g_rows) {
+  __shared__ int rows_s[1024];
+  const int g = threadIdx.x;
+  int tot = 0;
+  if (g < Gt)
+    for (int b = 0; b < blocks; b++) tot += blk_hist[(size_t)b * Gt + g];
+  rows_s[g] = tot;
+  __syncthreads();
+  if (g == 0) {  // Gt <= 1024: a short serial scan
+    int acc = 0;
+    for (int q = 0; q < Gt; q++) {
+      const int v = rows_s[q];
+      rows_s[q] = acc;
+      acc += v;
+    }
+    g_off[Gt] = acc;
+  }
+  __syncthreads();
+  if (g < Gt) {
+    g_rows[g] = tot;
+    int base = rows_s[g];
+    g_off[g] = base;
+    for (int b = 0; b < blocks; b++) {
+      const int v = blk_hist[(size_t)b * Gt + g];
+      blk_hist[(size_t)b * Gt + g] = base;
+      base += v;
+    }
+  }
+}
+
+// pass 3: scatter each (row, slot) to its group position; inv[row][slot] = position
+__global__ void sort_scatter_kernel(const uint8_t* __restrict__ meta, long long cap,
+                                    int meta_bytes, const int32_t* __restrict__ rtot,
+                                    int n_local, int rank_base, int k, int G,
+                                    const int32_t* __restrict__ blk_base,
+                                    int32_t* __restrict__ g_src, int32_t* __restrict__ inv) {
+  extern __shared__ int cursor[];
+  const int Gt = n_local * G;
+  for (int g = threadIdx.x; g < Gt; g += blockDim.x) cursor[g] = blk_base[(size_t)blockIdx.x * Gt + g];
+  __syncthreads();
+  const long long row = (long long)blockIdx.x * ROWS_PER_BLOCK + threadIdx.x;
+  if (row >= (long long)n_local * cap) return;
+  int r, i;
+  const bool valid = row_valid(row, cap, rtot, rank_base, r, i);
+  const int2* m = reinterpret_cast<const int2*>(meta + row * meta_bytes);
+  for (int s = 0; s < k; s++) {
+    const int e = valid ? m[s].x : -1;
+    int p = -1;
+    if (e >= 0) {
+      p = atomicAdd(&cursor[r * G + e], 1);
+      g_src[p] = (int)row;
+    }
+    inv[row * k + s] = p;
+  }
+}
+
+__global__ void gather_rows_kernel(const char* __restrict__ src, char* __restrict__ dst,
+                                   const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
+                                   int row_bytes) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int total = *count, vec = row_bytes >> 4;
+  for (int p = warp; p < total; p += nwarps) {
+    const int4* s = reinterpret_cast<const int4*>(src + (long long)idx[p] * row_bytes);
+    int4* d = reinterpret_cast<int4*>(dst + (long long)p * row_bytes);
+    for (int u0 = 0; u0 < vec; u0 += 256) {
+      int4 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if (u0 + q * 32 + lane < vec) v[q] = ld_nc_v4(s + u0 + q * 32 + lane);
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if (u0 + q * 32 + lane < vec) st_na_v4(d + u0 + q * 32 + lane, v[q]);
+    }
+  }
+}
+
+// y_row = sum_s w_s * yg[inv[row][s]] (fp32) -> bf16, warp per received row
+__global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
+                                     const int32_t* __restrict__ inv,
+                                     const uint8_t* __restrict__ meta, long long cap,
+                                     int meta_bytes, const int32_t* __restrict__ rtot, int n_local,
+                                     int rank_base, int k, int H, __nv_bfloat16* __restrict__ ybuf) {
+  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)n_local * cap) return;
+  int r, i;
+  if (!row_valid(row, cap, rtot, rank_base, r, i)) return;
+  const int2* m = reinterpret_cast<const int2*>(meta + row * meta_bytes);
+  const int4* src[MAX_SLOTS];
+  float w[MAX_SLOTS];
+  int ns = 0;
+  for (int s = 0; s < k; s++) {
+    const int p = inv[row * k + s];
+    if (p >= 0) {
+      src[ns] = reinterpret_cast<const int4*>(yg + (long long)p * H);
+      w[ns] = __int_as_float(m[s].y);
+      ns++;
+    }
+  }
+  int4* o = reinterpret_cast<int4*>(ybuf + row * H);
+  for (int u = lane; u < H / 8; u += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = 0; q < ns; q++) {
+      int4 v = ld_nc_v4(src[q] + u);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        float2 f = __bfloat1622float2(b[e]);
+        acc[2 * e] = fmaf(w[q], f.x, acc[2 * e]);
+        acc[2 * e + 1] = fmaf(w[q], f.y, acc[2 * e + 1]);
+      }
+    }
+    int4 res;
+    __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&res);
+#pragma unroll
+    for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
+    o[u] = res;
+  }
+}
+
+}  // namespace
+
+extern "C" int aurora_expert_sort(const void* meta, int64_t cap, int meta_bytes,
+                                  const int32_t* rtot, int n_local, int rank_base, int k, int G,
+                                  int32_t* g_off, int32_t* g_rows, int32_t* g_src, int32_t* inv,
+                                  int32_t* scratch, int scratch_ints, void* stream) {
+  const int Gt = n_local * G;
+  if (!meta || cap < 1 || meta_bytes < 8 * k || meta_bytes % 16 || !rtot || n_local < 1 ||
+      k < 1 || k > MAX_SLOTS || G < 1 || Gt > 1024 || !g_off || !g_rows || !g_src || !inv ||
+      !scratch)
+    return AURORA_EINVAL;
+  const long long rows = (long long)n_local * cap;
+  const int blocks = (int)((rows + ROWS_PER_BLOCK - 1) / ROWS_PER_BLOCK);
+  if ((long long)blocks * Gt > scratch_ints) return AURORA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint8_t* mb = (const uint8_t*)meta;
+  sort_count_kernel<<<blocks, ROWS_PER_BLOCK, Gt * sizeof(int), s>>>(mb, cap, meta_bytes, rtot,
+                                                                      n_local, rank_base, k, G,
+                                                                      scratch);
+  sort_scan_kernel<<<1, 1024, 0, s>>>(scratch, blocks, Gt, g_off, g_rows);
+  sort_scatter_kernel<<<blocks, ROWS_PER_BLOCK, Gt * sizeof(int), s>>>(
+      mb, cap, meta_bytes, rtot, n_local, rank_base, k, G, scratch, g_src, inv);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_gather_rows(const void* src, void* dst, const int32_t* idx,
+                                  const int32_t* count, int64_t max_rows, int row_bytes,
+                                  void* stream) {
+  if (!src || !dst || !idx || !count || row_bytes % 16 || max_rows < 0) return AURORA_EINVAL;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  gather_rows_kernel<<<sms * 4, 256, 0, (cudaStream_t)stream>>>((const char*)src, (char*)dst, idx,
+                                                                count, row_bytes);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta,
+                                    int64_t cap, int meta_bytes, const int32_t* rtot, int n_local,
+                                    int rank_base, int k, int H, void* ybuf, void* stream) {
+  if (!yg || !inv || !meta || cap < 1 || !rtot || k < 1 || k > MAX_SLOTS || H % 8 || !ybuf)
+    return AURORA_EINVAL;
+  const long long rows = (long long)n_local * cap;
+  const int blocks = (int)((rows * 32 + 255) / 256);
+  expert_reduce_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)yg, inv, (const uint8_t*)meta, cap, meta_bytes, rtot, n_local,
+      rank_base, k, H, (__nv_bfloat16*)ybuf);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}

@@ -25,8 +25,8 @@
 
 // the CTA-pair variant (gemm2sm.cu)
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
-                              const int32_t* m_rows, int G, int64_t cap, int N, int K,
-                              int epilogue, int num_sms, cudaStream_t stream);
+                              const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
+                              int K, int epilogue, int num_sms, cudaStream_t stream);
 
 namespace {
 
@@ -353,16 +353,21 @@ bool use_pair_kernel() {
 
 int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start,
                    const int32_t* m_rows, int G,
-                   int64_t cap, int N, int K, int epilogue, int num_sms, cudaStream_t stream) {
+                   int64_t cap, int64_t map_rows, int N, int K, int epilogue, int num_sms,
+                   cudaStream_t stream) {
+  // cap > 0: group g owns rows [g*cap, (g+1)*cap); cap == 0: groups packed,
+  // m_start[g] absolute, map_rows = rows of the A buffer
+  if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
+  if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (use_pair_kernel())
-    return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, N, K, epilogue, num_sms,
+    return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, num_sms,
                                      stream);
-  if (G < 1 || G > MAX_GROUPS || cap < 1 || N % BN || K % BK || N <= 0 || K <= 0 ||
+  if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
     return AURORA_EINVAL;
   if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) return AURORA_EINVAL;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, a, (uint64_t)G * cap, K, BM) || !make_map(&mb, b, (uint64_t)G * N, K, BN))
+  if (!make_map(&ma, a, (uint64_t)map_rows, K, BM) || !make_map(&mb, b, (uint64_t)G * N, K, BN))
     return AURORA_ECUDA;
   static bool attr_set = false;
   if (!attr_set) {
@@ -390,7 +395,7 @@ extern "C" int aurora_grouped_gemm(const void* a, const void* b, void* c, const 
                                    const int32_t* m_rows,
                                    int G, int64_t cap, int N, int K, int epilogue, int num_sms,
                                    void* stream) {
-  return launch_grouped(a, b, c, m_start, m_rows, G, cap, N, K, epilogue, num_sms,
+  return launch_grouped(a, b, c, m_start, m_rows, G, cap, 0, N, K, epilogue, num_sms,
                         (cudaStream_t)stream);
 }
 
@@ -399,10 +404,21 @@ extern "C" int aurora_expert_ffn(const void* a_buf, const void* w13, const void*
                                  int64_t cap, int H,
                                  int F, int num_sms, void* stream) {
   // h = silu(x W1^T) * (x W3^T): N = 2F interleaved, K = H
-  int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 2 * F, H, 1, num_sms,
+  int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 0, 2 * F, H, 1, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
   // y = h W2^T: N = H, K = F
-  return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, H, F, 0, num_sms,
+  return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, 0, H, F, 0, num_sms,
+                        (cudaStream_t)stream);
+}
+
+extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
+                                        void* h_buf, void* y_buf, const int32_t* g_off,
+                                        const int32_t* g_rows, int G, int64_t a_rows, int H, int F,
+                                        int num_sms, void* stream) {
+  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, num_sms,
+                          (cudaStream_t)stream);
+  if (rc != AURORA_OK) return rc;
+  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, num_sms,
                         (cudaStream_t)stream);
 }

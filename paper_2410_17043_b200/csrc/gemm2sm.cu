@@ -247,13 +247,15 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 
 // C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
-                              const int32_t* m_rows, int G, int64_t cap, int N, int K,
-                              int epilogue, int num_sms, cudaStream_t stream) {
-  if (G < 1 || G > MAX_GROUPS || cap < 1 || N % BN || K % BK || N <= 0 || K <= 0 ||
+                              const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
+                              int K, int epilogue, int num_sms, cudaStream_t stream) {
+  if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
+  if (map_rows <= 0) map_rows = (int64_t)G * cap;
+  if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
     return AURORA_EINVAL;
   CUtensorMap ma, mb;
-  if (!make_map_2d(&ma, a, (uint64_t)G * cap, K, HALF) ||
+  if (!make_map_2d(&ma, a, (uint64_t)map_rows, K, HALF) ||
       !make_map_2d(&mb, b, (uint64_t)G * N, K, HALF))
     return AURORA_ECUDA;
   static bool attr_set = false;

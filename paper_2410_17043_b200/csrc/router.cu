@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
     const int32_t* __restrict__ counts, int T, int k, int n, int rank_base, int tokens_per_rank,
     int32_t* __restrict__ send_list, int32_t* __restrict__ pos, int32_t* __restrict__ soff,
     int32_t* __restrict__ roff, int32_t* __restrict__ rtot, int32_t* __restrict__ rloc,
-    int32_t* __restrict__ rrem) {
+    int32_t* __restrict__ rrem, const int32_t* __restrict__ topk_idx,
+    const float* __restrict__ topk_w, const int32_t* __restrict__ local_of_expert,
+    uint8_t* __restrict__ meta, int meta_bytes) {
   __shared__ int base_s[AUR_MAXN];   // entries of earlier tiles of rank i, per destination
   __shared__ int soff_s[AUR_MAXN];   // start of list(i, j) in rank i's send list
   __shared__ int warp0_s[AUR_MAXN];  // entries of warp 0 per destination
@@ -228,7 +230,18 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
       const int j = full[s];
       const int p = base_s[j] + (warp ? warp0_s[j] : 0) + __popc(bal[j] & lt);
       pos[(size_t)t * k + s] = p;
-      if (slot_dst[(size_t)t * k + s] >= 0) list[soff_s[j] + p] = t - i_local * tokens_per_rank;
+      if (slot_dst[(size_t)t * k + s] >= 0) {
+        list[soff_s[j] + p] = t - i_local * tokens_per_rank;
+        if (meta) {  // the row's expert slots on rank j: {local expert, gate weight} or {-1, 0}
+          int2* m = reinterpret_cast<int2*>(meta + ((size_t)i_local * tokens_per_rank * k +
+                                                    soff_s[j] + p) * meta_bytes);
+          for (int q = 0; q < k; q++) {
+            const bool here = full[q] == j;
+            const int e = here ? local_of_expert[topk_idx[(size_t)t * k + q]] : -1;
+            m[q] = make_int2(e, here ? __float_as_int(topk_w[(size_t)t * k + q]) : 0);
+          }
+        }
+      }
     }
   }
 }
@@ -266,13 +279,15 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
 extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts,
                            int T, int k, int n, int rank_base, int tokens_per_rank,
                            int32_t* send_list, int32_t* pos, int32_t* soff, int32_t* roff,
-                           int32_t* rtot, int32_t* rloc, int32_t* rrem, void* stream) {
+                           int32_t* rtot, int32_t* rloc, int32_t* rrem,
+                           const int32_t* topk_idx, const float* topk_w,
+                           const int32_t* local_of_expert, void* meta, void* stream) {
   if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
       T % tokens_per_rank || !soff || !roff || !rtot || !rloc || !rrem)
     return AURORA_EINVAL;
   pack_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
       slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
-      rtot, rloc, rrem);
+      rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -14,12 +14,18 @@ from typing import Callable, Dict, List
 from . import _lib
 
 BUFFERS = ("recv", "ret", "ctr_d", "ctr_c")
+OPTIONAL = ("meta_recv",)  # present when ranks host several experts
+
+
+def _names(layer) -> tuple:
+    return BUFFERS + tuple(b for b in OPTIONAL if getattr(layer, b, None) is not None)
 
 
 def _strides(layer) -> Dict[str, int]:
     """Byte distance between consecutive ranks inside one process's buffer."""
     H = layer.cfg.hidden
-    return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 4, "ctr_c": 4}
+    return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 4, "ctr_c": 4,
+            "meta_recv": layer.cap * layer.meta_bytes}
 
 
 def local_export(layer) -> dict:
@@ -27,7 +33,7 @@ def local_export(layer) -> dict:
     L = _lib.load()
     nb = L.aurora_ipc_handle_bytes()
     out = {"rank_base": layer.rank_base, "n_local": layer.n_local}
-    for name in BUFFERS:
+    for name in _names(layer):
         t = getattr(layer, name)
         h = ctypes.create_string_buffer(nb)
         off = ctypes.c_int64(0)
@@ -41,10 +47,11 @@ def assemble_peer_tables(exports: List[dict], my_process: int, n: int, strides: 
     """Per buffer, the address of every global rank's region as seen from this
     process: local regions from ``local_ptrs``, remote ones through ``opener``
     (CUDA IPC in production; injectable for the CPU tests)."""
-    tables = {name: [0] * n for name in BUFFERS}
+    names = [b for b in BUFFERS + OPTIONAL if b in exports[0]]
+    tables = {name: [0] * n for name in names}
     covered = [False] * n
     for p, ex in enumerate(exports):
-        for name in BUFFERS:
+        for name in names:
             if p == my_process:
                 base = local_ptrs[name]
             else:
@@ -79,7 +86,7 @@ def connect_peers(layer, group=None) -> None:
                    "aurora_ipc_open")
         return int(out.value)
 
-    local = {name: getattr(layer, name).data_ptr() for name in BUFFERS}
+    local = {name: getattr(layer, name).data_ptr() for name in _names(layer)}
     tables = assemble_peer_tables(exports, me, layer.n, _strides(layer), local, opener)
     layer._peers = tables
     layer._tables_for(layer.x, tables)

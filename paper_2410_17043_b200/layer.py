@@ -54,9 +54,8 @@ class MoEConfig:
             raise ValueError("tokens per rank must be a multiple of 64")
         if self.hidden % 256 or self.ffn % 128 or (2 * self.ffn) % 256:
             raise ValueError("hidden must be a multiple of 256 and ffn of 128")
-        if self.experts != self.ranks:
-            raise ValueError("this build hosts one expert per rank (experts == ranks), as the reference's "
-                             "DeploymentPlan does (core.py:246-273)")
+        if self.experts % self.ranks or self.experts > 64:
+            raise ValueError("experts must be a multiple of ranks (contiguous expert blocks per rank), <= 64")
         if not (1 <= self.top_k <= min(8, self.experts)):
             raise ValueError("top_k out of range")
 
@@ -94,9 +93,21 @@ class AuroraMoELayer:
         self.n = n
         self.rank_base = rank_base
         self.n_local = n if n_local is None else n_local
-        self.plan = plan if plan is not None else DeploymentPlan.identity(n)
-        if self.plan.n != cfg.experts:
-            raise ValueError("plan must cover every expert")
+        # experts per rank: 1 = the reference's exclusive deployment (DeploymentPlan,
+        # core.py:253-304); > 1 = contiguous expert blocks e // G
+        self.G = cfg.experts // n
+        if self.G == 1:
+            self.plan = plan if plan is not None else DeploymentPlan.identity(n)
+            if self.plan.n != cfg.experts:
+                raise ValueError("plan must cover every expert")
+            gpu_of = list(self.plan.assignment_a)
+        else:
+            if plan is not None:
+                raise ValueError("a DeploymentPlan places one expert per GPU; with several experts per "
+                                 "rank the experts sit in contiguous blocks")
+            self.plan = None
+            gpu_of = [e // self.G for e in range(cfg.experts)]
+        self.gpu_of = gpu_of
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
         # copy CTAs per rank (two 256-thread CTAs fit per SM; all must be
@@ -112,12 +123,13 @@ class AuroraMoELayer:
 
         # ---- parameters (synthetic, seeded; experts hosted here only)
         if weights is None:
-            weights = self.synthetic_weights(cfg, dev, [self.expert_of_rank(r) for r in self.local_ranks])
+            weights = self.synthetic_weights(cfg, dev, [e for r in self.local_ranks for e in self.experts_of_rank(r)])
         self.w_gate = weights["w_gate"].to(dev, torch.bfloat16).contiguous()
         self.bias = weights["bias"].to(dev, torch.float32).contiguous()
         self.w13 = weights["w13"].to(dev, torch.bfloat16).contiguous()   # [n_local, 2F, H] interleaved
         self.w2 = weights["w2"].to(dev, torch.bfloat16).contiguous()     # [n_local, H, F]
-        self.gpu_of_expert = torch.tensor(self.plan.assignment_a, **i32)
+        self.gpu_of_expert = torch.tensor(gpu_of, **i32)
+        self.local_of_expert = torch.tensor([self.experts_of_rank(g).index(e) for e, g in enumerate(gpu_of)], **i32)
         self.bw = None if bandwidths is None else torch.tensor(np.asarray(bandwidths, float), dtype=torch.float64,
                                                                device=dev)
 
@@ -173,6 +185,26 @@ class AuroraMoELayer:
         self.out = torch.empty(self.T_local, H, **bf)
         self.ctr_d = torch.zeros(n, **i32)
         self.ctr_c = torch.zeros(n, **i32)
+        # several experts per rank: per-row expert metadata travels with the rows, the rows
+        # are grouped by local expert for the GEMM and pre-reduced before the combine
+        self.meta_bytes = ((k * 8 + 15) // 16) * 16
+        if self.G > 1:
+            E_loc = self.n_local * self.G
+            self.meta_send = torch.zeros(self.n_local * Tr * k, self.meta_bytes, dtype=torch.uint8, device=dev)
+            self.meta_recv = torch.zeros(self.n_local * self.cap, self.meta_bytes, dtype=torch.uint8, device=dev)
+            self.max_entries = cfg.tokens * k  # every (token, expert) pair at most once
+            self.g_off = torch.zeros(E_loc + 1, **i32)
+            self.g_rows = torch.zeros(E_loc, **i32)
+            self.g_src = torch.zeros(self.max_entries, **i32)
+            self.inv = torch.empty(self.n_local * self.cap * k, **i32)
+            blocks = (self.n_local * self.cap + 255) // 256
+            self.sort_scratch = torch.empty(blocks * E_loc, **i32)
+            self.a_g = torch.empty(self.max_entries, H, **bf)
+            self.h_g = torch.empty(self.max_entries, F, **bf)
+            self.y_g = torch.empty(self.max_entries, H, **bf)
+            self.overlap = False  # the local/network GEMM split assumes one expert per rank
+        else:
+            self.meta_send = self.meta_recv = None
         self.x = None
         self._tables_for(None)
 
@@ -182,7 +214,12 @@ class AuroraMoELayer:
         return list(range(self.rank_base, self.rank_base + self.n_local))
 
     def expert_of_rank(self, r: int) -> int:
-        return self.plan.assignment_a.index(r)
+        """The single expert on rank r (exclusive deployment)."""
+        return self.gpu_of.index(r)
+
+    def experts_of_rank(self, r: int) -> list:
+        """Experts hosted by rank r, in local-index order."""
+        return [e for e, g in enumerate(self.gpu_of) if g == r]
 
     @staticmethod
     def synthetic_weights(cfg: MoEConfig, dev, experts) -> dict:
@@ -223,6 +260,12 @@ class AuroraMoELayer:
         self.t_ctr_d = self._ptr_table(ctr_d)
         self.t_ctr_c = self._ptr_table(ctr_c)
         self.t_src_c = self._ptr_table([self.ybuf.data_ptr() + r * self.cap * H * esz for r in range(self.n_local)])
+        if self.G > 1:  # second plane: expert metadata beside every dispatched row
+            mb, k = self.meta_bytes, self.cfg.top_k
+            self.t_src2 = self._ptr_table([self.meta_send.data_ptr() + r * Tr * k * mb for r in range(self.n_local)])
+            meta_p = (peers["meta_recv"] if peers is not None else
+                      [self.meta_recv.data_ptr() + r * self.cap * mb for r in range(self.n)])
+            self.t_dst2 = self._ptr_table(meta_p)
         if x is not None:
             self.t_src_d = self._ptr_table([x.data_ptr() + r * Tr * H * esz for r in range(self.n_local)])
             self.x = x
@@ -257,7 +300,10 @@ class AuroraMoELayer:
                                       self.T_local, cfg.top_k, self.n, self.rank_base, cfg.tokens_per_rank,
                                       self.send_list.data_ptr(), self.pos.data_ptr(), self.soff.data_ptr(),
                                       self.roff.data_ptr(), self.rtot.data_ptr(), self.rloc.data_ptr(),
-                                      self.rrem.data_ptr(), stream), "aurora_pack")
+                                      self.rrem.data_ptr(), self.topk_idx.data_ptr(), self.topk_w.data_ptr(),
+                                      self.local_of_expert.data_ptr(),
+                                      None if self.meta_send is None else self.meta_send.data_ptr(), stream),
+                   "aurora_pack")
 
     # engine mode bits (include/aurora_b200.h): 1 combine, 2 system scope, 4 local only, 8 remote only
     def _engine(self, mode: int, stream: int) -> None:
@@ -267,12 +313,15 @@ class AuroraMoELayer:
         dst = self.t_dst_c if combine else self.t_dst_d
         ctr = self.t_ctr_c if combine else self.t_ctr_d
         sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
+        plane2 = self.G > 1 and not combine
         _lib.check(self.L.aurora_engine(
             mode | sys_scope, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.sched_i.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
-            src.data_ptr(), dst.data_ptr(), cfg.hidden * 2, ctr.data_ptr(), self.C, self.P, self.spin_limit,
-            self.engine_status.data_ptr(), stream), "aurora_engine")
+            src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
+            self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
+            self.meta_bytes if plane2 else 0,
+            ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), stream), "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all") -> None:
         self._engine({"all": 0, "local": 4, "remote": 8}[part] | self.unpaced, stream)
@@ -282,6 +331,9 @@ class AuroraMoELayer:
         local rows only (they need no schedule), or the network rows only."""
         cfg = self.cfg
         rb = self.rank_base
+        if self.G > 1:
+            self._experts_grouped(stream)
+            return
         if part == "all":
             m_start, m_rows = 0, self.rtot[rb:].data_ptr()
         elif part == "local":
@@ -293,6 +345,29 @@ class AuroraMoELayer:
                                             self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
                    "aurora_expert_ffn")
 
+    def _experts_grouped(self, stream: int) -> None:
+        """Several experts per rank: group the received rows by local expert,
+        run the packed grouped GEMMs, pre-reduce each row's expert outputs."""
+        cfg = self.cfg
+        L, k, H = self.L, cfg.top_k, cfg.hidden
+        _lib.check(L.aurora_expert_sort(self.meta_recv.data_ptr(), self.cap, self.meta_bytes, self.rtot.data_ptr(),
+                                        self.n_local, self.rank_base, k, self.G, self.g_off.data_ptr(),
+                                        self.g_rows.data_ptr(), self.g_src.data_ptr(), self.inv.data_ptr(),
+                                        self.sort_scratch.data_ptr(), self.sort_scratch.numel(), stream),
+                   "aurora_expert_sort")
+        E_loc = self.n_local * self.G
+        _lib.check(L.aurora_gather_rows(self.recv.data_ptr(), self.a_g.data_ptr(), self.g_src.data_ptr(),
+                                        self.g_off[E_loc:].data_ptr(), self.max_entries, H * 2, stream),
+                   "aurora_gather_rows")
+        _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+                                              self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
+                                              self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
+                                              self.num_sms, stream), "aurora_expert_ffn_packed")
+        _lib.check(L.aurora_expert_reduce(self.y_g.data_ptr(), self.inv.data_ptr(), self.meta_recv.data_ptr(),
+                                          self.cap, self.meta_bytes, self.rtot.data_ptr(), self.n_local,
+                                          self.rank_base, k, H, self.ybuf.data_ptr(), stream),
+                   "aurora_expert_reduce")
+
     def combine(self, stream: int) -> None:
         self._engine(1 | self.unpaced, stream)
 
@@ -301,7 +376,8 @@ class AuroraMoELayer:
         _lib.check(self.L.aurora_aggregate(self.ret.data_ptr(), self.ret_stride, self.soff.data_ptr(),
                                            self.pos.data_ptr(), self.slot_dst.data_ptr(), self.topk_w.data_ptr(),
                                            self.T_local, cfg.top_k, cfg.hidden, self.n, self.rank_base,
-                                           cfg.tokens_per_rank, 0, self.out.data_ptr(), stream), "aurora_aggregate")
+                                           cfg.tokens_per_rank, 1 if self.G > 1 else 0, self.out.data_ptr(),
+                                           stream), "aurora_aggregate")
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor) -> torch.Tensor:

@@ -36,7 +36,7 @@ def _check_layer(torch, cfg, plan=None, out_tol=3e-2):
     assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-5)
     # traffic matrix + token permutation
-    counts, lists, pos = pack_oracle(idx, layer.plan.assignment_a, n)
+    counts, lists, pos = pack_oracle(idx, layer.gpu_of, n)
     assert np.array_equal(layer.counts.cpu().numpy(), counts)
     assert np.array_equal(layer.pos.cpu().numpy(), pos)
     Tr = cfg.tokens_per_rank
@@ -61,7 +61,7 @@ def _check_layer(torch, cfg, plan=None, out_tol=3e-2):
     # combined output vs fp32 oracle
     F = cfg.ffn
     w1, w3 = _deinterleave(layer.w13, F)
-    experts = [layer.expert_of_rank(r) for r in range(n)]
+    experts = [e for r in range(n) for e in layer.experts_of_rank(r)]  # row order of the stacked weights
     order = np.argsort(experts)
     ref = moe_layer_oracle(x.float().cpu().numpy(), idx, layer.topk_w.cpu().numpy(),
                            w1.float().cpu().numpy()[order], w3.float().cpu().numpy()[order],
@@ -130,7 +130,7 @@ def test_layer_c2_full_size(torch):
     n, k = cfg.ranks, cfg.top_k
     _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), k)
     assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
-    counts, lists, pos = pack_oracle(idx, layer.plan.assignment_a, n)
+    counts, lists, pos = pack_oracle(idx, layer.gpu_of, n)
     assert np.array_equal(layer.counts.cpu().numpy(), counts)
     assert np.array_equal(layer.pos.cpu().numpy(), pos)
     d = counts.astype(float)
@@ -199,3 +199,22 @@ def test_layer_heterogeneous_cluster(torch):
     ref = ref_layer(x)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_layer_several_experts_per_rank(torch):
+    """E > n (C5-style): 16 experts top-4 on 4 ranks -- contiguous expert
+    blocks, one network row per (token, rank), expert metadata on the
+    engine's second plane, grouped packed GEMMs, pre-reduction, combine."""
+    _check_layer(torch, MoEConfig_(hidden=256, ffn=256, experts=16, top_k=4, tokens=1024, ranks=4, skew=1.0,
+                                   seed=3))
+
+
+def test_layer_deepseek_shape_small(torch):
+    """64 experts top-6 over 8 ranks (C5 routing), reduced hidden size."""
+    _check_layer(torch, MoEConfig_(hidden=512, ffn=256, experts=64, top_k=6, tokens=2048, ranks=8, skew=1.0,
+                                   seed=4))
+
+
+def MoEConfig_(**kw):
+    from paper_2410_17043_b200.layer import MoEConfig
+    return MoEConfig(**kw)
