@@ -48,15 +48,26 @@ def parse():
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--ranks", type=int, default=8, help="expert-parallel ranks (GPUs of the modelled cluster)")
+    ap.add_argument("--config", default="c2", choices=["c2", "c5"],
+                    help="c2: Mixtral-8x7B layer (the headline); c5: DeepSeek-style 64 experts top-6, "
+                         "hidden 5120, FFN 1536 (DeepSeek-V2 expert size; the config leaves F open)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
+def apply_preset(args):
+    if args.config == "c5":
+        args.hidden, args.ffn, args.experts, args.topk = 5120, 1536, 64, 6
+    return args
+
+
 def workload(args):
-    return {"workload": "C2 Mixtral-8x7B MoE layer (EP over 8 ranks)", "hidden": args.hidden, "ffn": args.ffn,
-            "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.experts,
+    name = ("C2 Mixtral-8x7B MoE layer" if args.config == "c2" else "C5 DeepSeek-style 64-expert top-6 MoE layer")
+    return {"workload": f"{name} (EP over {args.ranks} ranks)", "hidden": args.hidden, "ffn": args.ffn,
+            "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.ranks,
             "skew": args.skew, "seed": args.seed, "gpus": args.gpus,
-            "l2": "inputs larger than L2 (x 128 MiB, expert weights 2.6 GiB read every step)"}
+            "l2": "inputs larger than L2 (x >= 128 MiB, expert weights >= 2.6 GiB read every step)"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -134,7 +145,7 @@ def run_cpu(args, sample_tokens, reps, seed=0):
     import torch
     from oracle.oracle import build_schedule_oracle
     torch.set_num_threads(os.cpu_count() or 1)
-    H, F, E, k, n = args.hidden, args.ffn, args.experts, args.topk, args.experts
+    H, F, E, k, n = args.hidden, args.ffn, args.experts, args.topk, args.ranks
     g = torch.Generator().manual_seed(seed)
     from paper_2410_17043_b200.layer import zipf_bias
     w_gate = (torch.randn(E, H, generator=g) / math.sqrt(H)).to(torch.bfloat16)
@@ -151,7 +162,7 @@ def run_cpu(args, sample_tokens, reps, seed=0):
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        cpu_reference_step(xb, wb, bias, w1, w3, w2, k, n, list(range(E)))
+        cpu_reference_step(xb, wb, bias, w1, w3, w2, k, n, [e // (E // n) for e in range(E)])
         times.append(time.perf_counter() - t0)
     med = sorted(times)[len(times) // 2]
     # the schedule on a full-size (16384-token) traffic matrix: the reference's own hot path
@@ -193,7 +204,7 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------ our arm
 def main():
-    args = parse()
+    args = apply_preset(parse())
     if args.impl == "reference":
         return reference_arm(args)
     import numpy as np
@@ -208,7 +219,7 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    n = args.experts
+    n = args.ranks
     if n % world:
         raise SystemExit(f"{n} ranks do not split over {world} GPUs")
     n_local = n // world
@@ -319,8 +330,11 @@ def main():
 
     # ---- roofline of the dominant kernel (the tcgen05 expert GEMMs) and the all-to-all bound
     counts = layer.counts.cpu().numpy().astype(np.int64)
-    m_local = counts.sum(axis=0)[layer.rank_base:layer.rank_base + n_local]
-    gemm_flops = float(m_local.sum()) * 2 * 3 * cfg.hidden * cfg.ffn
+    if layer.G > 1:  # one GEMM row per (token, expert) pair
+        gemm_rows = float(layer.g_rows.sum().item())
+    else:
+        gemm_rows = float(counts.sum(axis=0)[layer.rank_base:layer.rank_base + n_local].sum())
+    gemm_flops = gemm_rows * 2 * 3 * cfg.hidden * cfg.ffn
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))

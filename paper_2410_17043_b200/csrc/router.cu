@@ -264,11 +264,13 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
                                                     rank_base, tokens_per_rank, topk_idx,        \
                                                     topk_w, slot_dst, blk_cnt, counts)
   switch (E) {
+    // 4 tokens x 8 experts per warp pass: the gate matrix is streamed once per
+    // 4 tokens (E/8 passes), x re-read from L1 between passes
     case 4: LAUNCH(8, 4); break;
-    case 8: LAUNCH(4, 8); break;
-    case 16: LAUNCH(2, 16); break;
-    case 32: LAUNCH(1, 32); break;
-    case 64: LAUNCH(1, 32); break;
+    case 8:
+    case 16:
+    case 32:
+    case 64: LAUNCH(4, 8); break;
     default: return AURORA_EUNSUPPORTED;
   }
 #undef LAUNCH
