@@ -203,6 +203,24 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
+def gemm_traffic(args):
+    """DRAM bytes (read + write) of the expert GEMM launches of one C2 step,
+    from the committed ncu --set full capture; None for other workloads."""
+    if args.config != "c2":
+        return None
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full.json")))["grouped_gemm_2sm_kernel"]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for launch in rec:
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, u = launch[key].split()
+                tot += float(v) * scale[u]
+        return tot
+    except Exception:
+        return None
+
+
 def main():
     args = apply_preset(parse())
     if args.impl == "reference":
@@ -370,10 +388,14 @@ def main():
                          "loopback: all 8 ranks on one GPU, peer stores land in local HBM (not NVLink)",
         },
         "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved_tf / peak_tf, "traffic": None, "kernel": "aurora grouped_gemm_kernel "
-                     "(GEMM1 SwiGLU + GEMM2), FLOPs = sum_e m_e * 2 * 3 * H * F", "peak_source": peak_src,
+                     "frac": achieved_tf / peak_tf, "traffic": gemm_traffic(args),
+                     "traffic_source": "profiles/r01_ncu_full.json (ncu --set full, both GEMM launches, C2)",
+                     "kernel": "aurora grouped_gemm_2sm_kernel (GEMM1 SwiGLU + GEMM2), "
+                     "FLOPs = sum over (token, expert) rows of 2 * 3 * H * F", "peak_source": peak_src,
                      "flops_per_step": gemm_flops},
-        "gpu_launches": 11 * args.steps,  # route, pack, K2, 3 engine, 4 GEMM, aggregate
+        # route, pack, K2, engine, 2 GEMM, engine, aggregate (+ sort x3, gather, reduce with G > 1;
+        # + local engine / GEMM pair when overlapped)
+        "gpu_launches": (8 + (5 if layer.G > 1 else 0) + (3 if layer.overlap else 0)) * args.steps,
         "e2e": {"value": cfg.tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(xh.numel() * 2), "d2h_bytes_per_step": int(outh.numel() * 2),
                 "ms_per_step": e2e_ms, "path": "AuroraMoELayer.__call__ on pinned host buffers"},
