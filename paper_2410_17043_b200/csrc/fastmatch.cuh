@@ -189,3 +189,150 @@ struct FastMatch {
     return true;
   }
 };
+
+// n <= 8 specialisation. Adjacency rows, DFS candidate stacks and BFS layers
+// are bytes of two 32-bit words, matches nibbles of one word, and a
+// byte-per-right-vertex copy of the match (mrb) turns every BFS level into a
+// handful of SWAR operations: reach = OR of the frontier's rows, next =
+// partners of the matched vertices reached. dist[w] == dist[u] + 1 becomes
+// "w is on BFS layer depth+1 and its dfs has not failed" (a vertex on the DFS
+// stack at depth d has BFS distance d).
+struct FastMatch8 {
+  uint32_t pref[2], sup[2];
+  uint32_t ml, mr;
+  uint32_t mrb[2];
+  uint32_t freeL, freeR;
+  uint32_t layer[2];
+  uint32_t alive;
+  uint32_t us, vs;
+  uint32_t left[2];
+
+  AUR_HD static uint32_t getb(const uint32_t (&a)[2], int i) {
+    return ((i < 4 ? a[0] : a[1]) >> ((i & 3) * 8)) & 0xFFu;
+  }
+  AUR_HD static void setb(uint32_t (&a)[2], int i, uint32_t v) {
+    const int sh = (i & 3) * 8;
+    const uint32_t m = 0xFFu << sh;
+    if (i < 4) a[0] = (a[0] & ~m) | (v << sh);
+    else a[1] = (a[1] & ~m) | (v << sh);
+  }
+  AUR_HD static uint32_t getn(uint32_t w, int i) { return (w >> (4 * i)) & 15u; }
+  AUR_HD static void setn(uint32_t& w, int i, uint32_t v) {
+    w = (w & ~(15u << (4 * i))) | (v << (4 * i));
+  }
+  // bit b of a 4-bit value -> 0xFF in byte b
+  AUR_HD static uint32_t spread4(uint32_t b) { return ((b * 0x00204081u) & 0x01010101u) * 0xFFu; }
+  // OR of the bytes of a[] whose index is set in mask
+  AUR_HD static uint32_t gather_or(const uint32_t (&a)[2], uint32_t mask) {
+    uint32_t r = (a[0] & spread4(mask & 15u)) | (a[1] & spread4((mask >> 4) & 15u));
+    r |= r >> 16;
+    r |= r >> 8;
+    return r & 0xFFu;
+  }
+  AUR_HD void match(int u, int v) {
+    setn(ml, u, v);
+    setn(mr, v, u);
+    setb(mrb, v, 1u << u);
+  }
+  AUR_HD void augment_path(int top, int v) {
+    setn(vs, top, v);
+    for (int l = top; l >= 0; l--) match((int)getn(us, l), (int)getn(vs, l));
+    freeL &= ~(1u << getn(us, 0));
+    freeR &= ~(1u << v);
+  }
+  AUR_HD bool hk_dfs(int root) {  // matching.py:57-65
+    int top = 0;
+    setn(us, 0, root);
+    setb(left, 0, getb(pref, root));
+    while (top >= 0) {
+      const uint32_t m = getb(left, top);
+      if (!m) {
+        alive &= ~(1u << getn(us, top));  // dist[u] = _INF
+        top--;
+        continue;
+      }
+      const int v = aur_ffs(m) - 1;
+      setb(left, top, m & (m - 1));
+      if ((freeR >> v) & 1u) {
+        augment_path(top, v);
+        return true;
+      }
+      const int w = (int)getn(mr, v);
+      if (top + 1 < 8 && (((getb(layer, top + 1) & alive) >> w) & 1u)) {
+        setn(vs, top, v);
+        top++;
+        setn(us, top, w);
+        setb(left, top, getb(pref, w));
+      }
+    }
+    return false;
+  }
+  AUR_HD bool kuhn(int root) {  // matching.py:96-106
+    uint32_t seen = 0;
+    int top = 0;
+    setn(us, 0, root);
+    setb(left, 0, getb(sup, root));
+    while (top >= 0) {
+      const uint32_t m = getb(left, top) & ~seen;
+      if (!m) {
+        top--;
+        continue;
+      }
+      const int v = aur_ffs(m) - 1;
+      setb(left, top, m & (m - 1));
+      seen |= 1u << v;
+      if ((freeR >> v) & 1u) {
+        augment_path(top, v);
+        return true;
+      }
+      const int w = (int)getn(mr, v);
+      setn(vs, top, v);
+      top++;
+      setn(us, top, w);
+      setb(left, top, getb(sup, w));
+    }
+    return false;
+  }
+  // pref / sup rows must be zero beyond n
+  AUR_HD bool run(int n) {
+    const uint32_t all = (1u << n) - 1;
+    freeL = freeR = all;
+    ml = mr = 0;
+    mrb[0] = mrb[1] = 0;
+    if (pref[0] | pref[1]) {
+      // first Hopcroft-Karp phase: all left free -> greedy lowest free preferred vertex
+      for (int u = 0; u < n; u++) {
+        const uint32_t m = getb(pref, u) & freeR;
+        if (m) {
+          const int v = aur_ffs(m) - 1;
+          match(u, v);
+          freeL &= ~(1u << u);
+          freeR &= ~(1u << v);
+        }
+      }
+      for (;;) {
+        layer[0] = layer[1] = 0;
+        uint32_t frontier = freeL, visited = freeL;
+        setb(layer, 0, frontier);
+        bool found = false;
+        int level = 0;
+        while (frontier) {  // bfs(), matching.py:37-55, one SWAR step per level
+          const uint32_t reach = gather_or(pref, frontier);
+          found |= (reach & freeR) != 0;
+          const uint32_t nxt = gather_or(mrb, reach & ~freeR) & ~visited;
+          visited |= nxt;
+          level++;
+          if (level < 8) setb(layer, level, nxt);
+          frontier = nxt;
+        }
+        if (!found) break;
+        alive = all;
+        for (int u = 0; u < n; u++)
+          if ((freeL >> u) & 1u) hk_dfs(u);
+      }
+    }
+    for (int u = 0; u < n; u++)
+      if (((freeL >> u) & 1u) && !kuhn(u)) return false;
+    return true;
+  }
+};

@@ -281,24 +281,51 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
     }
     if (!__any_sync(0xffffffffu, on && anyrow)) break;
     if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
-    if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
-    __syncwarp();
-    t1 = clock64();
-    if (lane == 0) {
-#pragma unroll
-      for (int u = 0; u < NB; u++) {
-        fm.pref.set(u, u < n ? pref_s[u] : 0);
-        fm.sup.set(u, u < n ? sup_s[u] : 0);
+    int pj;
+    if constexpr (NB == 8) {
+      // rows -> lane 0 as bytes of two words (warp OR-reductions), the
+      // permutation back as nibbles of one word (one shuffle)
+      t1 = clock64();
+      const uint32_t sh = 8u * (lane & 3);
+      const uint32_t p0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? pref << sh : 0u);
+      const uint32_t p1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? pref << sh : 0u);
+      const uint32_t s0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? sup << sh : 0u);
+      const uint32_t s1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? sup << sh : 0u);
+      uint32_t mlw = 0, ok = 0;
+      if (lane == 0) {
+        FastMatch8 f8;
+        f8.pref[0] = p0;
+        f8.pref[1] = p1;
+        f8.sup[0] = s0;
+        f8.sup[1] = s1;
+        ok = f8.run(n) ? 1u : 0u;
+        mlw = f8.ml;
       }
-      const bool ok = fm.run(n);
-      perm_s[0] = ok ? 1 : 0;
+      mlw = __shfl_sync(0xffffffffu, mlw, 0);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) { status = AURORA_ENOMATCH; break; }
+      t2 = clock64();
+      pj = on ? (int)((mlw >> (4 * lane)) & 15u) : 0;
+    } else {
+      if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
+      __syncwarp();
+      t1 = clock64();
+      if (lane == 0) {
 #pragma unroll
-      for (int u = 0; u < NB; u++) perm_s[1 + u] = (int)fm.ml.get(u);
+        for (int u = 0; u < NB; u++) {
+          fm.pref.set(u, u < n ? pref_s[u] : 0);
+          fm.sup.set(u, u < n ? sup_s[u] : 0);
+        }
+        const bool ok = fm.run(n);
+        perm_s[0] = ok ? 1 : 0;
+#pragma unroll
+        for (int u = 0; u < NB; u++) perm_s[1 + u] = (int)fm.ml.get(u);
+      }
+      __syncwarp();
+      if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
+      t2 = clock64();
+      pj = on ? perm_s[1 + lane] : 0;
     }
-    __syncwarp();
-    if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
-    t2 = clock64();
-    const int pj = on ? perm_s[1 + lane] : 0;
     const V dur = Dom<V>::warp_min(on ? row_pick<NB, V>(rem, pj) : INF);
     if (on) {
       row_put<NB, V>(rem, pj, row_pick<NB, V>(rem, pj) - dur);

@@ -44,9 +44,42 @@ static int check(std::mt19937& rng, int iters) {
   return bad;
 }
 
+static int check8(std::mt19937& rng, int iters) {
+  int bad = 0;
+  for (int it = 0; it < iters; it++) {
+    const int n = 1 + (int)(rng() % 8);
+    uint32_t sup[32], pref[32];
+    const double ps = 0.2 + 0.8 * (rng() % 1000) / 1000.0, pp = (rng() % 1000) / 1000.0;
+    for (int i = 0; i < n; i++) {
+      sup[i] = pref[i] = 0;
+      for (int j = 0; j < n; j++)
+        if ((rng() % 1000) / 1000.0 < ps) {
+          sup[i] |= 1u << j;
+          if ((rng() % 1000) / 1000.0 < pp) pref[i] |= 1u << j;
+        }
+    }
+    if (it % 3 == 0)
+      for (int i = 0; i < n; i++) sup[i] |= 1u << ((i + it) % n);
+    int ref[32];
+    const int ok_ref = oracle_perfect_matching_masks(n, sup, pref, ref);
+    FastMatch8 fm;
+    fm.pref[0] = fm.pref[1] = fm.sup[0] = fm.sup[1] = 0;
+    for (int u = 0; u < n; u++) {
+      FastMatch8::setb(fm.pref, u, pref[u]);
+      FastMatch8::setb(fm.sup, u, sup[u]);
+    }
+    const bool ok = fm.run(n);
+    bool same = ok == (bool)ok_ref;
+    if (same && ok)
+      for (int u = 0; u < n; u++) same &= (int)FastMatch8::getn(fm.ml, u) == ref[u];
+    if (!same && bad++ < 5) std::printf("mismatch FastMatch8 n=%d ok=%d/%d\n", n, (int)ok, ok_ref);
+  }
+  return bad;
+}
+
 int main() {
   std::mt19937 rng(12345);
-  int bad = check<8>(rng, 200000) + check<16>(rng, 100000);
+  int bad = check<8>(rng, 200000) + check<16>(rng, 100000) + check8(rng, 300000);
   std::printf("fastmatch mismatches: %d\n", bad);
   return bad != 0;
 }
