@@ -1,0 +1,98 @@
+"""Two MoE models colocated on the same GPUs per Aurora's colocation plan (config C3).
+
+Aurora pairs one expert of model a with one expert (slot) of model b on every
+GPU so that the combined per-GPU send/receive volume is balanced
+(``colocate_homogeneous``, reference placement.py:109-126; the combined matrix
+is ``combine_colocated``, core.py:348-367). Model b here has twice as many
+experts as there are GPUs, so its experts are first grouped into GPU "slots"
+of two with the reference's same-model pairing (``colocate_same_model``,
+baselines.py:126-137: most loaded with least loaded), and the slots are what
+gets paired with model a -- the policy SURVEY.md §7 hard part 7 lays out.
+
+Execution: each model runs its own :class:`~paper_2410_17043_b200.layer.AuroraMoELayer`
+over the same ranks -- model a with one expert per rank, model b with its two
+experts per rank as placed by the plan -- so the experts of both models that
+share a GPU run as that GPU's tcgen05 grouped GEMMs.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .commsched import bmax_heterogeneous
+from .core import DeploymentPlan, LayerProfile, TrafficMatrix, combine_colocated
+from .placement import colocate_homogeneous
+
+__all__ = ["lina_slots", "ColocationPlan", "plan_colocation", "combined_bmax", "ColocatedLayers"]
+
+
+def lina_slots(expert_loads) -> tuple:
+    """Pair a model's most loaded expert with its least loaded one (baselines.py:126-137).
+
+    Returns ``((e_hi, e_lo), ...)`` in slot order; ties resolve to the lower index
+    (stable sort on -load)."""
+    loads = np.asarray(expert_loads, dtype=float)
+    E = loads.shape[0]
+    if E % 2:
+        raise ValueError(f"same-model pairing needs an even expert count, got {E}")
+    order = np.argsort(-loads, kind="stable")
+    return tuple((int(order[k]), int(order[E - 1 - k])) for k in range(E // 2))
+
+
+def _profile(counts) -> LayerProfile:
+    return LayerProfile(0.0, 0.0, 0.0, 0.0, TrafficMatrix(np.asarray(counts, dtype=float)))
+
+
+@dataclass(frozen=True)
+class ColocationPlan:
+    plan: DeploymentPlan     # model a expert i on GPU assignment_a[i]; model-b slot s on assignment_b[s]
+    slots: tuple             # model-b expert pairs, one slot per GPU
+    gpu_of_a: tuple          # rank of every model-a expert
+    gpu_of_b: tuple          # rank of every model-b expert
+
+    @property
+    def n(self) -> int:
+        return self.plan.n
+
+
+def plan_colocation(counts_a, slot_counts_b, slots) -> ColocationPlan:
+    """``counts_a``: model a's GPU x GPU matrix with expert i on rank i;
+    ``slot_counts_b``: model b's matrix with slot s on rank s (both from a
+    calibration pass). Aurora's pairing (placement.py:109-126), model a on
+    identity GPUs (DeploymentPlan.from_pairing, core.py:279-287)."""
+    plan = colocate_homogeneous(_profile(counts_a), _profile(slot_counts_b))
+    gpu_of_b = [0] * (2 * len(slots))
+    for s, (e1, e2) in enumerate(slots):
+        gpu_of_b[e1] = gpu_of_b[e2] = plan.assignment_b[s]
+    return ColocationPlan(plan, tuple(slots), tuple(plan.assignment_a), tuple(gpu_of_b))
+
+
+def combined_bmax(counts_a, slot_counts_b, plan: DeploymentPlan) -> float:
+    """b_max of both models' traffic under the plan (the colocated all-to-all bound,
+    experiment.py:172-179)."""
+    comb = combine_colocated(TrafficMatrix(np.asarray(counts_a, float)),
+                             TrafficMatrix(np.asarray(slot_counts_b, float)), plan)
+    return bmax_heterogeneous(comb.entries)
+
+
+class ColocatedLayers:
+    """Model a (one expert per rank) and model b (two experts per rank) on the
+    same ranks, placed by a :class:`ColocationPlan`."""
+
+    def __init__(self, cfg_a, cfg_b, cplan: ColocationPlan, **kw):
+        from .layer import AuroraMoELayer
+        if cfg_a.ranks != cfg_b.ranks or cfg_b.experts != 2 * cfg_a.ranks or cfg_a.experts != cfg_a.ranks:
+            raise ValueError("expects model a with one expert per rank and model b with two")
+        self.cplan = cplan
+        self.a = AuroraMoELayer(cfg_a, DeploymentPlan(cplan.gpu_of_a), **kw)
+        self.b = AuroraMoELayer(cfg_b, None, gpu_of_expert=cplan.gpu_of_b, **kw)
+
+    def forward(self, x_a, x_b):
+        return self.a(x_a), self.b(x_b)
+
+    __call__ = forward
+
+    def check_status(self) -> None:
+        self.a.check_status()
+        self.b.check_status()

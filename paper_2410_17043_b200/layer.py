@@ -84,7 +84,7 @@ class AuroraMoELayer:
 
     def __init__(self, cfg: MoEConfig, plan: Optional[DeploymentPlan] = None, *, rank_base: int = 0,
                  n_local: Optional[int] = None, bandwidths=None, device=None, ctas_per_rank: Optional[int] = None,
-                 weights: Optional[dict] = None, spin_limit: int = 1 << 26):
+                 weights: Optional[dict] = None, spin_limit: int = 1 << 26, gpu_of_expert=None):
         cfg.validate()
         self.cfg = cfg
         self.L = _lib.load()
@@ -96,7 +96,12 @@ class AuroraMoELayer:
         # experts per rank: 1 = the reference's exclusive deployment (DeploymentPlan,
         # core.py:253-304); > 1 = contiguous expert blocks e // G
         self.G = cfg.experts // n
-        if self.G == 1:
+        if gpu_of_expert is not None:  # explicit placement (e.g. a colocation plan, colocation.py)
+            gpu_of = [int(g) for g in gpu_of_expert]
+            if len(gpu_of) != cfg.experts or sorted(gpu_of) != sorted(r for r in range(n) for _ in range(self.G)):
+                raise ValueError(f"gpu_of_expert must place exactly {self.G} expert(s) on each of {n} ranks")
+            self.plan = DeploymentPlan(tuple(gpu_of)) if self.G == 1 else None
+        elif self.G == 1:
             self.plan = plan if plan is not None else DeploymentPlan.identity(n)
             if self.plan.n != cfg.experts:
                 raise ValueError("plan must cover every expert")
@@ -104,7 +109,7 @@ class AuroraMoELayer:
         else:
             if plan is not None:
                 raise ValueError("a DeploymentPlan places one expert per GPU; with several experts per "
-                                 "rank the experts sit in contiguous blocks")
+                                 "rank pass gpu_of_expert (default: contiguous blocks)")
             self.plan = None
             gpu_of = [e // self.G for e in range(cfg.experts)]
         self.gpu_of = gpu_of

@@ -101,3 +101,24 @@ def test_reversed_and_validator_on_golden_schedules():
     bad = A.CommSchedule(3, (A.Phase(((0, 2), (1, 2)), 1.0),), 1.0)
     rep = A.validate_schedule(bad, A.TrafficMatrix([[0, 0, 1], [0, 0, 1], [0, 0, 0]]), A.ClusterSpec.uniform(3))
     assert not rep.contention_ok and not rep.optimal
+
+
+def test_lina_slots_spec_example():
+    """SPEC.md:444 (baselines.py:126-137): loads [8, 6, 2, 1] -> pairs (8,1), (6,2)."""
+    from paper_2410_17043_b200.colocation import lina_slots
+    assert lina_slots([8, 6, 2, 1]) == ((0, 3), (1, 2))
+    assert lina_slots([1, 1, 1, 1]) == ((0, 3), (1, 2))
+    with pytest.raises(ValueError):
+        lina_slots([1, 2, 3])
+
+
+@pytest.mark.reference
+def test_lina_slots_vs_reference(moeplan):
+    from paper_2410_17043_b200.colocation import lina_slots
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        n = int(rng.choice([2, 4, 6, 8, 16]))
+        d = rng.integers(0, 20, size=(n, n)).astype(float)
+        prof = moeplan.LayerProfile(0, 0, 0, 0, moeplan.TrafficMatrix(d))
+        ref = moeplan.colocate_same_model(prof)
+        assert lina_slots(moeplan.TrafficMatrix(d).col_sums()) == ref

@@ -218,3 +218,49 @@ def test_layer_deepseek_shape_small(torch):
 def MoEConfig_(**kw):
     from paper_2410_17043_b200.layer import MoEConfig
     return MoEConfig(**kw)
+
+
+def test_colocated_models(torch):
+    """C3: model a (4 experts) and model b (8 experts) on 4 ranks. Calibration
+    routing -> Lina slots for model b -> Aurora's colocate_homogeneous pairing
+    -> both layers on the same ranks (model-b experts placed by the plan);
+    each layer bit-exact / within tolerance vs the oracle."""
+    from oracle.oracle import bf16_bits, pack_oracle, router_oracle
+    import paper_2410_17043_b200 as A
+    from paper_2410_17043_b200.colocation import (ColocatedLayers, combined_bmax, lina_slots,
+                                                  plan_colocation)
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg_a = MoEConfig(hidden=256, ffn=256, experts=4, top_k=2, tokens=1024, ranks=4, skew=1.0, seed=5)
+    cfg_b = MoEConfig(hidden=256, ffn=128, experts=8, top_k=2, tokens=1024, ranks=4, skew=1.5, seed=6)
+    xa = torch.randn(cfg_a.tokens, cfg_a.hidden, device="cuda").to(torch.bfloat16)
+    xb = torch.randn(cfg_b.tokens, cfg_b.hidden, device="cuda").to(torch.bfloat16)
+    cal_a = AuroraMoELayer(cfg_a)
+    cal_a(xa)
+    cal_b = AuroraMoELayer(cfg_b)
+    cal_b(xb)
+    torch.cuda.synchronize()
+    loads_b = np.bincount(cal_b.topk_idx.cpu().numpy().ravel(), minlength=8)
+    slots = lina_slots(loads_b)
+    slot_of = {e: s for s, pair in enumerate(slots) for e in pair}
+    _, idx_b, _ = router_oracle(bf16_bits(xb), bf16_bits(cal_b.w_gate), cal_b.bias.cpu().numpy(), 2)
+    slot_counts, _, _ = pack_oracle(idx_b, [slot_of[e] for e in range(8)], 4)
+    cp = plan_colocation(cal_a.counts.cpu().numpy(), slot_counts, slots)
+    assert sorted(cp.gpu_of_b) == [0, 0, 1, 1, 2, 2, 3, 3]
+    pair = ColocatedLayers(cfg_a, cfg_b, cp)
+    out_a, out_b = pair(xa, xb)
+    torch.cuda.synchronize()
+    pair.check_status()
+    from oracle.oracle import moe_layer_oracle
+    for layer, x, out in ((pair.a, xa, out_a), (pair.b, xb, out_b)):
+        _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), 2)
+        assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
+        counts, _, _ = pack_oracle(idx, layer.gpu_of, 4)
+        assert np.array_equal(layer.counts.cpu().numpy(), counts)
+        F = layer.cfg.ffn
+        w1, w3 = _deinterleave(layer.w13, F)
+        order = np.argsort([e for r in range(4) for e in layer.experts_of_rank(r)])
+        ref = moe_layer_oracle(x.float().cpu().numpy(), idx, layer.topk_w.cpu().numpy(),
+                               w1.float().cpu().numpy()[order], w3.float().cpu().numpy()[order],
+                               layer.w2.float().cpu().numpy()[order])
+        assert np.abs(out.float().cpu().numpy() - ref).max() <= 3e-2 * np.abs(ref).max()
+    assert combined_bmax(cal_a.counts.cpu().numpy(), slot_counts, cp.plan) > 0
