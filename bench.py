@@ -203,6 +203,43 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
+def baseline_schedules(layer, x, sp, stream, reps=3):
+    """SURVEY 8(f)3 / PAPER.md:747: the paper's SJF and RCS schedules of the same
+    traffic matrix, executed by the same engine (host-built tables)."""
+    import numpy as np
+    import torch
+    from paper_2410_17043_b200 import baselines as B
+    from paper_2410_17043_b200.core import ClusterSpec, TrafficMatrix
+    d = layer.counts.cpu().numpy().astype(float)
+    np.fill_diagonal(d, 0)
+    tm, cl = TrafficMatrix(d), ClusterSpec.uniform(layer.n)
+    out = {}
+    for name, sched in (("sjf", B.schedule_sjf(tm, cl)), ("rcs", B.schedule_rcs(tm, cl, 0))):
+        if len(sched.phases) > layer.P:
+            continue
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        disp = comb = 0.0
+        for _ in range(reps):
+            layer.route(x, sp)
+            layer.pack(sp)
+            layer.load_schedule(sched)
+            ev[0].record(stream)
+            layer.dispatch(sp)
+            ev[1].record(stream)
+            layer.experts(sp)
+            ev[2].record(stream)
+            layer.combine(sp)
+            ev[3].record(stream)
+            layer.aggregate(sp)
+            torch.cuda.synchronize()
+            disp += ev[0].elapsed_time(ev[1])
+            comb += ev[2].elapsed_time(ev[3])
+        layer.check_status()
+        out[name] = {"dispatch_us": disp / reps * 1e3, "combine_us": comb / reps * 1e3,
+                     "makespan_tokens": sched.makespan, "phases": len(sched.phases)}
+    return out
+
+
 def gemm_traffic(args):
     """DRAM bytes (read + write) of the expert GEMM launches of one C2 step,
     from the committed ncu --set full capture; None for other workloads."""
@@ -320,6 +357,7 @@ def main():
     layer.check_status()
     layer.unpaced = 0
     unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
+    baseline_sched = baseline_schedules(layer, x, sp, stream) if world == 1 else {}
 
     # ---- end to end through the public API with host buffers (pinned), copies timed
     xh = x.cpu().pin_memory()
@@ -381,6 +419,7 @@ def main():
             "schedule_us": stage_ms["schedule"] * 1e3,
             "unscheduled_dispatch_us": unpaced_ms["dispatch"] * 1e3,
             "unscheduled_combine_us": unpaced_ms["combine"] * 1e3,
+            "baseline_schedules_on_engine": baseline_sched,
             "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
             "bound_basis": "b_max x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",

@@ -1,0 +1,121 @@
+"""Receiver-serialised baseline schedules (the paper's SJF / RCS comparison,
+PAPER.md:747) as CommSchedules the B200 engine can execute.
+
+Mirrors ``moeplan.baselines`` (reference ``pkg/src/moeplan/baselines.py``):
+
+* ``schedule_fixed_order``  baselines.py:29-74  each sender walks its own destination
+  order; a busy receiver makes later arrivals wait (earliest start, then
+  earliest arrival, then lowest sender first)
+* ``schedule_rcs``          baselines.py:91-99  random destination order per sender
+* ``schedule_sjf``          baselines.py:102-109 smallest volume first
+
+``to_engine_tables`` turns any CommSchedule with whole-token durations into the
+engine's chunk tables, so Aurora's schedule, these baselines and the unpaced
+mode run on the same copy engine. Host-side: these are
+offline comparison plans, not the per-batch path.
+"""
+from __future__ import annotations
+
+import math
+from typing import Sequence
+
+import numpy as np
+
+from .commsched import CommSchedule, Phase, time_normalize_entries
+
+__all__ = ["schedule_fixed_order", "schedule_rcs", "schedule_sjf", "to_engine_tables"]
+
+
+def schedule_fixed_order(d, cluster, orders: Sequence[Sequence[int]]) -> CommSchedule:
+    t = time_normalize_entries(d, cluster)
+    n = t.shape[0]
+    pending = []
+    for i, order in enumerate(orders):
+        listed = set(int(j) for j in order)
+        if any(int(j) not in listed for j in np.flatnonzero(t[i] > 0)):
+            raise ValueError(f"order for sender {i} misses destinations with demand")
+        pending.append([(int(j), float(t[i, j])) for j in order if t[i, j] > 0])
+    sender_free = [0.0] * n
+    receiver_free = [0.0] * n
+    busy = []  # (start, end, sender, receiver)
+    left = sum(len(q) for q in pending)
+    while left:
+        pick = None
+        for i in range(n):
+            if not pending[i]:
+                continue
+            j, dur = pending[i][0]
+            arrival = sender_free[i]
+            key = (max(arrival, receiver_free[j]), arrival, i)
+            if pick is None or key < pick[0]:
+                pick = (key, i, j, dur)
+        (start, _, _), i, j, dur = pick
+        end = start + dur
+        busy.append((start, end, i, j))
+        sender_free[i] = receiver_free[j] = end
+        pending[i].pop(0)
+        left -= 1
+    if not busy:
+        return CommSchedule(n, (), 0.0)
+    edges = sorted({x for s, e, _, _ in busy for x in (s, e)})
+    phases = []
+    for a, b in zip(edges, edges[1:]):
+        if b - a <= 0:
+            continue
+        active = tuple(sorted((i, j) for s, e, i, j in busy if s <= a and e >= b))
+        phases.append(Phase(active, b - a))
+    return CommSchedule(n, tuple(phases), math.fsum(p.duration for p in phases))
+
+
+def schedule_rcs(d, cluster, seed: int) -> CommSchedule:
+    rng = np.random.default_rng(seed)
+    orders = []
+    for i in range(d.n):
+        dests = list(np.nonzero(np.asarray(d.entries)[i] > 0)[0])
+        rng.shuffle(dests)
+        orders.append([int(j) for j in dests])
+    return schedule_fixed_order(d, cluster, orders)
+
+
+def schedule_sjf(d, cluster) -> CommSchedule:
+    e = np.asarray(d.entries)
+    orders = [[int(j) for j in sorted(np.nonzero(e[i] > 0)[0], key=lambda j: (e[i, j], j))] for i in range(d.n)]
+    return schedule_fixed_order(d, cluster, orders)
+
+
+def to_engine_tables(sched: CommSchedule, n: int):
+    """CommSchedule (token-unit durations) -> (chunks[P,n,4], rchunks[P,n,4],
+    n_in[n], n_out[n]) in the engine's format (include/aurora_b200.h): per phase
+    and sender {receiver, first token, count, arrival index}; same-pair runs that
+    are consecutive for both ends form one chunk."""
+    P = max(1, len(sched.phases))
+    ch = np.full((P, n, 4), 0, dtype=np.int32)
+    ch[:, :, 0] = -1
+    rch = ch.copy()
+    issued = np.zeros((n, n), dtype=np.int64)
+    cum = np.zeros((n, n))
+    rcnt = np.zeros(n, dtype=np.int32)
+    sseq = np.zeros(n, dtype=np.int32)
+    last_j, last_k, last_from = [-1] * n, [-1] * n, [-1] * n
+    for k, ph in enumerate(sched.phases):
+        opened = []
+        for i, j in ph.transfers:
+            cum[i, j] += ph.duration
+            tok = int(round(cum[i, j])) - int(issued[i, j])
+            start = int(issued[i, j])
+            issued[i, j] += tok
+            if last_j[i] == j and last_from[j] == i:
+                kk = last_k[i]
+                ch[kk, i, 2] += tok
+                rch[kk, j, 2] += tok
+            else:
+                ch[k, i] = (j, start, tok, rcnt[j])
+                rch[k, j] = (i, start, tok, sseq[i])
+                sseq[i] += 1
+                last_j[i], last_k[i] = j, k
+                opened.append(j)
+        for i, j in ph.transfers:
+            last_from[j] = i
+        for j in opened:
+            rcnt[j] += 1
+    return ch, rch, rcnt, sseq

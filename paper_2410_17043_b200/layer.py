@@ -474,6 +474,21 @@ class AuroraMoELayer:
         if es != 0:
             raise RuntimeError(f"engine status {es} (timeout)")
 
+    def load_schedule(self, sched) -> None:
+        """Replace this batch's engine tables with an arbitrary CommSchedule in
+        token units (e.g. baselines.schedule_sjf of the same counts) -- the
+        schedule ablation of SURVEY 8(f)3. Host -> device copy; diagnostics only."""
+        from .baselines import to_engine_tables
+        ch, rch, n_in, n_out = to_engine_tables(sched, self.n)
+        if ch.shape[0] > self.P:
+            raise ValueError(f"{ch.shape[0]} phases exceed the table capacity {self.P}")
+        P = ch.shape[0]
+        self.chunks[:P].copy_(torch.from_numpy(ch))
+        self.rchunks[:P].copy_(torch.from_numpy(rch))
+        self.n_in.copy_(torch.from_numpy(n_in))
+        self.n_out.copy_(torch.from_numpy(n_out))
+        self.sched_i[0] = len(sched.phases)
+
     def schedule_objects(self):
         """The current batch's schedule as reference-shaped CommSchedule (debug / drop-in parity)."""
         from .commsched import CommSchedule, Phase

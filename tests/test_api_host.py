@@ -122,3 +122,36 @@ def test_lina_slots_vs_reference(moeplan):
         prof = moeplan.LayerProfile(0, 0, 0, 0, moeplan.TrafficMatrix(d))
         ref = moeplan.colocate_same_model(prof)
         assert lina_slots(moeplan.TrafficMatrix(d).col_sums()) == ref
+
+
+def test_baseline_schedules_fig4_and_tables():
+    from paper_2410_17043_b200 import baselines as B
+    fig4 = A.TrafficMatrix([[0, 1, 1], [1, 0, 1], [0, 0, 0]])
+    c3 = A.ClusterSpec.uniform(3)
+    naive = B.schedule_fixed_order(fig4, c3, [[1, 2], [0, 2], []])
+    assert naive.makespan == spec_examples()["fig4_naive_makespan"] == 3.0
+    assert A.validate_schedule(naive, fig4, c3).contention_ok
+    ch, rch, n_in, n_out = B.to_engine_tables(naive, 3)
+    tot = np.zeros((3, 3))
+    for row in ch:
+        for i, (j, first, cnt, seq) in enumerate(row):
+            if j >= 0:
+                tot[i, j] += cnt
+    assert tot.tolist() == fig4.entries.tolist()
+    assert n_in.sum() == n_out.sum()
+
+
+@pytest.mark.reference
+def test_baseline_schedules_vs_reference(moeplan):
+    from paper_2410_17043_b200 import baselines as B
+    rng = np.random.default_rng(11)
+    for it in range(60):
+        n = int(rng.choice([2, 3, 4, 6, 8]))
+        d = (rng.integers(0, 30, size=(n, n)) * (rng.random((n, n)) < 0.7)).astype(float)
+        cl_ref = moeplan.ClusterSpec.uniform(n)
+        tm_ref = moeplan.TrafficMatrix(d)
+        cl, tm = A.ClusterSpec.uniform(n), A.TrafficMatrix(d)
+        for ref, got in ((moeplan.schedule_sjf(tm_ref, cl_ref), B.schedule_sjf(tm, cl)),
+                         (moeplan.schedule_rcs(tm_ref, cl_ref, it), B.schedule_rcs(tm, cl, it))):
+            assert [(p.transfers, p.duration) for p in ref.phases] == [(p.transfers, p.duration) for p in got.phases]
+            assert ref.makespan == got.makespan

@@ -264,3 +264,31 @@ def test_colocated_models(torch):
                                layer.w2.float().cpu().numpy()[order])
         assert np.abs(out.float().cpu().numpy() - ref).max() <= 3e-2 * np.abs(ref).max()
     assert combined_bmax(cal_a.counts.cpu().numpy(), slot_counts, cp.plan) > 0
+
+
+def test_engine_runs_baseline_schedules(torch):
+    """SJF / RCS schedules (baselines.py) executed by the same engine deliver
+    the same rows: identical layer output to the Aurora-scheduled run."""
+    import paper_2410_17043_b200 as A
+    from paper_2410_17043_b200 import baselines as B
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=8, top_k=2, tokens=2048, ranks=8, skew=1.0, seed=8)
+    layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = layer(x).clone()
+    torch.cuda.synchronize()
+    d = layer.counts.cpu().numpy().astype(float)
+    np.fill_diagonal(d, 0)
+    tm, cl = A.TrafficMatrix(d), A.ClusterSpec.uniform(8)
+    for sched in (B.schedule_sjf(tm, cl), B.schedule_rcs(tm, cl, 0)):
+        s = torch.cuda.current_stream().cuda_stream
+        layer.route(x, s)
+        layer.pack(s)
+        layer.load_schedule(sched)
+        layer.dispatch(s)
+        layer.experts(s)
+        layer.combine(s)
+        layer.aggregate(s)
+        torch.cuda.synchronize()
+        layer.check_status()
+        assert torch.equal(layer.out, ref)
