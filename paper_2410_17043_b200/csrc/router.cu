@@ -38,7 +38,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const int4& v, float* f) {
 template <int TG, int EP>
 __device__ __forceinline__ float warp_logits(const int4* __restrict__ xrow[TG],
                                              const int4* __restrict__ wrow, int h_chunks, int lane,
-                                             int hv) {
+                                             int hv, int e_valid) {
   static_assert(TG * EP == 32, "tile");
   float acc[TG][EP];
 #pragma unroll
@@ -55,7 +55,8 @@ __device__ __forceinline__ float warp_logits(const int4* __restrict__ xrow[TG],
     }
 #pragma unroll
     for (int e = 0; e < EP; e++) {
-      int4 wv = __ldg(wrow + (size_t)e * hv + c);
+      // experts past the last one of this pass re-read a valid row; their sums are dropped
+      int4 wv = __ldg(wrow + (size_t)min(e, e_valid - 1) * hv + c);
       float wf[8];
       bf16x8_to_f32(wv, wf);
 #pragma unroll
@@ -108,9 +109,9 @@ __global__ void __launch_bounds__(WARPS * 32) route_kernel(
     }
     for (int e0 = 0; e0 < E; e0 += EP) {
       const int4* wrow = reinterpret_cast<const int4*>(wg + (size_t)e0 * H);
-      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv);
+      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv, min(EP, E - e0));
       const int tq = lane / EP, eq = e0 + lane % EP;
-      logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
+      if (eq < E) logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
     }
   }
   __syncthreads();
@@ -263,16 +264,13 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
   route_kernel<TG, EP><<<blocks, WARPS * 32, 0, s>>>(xb, wb, bias, T, H, E, k, gpu_of_expert, n, \
                                                     rank_base, tokens_per_rank, topk_idx,        \
                                                     topk_w, slot_dst, blk_cnt, counts)
-  switch (E) {
-    // 4 tokens x 8 experts per warp pass: the gate matrix is streamed once per
-    // 4 tokens (E/8 passes), x re-read from L1 between passes
-    case 4: LAUNCH(8, 4); break;
-    case 8:
-    case 16:
-    case 32:
-    case 64: LAUNCH(4, 8); break;
-    default: return AURORA_EUNSUPPORTED;
-  }
+  // 4 tokens x 8 experts per warp pass: the gate matrix is streamed once per
+  // 4 tokens (ceil(E/8) passes), x re-read from L1 between passes; E <= 4 in one pass
+  if (E < 1 || E > MAXE) return AURORA_EUNSUPPORTED;
+  if (E <= 4)
+    LAUNCH(8, 4);
+  else
+    LAUNCH(4, 8);
 #undef LAUNCH
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

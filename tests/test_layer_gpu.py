@@ -292,3 +292,17 @@ def test_engine_runs_baseline_schedules(torch):
         torch.cuda.synchronize()
         layer.check_status()
         assert torch.equal(layer.out, ref)
+
+
+@pytest.mark.parametrize("shape", [
+    dict(experts=1, top_k=1, ranks=1, tokens=256),           # one rank: no all-to-all, empty schedule
+    dict(experts=2, top_k=1, ranks=2, tokens=512),
+    dict(experts=6, top_k=2, ranks=2, tokens=512),           # E not a power of two, 3 experts per rank
+    dict(experts=8, top_k=2, ranks=8, tokens=2048, skew=30.0),  # nearly every token to two experts
+    dict(experts=4, top_k=4, ranks=4, tokens=1024),          # every token to every rank
+])
+def test_layer_edge_shapes(torch, shape):
+    from paper_2410_17043_b200.layer import MoEConfig
+    kw = dict(hidden=256, ffn=128, skew=1.0, seed=7)
+    kw.update(shape)
+    _check_layer(torch, MoEConfig(**kw))
