@@ -63,21 +63,35 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
 /* aurora_schedule_counts: the in-layer variant. Same schedule, computed from
  * the router's int32 GPU x GPU token counts (diagonal = local tokens,
  * ignored by the schedule like TrafficMatrix does, core.py:95), plus the
- * engine tables:
- *   chunks[P][n][4]   per phase k and sender i: {receiver, first token of the
- *                     pair's send list, token count, arrival index at receiver}
- *   rchunks[P][n][4]  the same chunks indexed by receiver j: {sender, first,
- *                     count, index in the sender's send order} (the combine
- *                     runs CommSchedule.reversed(), commsched.py:310-319)
- *   n_in[n], n_out[n] chunks arriving at / leaving each rank
+ * engine tables, one entry per (coalesced) phase:
+ *   chunks[P][n][4]   per phase k and sender i: {receiver j (-1: idle), first
+ *                     token of pair (i,j) in this phase, token count, run code}.
+ *                     A run is a maximal stretch of consecutive phases in which
+ *                     i sends to j; run code = r (index of the run among the
+ *                     runs into j) on a run's first entry, -1-r on its
+ *                     continuation entries (no hand-over needed: nobody else
+ *                     sends to j in between).
+ *   rchunks[P][n][4]  the same entries indexed by receiver j: {sender, first,
+ *                     count, run code counted among the sender's runs} (the
+ *                     combine runs CommSchedule.reversed(), commsched.py:310-319)
+ *   n_in[n], n_out[n] runs arriving at / leaving each rank
+ *   progress[1]       (nullable) written while the kernel runs: the number of
+ *                     leading phases whose entries are final, then
+ *                     n_phases | AURORA_PROGRESS_DONE once every output is
+ *                     written. The engine polls it, so dispatch can start on
+ *                     phase 0 while later phases are still being computed. The
+ *                     caller zeroes it (stream-ordered) before the launch.
  * (the buffer layout soff / roff the chunk offsets refer to comes from aurora_pack)
  * Heterogeneous durations (time units, commsched.py:338-347) are converted to
- * whole tokens per chunk by rounding each pair's cumulative time x
- * min(B_i,B_j); the last chunk absorbs the rounding so per-pair totals are exact. */
+ * whole tokens per entry by rounding each pair's cumulative time x
+ * min(B_i,B_j); the pair's last entry absorbs the rounding so per-pair totals
+ * are exact (such schedules publish progress only when complete). */
+#define AURORA_PROGRESS_DONE (1 << 20)
+#define AURORA_PROGRESS_COUNT ((1 << 20) - 1)
 int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32_t* phase_recv,
                            double* phase_dur, int32_t* n_phases, int32_t* chunks,
                            int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* status,
-                           void* stream);
+                           int32_t* progress, void* stream);
 
 /* ---------------------------------------------------------------- K1 ----
  * aurora_route: top-k gating + GPU x GPU traffic matrix. No reference
@@ -122,8 +136,8 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
 
 /* ------------------------------------------------------------ K4 / K6 ----
  * aurora_engine: executes the schedule as in-kernel stores into peer
- * memory, self-timed per chunk (a chunk i->j starts once every earlier chunk
- * into j has landed), replacing a single NCCL alltoallv. mode bit 0: 0 =
+ * memory, self-timed per run (a run i->j starts once every earlier run into j
+ * has landed), replacing a single NCCL alltoallv. mode bit 0: 0 =
  * dispatch (CommSchedule phases, commsched.py:112-132), 1 = combine (the
  * reversed schedule, commsched.py:310-319: same phases, directions flipped);
  * mode bit 1: peers live on other GPUs (system-scope flag ordering) -- clear
@@ -131,10 +145,16 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * mode bit 2: local (diagonal) rows only -- no schedule needed, so it can run
  * while K2 is still computing; mode bit 3: scheduled remote chunks only;
  * mode bit 4: ablation -- no pacing, every sender pushes all of its chunks at
- * once (the unscheduled all-pairs-concurrent all-to-all).
- * Consecutive phases of one pair are one chunk (aurora_schedule_counts merges
- * them), so a handshake only happens where the schedule changes partners.
- *   tables from aurora_schedule_counts; counts[n][n] from aurora_route;
+ * once (the unscheduled all-pairs-concurrent all-to-all);
+ * mode bit 5: launch as a programmatic dependent (PDL) of the immediately
+ * preceding aurora_schedule_counts on the same stream -- the engine starts
+ * while K2 runs (K2 triggers its dependents on entry, so it is resident first)
+ * and consumes phases through `progress`. Continuation entries of a run need no hand-over, so a handshake only
+ * happens where the schedule changes partners. Local (diagonal) rows are
+ * copied first; then phase k is executed as soon as progress (K2's progress
+ * word) covers it, so the engine may run concurrently with K2 on another
+ * stream of the same device.
+ *   tables + progress from aurora_schedule_counts; counts[n][n] from aurora_route;
  *   n_local ranks [rank_base, rank_base+n_local) are served by this call
  *   dispatch: src rows = x_local[i_local] gathered through send_list,
  *             dst = recv_buf[j] rows roff[i][j] + first ...
@@ -148,7 +168,7 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  *   ctas_per_rank copy CTAs per local rank; all must be co-resident.
  *   spin_limit bounds every flag wait (0 = unbounded); on expiry status = ETIMEOUT. */
 int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,
-                  const int32_t* chunks, const int32_t* rchunks, const int32_t* n_phases,
+                  const int32_t* chunks, const int32_t* rchunks, const int32_t* progress,
                   const int32_t* n_in, const int32_t* n_out, const int32_t* soff,
                   const int32_t* roff, const int32_t* send_list, int send_list_stride,
                   const void* const* src_bufs, void* const* dst_bufs, int row_bytes,

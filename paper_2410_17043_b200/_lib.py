@@ -23,7 +23,7 @@ _SIGNATURES = {
     "aurora_raw_phase_cap": [_c_int],
     "aurora_phase_cap": [_c_int],
     "aurora_schedule_f64": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "aurora_schedule_counts": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "aurora_schedule_counts": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_route": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
                      _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -85,9 +85,10 @@ def schedule_sjf(d, cluster) -> CommSchedule:
 
 def to_engine_tables(sched: CommSchedule, n: int):
     """CommSchedule (token-unit durations) -> (chunks[P,n,4], rchunks[P,n,4],
-    n_in[n], n_out[n]) in the engine's format (include/aurora_b200.h): per phase
-    and sender {receiver, first token, count, arrival index}; same-pair runs that
-    are consecutive for both ends form one chunk."""
+    n_in[n], n_out[n]) in the engine's format (include/aurora_b200.h): one entry
+    per phase and sender {receiver, first token, count, run code}; a run is a
+    stretch of consecutive phases of one pair, coded r (its index among the runs
+    into the receiver) on its first entry and -1-r on continuations."""
     P = max(1, len(sched.phases))
     ch = np.full((P, n, 4), 0, dtype=np.int32)
     ch[:, :, 0] = -1
@@ -95,27 +96,24 @@ def to_engine_tables(sched: CommSchedule, n: int):
     issued = np.zeros((n, n), dtype=np.int64)
     cum = np.zeros((n, n))
     rcnt = np.zeros(n, dtype=np.int32)
-    sseq = np.zeros(n, dtype=np.int32)
-    last_j, last_k, last_from = [-1] * n, [-1] * n, [-1] * n
+    scnt = np.zeros(n, dtype=np.int32)
+    prev = [-1] * n
     for k, ph in enumerate(sched.phases):
-        opened = []
+        cur = [-1] * n
         for i, j in ph.transfers:
             cum[i, j] += ph.duration
-            tok = int(round(cum[i, j])) - int(issued[i, j])
             start = int(issued[i, j])
+            tok = int(round(cum[i, j])) - start
             issued[i, j] += tok
-            if last_j[i] == j and last_from[j] == i:
-                kk = last_k[i]
-                ch[kk, i, 2] += tok
-                rch[kk, j, 2] += tok
+            cont = prev[i] == j
+            if cont:
+                r, s_ = rcnt[j] - 1, scnt[i] - 1
             else:
-                ch[k, i] = (j, start, tok, rcnt[j])
-                rch[k, j] = (i, start, tok, sseq[i])
-                sseq[i] += 1
-                last_j[i], last_k[i] = j, k
-                opened.append(j)
-        for i, j in ph.transfers:
-            last_from[j] = i
-        for j in opened:
-            rcnt[j] += 1
-    return ch, rch, rcnt, sseq
+                r, s_ = rcnt[j], scnt[i]
+                rcnt[j] += 1
+                scnt[i] += 1
+            ch[k, i] = (j, start, tok, -1 - r if cont else r)
+            rch[k, j] = (i, start, tok, -1 - s_ if cont else s_)
+            cur[i] = j
+        prev = cur
+    return ch, rch, rcnt, scnt

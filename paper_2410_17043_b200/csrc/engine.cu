@@ -4,14 +4,18 @@
 // Schedule semantics (reference pkg/src/moeplan/commsched.py:112-162): in
 // phase k sender i transmits `duration` tokens of its pair (i, j) while no
 // other sender targets j and i targets nobody else. Instead of a global
-// barrier per phase, every copy CTA runs its sender's chunk list in phase
-// order and starts a chunk once ALL earlier chunks into the same receiver
-// have landed (per-receiver arrival counter, release/acquire at system
-// scope). Each GPU's send order and receive order are exactly the
-// schedule's, so the execution stays contention-free while never waiting
-// longer than the phase-aligned timeline would. Correctness does not depend
-// on pacing: every chunk owns a disjoint, precomputed region of the peer
-// buffer.
+// barrier per phase, every copy CTA runs its sender's entries in phase order
+// and starts a run (consecutive phases of one pair) once ALL earlier runs into
+// the same receiver have landed (per-receiver arrival counter, release/acquire
+// at system scope); continuation entries of a run need no hand-over. Each
+// GPU's send order and receive order are exactly the schedule's, so the
+// execution stays contention-free while never waiting longer than the
+// phase-aligned timeline would. Correctness does not depend on pacing: every
+// entry owns a disjoint, precomputed region of the peer buffer.
+//
+// The dispatch consumes the schedule while K2 is still producing it: phase k
+// is used as soon as K2's progress word says its entries are final, so the
+// scheduler's latency hides behind the first phases' copies.
 //
 // Combine (mode 1) replays the same phases with directions flipped -- the
 // reference's CommSchedule.reversed() (commsched.py:310-319) -- from the
@@ -28,7 +32,7 @@ struct EngineParams {
   const int32_t* counts;
   const int4* chunks;
   const int4* rchunks;
-  const int32_t* n_phases;
+  const int32_t* progress;  // K2's progress word (AURORA_PROGRESS_*)
   const int32_t* n_in;
   const int32_t* n_out;
   const int32_t* soff;
@@ -107,8 +111,6 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
   const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
   const int n = p.n;
-  // the schedule may still be running when a local-only copy starts: read it only when used
-  const int nph = (p.mode & 4) ? 0 : min(*p.n_phases, p.max_phases);
   const bool dispatch = (p.mode & 1) == 0;
   const bool sys = (p.mode & 2) != 0;          // peers on other GPUs: system-scope ordering
   const bool do_remote = (p.mode & 4) == 0;    // bit 2: local rows only
@@ -116,24 +118,74 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const bool paced = (p.mode & 16) == 0;       // bit 4: ablation, every pair at once (no schedule)
   const char* src = p.src_bufs[r_local];
   const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
-  __shared__ int abort_s;
+  const int4* table = dispatch ? p.chunks : p.rchunks;
+  __shared__ int abort_s, avail_s, done_s;
   if (threadIdx.x == 0) abort_s = 0;
   __syncthreads();
 
-  for (int k = 0; k < (do_remote ? nph : 0); k++) {
-    // dispatch: chunk of sender g; combine: chunk of the reversed schedule where g sends back
-    const int4 ch = dispatch ? p.chunks[k * n + g] : p.rchunks[k * n + g];
+  // local (diagonal) rows never cross the network (TrafficMatrix zeroes them,
+  // core.py:95) and need no schedule: copy them while K2 is still running
+  if (do_local) {
+    const int nloc = p.counts[g * n + g];
+    const int per = (nloc + p.C - 1) / p.C;
+    const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
+    if (dispatch) {
+      copy_rows<true>(p.row_bytes, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g], r0, r1);
+      if (p.src2_bufs)
+        copy_rows<false>(p.row2_bytes, p.src2_bufs[r_local], nullptr, p.soff[g * n + g], p.dst2_bufs[g],
+                         p.roff[g * n + g], r0, r1);
+    } else {
+      copy_rows<false>(p.row_bytes, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0, r1);
+    }
+  }
+  if (!do_remote) return;
+
+  // wait until phase `need` is final (or the schedule is complete)
+  int avail = 0;
+  bool done = false;
+  auto refresh = [&](int need) {
+    if (threadIdx.x == 0) {
+      long long spins = 0;
+      int pr;
+      for (;;) {
+        pr = ld_acquire_gpu(p.progress);
+        if ((pr & AURORA_PROGRESS_COUNT) > need || (pr & AURORA_PROGRESS_DONE)) break;
+        if (p.spin_limit && ++spins > p.spin_limit) {
+          atomicExch(p.status, AURORA_ETIMEOUT);
+          abort_s = 1;
+          break;
+        }
+        if (spins > 16) __nanosleep(32);
+      }
+      avail_s = min(pr & AURORA_PROGRESS_COUNT, p.max_phases);
+      done_s = (pr & AURORA_PROGRESS_DONE) != 0;
+    }
+    __syncthreads();
+    avail = avail_s;
+    done = done_s;
+  };
+
+  for (int k = 0;; k++) {
+    if (k >= avail) {
+      if (done) break;
+      refresh(k);
+      if (abort_s) return;
+      if (k >= avail) break;
+    }
+    // dispatch: entry of sender g; combine: entry of the reversed schedule where g sends back
+    const int4 ch = __ldcg(&table[k * n + g]);
     const int peer = ch.x;  // dispatch: receiver j; combine: original sender i (now receiver)
     if (peer < 0) continue;
-    const int first = ch.y, ntok = ch.z, seq = ch.w;
-    if (threadIdx.x == 0) {
-      if (paced && !wait_ge(p.ctrs[peer], seq * p.C, p.spin_limit, sys)) {
+    const int first = ch.y, ntok = ch.z;
+    const bool cont = ch.w < 0;
+    if (paced && !cont) {  // a run starts once every earlier run into `peer` has landed
+      if (threadIdx.x == 0 && !wait_ge(p.ctrs[peer], ch.w * p.C, p.spin_limit, sys)) {
         abort_s = 1;
         atomicExch(p.status, AURORA_ETIMEOUT);
       }
+      __syncthreads();
+      if (abort_s) return;
     }
-    __syncthreads();
-    if (abort_s) return;
     const int per = (ntok + p.C - 1) / p.C;
     const int r0 = min(ntok, c * per), r1 = min(ntok, r0 + per);
     if (dispatch) {
@@ -148,30 +200,22 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
       copy_rows<false>(p.row_bytes, src, nullptr, p.roff[peer * n + g] + first, p.dst_bufs[peer],
                        p.soff[peer * n + g] + first, r0, r1);
     }
-    signal(p.ctrs[peer], sys);
-  }
-
-  // local (diagonal) rows never cross the network (TrafficMatrix zeroes them, core.py:95)
-  if (do_local) {
-    const int nloc = p.counts[g * n + g];
-    const int per = (nloc + p.C - 1) / p.C;
-    const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
-    if (dispatch)
-    {
-      copy_rows<true>(p.row_bytes, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g],
-                      r0, r1);
-      if (p.src2_bufs)
-        copy_rows<false>(p.row2_bytes, p.src2_bufs[r_local], nullptr, p.soff[g * n + g],
-                         p.dst2_bufs[g], p.roff[g * n + g], r0, r1);
+    // the run ends unless this sender's next entry continues it
+    if (k + 1 >= avail && !done) {
+      refresh(k + 1);
+      if (abort_s) return;
     }
-    else
-      copy_rows<false>(p.row_bytes, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0,
-                       r1);
+    bool run_end = true;
+    if (k + 1 < avail) {
+      const int4 nx = __ldcg(&table[(k + 1) * n + g]);
+      run_end = !(nx.x == peer && nx.w < 0);
+    }
+    if (run_end) signal(p.ctrs[peer], sys);
   }
 
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
-  if (do_remote && c == 0 && threadIdx.x == 0) {
-    const int expect = (dispatch ? p.n_in[g] : p.n_out[g]) * p.C;
+  if (c == 0 && threadIdx.x == 0) {
+    const int expect = (dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g])) * p.C;
     if (!wait_ge(p.ctrs[g], expect, p.spin_limit, sys)) {
       atomicExch(p.status, AURORA_ETIMEOUT);
     } else {
@@ -228,17 +272,17 @@ __global__ void __launch_bounds__(THREADS) aggregate_kernel(
 
 extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,
                              const int32_t* chunks, const int32_t* rchunks,
-                             const int32_t* n_phases, const int32_t* n_in, const int32_t* n_out,
+                             const int32_t* progress, const int32_t* n_in, const int32_t* n_out,
                              const int32_t* soff, const int32_t* roff, const int32_t* send_list,
                              int send_list_stride, const void* const* src_bufs,
                              void* const* dst_bufs, int row_bytes, const void* const* src2_bufs,
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
-  if (mode < 0 || mode > 31 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+  if (mode < 0 || mode > 63 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
-      !rchunks || !n_phases || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
+      !rchunks || !progress || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
       ((mode & 1) == 0 && !send_list))
     return AURORA_EINVAL;
   int dev = 0, sms = 0, occ = 0;
@@ -259,7 +303,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.counts = counts;
   p.chunks = reinterpret_cast<const int4*>(chunks);
   p.rchunks = reinterpret_cast<const int4*>(rchunks);
-  p.n_phases = n_phases;
+  p.progress = progress;
   p.n_in = n_in;
   p.n_out = n_out;
   p.soff = soff;
@@ -278,7 +322,18 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.max_phases = max_phases;
   p.spin_limit = spin_limit;
   p.status = status;
-  engine_kernel<<<n_local * ctas_per_rank, THREADS, 0, (cudaStream_t)stream>>>(p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_local * ctas_per_rank);
+  cfg.blockDim = dim3(THREADS);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  if (mode & 32) {  // programmatic dependent of the preceding K2 launch: start while it runs
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, engine_kernel, p) != cudaSuccess) return AURORA_ECUDA;
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -42,6 +42,8 @@ struct SchedParams {
   int32_t* n_in;          // [n]             (nullable) chunks arriving at each receiver
   int32_t* n_out;         // [n]             chunks leaving each sender
   long long* prof;        // [8]             (nullable) diagnostics: cycles per section
+  int32_t* progress;      // [1]             (nullable) phases whose chunk entries are final,
+                          //                 | AURORA_PROGRESS_DONE once everything is written
 };
 
 // numpy pairwise_sum (n <= 128 branch, and n < 8 sequential), row-major row of t
@@ -243,30 +245,156 @@ __device__ __forceinline__ void row_put(V (&a)[NB], int j, V v) {
     if (q == j) a[q] = v;
 }
 
-// decompose (commsched.py:406-435) + strip/_coalesce (463-479), n <= NB <= 16,
-// every lane holding its row of remaining / real / undelivered in registers.
+// ============================================================================
+// Engine chunk tables, built one (coalesced) phase at a time so the engine can
+// start on phase k while later phases are still being computed.
+//
+// Entry (phase k, sender i) = {receiver j, first token of pair (i, j) in this
+// phase, token count, run code}. A run is a maximal stretch of consecutive
+// phases in which i sends to j (commsched.py:463-479 splits and coalesces
+// phases, so a pair often stays matched across several of them); inside a run
+// no other sender touches j, so only the first entry of a run needs the
+// receiver's hand-over. Run code = r (the run's index among the runs into j)
+// on the first entry, -1 - r on continuation entries. rchunks holds the same
+// entries indexed by receiver with the run's index among the sender's runs
+// (the combine replays CommSchedule.reversed(), commsched.py:310-319).
+// n_in[j] / n_out[i] = runs into j / out of i.
+// ============================================================================
+struct ChunkCtx {
+  double* cum;        // [MAXN][ld]  cumulative scheduled time per pair
+  int* tok;           // [MAXN][ld]  tokens issued per pair
+  int* lastc;         // [MAXN][ld]  phase of the pair's last entry (-1: none)
+  int* rcnt;          // [MAXN]      runs into each receiver so far
+  int4* rtmp;         // [MAXN]      per-receiver staging of the current phase
+  const int32_t* want;  // pair totals (counts), row stride wld
+  const double* bw;   // [n] bandwidths or nullptr
+  int ld, wld;
+};
+
+struct ChunkLane {
+  int prev_j = -1;  // this sender's receiver in the previous phase
+  int scnt = 0;     // runs this sender has opened
+};
+
+__device__ void chunk_init(const ChunkCtx& c, int n, int lane) {
+  if (lane < n) {
+    for (int j = 0; j < n; j++) {
+      c.cum[lane * c.ld + j] = 0.0;
+      c.tok[lane * c.ld + j] = 0;
+      c.lastc[lane * c.ld + j] = -1;
+    }
+    c.rcnt[lane] = 0;
+  }
+}
+
+// one phase k of a single warp (lane = sender); j = this lane's receiver or -1
+__device__ void chunk_step(const SchedParams& p, const ChunkCtx& c, ChunkLane& cl, int k, int j,
+                           double dk, double bw_i, int lane) {
+  const int n = p.n;
+  const bool on = lane < n;
+  if (on) c.rtmp[lane] = make_int4(-1, 0, 0, 0);
+  __syncwarp();
+  int4 e = make_int4(-1, 0, 0, 0);
+  if (on && j >= 0) {
+    const int q = lane * c.ld + j;
+    const double cum = c.cum[q] + dk;
+    c.cum[q] = cum;
+    const double bw_j = c.bw ? c.bw[j] : 1.0;
+    const double scale = bw_j < bw_i ? bw_j : bw_i;
+    const int want = c.want[lane * c.wld + j];
+    const int start = c.tok[q];
+    int tk = (int)rint(cum * scale);  // per-pair cumulative time -> whole tokens
+    if (tk > want) tk = want;
+    if (tk < start) tk = start;
+    c.tok[q] = tk;
+    c.lastc[q] = k;
+    const bool cont = cl.prev_j == j;
+    int rseq, sseq;
+    if (cont) {
+      rseq = c.rcnt[j] - 1;
+      sseq = cl.scnt - 1;
+    } else {
+      rseq = c.rcnt[j];
+      c.rcnt[j] = rseq + 1;  // receivers are distinct within a phase
+      sseq = cl.scnt++;
+    }
+    e = make_int4(j, start, tk - start, cont ? -1 - rseq : rseq);
+    c.rtmp[j] = make_int4(lane, start, tk - start, cont ? -1 - sseq : sseq);
+  }
+  if (on) cl.prev_j = j;
+  __syncwarp();
+  if (on) {
+    __stcg(&p.chunks[k * n + lane], e);
+    __stcg(&p.rchunks[k * n + lane], c.rtmp[lane]);
+  }
+}
+
+// after the last phase: exact per-pair totals for fractional (heterogeneous)
+// durations, run counts, then the DONE word the engine waits for
+__device__ void chunk_finish(const SchedParams& p, const ChunkCtx& c, const ChunkLane& cl, int lane) {
+  const int n = p.n;
+  if (lane < n) {
+    for (int j = 0; j < n; j++) {
+      const int q = lane * c.ld + j;
+      const int want = c.want[lane * c.wld + j], got = c.tok[q], kl = c.lastc[q];
+      if (kl >= 0 && got != want) {
+        p.chunks[kl * n + lane].z += want - got;
+        p.rchunks[kl * n + j].z += want - got;
+      }
+    }
+    p.n_out[lane] = cl.scnt;
+  }
+  __syncwarp();
+  if (lane < n) p.n_in[lane] = c.rcnt[lane];
+}
+
+__device__ __forceinline__ void publish(int32_t* progress, int value, int lane) {
+  __syncwarp();
+  if (lane == 0 && progress) {
+    __threadfence();
+    st_release_gpu(progress, value);
+  }
+}
+
+// ============================================================================
+// n <= 16: two warps.
+//   warp 0 -- decompose (commsched.py:406-435): snap / min / masks per lane row
+//             in registers, the matching (FastMatch8 / FastMatch<16>, lane 0),
+//             the update; every raw (perm, duration) goes to a shared ring.
+//   warp 1 -- strip + _coalesce (commsched.py:463-479) of each raw phase as
+//             soon as it is published, the chunk entries of every phase that
+//             closes, and the progress word the engine polls.
+// The strip only needs the raw phases produced so far, so warp 1 is never
+// ahead of warp 0 and never on its critical path.
+// ============================================================================
+template <int NB>
+struct RawRing {  // the flags lead so every NB shares their offsets
+  static constexpr int R = NB * NB - 2 * NB + 2;
+  volatile int published;  // raw phases ready
+  volatile int done;       // 1 + status once warp 0 has finished
+  double dur[R];
+  signed char perm[R * NB];
+};
+
 template <int NB, typename V>
-__device__ void decompose_fast(const SchedParams& p, const double* rem_in, const double* real_in,
-                               const double* t_in, int ld, uint32_t* pref_s,
-                               uint32_t* sup_s, int* perm_s, Dom<V> dom, signed char* precv_s,
-                               double* pdur_s, int& nr_out, int& np_out, int& status) {
-  const int lane = threadIdx.x, n = p.n;
+__device__ void decompose_warp(const SchedParams& p, const double* rem_in, const double* real_in, int ld,
+                               uint32_t* pref_s, uint32_t* sup_s, int* perm_s, Dom<V> dom,
+                               RawRing<NB>& ring) {
+  const int lane = threadIdx.x & 31, n = p.n;
   const bool on = lane < n;
   const V INF = Dom<V>::inf();
-  const int R_MAX = n * n - 2 * n + 2, P_MAX = 2 * n * n - 3 * n + 2;
-  V rem[NB], real[NB], lr[NB];
+  const int R_MAX = n * n - 2 * n + 2;
+  V rem[NB], real[NB];
 #pragma unroll
   for (int j = 0; j < NB; j++) {
     rem[j] = (on && j < n) ? (V)rem_in[lane * ld + j] : (V)0;
     real[j] = (on && j < n) ? (V)real_in[lane * ld + j] : (V)0;
-    lr[j] = (on && j < n) ? (V)t_in[lane * ld + j] : (V)0;
   }
-  int nr = 0, np_ = 0, last_recv = -2;
-  V cur_dur = 0;
+  int nr = 0, status = AURORA_OK;
   FastMatch<NB> fm;
-  long long cy[4] = {0, 0, 0, 0}, t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  long long cy[3] = {0, 0, 0};
   while (true) {
-    t0 = clock64();
+    const long long t0 = clock64();
     bool anyrow = false;
     uint32_t sup = 0, pref = 0;
 #pragma unroll
@@ -281,11 +409,11 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
     }
     if (!__any_sync(0xffffffffu, on && anyrow)) break;
     if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
+    const long long t1 = clock64();
     int pj;
     if constexpr (NB == 8) {
       // rows -> lane 0 as bytes of two words (warp OR-reductions), the
       // permutation back as nibbles of one word (one shuffle)
-      t1 = clock64();
       const uint32_t sh = 8u * (lane & 3);
       const uint32_t p0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? pref << sh : 0u);
       const uint32_t p1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? pref << sh : 0u);
@@ -304,12 +432,10 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
       mlw = __shfl_sync(0xffffffffu, mlw, 0);
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (!ok) { status = AURORA_ENOMATCH; break; }
-      t2 = clock64();
       pj = on ? (int)((mlw >> (4 * lane)) & 15u) : 0;
     } else {
       if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
       __syncwarp();
-      t1 = clock64();
       if (lane == 0) {
 #pragma unroll
         for (int u = 0; u < NB; u++) {
@@ -323,158 +449,249 @@ __device__ void decompose_fast(const SchedParams& p, const double* rem_in, const
       }
       __syncwarp();
       if (!perm_s[0]) { status = AURORA_ENOMATCH; break; }
-      t2 = clock64();
       pj = on ? perm_s[1 + lane] : 0;
     }
+    const long long t2 = clock64();
     const V dur = Dom<V>::warp_min(on ? row_pick<NB, V>(rem, pj) : INF);
     if (on) {
       row_put<NB, V>(rem, pj, row_pick<NB, V>(rem, pj) - dur);
       const V re = row_pick<NB, V>(real, pj) - dur;
       row_put<NB, V>(real, pj, re < 0 ? (V)0 : re);
+      ring.perm[nr * NB + lane] = (signed char)pj;
       if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
     }
-    if (lane == 0 && p.raw_dur) p.raw_dur[nr] = (double)dur;
+    if (lane == 0) {
+      ring.dur[nr] = (double)dur;
+      if (p.raw_dur) p.raw_dur[nr] = (double)dur;
+    }
     nr++;
-    t3 = clock64();
-    V left = dur;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      ring.published = nr;
+    }
+    const long long t3 = clock64();
+    cy[0] += t1 - t0;
+    cy[1] += t2 - t1;
+    cy[2] += t3 - t2;
+  }
+  if (lane == 0) {
+    if (p.n_raw) *p.n_raw = nr;
+    if (p.prof)
+      for (int q = 0; q < 3; q++) p.prof[q] = cy[q];
+    __threadfence_block();
+    ring.done = 1 + status;
+  }
+}
+
+template <int NB, typename V>
+__device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom<V> dom, RawRing<NB>& ring,
+                           const ChunkCtx& cc, double bw_i, bool stream, int& np_out, int& status) {
+  const int lane = threadIdx.x & 31, n = p.n;
+  const bool on = lane < n;
+  const V INF = Dom<V>::inf();
+  const int P_MAX = 2 * n * n - 3 * n + 2;
+  V lr[NB];  // real demand not yet delivered (commsched.py:463)
+#pragma unroll
+  for (int j = 0; j < NB; j++) lr[j] = (on && j < n) ? (V)t_in[lane * ld + j] : (V)0;
+  ChunkLane cl;
+  int np_ = 0, last_recv = -2, r = 0, avail = 0;
+  V cur_dur = 0;
+  bool closing_ok = true;
+  const long long t_begin = clock64();
+  long long busy = 0;
+  // close the open phase np_-1: outputs, chunk entries, progress
+  auto close_phase = [&]() {
+    const int k = np_ - 1;
+    if (on) p.phase_recv[k * n + lane] = last_recv;
+    if (lane == 0) p.phase_dur[k] = (double)cur_dur;
+    if (p.chunks) {
+      chunk_step(p, cc, cl, k, on ? last_recv : -1, (double)cur_dur, bw_i, lane);
+      if (stream) publish(p.progress, k + 1, lane);
+    }
+  };
+  for (;;) {
+    int dn = 0;
+    if (r >= avail) {  // wait for warp 0
+      if (lane == 0) {
+        for (;;) {
+          avail = ring.published;
+          dn = ring.done;
+          if (avail > r || dn) break;
+        }
+        if (dn) avail = ring.published;
+      }
+      avail = __shfl_sync(0xffffffffu, avail, 0);
+      dn = __shfl_sync(0xffffffffu, dn, 0);
+      __threadfence_block();
+      if (r >= avail) {
+        if (dn > 1) status = dn - 1;
+        break;
+      }
+    }
+    const long long b0 = clock64();
+    const int pj = on ? (int)ring.perm[r * NB + lane] : 0;
+    V left = (V)ring.dur[r];
+    r++;
     while (dom.pos(left)) {
       const V lv = on ? row_pick<NB, V>(lr, pj) : (V)0;
       const bool act = on && dom.pos(lv);
       const unsigned amask = __ballot_sync(0xffffffffu, act);
       V step;
       if (amask == 0) {
-        step = left;
+        step = left;  // idle Phase((), left) (commsched.py:469-473)
       } else {
         const V m = Dom<V>::warp_min(act ? lv : INF);
         step = m < left ? m : left;
       }
       const int recv = act ? pj : -1;
-      if (dom.pos(step)) {
+      if (dom.pos(step)) {  // drop <= eps phases, then _coalesce identical neighbours
         const bool same = np_ > 0 && __all_sync(0xffffffffu, !on || recv == last_recv);
         if (same) {
           cur_dur = cur_dur + step;
         } else {
-          if (np_ >= P_MAX) { status = AURORA_EOVERFLOW; break; }
+          if (np_ > 0) close_phase();
+          if (np_ >= P_MAX) { status = AURORA_EOVERFLOW; closing_ok = false; break; }
           np_++;
           cur_dur = step;
           last_recv = recv;
-          if (on) {
-            p.phase_recv[(np_ - 1) * n + lane] = recv;
-            precv_s[(np_ - 1) * n + lane] = (signed char)recv;
-          }
-        }
-        if (lane == 0) {
-          p.phase_dur[np_ - 1] = (double)cur_dur;
-          pdur_s[np_ - 1] = (double)cur_dur;
         }
       }
       if (amask == 0) break;
       if (act) row_put<NB, V>(lr, pj, lv - step);
       left -= step;
     }
+    busy += clock64() - b0;
     if (status != AURORA_OK) break;
-    const long long t4 = clock64();
-    cy[0] += t1 - t0;
-    cy[1] += t2 - t1;
-    cy[2] += t3 - t2;
-    cy[3] += t4 - t3;
   }
-  if (p.prof && lane == 0)
-    for (int q = 0; q < 4; q++) p.prof[q] = cy[q];
-  nr_out = nr;
-  np_out = np_;
+  if (status == AURORA_OK && np_ > 0 && closing_ok) close_phase();
+  if (p.prof && lane == 0) {
+    p.prof[3] = busy;
+    p.prof[7] = clock64() - t_begin;
+  }
+  np_out = status == AURORA_OK ? np_ : 0;
+  if (p.chunks && status == AURORA_OK) chunk_finish(p, cc, cl, lane);
+}
+
+template <int NB, typename V>
+__device__ void schedule_two_warps(const SchedParams& p, const double* R, const double* Q, const double* Tt,
+                                   int ld, MatchState& ms, Dom<V> dom, RawRing<NB>& ring, const ChunkCtx& cc,
+                                   double bw_i, bool stream, int& np_, int& status) {
+  if (threadIdx.x < 32) {
+    decompose_warp<NB, V>(p, R, Q, ld, ms.pref, ms.sup, ms.ml, dom, ring);
+  } else {
+    strip_warp<NB, V>(p, Tt, ld, dom, ring, cc, bw_i, stream, np_, status);
+  }
 }
 
 __device__ long long* g_sched_prof = nullptr;
 
-// MAXN = 16 or 32: shared memory sized for the launch (a 16-rank schedule
-// needs 7 KB, so it co-resides with a persistent GEMM CTA on the same SM).
+// MAXN = 16: two warps (n <= 16, the shapes the layer uses). MAXN = 32: one
+// warp, generic matcher, chunk pass after the decomposition.
 template <int MAXN>
-__global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
-  // phase tables staged in shared memory for the chunk pass (fast path only)
-  constexpr int PST = MAXN <= 16 ? 2 * MAXN * MAXN - 3 * MAXN + 2 : 1;
-  __shared__ signed char precv_s[PST * MAXN];
-  __shared__ double pdur_s[PST];
+__global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kernel(SchedParams p) {
+  constexpr bool TWO = MAXN <= 16;
   __shared__ double t_s[MAXN][MAXN + 1];     // time matrix; later "remaining" of strip
   __shared__ double rem_s[MAXN][MAXN + 1];   // decompose remaining (d')
   __shared__ double real_s[MAXN][MAXN + 1];  // decompose real
   __shared__ double rr_s[MAXN], cr_s[MAXN];
   __shared__ MatchState ms;
   __shared__ int rcnt_s[MAXN];
+  __shared__ int4 rtmp_s[MAXN];
+  __shared__ double bw_s[MAXN];
+  __shared__ int status_s, np_s;
+  __shared__ double bmax_s;
+  // two-warp path only: raw ring, chunk state, pair totals
+  __shared__ RawRing<TWO ? MAXN : 1> ring;
+  __shared__ double cum_s[TWO ? MAXN * MAXN : 1];
+  __shared__ int tok_s[TWO ? MAXN * MAXN : 1], lastc_s[TWO ? MAXN * MAXN : 1], want_s[TWO ? MAXN * MAXN : 1];
 
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = p.n;
   const bool on = lane < n;
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  int status = AURORA_OK;
   const long long k_start = clock64();
+  // let a programmatically dependent launch (the dispatch engine, which polls
+  // `progress` instead of waiting for this grid) start now: this CTA is
+  // resident, so the engine can never starve it of an SM
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (!p.prof) p.prof = g_sched_prof;  // diagnostics hook (aurora_debug_set_schedule_profile)
-
-  // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
-  double bw_i = (on && p.bw) ? p.bw[lane] : 1.0;
-  bool bad = false;
-  if (on) {
-    for (int j = 0; j < n; j++) {
-      double dij = p.d64 ? p.d64[lane * n + j] : (double)p.d32[lane * n + j];
-      double bw_j = p.bw ? p.bw[j] : 1.0;
-      double m = bw_j < bw_i ? bw_j : bw_i;
-      double v = p.bw ? dij / m : dij;  // x / 1.0 == x exactly
-      if (v != v || v < 0) bad = true;
-      t_s[lane][j] = (lane == j) ? 0.0 : v;
+  if (tid == 0) {
+    status_s = AURORA_OK;
+    np_s = 0;
+    bmax_s = 0.0;
+    if constexpr (TWO) {
+      ring.published = 0;
+      ring.done = 0;
     }
   }
-  if (__any_sync(0xffffffffu, bad)) status = AURORA_EINVAL;
-  __syncwarp();
+  if (warp == 0 && on) bw_s[lane] = p.bw ? p.bw[lane] : 1.0;
+  if (TWO && warp == 1 && p.chunks && on)  // pair totals for the chunk pass (k-invariant)
+    for (int j = 0; j < n; j++) want_s[lane * MAXN + j] = p.d32[lane * n + j];
+  __syncthreads();
+  const double bw_i = on ? bw_s[lane] : 1.0;
 
-  // ---- bmax_heterogeneous (commsched.py:350-352): numpy-order row/col sums
-  double row = on ? np_pairwise_row(&t_s[lane][0], n) : -INF;
-  double col = -INF;
-  if (on) {
-    col = 0.0;
-    for (int i = 0; i < n; i++) col += t_s[i][lane];
-  }
-  const double rmax = warp_max_d(row), cmax = warp_max_d(col);
-  const double b_max = cmax > rmax ? cmax : rmax;
-  const double eps = 1e-12 * (b_max > 1.0 ? b_max : 1.0);  // _snap_eps, commsched.py:43-45
-  if (lane == 0 && p.b_max) *p.b_max = b_max;
-
-  int nr = 0, np_ = 0;
-  const int R_MAX = n * n - 2 * n + 2;
-  const int P_MAX = 2 * n * n - 3 * n + 2;
-
-  if (status == AURORA_OK && b_max > 0) {
-    // ---- augment (commsched.py:367-391): greedy transportation fill on lane 0
-    if (on) { rr_s[lane] = b_max - row; cr_s[lane] = b_max - col; }
-    if (on) for (int j = 0; j < n; j++) real_s[lane][j] = 0.0;  // x
+  double b_max = 0.0, eps = 0.0, row = -INF, col = -INF;
+  if (warp == 0) {
+    // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
+    bool bad = false;
+    if (on) {
+      for (int j = 0; j < n; j++) {
+        double dij = p.d64 ? p.d64[lane * n + j] : (double)p.d32[lane * n + j];
+        double bw_j = bw_s[j];
+        double m = bw_j < bw_i ? bw_j : bw_i;
+        double v = p.bw ? dij / m : dij;  // x / 1.0 == x exactly
+        if (v != v || v < 0) bad = true;
+        t_s[lane][j] = (lane == j) ? 0.0 : v;
+      }
+    }
+    int status = __any_sync(0xffffffffu, bad) ? AURORA_EINVAL : AURORA_OK;
     __syncwarp();
-    if (lane == 0) {
-      for (int i = 0; i < n; i++) {
-        if (rr_s[i] <= 0) continue;
-        for (int j = 0; j < n; j++) {
-          if (i == j || cr_s[j] <= 0) continue;
-          double fill = cr_s[j] < rr_s[i] ? cr_s[j] : rr_s[i];
-          real_s[i][j] = fill;
-          rr_s[i] -= fill;
-          cr_s[j] -= fill;
-          if (rr_s[i] <= 0) break;
+
+    // ---- bmax_heterogeneous (commsched.py:350-352): numpy-order row/col sums
+    if (on) {
+      row = np_pairwise_row(&t_s[lane][0], n);
+      col = 0.0;
+      for (int i = 0; i < n; i++) col += t_s[i][lane];
+    }
+    const double rmax = warp_max_d(row), cmax = warp_max_d(col);
+    b_max = cmax > rmax ? cmax : rmax;
+    eps = 1e-12 * (b_max > 1.0 ? b_max : 1.0);  // _snap_eps, commsched.py:43-45
+    if (lane == 0 && p.b_max) *p.b_max = b_max;
+    if (lane == 0) bmax_s = b_max;
+
+    if (status == AURORA_OK && b_max > 0) {
+      // ---- augment (commsched.py:367-391): greedy transportation fill on lane 0
+      if (on) { rr_s[lane] = b_max - row; cr_s[lane] = b_max - col; }
+      if (on) for (int j = 0; j < n; j++) real_s[lane][j] = 0.0;  // x
+      __syncwarp();
+      if (lane == 0) {
+        for (int i = 0; i < n; i++) {
+          if (rr_s[i] <= 0) continue;
+          for (int j = 0; j < n; j++) {
+            if (i == j || cr_s[j] <= 0) continue;
+            double fill = cr_s[j] < rr_s[i] ? cr_s[j] : rr_s[i];
+            real_s[i][j] = fill;
+            rr_s[i] -= fill;
+            cr_s[j] -= fill;
+            if (rr_s[i] <= 0) break;
+          }
         }
       }
-    }
-    __syncwarp();
-    if (on) {
-      if (rr_s[lane] > eps) real_s[lane][lane] = rr_s[lane];
-      for (int j = 0; j < n; j++) {
-        double x = real_s[lane][j];
-        if (x < 0) x = 0.0;
-        double dp = t_s[lane][j] + x;
-        rem_s[lane][j] = dp;
-        double r = dp - x;  // np.clip(a.d_prime - a.x, 0, None)
-        real_s[lane][j] = r < 0.0 ? 0.0 : r;
+      __syncwarp();
+      if (on) {
+        if (rr_s[lane] > eps) real_s[lane][lane] = rr_s[lane];
+        for (int j = 0; j < n; j++) {
+          double x = real_s[lane][j];
+          if (x < 0) x = 0.0;
+          double dp = t_s[lane][j] + x;
+          rem_s[lane][j] = dp;
+          double r = dp - x;  // np.clip(a.d_prime - a.x, 0, None)
+          real_s[lane][j] = r < 0.0 ? 0.0 : r;
+        }
       }
-    }
-    __syncwarp();
-    // AugmentedMatrix.__post_init__ balance check (commsched.py:252-258)
-    {
+      __syncwarp();
+      // AugmentedMatrix.__post_init__ balance check (commsched.py:252-258)
       const double tol = 1e-9 * (b_max > 1.0 ? b_max : 1.0);
       bool unbal = false;
       if (on) {
@@ -483,34 +700,68 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
         unbal = fabs(rs - b_max) > tol || fabs(cs - b_max) > tol;
       }
       if (__any_sync(0xffffffffu, unbal)) status = AURORA_EINVAL;
+    } else if (status == AURORA_OK) {
+      status = -1;  // b_max == 0: empty schedule (commsched.py:302-303 analogue)
     }
+    if (lane == 0) status_s = status;
+    if (lane == 0 && p.prof) p.prof[5] = clock64() - k_start;  // prologue
+  }
+  __syncthreads();
+  b_max = bmax_s;
+  eps = 1e-12 * (b_max > 1.0 ? b_max : 1.0);
+  int status = status_s;
+  const bool run = status == AURORA_OK;
+  if (status < 0) status = AURORA_OK;
+  int np_ = 0;
+  // streaming publication: integer tokens only (fractional durations get a
+  // final fix-up of each pair's last entry, so they publish once at the end)
+  const bool stream = p.chunks && !p.bw;
 
-    // ---- decompose (commsched.py:406-435) interleaved with the strip (463-479)
-    int last_recv = -2;  // receiver of this lane in the last kept phase
-    double cur_dur = 0.0;
-    long long cyc[5] = {0, 0, 0, 0, clock64()};
-    if (p.prof && lane == 0) p.prof[5] = cyc[4] - k_start;  // prologue: normalise, bmax, augment
-    if (status == AURORA_OK && n <= 16) {
-      // integer domain: int32 counts on a uniform cluster (every value an integer < 2^31)
+  if constexpr (TWO) {
+    ChunkCtx cc{cum_s, tok_s, lastc_s, rcnt_s, rtmp_s, want_s, p.bw ? bw_s : nullptr, MAXN, MAXN};
+    if (warp == 1 && p.chunks) chunk_init(cc, n, lane);
+    __syncwarp();
+    if (run) {
       const bool int_dom = p.d32 && !p.bw;
       const double* R = &rem_s[0][0];
       const double* Q = &real_s[0][0];
       const double* Tt = &t_s[0][0];
+      RawRing<MAXN>& rg = ring;
       if (n <= 8) {
-        if (int_dom)
-          decompose_fast<8, int>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<int>{}, precv_s, pdur_s, nr, np_, status);
-        else
-          decompose_fast<8, double>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<double>{eps}, precv_s, pdur_s, nr, np_, status);
+        auto& r8 = reinterpret_cast<RawRing<8>&>(rg);  // fits: R_8 * 8 < R_16 * 16
+        if (int_dom) schedule_two_warps<8, int>(p, R, Q, Tt, MAXN + 1, ms, Dom<int>{}, r8, cc, bw_i, stream, np_, status);
+        else schedule_two_warps<8, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r8, cc, bw_i, stream, np_, status);
       } else {
-        if (int_dom)
-          decompose_fast<16, int>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<int>{}, precv_s, pdur_s, nr, np_, status);
-        else
-          decompose_fast<16, double>(p, R, Q, Tt, MAXN + 1, ms.pref, ms.sup, ms.ml, Dom<double>{eps}, precv_s, pdur_s, nr, np_, status);
+        auto& r16 = reinterpret_cast<RawRing<16>&>(rg);
+        if (int_dom) schedule_two_warps<16, int>(p, R, Q, Tt, MAXN + 1, ms, Dom<int>{}, r16, cc, bw_i, stream, np_, status);
+        else schedule_two_warps<16, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r16, cc, bw_i, stream, np_, status);
       }
-      if (p.prof && lane == 0) p.prof[4] = clock64() - cyc[4];
+    } else if (warp == 1 && p.chunks && status == AURORA_OK) {
+      ChunkLane cl;
+      chunk_finish(p, cc, cl, lane);  // empty schedule: no runs
     }
-    while (status == AURORA_OK && n > 16) {
-      long long c0 = clock64();
+    if (warp == 1 && lane == 0) {
+      status_s = status;
+      np_s = np_;
+    }
+    __syncthreads();
+    status = status_s;
+    np_ = np_s;
+    if (warp == 1) {
+      if (lane == 0) {
+        *p.status = status;
+        *p.n_phases = status == AURORA_OK ? np_ : 0;
+      }
+      if (status != AURORA_OK && p.chunks && on) { p.n_in[lane] = 0; p.n_out[lane] = 0; }
+      publish(p.progress, (status == AURORA_OK ? np_ : 0) | AURORA_PROGRESS_DONE, lane);
+      if (p.prof && lane == 0) p.prof[6] = clock64() - k_start;
+    }
+  } else {
+    // ---- generic path (16 < n <= 32): one warp, decompose interleaved with the strip
+    int nr = 0, last_recv = -2;
+    const int R_MAX = n * n - 2 * n + 2, P_MAX = 2 * n * n - 3 * n + 2;
+    double cur_dur = 0.0;
+    while (run && status == AURORA_OK) {
       bool anyrow = false;
       uint32_t sup = 0, pref = 0;
       if (on) {
@@ -528,12 +779,8 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
       if (on) { ms.sup[lane] = sup; ms.pref[lane] = pref; }
       __syncwarp();
-      long long c1 = clock64();
       if (lane == 0) ms.ok = perfect_matching(ms, n);
       __syncwarp();
-      long long c2 = clock64();
-      cyc[0] += c1 - c0;
-      cyc[1] += c2 - c1;
       if (!ms.ok) { status = AURORA_ENOMATCH; break; }
       const int pj = on ? ms.ml[lane] : 0;
       const double dur = warp_min_d(on ? rem_s[lane][pj] : INF);
@@ -545,9 +792,6 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
       }
       if (lane == 0 && p.raw_dur) p.raw_dur[nr] = dur;
       nr++;
-      long long c3 = clock64();
-      cyc[2] += c3 - c2;
-
       // strip this raw phase against the real demand still undelivered (t_s)
       double left = dur;
       while (left > eps) {
@@ -579,112 +823,31 @@ __global__ void __launch_bounds__(32, 1) aurora_schedule_kernel(SchedParams p) {
         if (act) t_s[lane][pj] = lv - step;
         left -= step;
       }
-      cyc[3] += clock64() - c3;
     }
-    if (p.prof && lane == 0 && n > 16) {
-      for (int q = 0; q < 4; q++) p.prof[q] = cyc[q];
-      p.prof[4] = clock64() - cyc[4];
-    }
-  }
-  if (lane == 0) {
-    *p.status = status;
-    *p.n_phases = status == AURORA_OK ? np_ : 0;
-    if (p.n_raw) *p.n_raw = nr;
-  }
-  if (status != AURORA_OK) np_ = 0;
-
-  // ---- engine chunk list (CommSchedule.per_pair_totals order, commsched.py:291-297,
-  // split per phase); the buffer layout itself comes from aurora_pack
-  const long long c_start = clock64();
-  if (p.chunks) {
-    // rem_s: cumulative delivered time per pair; real_s (as int): tokens issued so far
-    int* tok = reinterpret_cast<int*>(&real_s[0][0]);
-    int* lastc = reinterpret_cast<int*>(&real_s[0][0]) + MAXN * MAXN;
-    if (on) {
-      for (int j = 0; j < n; j++) {
-        rem_s[lane][j] = 0.0;
-        tok[lane * MAXN + j] = 0;
-        lastc[lane * MAXN + j] = -1;
-      }
-      rcnt_s[lane] = 0;
-    }
-    // A pair that stays matched across consecutive phases of BOTH its sender
-    // and its receiver (typical: a raw phase split because another pair ran
-    // out) is one continuous transfer; it becomes one chunk, so the engine
-    // never pays a handshake inside it. Send and receive orders are unchanged.
-    int sseq = 0;                    // this sender's chunk count so far
-    int my_last_j = -1, my_last_k = -1;
-    int4 pend_c = make_int4(-1, 0, 0, 0), pend_rc = make_int4(-1, 0, 0, 0);  // open chunk
-    const bool staged = n <= 16;     // phase tables also in shared memory
-    __shared__ int lastfrom_s[MAXN];
-    if (on) lastfrom_s[lane] = -1;
+    if (lane == 0 && p.n_raw) *p.n_raw = nr;
+    if (status != AURORA_OK) np_ = 0;
     __syncwarp();
-    for (int k = 0; k < np_; k++) {
-      if (on) p.rchunks[k * n + lane] = make_int4(-1, 0, 0, 0);
+    if (p.chunks) {
+      // chunk pass over the finished phase tables; chunk state reuses the
+      // decomposition's shared matrices
+      ChunkCtx cc{&rem_s[0][0], reinterpret_cast<int*>(&real_s[0][0]),
+                  reinterpret_cast<int*>(&real_s[0][0]) + MAXN * (MAXN + 1), rcnt_s, rtmp_s, p.d32,
+                  p.bw ? bw_s : nullptr, MAXN + 1, n};
+      ChunkLane cl;
+      chunk_init(cc, n, lane);
       __syncwarp();
-      const double dk = staged ? pdur_s[k] : p.phase_dur[k];
-      const int j = on ? (staged ? (int)precv_s[k * n + lane] : p.phase_recv[k * n + lane]) : -1;
-      bool opened = false;
-      if (j >= 0) {
-        double cum = rem_s[lane][j] + dk;
-        rem_s[lane][j] = cum;
-        const double bw_j = p.bw ? p.bw[j] : 1.0;
-        const double scale = bw_j < bw_i ? bw_j : bw_i;
-        const int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
-        int tk = (int)rint(cum * scale);
-        if (tk > want) tk = want;
-        const int start = tok[lane * MAXN + j];
-        if (tk < start) tk = start;
-        tok[lane * MAXN + j] = tk;
-        if (my_last_j == j && lastfrom_s[j] == lane) {  // continues the open chunk
-          pend_c.z += tk - start;
-          pend_rc.z += tk - start;
-        } else {
-          if (my_last_k >= 0) {  // close the previous chunk of this sender
-            p.chunks[my_last_k * n + lane] = pend_c;
-            p.rchunks[my_last_k * n + my_last_j] = pend_rc;
-          }
-          pend_c = make_int4(j, start, tk - start, rcnt_s[j]);
-          pend_rc = make_int4(lane, start, tk - start, sseq);
-          sseq++;
-          my_last_j = j;
-          my_last_k = k;
-          opened = true;
-        }
-        lastc[lane * MAXN + j] = my_last_k;
-      }
-      __syncwarp();
-      if (j >= 0) {  // receivers are distinct within a phase
-        if (opened) rcnt_s[j] += 1;
-        lastfrom_s[j] = lane;
-      }
-      if (on && !opened) p.chunks[k * n + lane] = make_int4(-1, 0, 0, 0);
-      __syncwarp();
+      for (int k = 0; k < np_; k++)
+        chunk_step(p, cc, cl, k, on ? __ldcg(&p.phase_recv[k * n + lane]) : -1, __ldcg(&p.phase_dur[k]), bw_i,
+                   lane);
+      if (status == AURORA_OK) chunk_finish(p, cc, cl, lane);
+      else if (on) { p.n_in[lane] = 0; p.n_out[lane] = 0; }
     }
-    if (on && my_last_k >= 0) {
-      p.chunks[my_last_k * n + lane] = pend_c;
-      p.rchunks[my_last_k * n + my_last_j] = pend_rc;
+    if (lane == 0) {
+      *p.status = status;
+      *p.n_phases = status == AURORA_OK ? np_ : 0;
     }
-    __syncwarp();
-    // fractional (heterogeneous) durations: make every pair's chunk total exact
-    if (on) {
-      for (int j = 0; j < n; j++) {
-        int want = p.d32 ? p.d32[lane * n + j] : (int)p.d64[lane * n + j];
-        int got = tok[lane * MAXN + j];
-        int kl = lastc[lane * MAXN + j];
-        if (kl >= 0 && got != want) {
-          p.chunks[kl * n + lane].z += want - got;
-          p.rchunks[kl * n + j].z += want - got;
-        }
-      }
-      p.n_in[lane] = rcnt_s[lane];
-      p.n_out[lane] = sseq;
-    }
-  }
-  if (p.prof && lane == 0) {
-    const long long now = clock64();
-    p.prof[6] = now - k_start;  // whole kernel
-    p.prof[7] = now - c_start;  // chunk pass
+    publish(p.progress, np_ | AURORA_PROGRESS_DONE, lane);
+    if (p.prof && lane == 0) p.prof[6] = clock64() - k_start;
   }
 }
 
@@ -701,7 +864,7 @@ namespace {
 
 void launch_schedule(const SchedParams& p, cudaStream_t s) {
   if (p.n <= 16)
-    aurora_schedule_kernel<16><<<1, 32, 0, s>>>(p);
+    aurora_schedule_kernel<16><<<1, 64, 0, s>>>(p);
   else
     aurora_schedule_kernel<32><<<1, 32, 0, s>>>(p);
 }
@@ -734,7 +897,8 @@ extern "C" int aurora_schedule_f64(const double* d, const double* bw, int n, int
 extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, int n,
                                       int32_t* phase_recv, double* phase_dur, int32_t* n_phases,
                                       int32_t* chunks, int32_t* rchunks, int32_t* n_in,
-                                      int32_t* n_out, int32_t* status, void* stream) {
+                                      int32_t* n_out, int32_t* status, int32_t* progress,
+                                      void* stream) {
   if (n < 1 || n > AUR_MAXN || !counts || !phase_recv || !phase_dur || !n_phases || !status ||
       !chunks || !rchunks || !n_in || !n_out)
     return AURORA_EINVAL;
@@ -750,6 +914,7 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
   p.rchunks = reinterpret_cast<int4*>(rchunks);
   p.n_in = n_in;
   p.n_out = n_out;
+  p.progress = progress;
   launch_schedule(p, (cudaStream_t)stream);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

@@ -31,6 +31,8 @@ from .core import DeploymentPlan
 
 __all__ = ["MoEConfig", "AuroraMoELayer", "zipf_bias", "interleave_gate_up"]
 
+PROGRESS_DONE = 1 << 20  # AURORA_PROGRESS_DONE (include/aurora_b200.h)
+
 
 @dataclass(frozen=True)
 class MoEConfig:
@@ -157,6 +159,9 @@ class AuroraMoELayer:
         self.rchunks = torch.empty(P, n, 4, **i32)
         self.n_in = torch.empty(n, **i32)
         self.n_out = torch.empty(n, **i32)
+        # K2's progress word: phases whose engine entries are final (| DONE): the
+        # dispatch starts on phase 0 while K2 is still computing later phases
+        self.progress = torch.zeros(1, **i32)
         # buffer layout (written by K3 from the counts): local rows first in every receive buffer
         self.soff = torch.empty(n, n, **i32)
         self.roff = torch.empty(n, n, **i32)
@@ -179,6 +184,10 @@ class AuroraMoELayer:
         self.side = torch.cuda.Stream(device=dev)
         self._ev_pack = torch.cuda.Event()
         self._ev_local = torch.cuda.Event()
+        # the dispatch engine is a programmatic dependent launch of K2 and consumes
+        # its phases while K2 computes the later ones (AURORA_STREAM_SCHEDULE=0:
+        # K2, then the dispatch)
+        self.stream_schedule = os.environ.get("AURORA_STREAM_SCHEDULE", "1") != "0"
 
         # ---- data buffers. A rank can receive at most every token once.
         self.cap = cfg.tokens
@@ -271,9 +280,24 @@ class AuroraMoELayer:
             meta_p = (peers["meta_recv"] if peers is not None else
                       [self.meta_recv.data_ptr() + r * self.cap * mb for r in range(self.n)])
             self.t_dst2 = self._ptr_table(meta_p)
+        self._src_tables = {}
         if x is not None:
-            self.t_src_d = self._ptr_table([x.data_ptr() + r * Tr * H * esz for r in range(self.n_local)])
-            self.x = x
+            self._use_input(x)
+
+    def _use_input(self, x: torch.Tensor) -> None:
+        """Point the dispatch at ``x``. Tables are cached per input address, so
+        alternating between a few (e.g. double-buffered) inputs never builds a
+        table -- a host->device copy -- inside the forward."""
+        key = x.data_ptr()
+        t = self._src_tables.get(key)
+        if t is None:
+            Tr, H = self.cfg.tokens_per_rank, self.cfg.hidden
+            t = self._ptr_table([key + r * Tr * H * 2 for r in range(self.n_local)])
+            if len(self._src_tables) >= 8:
+                self._src_tables.clear()
+            self._src_tables[key] = t
+        self.t_src_d = t
+        self.x = x
 
     # ------------------------------------------------------------ stages
     def route(self, x: torch.Tensor, stream: int) -> None:
@@ -297,7 +321,7 @@ class AuroraMoELayer:
             self.counts.data_ptr(), None if self.bw is None else self.bw.data_ptr(), self.n,
             self.phase_recv.data_ptr(), self.phase_dur.data_ptr(), self.sched_i.data_ptr(),
             self.chunks.data_ptr(), self.rchunks.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
-            self.sched_i[1:].data_ptr(), stream), "aurora_schedule_counts")
+            self.sched_i[1:].data_ptr(), self.progress.data_ptr(), stream), "aurora_schedule_counts")
 
     def pack(self, stream: int) -> None:
         cfg = self.cfg
@@ -321,15 +345,18 @@ class AuroraMoELayer:
         plane2 = self.G > 1 and not combine
         _lib.check(self.L.aurora_engine(
             mode | sys_scope, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
-            self.rchunks.data_ptr(), self.sched_i.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
+            self.rchunks.data_ptr(), self.progress.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
             self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
             self.meta_bytes if plane2 else 0,
             ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), stream), "aurora_engine")
 
-    def dispatch(self, stream: int, part: str = "all") -> None:
-        self._engine({"all": 0, "local": 4, "remote": 8}[part] | self.unpaced, stream)
+    def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
+        """``overlap_schedule``: launched right after :meth:`schedule` on the same
+        stream, start while K2 still runs (PDL) and follow its progress word."""
+        self._engine({"all": 0, "local": 4, "remote": 8}[part] | self.unpaced | (32 if overlap_schedule else 0),
+                     stream)
 
     def experts(self, stream: int, part: str = "all") -> None:
         """SwiGLU experts over this process's receive buffers: all rows, the
@@ -376,27 +403,36 @@ class AuroraMoELayer:
     def combine(self, stream: int) -> None:
         self._engine(1 | self.unpaced, stream)
 
-    def aggregate(self, stream: int) -> None:
+    def aggregate(self, stream: int, out: Optional[torch.Tensor] = None) -> None:
         cfg = self.cfg
+        out = self.out if out is None else out
         _lib.check(self.L.aurora_aggregate(self.ret.data_ptr(), self.ret_stride, self.soff.data_ptr(),
                                            self.pos.data_ptr(), self.slot_dst.data_ptr(), self.topk_w.data_ptr(),
                                            self.T_local, cfg.top_k, cfg.hidden, self.n, self.rank_base,
-                                           cfg.tokens_per_rank, 1 if self.G > 1 else 0, self.out.data_ptr(),
+                                           cfg.tokens_per_rank, 1 if self.G > 1 else 0, out.data_ptr(),
                                            stream), "aurora_aggregate")
 
     # ------------------------------------------------------------ forward
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
-        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape.
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape,
+        written to ``out`` when given (e.g. one of several pipelined output
+        buffers), else to the layer's own ``self.out``.
 
         Stream plan (no host synchronisation anywhere):
-          main: route -> (counts exchange) -> pack -+-> schedule -> dispatch(network rows) --+
-          side:                                     +-> copy local rows -> experts(local) ---+
-          main: experts(network rows) -> combine (reversed schedule) -> aggregate
+          route -> (counts exchange) -> pack -> K2 schedule ---------------------------+
+                                                  \-> dispatch (PDL: local rows, then phase k
+                                                       as soon as K2 publishes it) -> experts
+          -> combine (reversed schedule) -> aggregate
+        AURORA_OVERLAP=schedule|full instead runs the local rows' expert GEMM on a
+        side stream beside K2 and the network dispatch (measured slower).
         """
         if x.dtype != torch.bfloat16 or x.shape != (self.T_local, self.cfg.hidden) or not x.is_contiguous():
             raise ValueError(f"x must be contiguous bf16 [{self.T_local}, {self.cfg.hidden}]")
+        if out is not None and (out.dtype != torch.bfloat16 or out.shape != x.shape or not out.is_contiguous()
+                                or out.device != x.device):
+            raise ValueError("out must be a contiguous bf16 tensor shaped like x on the same device")
         if self.x is None or x.data_ptr() != self.x.data_ptr():
-            self._tables_for(x, getattr(self, "_peers", None))
+            self._use_input(x)
         main = torch.cuda.current_stream(self.dev)
         s = int(main.cuda_stream)
         tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
@@ -411,9 +447,16 @@ class AuroraMoELayer:
         self.pack(s)
         mark("packed", main)
         if not self.overlap:
-            self.schedule(s)
-            self.dispatch(s)
-            self.experts(s)
+            if self.stream_schedule:
+                self.progress.zero_()  # stream-ordered before both K2 and the engine read it
+                self.schedule(s)
+                self.dispatch(s, overlap_schedule=True)
+                mark("dispatched", main)
+                self.experts(s)
+            else:
+                self.schedule(s)
+                self.dispatch(s)
+                self.experts(s)
         else:
             self._ev_pack.record(main)
             self.side.wait_event(self._ev_pack)
@@ -446,9 +489,9 @@ class AuroraMoELayer:
         mark("experts_done", main)
         self.combine(s)
         mark("combined", main)
-        self.aggregate(s)
+        self.aggregate(s, out)
         mark("end", main)
-        return self.out
+        return self.out if out is None else out
 
     TRACE_POINTS = ("start", "packed", "local_copied", "local_gemm_done", "scheduled", "dispatched", "joined",
                     "experts_done", "combined", "end")
@@ -488,6 +531,7 @@ class AuroraMoELayer:
         self.n_in.copy_(torch.from_numpy(n_in))
         self.n_out.copy_(torch.from_numpy(n_out))
         self.sched_i[0] = len(sched.phases)
+        self.progress.fill_(len(sched.phases) | PROGRESS_DONE)
 
     def schedule_objects(self):
         """The current batch's schedule as reference-shaped CommSchedule (debug / drop-in parity)."""

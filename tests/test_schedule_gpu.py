@@ -82,41 +82,34 @@ def test_device_schedule_errors(A):
 
 
 def _expected_chunks(phases, counts, n):
-    """Host restatement of the engine tables: per phase and sender the
-    (receiver, first, count, arrival index); same-pair runs that are
-    consecutive for both sender and receiver are one chunk."""
+    """Host restatement of the engine tables: one entry per phase and sender
+    (receiver, first, count, run code); a run = consecutive phases of one pair,
+    coded r (index among the receiver's runs) first, -1-r on continuations."""
     P = len(phases)
     ch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
     rch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
     issued = np.zeros((n, n), dtype=np.int64)
     rcnt = [0] * n
-    sseq = [0] * n
-    last_j = [-1] * n
-    last_k = [-1] * n
-    last_from = [-1] * n
+    scnt = [0] * n
+    prev = [-1] * n
     for k, (transfers, dur) in enumerate(phases):
         tok = int(round(dur))
-        opened = []
+        cur = [-1] * n
         for i, j in transfers:
             start = int(issued[i, j])
             issued[i, j] += tok
-            if last_j[i] == j and last_from[j] == i:
-                kk = last_k[i]
-                a = ch[kk][i]
-                ch[kk][i] = (a[0], a[1], a[2] + tok, a[3])
-                b = rch[kk][j]
-                rch[kk][j] = (b[0], b[1], b[2] + tok, b[3])
+            cont = prev[i] == j
+            if cont:
+                r, s = rcnt[j] - 1, scnt[i] - 1
             else:
-                ch[k][i] = (j, start, tok, rcnt[j])
-                rch[k][j] = (i, start, tok, sseq[i])
-                sseq[i] += 1
-                last_j[i], last_k[i] = j, k
-                opened.append(j)
-        for i, j in transfers:
-            last_from[j] = i
-        for j in opened:
-            rcnt[j] += 1
-    return ch, rch, rcnt, sseq
+                r, s = rcnt[j], scnt[i]
+                rcnt[j] += 1
+                scnt[i] += 1
+            ch[k][i] = (j, start, tok, -1 - r if cont else r)
+            rch[k][j] = (i, start, tok, -1 - s if cont else s)
+            cur[i] = j
+        prev = cur
+    return ch, rch, rcnt, scnt
 
 
 def test_counts_path_int_domain_and_chunk_tables(A):
@@ -141,9 +134,10 @@ def test_counts_path_int_domain_and_chunk_tables(A):
         rchunks = torch.empty(P, n, 4, **i32)
         n_in = torch.empty(n, **i32)
         n_out = torch.empty(n, **i32)
+        prog = torch.zeros(1, **i32)
         rc = L.aurora_schedule_counts(counts.data_ptr(), None, n, pr.data_ptr(), pd.data_ptr(), si.data_ptr(),
                                       chunks.data_ptr(), rchunks.data_ptr(), n_in.data_ptr(), n_out.data_ptr(),
-                                      si[1:].data_ptr(), _lib.stream_ptr())
+                                      si[1:].data_ptr(), prog.data_ptr(), _lib.stream_ptr())
         assert rc == 0
         torch.cuda.synchronize()
         nph, status = si.tolist()
@@ -158,3 +152,4 @@ def test_counts_path_int_domain_and_chunk_tables(A):
         assert [[tuple(x) for x in row] for row in chunks[:nph].tolist()] == ch
         assert [[tuple(x) for x in row] for row in rchunks[:nph].tolist()] == rch
         assert n_in.tolist() == rcnt and n_out.tolist() == sseq
+        assert int(prog.item()) == nph | (1 << 20)

@@ -6,7 +6,7 @@ from paper_2410_17043_b200 import _lib
 from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
 
 L = _lib.load()
-names = ["snap+mask", "match", "update", "strip", "decompose", "prologue", "kernel", "chunks"]
+names = ["w0:snap+mask", "w0:match", "w0:update+publish", "w1:strip+chunks busy", "-", "prologue", "kernel", "w1:total"]
 for n, T in ((8, 16384), (16, 16384)):
     cfg = MoEConfig(hidden=256, ffn=256, experts=n, top_k=2, tokens=T, ranks=n, skew=1.0, seed=0)
     layer = AuroraMoELayer(cfg)
