@@ -149,7 +149,12 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * mode bit 5: launch as a programmatic dependent (PDL) of the immediately
  * preceding aurora_schedule_counts on the same stream -- the engine starts
  * while K2 runs (K2 triggers its dependents on entry, so it is resident first)
- * and consumes phases through `progress`. Continuation entries of a run need no hand-over, so a handshake only
+ * and consumes phases through `progress`; mode bit 6: copy with 256-thread
+ * CTAs of 16-byte vector loads/stores instead of the default TMA engine (two
+ * warps per CTA: a producer streaming rows into shared-memory slots with
+ * cp.async.bulk, a consumer bulk-storing them into the receiver once its
+ * run may start -- the next run's rows are prefetched across the hand-over).
+ * Continuation entries of a run need no hand-over, so a handshake only
  * happens where the schedule changes partners. Local (diagonal) rows are
  * copied first; then phase k is executed as soon as progress (K2's progress
  * word) covers it, so the engine may run concurrently with K2 on another

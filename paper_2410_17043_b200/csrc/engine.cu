@@ -21,6 +21,7 @@
 // reference's CommSchedule.reversed() (commsched.py:310-319) -- from the
 // rchunks table, sending expert outputs back to the token owners.
 #include "common.cuh"
+#include "tc_helpers.cuh"
 
 namespace {
 
@@ -225,6 +226,310 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   }
 }
 
+// ============================================================================
+// TMA engine (default): the same schedule semantics, rows moved by the bulk
+// copy engine -- cp.async.bulk global -> shared (the sender's rows, gathered
+// through the send list) and cp.async.bulk shared -> global (the receiver's
+// buffer, peer memory over NVSwitch at N > 1). Two warps per CTA:
+//   warp 0 (producer) walks the CTA's rows in schedule order and keeps up to
+//          S row slots of shared memory filling; it never waits for a
+//          receiver, so the next run's rows are already on chip while the
+//          previous sender into that receiver finishes (prefetch across the
+//          hand-over);
+//   warp 1 (consumer) waits for the hand-over at each run start, stores the
+//          landed rows with bulk stores, recycles slots once a store has read
+//          them, and at each run end waits for its stores to complete and
+//          signals the receiver's arrival counter.
+// A row's slot holds the row and its optional second-plane record.
+// ============================================================================
+constexpr int TMA_THREADS = 64;
+
+__device__ __forceinline__ void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_smem),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+// bounded wait: false if *abort was raised meanwhile
+__device__ __forceinline__ bool mbar_wait_or_abort(uint64_t* bar, uint32_t parity, volatile int* abort) {
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(tc::smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return true;
+    if (*abort) return false;
+  }
+}
+
+// One warp's view of the schedule: entries of sender g in phase order, read 32
+// at a time (one L2 round trip per window) as K2 publishes them.
+struct EntryWindow {
+  int4* win;      // [32] shared
+  int base, cnt;  // window covers entries [base, base + cnt)
+  int avail;      // phases known final
+  bool done;
+};
+
+// warp-collective. Returns false at the end of the schedule (or on timeout).
+__device__ bool entry_at(const EngineParams& p, const int4* table, int g, int k, EntryWindow& w, int4& e,
+                         volatile int* abort) {
+  const int lane = threadIdx.x & 31;
+  if (k >= w.base + w.cnt) {
+    if (k >= w.avail && !w.done) {
+      int pr = 0, fail = 0;
+      if (lane == 0) {
+        long long spins = 0;
+        for (;;) {
+          pr = ld_acquire_gpu(p.progress);
+          if ((pr & AURORA_PROGRESS_COUNT) > k || (pr & AURORA_PROGRESS_DONE)) break;
+          if (*abort) { fail = 1; break; }
+          if (p.spin_limit && ++spins > p.spin_limit) {
+            atomicExch(p.status, AURORA_ETIMEOUT);
+            *abort = 1;
+            fail = 1;
+            break;
+          }
+          if (spins > 16) __nanosleep(32);
+        }
+      }
+      pr = __shfl_sync(0xffffffffu, pr, 0);
+      if (__shfl_sync(0xffffffffu, fail, 0)) return false;
+      w.avail = min(pr & AURORA_PROGRESS_COUNT, p.max_phases);
+      w.done = (pr & AURORA_PROGRESS_DONE) != 0;
+    }
+    if (k >= w.avail) return false;  // done and exhausted
+    w.base = k;
+    w.cnt = min(32, w.avail - k);
+    if (lane < w.cnt) w.win[lane] = __ldcg(&table[(size_t)(k + lane) * p.n + g]);
+    __syncwarp();
+  }
+  e = w.win[k - w.base];
+  return true;
+}
+
+struct TmaShared {
+  uint64_t full[16], empty[16];
+  int4 win[2][32];
+  int32_t idx[32];
+  // per-call metadata staged once: every per-entry lookup is a shared-memory read
+  int32_t soff[AUR_MAXN * AUR_MAXN], roff[AUR_MAXN * AUR_MAXN];
+  char* dst[AUR_MAXN];
+  char* dst2[AUR_MAXN];
+  int32_t* ctr[AUR_MAXN];
+  int nloc;
+  int abort;
+  long long issued, consumed;
+};
+
+__global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p, int S, int slot_bytes) {
+  extern __shared__ __align__(128) unsigned char slots[];
+  __shared__ TmaShared sh;
+  const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
+  const int g = p.rank_base + r_local;
+  const int n = p.n, C = p.C;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool dispatch = (p.mode & 1) == 0;
+  const bool sys = (p.mode & 2) != 0;
+  const bool do_remote = (p.mode & 4) == 0;
+  const bool do_local = (p.mode & 8) == 0;
+  const bool paced = (p.mode & 16) == 0;
+  const int rb = p.row_bytes, rb2 = p.src2_bufs ? p.row2_bytes : 0;
+  const int4* table = dispatch ? p.chunks : p.rchunks;
+  volatile int* abort = &sh.abort;
+  for (int q = threadIdx.x; q < n * n; q += TMA_THREADS) {
+    sh.soff[q] = p.soff[q];
+    sh.roff[q] = p.roff[q];
+  }
+  for (int q = threadIdx.x; q < n; q += TMA_THREADS) {
+    sh.dst[q] = p.dst_bufs[q];
+    sh.dst2[q] = rb2 ? p.dst2_bufs[q] : nullptr;
+    sh.ctr[q] = p.ctrs[q];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; s++) {
+      tc::mbar_init(&sh.full[s], 1);
+      tc::mbar_init(&sh.empty[s], 1);
+    }
+    sh.abort = 0;
+    sh.nloc = p.counts[g * n + g];
+    sh.issued = sh.consumed = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t slot0 = tc::smem_u32(slots);
+
+  // item = the local rows (k = -1) or schedule entry k; this CTA's rows [r0, r1)
+  auto slice = [&](int ntok, int& r0, int& r1) {
+    const int per = (ntok + C - 1) / C;
+    r0 = min(ntok, c * per);
+    r1 = min(ntok, r0 + per);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    EntryWindow w{sh.win[0], 0, 0, 0, false};
+    long long t = 0;  // rows issued
+    int s = 0;        // slot of row t
+    uint32_t u = 0;   // fill round of slot s (t / S)
+    const char* src = p.src_bufs[r_local];
+    const char* src2 = rb2 ? p.src2_bufs[r_local] : nullptr;
+    const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
+    for (int k = do_local ? -1 : 0; do_remote || k < 0; k++) {
+      int peer, first, ntok;
+      if (k < 0) {
+        peer = g, first = 0, ntok = sh.nloc;
+      } else {
+        int4 e;
+        if (!entry_at(p, table, g, k, w, e, abort)) break;
+        if (e.x < 0) continue;
+        peer = e.x, first = e.y, ntok = e.z;
+      }
+      int r0, r1;
+      slice(ntok, r0, r1);
+      // source rows: dispatch gathers x rows through the send list (pair (g, peer)
+      // starts at soff[g][peer]); combine reads expert outputs of pair (peer, g)
+      const int base = dispatch ? sh.soff[g * n + peer] + first : sh.roff[peer * n + g] + first;
+      for (int b = r0; b < r1; b += 32) {
+        const int cnt = min(32, r1 - b);
+        if (dispatch) {
+          if (lane < cnt) sh.idx[lane] = __ldg(&list[base + b + lane]);
+          __syncwarp();
+        }
+        if (lane == 0) {
+          for (int q = 0; q < cnt; q++) {
+            if (u > 0 && !mbar_wait_or_abort(&sh.empty[s], (u - 1) & 1, abort)) break;
+            const long long row = dispatch ? sh.idx[q] : (long long)(base + b + q);
+            const uint32_t dst = slot0 + (uint32_t)(s * slot_bytes);
+            tc::mbar_expect_tx(&sh.full[s], rb + rb2);
+            bulk_load(dst, src + row * rb, rb, &sh.full[s]);
+            if (rb2) bulk_load(dst + rb, src2 + (long long)(base + b + q) * rb2, rb2, &sh.full[s]);
+            t++;
+            if (++s == S) { s = 0; u++; }
+          }
+        }
+        __syncwarp();
+        if (*abort) break;
+      }
+      if (*abort) break;
+    }
+    if (lane == 0) sh.issued = t;
+  } else {
+    // ------------------------------------------------------------ consumer
+    EntryWindow w{sh.win[1], 0, 0, 0, false};
+    long long t = 0, released = 0;
+    int s = 0, rs = 0;  // slot of row t; slot of row `released`
+    uint32_t u = 0;
+    auto release_upto = [&](long long upto) {  // slots of rows < upto may be refilled
+      for (; released < upto; released++) {
+        mbar_arrive(&sh.empty[rs]);
+        if (++rs == S) rs = 0;
+      }
+    };
+    int prev_peer = -1;  // peer of the open run (-1: none)
+    for (int k = do_local ? -1 : 0; do_remote || k < 0; k++) {
+      int peer, first, ntok;
+      if (k < 0) {
+        peer = g, first = 0, ntok = sh.nloc;
+      } else {
+        int4 e;
+        const bool more = entry_at(p, table, g, k, w, e, abort);
+        // a run ends where this sender's entries stop continuing it
+        const bool cont = more && e.x >= 0 && e.x == prev_peer && e.w < 0;
+        if (prev_peer >= 0 && !cont) {
+          if (lane == 0) {
+            bulk_wait_all();  // every store of the run has completed
+            release_upto(t);
+            // async-proxy writes -> generic release (cumulative) on the receiver's counter
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (sys) red_release_sys_add(sh.ctr[prev_peer], 1);
+            else red_release_gpu_add(sh.ctr[prev_peer], 1);
+          }
+          prev_peer = -1;
+        }
+        if (!more) break;
+        if (e.x < 0) continue;
+        peer = e.x, first = e.y, ntok = e.z;
+        if (!cont) {  // run start: every earlier run into `peer` must have landed
+          prev_peer = peer;
+          if (paced && lane == 0 && !wait_ge(sh.ctr[peer], e.w * C, p.spin_limit, sys)) {
+            atomicExch(p.status, AURORA_ETIMEOUT);
+            *abort = 1;
+          }
+          __syncwarp();
+          if (*abort) break;
+        }
+      }
+      int r0, r1;
+      slice(ntok, r0, r1);
+      const long long drow0 = dispatch ? (long long)sh.roff[g * n + peer] + first : (long long)sh.soff[peer * n + g] + first;
+      char* dst = sh.dst[peer];
+      char* dst2 = sh.dst2[peer];
+      if (lane == 0) {
+        for (int r = r0; r < r1; r++) {
+          if (!mbar_wait_or_abort(&sh.full[s], u & 1, abort)) break;
+          const uint32_t sp = slot0 + (uint32_t)(s * slot_bytes);
+          bulk_store(dst + (drow0 + r) * rb, sp, rb);
+          if (rb2) bulk_store(dst2 + (drow0 + r) * rb2, sp + rb, rb2);
+          bulk_commit();
+          t++;
+          if (++s == S) { s = 0; u++; }
+          // keep a few stores reading their slots; older slots go back to the producer
+          if (S >= 8) {
+            bulk_wait_read<4>();
+            release_upto(t - 4);
+          } else {
+            bulk_wait_read<1>();
+            release_upto(t - 1);
+          }
+        }
+      }
+      __syncwarp();
+      if (*abort) break;
+    }
+    if (lane == 0) {
+      bulk_wait_all();
+      release_upto(t);
+      sh.consumed = t;
+    }
+    // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
+    if (do_remote && !*abort && c == 0 && lane == 0) {
+      const int expect = (dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g])) * C;
+      if (!wait_ge(sh.ctr[g], expect, p.spin_limit, sys)) {
+        atomicExch(p.status, AURORA_ETIMEOUT);
+      } else {
+        *(volatile int32_t*)sh.ctr[g] = 0;
+        __threadfence_system();
+      }
+    }
+  }
+  // on abort: let every issued load land before the CTA's shared memory is released
+  __syncthreads();
+  if (threadIdx.x == 0 && sh.abort)
+    for (long long q = sh.consumed; q < sh.issued; q++) tc::mbar_wait(&sh.full[q % S], (uint32_t)(q / S) & 1);
+}
+
 // K7: out[t] = sum over slots of (w *) returned rows, fp32 accumulate, bf16 out. Warp per token.
 __global__ void __launch_bounds__(THREADS) aggregate_kernel(
     const __nv_bfloat16* __restrict__ ret, long long ret_stride_rows, const int32_t* __restrict__ soff,
@@ -279,7 +584,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, void* stream) {
-  if (mode < 0 || mode > 63 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+  if (mode < 0 || mode > 127 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !progress || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
@@ -288,9 +593,21 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0) != cudaSuccess ||
-      occ < 1)
+  // mode bit 6: the LSU engine (256-thread CTAs, 16-byte vector loads/stores)
+  // instead of the TMA bulk-copy engine
+  const bool lsu = (mode & 64) != 0;
+  const int rb2 = src2_bufs ? row2_bytes : 0;
+  const int slot_bytes = ((row_bytes + rb2 + 127) / 128) * 128;
+  const int S = max(2, min(16, (96 * 1024) / slot_bytes));
+  const size_t dyn = lsu ? 0 : (size_t)S * slot_bytes;
+  if (!lsu && dyn > 200 * 1024) return AURORA_EINVAL;
+  if (!lsu && cudaFuncSetAttribute(engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+                  cudaSuccess)
     return AURORA_ECUDA;
+  const cudaError_t oe = lsu ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_tma_kernel,
+                                                                             TMA_THREADS, dyn);
+  if (oe != cudaSuccess || occ < 1) return AURORA_ECUDA;
   // every copy CTA spins on flags written by others: all of them must be
   // co-resident. Clamp deterministically (every process computes the same C).
   ctas_per_rank = min(ctas_per_rank, (occ * sms) / n_local);
@@ -324,7 +641,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.status = status;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_local * ctas_per_rank);
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(lsu ? THREADS : TMA_THREADS);
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute attr[1];
   if (mode & 32) {  // programmatic dependent of the preceding K2 launch: start while it runs
@@ -333,7 +651,9 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  if (cudaLaunchKernelEx(&cfg, engine_kernel, p) != cudaSuccess) return AURORA_ECUDA;
+  const cudaError_t le = lsu ? cudaLaunchKernelEx(&cfg, engine_kernel, p)
+                             : cudaLaunchKernelEx(&cfg, engine_tma_kernel, p, S, slot_bytes);
+  if (le != cudaSuccess) return AURORA_ECUDA;
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -180,6 +180,8 @@ class AuroraMoELayer:
             self.overlap = False
         self.C_overlap = int(os.environ.get("AURORA_C_OVERLAP", "0"))  # copy CTAs/rank beside the GEMM
         self.unpaced = 0  # 16: ablation -- run the all-to-all without the schedule's pacing
+        # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
+        self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         self.trace = None
         self.side = torch.cuda.Stream(device=dev)
         self._ev_pack = torch.cuda.Event()
@@ -344,7 +346,7 @@ class AuroraMoELayer:
         sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
         plane2 = self.G > 1 and not combine
         _lib.check(self.L.aurora_engine(
-            mode | sys_scope, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            mode | sys_scope | self.engine_lsu, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.progress.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
@@ -414,7 +416,7 @@ class AuroraMoELayer:
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape,
+        r"""x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape,
         written to ``out`` when given (e.g. one of several pipelined output
         buffers), else to the layer's own ``self.out``.
 
