@@ -199,6 +199,7 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 // ============================================================================
 
 #include "fastmatch.cuh"
+#include "fastmatch8b.cuh"
 
 // Value domain of the fast path. Homogeneous integer traffic (the in-layer
 // path: int32 token counts, B = 1) is exact in int32, where every eps test of
@@ -419,20 +420,20 @@ __device__ void decompose_warp(const SchedParams& p, const double* rem_in, const
       const uint32_t p1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? pref << sh : 0u);
       const uint32_t s0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? sup << sh : 0u);
       const uint32_t s1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? sup << sh : 0u);
-      uint32_t mlw = 0, ok = 0;
+      uint32_t mlo = 0, mhi = 0, ok = 0;
       if (lane == 0) {
-        FastMatch8 f8;
-        f8.pref[0] = p0;
-        f8.pref[1] = p1;
-        f8.sup[0] = s0;
-        f8.sup[1] = s1;
+        FastMatch8b f8;
+        f8.P = ((uint64_t)p1 << 32) | p0;
+        f8.S = ((uint64_t)s1 << 32) | s0;
         ok = f8.run(n) ? 1u : 0u;
-        mlw = f8.ml;
+        mlo = (uint32_t)f8.ML;
+        mhi = (uint32_t)(f8.ML >> 32);
       }
-      mlw = __shfl_sync(0xffffffffu, mlw, 0);
+      mlo = __shfl_sync(0xffffffffu, mlo, 0);
+      mhi = __shfl_sync(0xffffffffu, mhi, 0);
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (!ok) { status = AURORA_ENOMATCH; break; }
-      pj = on ? (int)((mlw >> (4 * lane)) & 15u) : 0;
+      pj = on ? (int)(((lane < 4 ? mlo : mhi) >> (8 * (lane & 3))) & 15u) : 0;
     } else {
       if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
       __syncwarp();

@@ -5,6 +5,7 @@
 #include <random>
 
 #include "../../paper_2410_17043_b200/csrc/fastmatch.cuh"
+#include "../../paper_2410_17043_b200/csrc/fastmatch8b.cuh"
 
 extern "C" int oracle_perfect_matching_masks(int n, const uint32_t* sup, const uint32_t* pref, int* perm);
 
@@ -73,6 +74,18 @@ static int check8(std::mt19937& rng, int iters) {
     if (same && ok)
       for (int u = 0; u < n; u++) same &= (int)FastMatch8::getn(fm.ml, u) == ref[u];
     if (!same && bad++ < 5) std::printf("mismatch FastMatch8 n=%d ok=%d/%d\n", n, (int)ok, ok_ref);
+    // the K2 fast path (shift-register stacks, byte tables)
+    FastMatch8b fb;
+    fb.P = fb.S = 0;
+    for (int u = 0; u < n; u++) {
+      fb.P |= (uint64_t)pref[u] << (8 * u);
+      fb.S |= (uint64_t)sup[u] << (8 * u);
+    }
+    const bool okb = fb.run(n);
+    bool sameb = okb == (bool)ok_ref;
+    if (sameb && okb)
+      for (int u = 0; u < n; u++) sameb &= (int)((fb.ML >> (8 * u)) & 15) == ref[u];
+    if (!sameb && bad++ < 5) std::printf("mismatch FastMatch8b n=%d ok=%d/%d\n", n, (int)okb, ok_ref);
   }
   return bad;
 }
