@@ -260,6 +260,11 @@ int aurora_debug_schedule_cycles(const double* d, int n, long long* prof, int32_
  * cycles to the device array prof[8] = {snap+masks, matching, update, strip,
  * decompose, prologue, whole kernel, chunk pass}; NULL turns it off. */
 int aurora_debug_set_schedule_profile(long long* prof);
+/* Diagnostics timelines (%globaltimer ns; NULL switches off): K2 records the
+ * time each phase is published at trace[count & 511]; the TMA engine records
+ * per copy CTA {start, local rows done, end, -} at trace[4 * cta]. */
+int aurora_debug_set_schedule_trace(long long* trace);
+int aurora_debug_set_engine_trace(long long* trace);
 
 #ifdef __cplusplus
 }

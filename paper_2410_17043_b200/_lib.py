@@ -41,6 +41,8 @@ _SIGNATURES = {
     "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "aurora_debug_set_schedule_profile": [_vp],
+    "aurora_debug_set_schedule_trace": [_vp],
+    "aurora_debug_set_engine_trace": [_vp],
     "aurora_ipc_handle_bytes": [],
     "aurora_ipc_get": [_vp, _vp, _vp],
     "aurora_ipc_open": [_vp, _c_i64, _vp],

@@ -329,9 +329,21 @@ __device__ bool entry_at(const EngineParams& p, const int4* table, int g, int k,
   return true;
 }
 
+constexpr int RING = 128;
+
+// diagnostics: per copy CTA {start, local rows done, end} in %globaltimer ns
+__device__ long long* g_engine_trace = nullptr;
+__device__ __forceinline__ long long eng_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}  // schedule entries the producer may run ahead of the consumer
+
 struct TmaShared {
   uint64_t full[16], empty[16];
-  int4 win[2][32];
+  int4 win[32];     // producer's window of global entries
+  int4 ring[RING];  // entries handed to the consumer (producer -> consumer, in order)
+  volatile int known, known_done, cons_k;
   int32_t idx[32];
   // per-call metadata staged once: every per-entry lookup is a shared-memory read
   int32_t soff[AUR_MAXN * AUR_MAXN], roff[AUR_MAXN * AUR_MAXN];
@@ -375,9 +387,13 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     sh.abort = 0;
     sh.nloc = p.counts[g * n + g];
     sh.issued = sh.consumed = 0;
+    sh.known = 0;
+    sh.known_done = 0;
+    sh.cons_k = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0 && g_engine_trace) g_engine_trace[blockIdx.x * 4] = eng_ns();
   const uint32_t slot0 = tc::smem_u32(slots);
 
   // item = the local rows (k = -1) or schedule entry k; this CTA's rows [r0, r1)
@@ -389,7 +405,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    EntryWindow w{sh.win[0], 0, 0, 0, false};
+    EntryWindow w{sh.win, 0, 0, 0, false};
     long long t = 0;  // rows issued
     int s = 0;        // slot of row t
     uint32_t u = 0;   // fill round of slot s (t / S)
@@ -403,6 +419,15 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       } else {
         int4 e;
         if (!entry_at(p, table, g, k, w, e, abort)) break;
+        // hand the entry to the consumer (it never reads the global table itself)
+        if (lane == 0) {
+          while (k - sh.cons_k >= RING - 1 && !*abort) {
+          }
+          sh.ring[k & (RING - 1)] = e;
+          __threadfence_block();
+          sh.known = k + 1;
+        }
+        __syncwarp();
         if (e.x < 0) continue;
         peer = e.x, first = e.y, ntok = e.z;
       }
@@ -434,10 +459,13 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       }
       if (*abort) break;
     }
-    if (lane == 0) sh.issued = t;
+    if (lane == 0) {
+      sh.issued = t;
+      __threadfence_block();
+      sh.known_done = 1;
+    }
   } else {
     // ------------------------------------------------------------ consumer
-    EntryWindow w{sh.win[1], 0, 0, 0, false};
     long long t = 0, released = 0;
     int s = 0, rs = 0;  // slot of row t; slot of row `released`
     uint32_t u = 0;
@@ -453,8 +481,16 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       if (k < 0) {
         peer = g, first = 0, ntok = sh.nloc;
       } else {
-        int4 e;
-        const bool more = entry_at(p, table, g, k, w, e, abort);
+        int4 e = make_int4(-1, 0, 0, 0);
+        if (lane == 0) {
+          while (k >= sh.known && !sh.known_done && !*abort) {
+          }
+          sh.cons_k = k;
+        }
+        __syncwarp();
+        __threadfence_block();
+        const bool more = k < sh.known && !*abort;
+        if (more) e = sh.ring[k & (RING - 1)];
         // a run ends where this sender's entries stop continuing it
         const bool cont = more && e.x >= 0 && e.x == prev_peer && e.w < 0;
         if (prev_peer >= 0 && !cont) {
@@ -506,12 +542,14 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
         }
       }
       __syncwarp();
+      if (k < 0 && lane == 0 && g_engine_trace) g_engine_trace[blockIdx.x * 4 + 1] = eng_ns();
       if (*abort) break;
     }
     if (lane == 0) {
       bulk_wait_all();
       release_upto(t);
       sh.consumed = t;
+      if (g_engine_trace) g_engine_trace[blockIdx.x * 4 + 2] = eng_ns();
     }
     // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
     if (do_remote && !*abort && c == 0 && lane == 0) {
@@ -656,6 +694,10 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   if (le != cudaSuccess) return AURORA_ECUDA;
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
+}
+
+extern "C" int aurora_debug_set_engine_trace(long long* trace) {
+  return cudaMemcpyToSymbol(g_engine_trace, &trace, sizeof(trace)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }
 
 extern "C" int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows,

@@ -349,11 +349,22 @@ __device__ void chunk_finish(const SchedParams& p, const ChunkCtx& c, const Chun
   if (lane < n) p.n_in[lane] = c.rcnt[lane];
 }
 
+// diagnostics: when set, every publication records %globaltimer (ns) at
+// g_sched_trace[count & 511] (aurora_debug_set_schedule_trace)
+__device__ long long* g_sched_trace = nullptr;
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void publish(int32_t* progress, int value, int lane) {
   __syncwarp();
   if (lane == 0 && progress) {
     __threadfence();
     st_release_gpu(progress, value);
+    if (g_sched_trace) g_sched_trace[(value & AURORA_PROGRESS_COUNT) & 511] = global_ns();
   }
 }
 
@@ -616,6 +627,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   // `progress` instead of waiting for this grid) start now: this CTA is
   // resident, so the engine can never starve it of an SM
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0 && g_sched_trace) g_sched_trace[0] = global_ns();
   if (!p.prof) p.prof = g_sched_prof;  // diagnostics hook (aurora_debug_set_schedule_profile)
   if (tid == 0) {
     status_s = AURORA_OK;
@@ -856,6 +868,10 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
 
 // Diagnostics: make every subsequent K2 launch record its section cycles in
 // prof[8] (NULL switches it off).
+extern "C" int aurora_debug_set_schedule_trace(long long* trace) {
+  return cudaMemcpyToSymbol(g_sched_trace, &trace, sizeof(trace)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
+}
+
 extern "C" int aurora_debug_set_schedule_profile(long long* prof) {
   return cudaMemcpyToSymbol(g_sched_prof, &prof, sizeof(prof)) == cudaSuccess ? AURORA_OK
                                                                                 : AURORA_ECUDA;
@@ -864,8 +880,15 @@ extern "C" int aurora_debug_set_schedule_profile(long long* prof) {
 namespace {
 
 void launch_schedule(const SchedParams& p, cudaStream_t s) {
-  if (p.n <= 16)
-    aurora_schedule_kernel<16><<<1, 64, 0, s>>>(p);
+  if (p.n <= 16) {
+    // K2 is a latency-bound single-CTA kernel that the dispatch engine overlaps
+    // (PDL): reserve most of its SM's shared memory so no engine CTA -- whose
+    // waiting warps would share K2's issue slots -- is placed beside it
+    constexpr int kReserve = 150 * 1024;
+    static bool attr = cudaFuncSetAttribute(aurora_schedule_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            kReserve) == cudaSuccess;
+    aurora_schedule_kernel<16><<<1, 64, attr ? kReserve : 0, s>>>(p);
+  }
   else
     aurora_schedule_kernel<32><<<1, 32, 0, s>>>(p);
 }

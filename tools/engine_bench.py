@@ -53,3 +53,22 @@ for eng in ("tma", "lsu"):
     print(eng, "schedule+dispatch overlapped", res[f"{eng}/schedule+dispatch"], flush=True)
 json.dump(res, open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
                                  "engine_bench.json"), "w"), indent=1)
+
+# K2's own cycles when it runs alone vs. beside the PDL-launched engine
+layer.engine_lsu = 0
+prof = torch.zeros(8, dtype=torch.int64, device="cuda")
+L = _lib.load()
+L.aurora_debug_set_schedule_profile(prof.data_ptr())
+for mode in ("alone", "overlapped"):
+    tot = torch.zeros(8, dtype=torch.int64)
+    for _ in range(5):
+        layer.route(x, s); layer.pack(s); layer.progress.zero_()
+        layer.schedule(s)
+        if mode == "alone":
+            torch.cuda.synchronize()
+        layer.dispatch(s, overlap_schedule=(mode == "overlapped"))
+        torch.cuda.synchronize()
+        tot += prof.cpu()
+    print("K2", mode, "kernel cycles", int(tot[6]) // 5, "match", int(tot[1]) // 5, "w1 total", int(tot[7]) // 5, flush=True)
+L.aurora_debug_set_schedule_profile(None)
+layer.check_status()
