@@ -72,9 +72,14 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  *                     continuation entries (no hand-over needed: nobody else
  *                     sends to j in between).
  *   rchunks[P][n][4]  the same entries indexed by receiver j: {sender, first,
- *                     count, run code counted among the sender's runs} (the
+ *                     count, run code of the reversed run into the sender} (the
  *                     combine runs CommSchedule.reversed(), commsched.py:310-319)
- *   n_in[n], n_out[n] runs arriving at / leaving each rank
+ *   n_in[n], n_out[n] arrival signals each rank receives in the dispatch / combine
+ *   Hand-over thresholds and n_in / n_out count arrival signals: every copy CTA of
+ *   the sending rank signals once per run. The copy CTAs are the engine's
+ *   (aurora_engine_ctas): each process drives n_local ranks with ctas_dispatch /
+ *   ctas_combine CTAs in total, split among them by `split` (AURORA_SPLIT_*,
+ *   csrc/apportion.cuh). ctas_dispatch == 0: thresholds in runs (one signal per run).
  *   progress[1]       (nullable) written while the kernel runs: the number of
  *                     leading phases whose entries are final, then
  *                     n_phases | AURORA_PROGRESS_DONE once every output is
@@ -87,11 +92,15 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  * min(B_i,B_j); the pair's last entry absorbs the rounding so per-pair totals
  * are exact (such schedules publish progress only when complete). */
 #define AURORA_PROGRESS_DONE (1 << 20)
+#define AURORA_SPLIT_EVEN 0
+#define AURORA_SPLIT_VOLUME 1
+#define AURORA_SPLIT_BANDWIDTH 2
 #define AURORA_PROGRESS_COUNT ((1 << 20) - 1)
 int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32_t* phase_recv,
                            double* phase_dur, int32_t* n_phases, int32_t* chunks,
                            int32_t* rchunks, int32_t* n_in, int32_t* n_out, int32_t* status,
-                           int32_t* progress, void* stream);
+                           int32_t* progress, int n_local, int ctas_dispatch, int ctas_combine,
+                           int split, void* stream);
 
 /* ---------------------------------------------------------------- K1 ----
  * aurora_route: top-k gating + GPU x GPU traffic matrix. No reference
@@ -179,7 +188,13 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
                   const void* const* src_bufs, void* const* dst_bufs, int row_bytes,
                   const void* const* src2_bufs, void* const* dst2_bufs, int row2_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
-                  int32_t* status, void* stream);
+                  int32_t* status, int split, const double* bw, void* stream);
+/* aurora_engine_ctas: copy CTAs per local rank the engine will actually use
+ * (ctas_per_rank clamped so every copy CTA is co-resident), or -AURORA_E* on
+ * error. K2 needs n_local x this value to count hand-over thresholds. The
+ * engine's grid (n_local x that value) is split among its ranks by `split`
+ * (csrc/apportion.cuh; bw: rank bandwidths for AURORA_SPLIT_BANDWIDTH). */
+int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu);
 
 /* ---------------------------------------------------------------- K7 ----
  * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret_i[soff[i][dst_s] + pos[t][s]]

@@ -23,13 +23,15 @@ _SIGNATURES = {
     "aurora_raw_phase_cap": [_c_int],
     "aurora_phase_cap": [_c_int],
     "aurora_schedule_f64": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "aurora_schedule_counts": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "aurora_schedule_counts": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
+                               _c_int, _c_int, _vp],
     "aurora_route": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
                      _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
-                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _vp],
+                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp],
+    "aurora_engine_ctas": [_c_int, _c_int, _c_int, _c_int, _c_int],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp],
     "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],

@@ -83,12 +83,16 @@ def schedule_sjf(d, cluster) -> CommSchedule:
     return schedule_fixed_order(d, cluster, orders)
 
 
-def to_engine_tables(sched: CommSchedule, n: int):
+def to_engine_tables(sched: CommSchedule, n: int, ctas_d=None, ctas_c=None):
     """CommSchedule (token-unit durations) -> (chunks[P,n,4], rchunks[P,n,4],
     n_in[n], n_out[n]) in the engine's format (include/aurora_b200.h): one entry
     per phase and sender {receiver, first token, count, run code}; a run is a
-    stretch of consecutive phases of one pair, coded r (its index among the runs
-    into the receiver) on its first entry and -1-r on continuations."""
+    stretch of consecutive phases of one pair, coded by its hand-over threshold
+    (arrival signals of the earlier runs into the receiver; ctas_d / ctas_c =
+    copy CTAs per rank, each signalling once per run, default 1) on its first
+    entry and -1 on continuations."""
+    cd = [1] * n if ctas_d is None else list(ctas_d)
+    cc = [1] * n if ctas_c is None else list(ctas_c)
     P = max(1, len(sched.phases))
     ch = np.full((P, n, 4), 0, dtype=np.int32)
     ch[:, :, 0] = -1
@@ -106,14 +110,13 @@ def to_engine_tables(sched: CommSchedule, n: int):
             tok = int(round(cum[i, j])) - start
             issued[i, j] += tok
             cont = prev[i] == j
-            if cont:
-                r, s_ = rcnt[j] - 1, scnt[i] - 1
-            else:
+            r = s_ = -1
+            if not cont:
                 r, s_ = rcnt[j], scnt[i]
-                rcnt[j] += 1
-                scnt[i] += 1
-            ch[k, i] = (j, start, tok, -1 - r if cont else r)
-            rch[k, j] = (i, start, tok, -1 - s_ if cont else s_)
+                rcnt[j] += cd[i]
+                scnt[i] += cc[j]
+            ch[k, i] = (j, start, tok, r)
+            rch[k, j] = (i, start, tok, s_)
             cur[i] = j
         prev = cur
     return ch, rch, rcnt, scnt

@@ -22,6 +22,7 @@
 // rchunks table, sending expert outputs back to the token owners.
 #include "common.cuh"
 #include "tc_helpers.cuh"
+#include "apportion.cuh"
 
 namespace {
 
@@ -47,11 +48,38 @@ struct EngineParams {
   char* const* dst2_bufs;
   int row2_bytes;
   int32_t* const* ctrs;
-  int C;
+  int C;                 // copy CTAs per local rank at launch (grid = n_local * C)
+  int split;             // apportion.cuh mode: how the grid is split among local ranks
+  const double* bw;      // rank bandwidths (split mode 2) or nullptr
   int max_phases;
   long long spin_limit;
   int32_t* status;
 };
+
+// This CTA's rank (local index), its index among the rank's CTAs and the
+// rank's CTA count, from the same apportioning K2 used for the thresholds.
+__device__ void cta_assign(const EngineParams& p, int* cs /* smem [AUR_MAXN] */, int& r_local, int& c,
+                           int& C) {
+  __shared__ long long w_s[AUR_MAXN];
+  if (p.split == 0 || p.n_local == 1) {  // nothing to weigh
+    if (threadIdx.x < p.n_local) cs[threadIdx.x] = p.C;
+  } else {
+    for (int i = threadIdx.x; i < p.n; i += blockDim.x)
+      w_s[i] = aur_weight(p.counts, p.n, p.bw, p.n, i, p.split, (p.mode & 1) != 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int all[AUR_MAXN];
+      aur_apportion_w(w_s, p.n, p.n_local, p.n_local * p.C, all);
+      for (int r = 0; r < p.n_local; r++) cs[r] = all[p.rank_base + r];
+    }
+  }
+  __syncthreads();
+  int b = blockIdx.x, r = 0;
+  while (r < p.n_local - 1 && b >= cs[r]) b -= cs[r++];
+  r_local = r;
+  c = b;
+  C = cs[r];
+}
 
 // wait until *ctr >= target (thread 0), bounded. `sys`: the counter is written
 // by other GPUs (system scope); otherwise every rank lives on this GPU.
@@ -109,7 +137,9 @@ __device__ __forceinline__ void signal(int32_t* ctr, bool sys) {
 }
 
 __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
-  const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
+  __shared__ int cs[AUR_MAXN];
+  int r_local, c, C;
+  cta_assign(p, cs, r_local, c, C);
   const int g = p.rank_base + r_local;  // this CTA's rank (sender in this mode)
   const int n = p.n;
   const bool dispatch = (p.mode & 1) == 0;
@@ -128,7 +158,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   // core.py:95) and need no schedule: copy them while K2 is still running
   if (do_local) {
     const int nloc = p.counts[g * n + g];
-    const int per = (nloc + p.C - 1) / p.C;
+    const int per = (nloc + C - 1) / C;
     const int r0 = min(nloc, c * per), r1 = min(nloc, r0 + per);
     if (dispatch) {
       copy_rows<true>(p.row_bytes, src, list, p.soff[g * n + g], p.dst_bufs[g], p.roff[g * n + g], r0, r1);
@@ -180,14 +210,14 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     const int first = ch.y, ntok = ch.z;
     const bool cont = ch.w < 0;
     if (paced && !cont) {  // a run starts once every earlier run into `peer` has landed
-      if (threadIdx.x == 0 && !wait_ge(p.ctrs[peer], ch.w * p.C, p.spin_limit, sys)) {
+      if (threadIdx.x == 0 && !wait_ge(p.ctrs[peer], ch.w, p.spin_limit, sys)) {
         abort_s = 1;
         atomicExch(p.status, AURORA_ETIMEOUT);
       }
       __syncthreads();
       if (abort_s) return;
     }
-    const int per = (ntok + p.C - 1) / p.C;
+    const int per = (ntok + C - 1) / C;
     const int r0 = min(ntok, c * per), r1 = min(ntok, r0 + per);
     if (dispatch) {
       // x rows of list(g, peer) -> recv_buf[peer] rows roff[g][peer] + first ...
@@ -216,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
 
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
   if (c == 0 && threadIdx.x == 0) {
-    const int expect = (dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g])) * p.C;
+    const int expect = dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g]);
     if (!wait_ge(p.ctrs[g], expect, p.spin_limit, sys)) {
       atomicExch(p.status, AURORA_ETIMEOUT);
     } else {
@@ -358,9 +388,11 @@ struct TmaShared {
 __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p, int S, int slot_bytes) {
   extern __shared__ __align__(128) unsigned char slots[];
   __shared__ TmaShared sh;
-  const int r_local = blockIdx.x / p.C, c = blockIdx.x % p.C;
+  __shared__ int cs[AUR_MAXN];
+  int r_local, c, C;
+  cta_assign(p, cs, r_local, c, C);
   const int g = p.rank_base + r_local;
-  const int n = p.n, C = p.C;
+  const int n = p.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool dispatch = (p.mode & 1) == 0;
   const bool sys = (p.mode & 2) != 0;
@@ -509,7 +541,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
         peer = e.x, first = e.y, ntok = e.z;
         if (!cont) {  // run start: every earlier run into `peer` must have landed
           prev_peer = peer;
-          if (paced && lane == 0 && !wait_ge(sh.ctr[peer], e.w * C, p.spin_limit, sys)) {
+          if (paced && lane == 0 && !wait_ge(sh.ctr[peer], e.w, p.spin_limit, sys)) {
             atomicExch(p.status, AURORA_ETIMEOUT);
             *abort = 1;
           }
@@ -553,7 +585,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     }
     // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
     if (do_remote && !*abort && c == 0 && lane == 0) {
-      const int expect = (dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g])) * C;
+      const int expect = dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g]);
       if (!wait_ge(sh.ctr[g], expect, p.spin_limit, sys)) {
         atomicExch(p.status, AURORA_ETIMEOUT);
       } else {
@@ -613,6 +645,39 @@ __global__ void __launch_bounds__(THREADS) aggregate_kernel(
 
 }  // namespace
 
+// Copy CTAs per local rank after clamping to co-residency (every copy CTA
+// spins on flags written by others, so all must be resident); also the TMA
+// engine's slot geometry. Returns the clamped count, 0 if none fit, -1 on a
+// CUDA error. Deterministic: every process computes the same value.
+static int engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int rb2, bool lsu, int* S_out,
+                       int* slot_out, size_t* dyn_out) {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int slot_bytes = ((row_bytes + rb2 + 127) / 128) * 128;
+  const int S = max(2, min(16, (96 * 1024) / slot_bytes));
+  const size_t dyn = lsu ? 0 : (size_t)S * slot_bytes;
+  if (!lsu && dyn > 200 * 1024) return 0;
+  if (!lsu && cudaFuncSetAttribute(engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+                  cudaSuccess)
+    return -1;
+  const cudaError_t oe = lsu ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_tma_kernel,
+                                                                             TMA_THREADS, dyn);
+  if (oe != cudaSuccess || occ < 1) return -1;
+  if (S_out) *S_out = S;
+  if (slot_out) *slot_out = slot_bytes;
+  if (dyn_out) *dyn_out = dyn;
+  return min(ctas_per_rank, (occ * sms) / n_local);
+}
+
+extern "C" int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu) {
+  if (n_local < 1 || ctas_per_rank < 1 || row_bytes < 16 || row_bytes % 16 || row2_bytes < 0 || row2_bytes % 16)
+    return -AURORA_EINVAL;
+  const int c = engine_ctas(n_local, ctas_per_rank, row_bytes, row2_bytes, lsu != 0, nullptr, nullptr, nullptr);
+  return c > 0 ? c : (c == 0 ? -AURORA_EINVAL : -AURORA_ECUDA);
+}
+
 extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,
                              const int32_t* chunks, const int32_t* rchunks,
                              const int32_t* progress, const int32_t* n_in, const int32_t* n_out,
@@ -621,35 +686,21 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst_bufs, int row_bytes, const void* const* src2_bufs,
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
-                             int32_t* status, void* stream) {
+                             int32_t* status, int split, const double* bw, void* stream) {
+  if (split < 0 || split > 2) return AURORA_EINVAL;
   if (mode < 0 || mode > 127 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !progress || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
       ((mode & 1) == 0 && !send_list))
     return AURORA_EINVAL;
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // mode bit 6: the LSU engine (256-thread CTAs, 16-byte vector loads/stores)
-  // instead of the TMA bulk-copy engine
   const bool lsu = (mode & 64) != 0;
   const int rb2 = src2_bufs ? row2_bytes : 0;
-  const int slot_bytes = ((row_bytes + rb2 + 127) / 128) * 128;
-  const int S = max(2, min(16, (96 * 1024) / slot_bytes));
-  const size_t dyn = lsu ? 0 : (size_t)S * slot_bytes;
-  if (!lsu && dyn > 200 * 1024) return AURORA_EINVAL;
-  if (!lsu && cudaFuncSetAttribute(engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
-                  cudaSuccess)
-    return AURORA_ECUDA;
-  const cudaError_t oe = lsu ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_tma_kernel,
-                                                                             TMA_THREADS, dyn);
-  if (oe != cudaSuccess || occ < 1) return AURORA_ECUDA;
-  // every copy CTA spins on flags written by others: all of them must be
-  // co-resident. Clamp deterministically (every process computes the same C).
-  ctas_per_rank = min(ctas_per_rank, (occ * sms) / n_local);
-  if (ctas_per_rank < 1) return AURORA_EINVAL;
+  int S = 0, slot_bytes = 0;
+  size_t dyn = 0;
+  const int c_clamped = engine_ctas(n_local, ctas_per_rank, row_bytes, rb2, lsu, &S, &slot_bytes, &dyn);
+  if (c_clamped < 1) return c_clamped == 0 ? AURORA_EINVAL : AURORA_ECUDA;
+  ctas_per_rank = c_clamped;
   EngineParams p;
   p.mode = mode;
   p.n = n;
@@ -674,6 +725,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   if (src2_bufs && (!dst2_bufs || row2_bytes <= 0 || row2_bytes % 16)) return AURORA_EINVAL;
   p.ctrs = ctrs;
   p.C = ctas_per_rank;
+  p.split = split;
+  p.bw = bw;
   p.max_phases = max_phases;
   p.spin_limit = spin_limit;
   p.status = status;

@@ -44,6 +44,10 @@ struct SchedParams {
   long long* prof;        // [8]             (nullable) diagnostics: cycles per section
   int32_t* progress;      // [1]             (nullable) phases whose chunk entries are final,
                           //                 | AURORA_PROGRESS_DONE once everything is written
+  // engine copy CTAs (apportion.cuh): hand-over thresholds are counted in
+  // arrival signals, one per copy CTA of the sending rank per run. ctas_* == 0:
+  // thresholds in runs (one signal per run)
+  int n_local, ctas_d, ctas_c, split;
 };
 
 // numpy pairwise_sum (n <= 128 branch, and n < 8 sequential), row-major row of t
@@ -200,6 +204,7 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 
 #include "fastmatch.cuh"
 #include "fastmatch8b.cuh"
+#include "apportion.cuh"
 
 // Value domain of the fast path. Homogeneous integer traffic (the in-layer
 // path: int32 token counts, B = 1) is exact in int32, where every eps test of
@@ -262,10 +267,12 @@ __device__ __forceinline__ void row_put(V (&a)[NB], int j, V v) {
 // n_in[j] / n_out[i] = runs into j / out of i.
 // ============================================================================
 struct ChunkCtx {
+  const int* Cd;      // [n] dispatch copy CTAs of each rank (arrival signals per run)
+  const int* Cc;      // [n] combine copy CTAs of each rank
   double* cum;        // [MAXN][ld]  cumulative scheduled time per pair
   int* tok;           // [MAXN][ld]  tokens issued per pair
   int* lastc;         // [MAXN][ld]  phase of the pair's last entry (-1: none)
-  int* rcnt;          // [MAXN]      runs into each receiver so far
+  int* rcnt;          // [MAXN]      arrival signals into each receiver so far
   int4* rtmp;         // [MAXN]      per-receiver staging of the current phase
   const int32_t* want;  // pair totals (counts), row stride wld
   const double* bw;   // [n] bandwidths or nullptr
@@ -274,7 +281,7 @@ struct ChunkCtx {
 
 struct ChunkLane {
   int prev_j = -1;  // this sender's receiver in the previous phase
-  int scnt = 0;     // runs this sender has opened
+  int scnt = 0;     // combine arrival signals into this sender so far
 };
 
 __device__ void chunk_init(const ChunkCtx& c, int n, int lane) {
@@ -310,17 +317,15 @@ __device__ void chunk_step(const SchedParams& p, const ChunkCtx& c, ChunkLane& c
     c.tok[q] = tk;
     c.lastc[q] = k;
     const bool cont = cl.prev_j == j;
-    int rseq, sseq;
-    if (cont) {
-      rseq = c.rcnt[j] - 1;
-      sseq = cl.scnt - 1;
-    } else {
+    int rseq = -1, sseq = -1;
+    if (!cont) {  // run start: its hand-over threshold = signals of every earlier run into the receiver
       rseq = c.rcnt[j];
-      c.rcnt[j] = rseq + 1;  // receivers are distinct within a phase
-      sseq = cl.scnt++;
+      c.rcnt[j] = rseq + c.Cd[lane];  // receivers are distinct within a phase
+      sseq = cl.scnt;
+      cl.scnt += c.Cc[j];
     }
-    e = make_int4(j, start, tk - start, cont ? -1 - rseq : rseq);
-    c.rtmp[j] = make_int4(lane, start, tk - start, cont ? -1 - sseq : sseq);
+    e = make_int4(j, start, tk - start, rseq);
+    c.rtmp[j] = make_int4(lane, start, tk - start, sseq);
   }
   if (on) cl.prev_j = j;
   __syncwarp();
@@ -613,6 +618,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   __shared__ double bw_s[MAXN];
   __shared__ int status_s, np_s;
   __shared__ double bmax_s;
+  __shared__ int cd_s[MAXN], cc_s[MAXN];
   // two-warp path only: raw ring, chunk state, pair totals
   __shared__ RawRing<TWO ? MAXN : 1> ring;
   __shared__ double cum_s[TWO ? MAXN * MAXN : 1];
@@ -639,9 +645,28 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
     }
   }
   if (warp == 0 && on) bw_s[lane] = p.bw ? p.bw[lane] : 1.0;
+
   if (TWO && warp == 1 && p.chunks && on)  // pair totals for the chunk pass (k-invariant)
     for (int j = 0; j < n; j++) want_s[lane * MAXN + j] = p.d32[lane * n + j];
   __syncthreads();
+  // copy CTAs per rank -> arrival signals per run (apportion.cuh); off warp 0's path
+  auto split_ctas = [&]() {
+    __shared__ long long wd_s[MAXN], wc_s[MAXN];
+    if (p.ctas_d > 0 && p.n_local > 0) {
+      if (on) {
+        wd_s[lane] = aur_weight(p.d32, n, p.bw, n, lane, p.split, false);
+        wc_s[lane] = aur_weight(p.d32, n, p.bw, n, lane, p.split, true);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        aur_apportion_w(wd_s, n, p.n_local, p.ctas_d, cd_s);
+        aur_apportion_w(wc_s, n, p.n_local, p.ctas_c, cc_s);
+      }
+    } else if (on) {
+      cd_s[lane] = cc_s[lane] = 1;
+    }
+    __syncwarp();
+  };
   const double bw_i = on ? bw_s[lane] : 1.0;
 
   double b_max = 0.0, eps = 0.0, row = -INF, col = -INF;
@@ -731,8 +756,11 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   const bool stream = p.chunks && !p.bw;
 
   if constexpr (TWO) {
-    ChunkCtx cc{cum_s, tok_s, lastc_s, rcnt_s, rtmp_s, want_s, p.bw ? bw_s : nullptr, MAXN, MAXN};
-    if (warp == 1 && p.chunks) chunk_init(cc, n, lane);
+    ChunkCtx cc{cd_s, cc_s, cum_s, tok_s, lastc_s, rcnt_s, rtmp_s, want_s, p.bw ? bw_s : nullptr, MAXN, MAXN};
+    if (warp == 1 && p.chunks) {
+      split_ctas();
+      chunk_init(cc, n, lane);
+    }
     __syncwarp();
     if (run) {
       const bool int_dom = p.d32 && !p.bw;
@@ -843,10 +871,11 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
     if (p.chunks) {
       // chunk pass over the finished phase tables; chunk state reuses the
       // decomposition's shared matrices
-      ChunkCtx cc{&rem_s[0][0], reinterpret_cast<int*>(&real_s[0][0]),
+      ChunkCtx cc{cd_s, cc_s, &rem_s[0][0], reinterpret_cast<int*>(&real_s[0][0]),
                   reinterpret_cast<int*>(&real_s[0][0]) + MAXN * (MAXN + 1), rcnt_s, rtmp_s, p.d32,
                   p.bw ? bw_s : nullptr, MAXN + 1, n};
       ChunkLane cl;
+      split_ctas();
       chunk_init(cc, n, lane);
       __syncwarp();
       for (int k = 0; k < np_; k++)
@@ -922,6 +951,7 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
                                       int32_t* phase_recv, double* phase_dur, int32_t* n_phases,
                                       int32_t* chunks, int32_t* rchunks, int32_t* n_in,
                                       int32_t* n_out, int32_t* status, int32_t* progress,
+                                      int n_local, int ctas_dispatch, int ctas_combine, int split,
                                       void* stream) {
   if (n < 1 || n > AUR_MAXN || !counts || !phase_recv || !phase_dur || !n_phases || !status ||
       !chunks || !rchunks || !n_in || !n_out)
@@ -939,6 +969,13 @@ extern "C" int aurora_schedule_counts(const int32_t* counts, const double* bw, i
   p.n_in = n_in;
   p.n_out = n_out;
   p.progress = progress;
+  if (ctas_dispatch > 0 && (n_local < 1 || n % n_local || ctas_dispatch < n_local || ctas_combine < n_local ||
+                            split < 0 || split > 2))
+    return AURORA_EINVAL;
+  p.n_local = n_local;
+  p.ctas_d = ctas_dispatch;
+  p.ctas_c = ctas_combine;
+  p.split = split;
   launch_schedule(p, (cudaStream_t)stream);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

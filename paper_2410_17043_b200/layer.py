@@ -182,6 +182,12 @@ class AuroraMoELayer:
         self.unpaced = 0  # 16: ablation -- run the all-to-all without the schedule's pacing
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
+        # how a process's copy CTAs are split among the ranks it drives (csrc/apportion.cuh):
+        # by bandwidth when the cluster is heterogeneous (C4: a rank's copy rate follows its
+        # bandwidth), else by volume (one rank per GPU: identity; loopback: the hot rank gets the
+        # copy capacity its own GPU would have); AURORA_CTA_SPLIT=even|volume|bandwidth overrides
+        split = os.environ.get("AURORA_CTA_SPLIT", "bandwidth" if bandwidths is not None else "volume")
+        self.split = {"even": 0, "volume": 1, "bandwidth": 2}[split]
         self.trace = None
         self.side = torch.cuda.Stream(device=dev)
         self._ev_pack = torch.cuda.Event()
@@ -318,12 +324,29 @@ class AuroraMoELayer:
             import torch.distributed as dist
             dist.all_reduce(self.counts)
 
+    def engine_ctas(self, combine: bool) -> int:
+        """Copy CTAs per local rank the engine launches (clamped to co-residency)."""
+        row2 = self.meta_bytes if (self.G > 1 and not combine) else 0
+        c = self.L.aurora_engine_ctas(self.n_local, self.C, self.cfg.hidden * 2, row2, 1 if self.engine_lsu else 0)
+        if c < 1:
+            _lib.check(-c, "aurora_engine_ctas")
+        return c
+
+    def cta_split(self, combine: bool) -> list:
+        """Copy CTAs of every rank (host mirror of the device apportioning)."""
+        from .apportion import apportion
+        bw = None if self.bw is None else self.bw.cpu().numpy()
+        return apportion(self.counts.cpu().numpy(), self.n, self.n_local, self.n_local * self.engine_ctas(combine),
+                         self.split, combine, bw)
+
     def schedule(self, stream: int) -> None:
         _lib.check(self.L.aurora_schedule_counts(
             self.counts.data_ptr(), None if self.bw is None else self.bw.data_ptr(), self.n,
             self.phase_recv.data_ptr(), self.phase_dur.data_ptr(), self.sched_i.data_ptr(),
             self.chunks.data_ptr(), self.rchunks.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
-            self.sched_i[1:].data_ptr(), self.progress.data_ptr(), stream), "aurora_schedule_counts")
+            self.sched_i[1:].data_ptr(), self.progress.data_ptr(), self.n_local,
+            self.n_local * self.engine_ctas(False), self.n_local * self.engine_ctas(True), self.split, stream),
+            "aurora_schedule_counts")
 
     def pack(self, stream: int) -> None:
         cfg = self.cfg
@@ -352,7 +375,8 @@ class AuroraMoELayer:
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
             self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
             self.meta_bytes if plane2 else 0,
-            ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), stream), "aurora_engine")
+            ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
+            None if self.bw is None else self.bw.data_ptr(), stream), "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
         """``overlap_schedule``: launched right after :meth:`schedule` on the same
@@ -524,7 +548,7 @@ class AuroraMoELayer:
         token units (e.g. baselines.schedule_sjf of the same counts) -- the
         schedule ablation of SURVEY 8(f)3. Host -> device copy; diagnostics only."""
         from .baselines import to_engine_tables
-        ch, rch, n_in, n_out = to_engine_tables(sched, self.n)
+        ch, rch, n_in, n_out = to_engine_tables(sched, self.n, self.cta_split(False), self.cta_split(True))
         if ch.shape[0] > self.P:
             raise ValueError(f"{ch.shape[0]} phases exceed the table capacity {self.P}")
         P = ch.shape[0]

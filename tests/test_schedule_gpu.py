@@ -81,10 +81,12 @@ def test_device_schedule_errors(A):
         A.build_schedule(A.TrafficMatrix(np.ones((3, 3))), A.ClusterSpec.uniform(2))
 
 
-def _expected_chunks(phases, counts, n):
+def _expected_chunks(phases, counts, n, cd=None, cc=None):
     """Host restatement of the engine tables: one entry per phase and sender
     (receiver, first, count, run code); a run = consecutive phases of one pair,
     coded r (index among the receiver's runs) first, -1-r on continuations."""
+    cd = cd or [1] * n
+    cc = cc or [1] * n
     P = len(phases)
     ch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
     rch = [[(-1, 0, 0, 0)] * n for _ in range(P)]
@@ -99,14 +101,13 @@ def _expected_chunks(phases, counts, n):
             start = int(issued[i, j])
             issued[i, j] += tok
             cont = prev[i] == j
-            if cont:
-                r, s = rcnt[j] - 1, scnt[i] - 1
-            else:
+            r = s = -1
+            if not cont:
                 r, s = rcnt[j], scnt[i]
-                rcnt[j] += 1
-                scnt[i] += 1
-            ch[k][i] = (j, start, tok, -1 - r if cont else r)
-            rch[k][j] = (i, start, tok, -1 - s if cont else s)
+                rcnt[j] += cd[i]
+                scnt[i] += cc[j]
+            ch[k][i] = (j, start, tok, r)
+            rch[k][j] = (i, start, tok, s)
             cur[i] = j
         prev = cur
     return ch, rch, rcnt, scnt
@@ -135,9 +136,22 @@ def test_counts_path_int_domain_and_chunk_tables(A):
         n_in = torch.empty(n, **i32)
         n_out = torch.empty(n, **i32)
         prog = torch.zeros(1, **i32)
+        # thresholds in runs, or in signals of apportioned copy CTAs (one process driving all ranks,
+        # or n_local-rank groups), checked against the host mirror of the apportioning
+        from paper_2410_17043_b200.apportion import apportion
+        mode = it % 4
+        if mode == 0:
+            split_args, cd, cc = (0, 0, 0, 0), None, None
+        else:
+            nl = n if mode != 3 or n % 2 else n // 2
+            tot = nl * (3 + it % 5)
+            sp = (1, 0, 1)[mode - 1]
+            split_args = (nl, tot, tot + nl, sp)
+            cd = apportion(c, n, nl, tot, sp, False)
+            cc = apportion(c, n, nl, tot + nl, sp, True)
         rc = L.aurora_schedule_counts(counts.data_ptr(), None, n, pr.data_ptr(), pd.data_ptr(), si.data_ptr(),
                                       chunks.data_ptr(), rchunks.data_ptr(), n_in.data_ptr(), n_out.data_ptr(),
-                                      si[1:].data_ptr(), prog.data_ptr(), _lib.stream_ptr())
+                                      si[1:].data_ptr(), prog.data_ptr(), *split_args, _lib.stream_ptr())
         assert rc == 0
         torch.cuda.synchronize()
         nph, status = si.tolist()
@@ -148,7 +162,7 @@ def test_counts_path_int_domain_and_chunk_tables(A):
         got = [(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(t))
                for row, t in zip(pr[:nph].tolist(), pd[:nph].tolist())]
         assert got == o["phases"], (n, it)
-        ch, rch, rcnt, sseq = _expected_chunks(o["phases"], d, n)
+        ch, rch, rcnt, sseq = _expected_chunks(o["phases"], d, n, cd, cc)
         assert [[tuple(x) for x in row] for row in chunks[:nph].tolist()] == ch
         assert [[tuple(x) for x in row] for row in rchunks[:nph].tolist()] == rch
         assert n_in.tolist() == rcnt and n_out.tolist() == sseq
