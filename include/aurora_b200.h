@@ -177,8 +177,12 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  *   optional second plane (dispatch only; NULL to skip): src2_bufs[n_local] rows
  *   of row2_bytes in send-list order (aurora_pack's meta), landing beside the
  *   token rows in dst2_bufs[n] at the same row index;
- *   src_bufs[n_local], dst_bufs[n] (peer-mapped), ctrs[n] (peer-mapped int32
- *   arrival counters, zero on entry, left zero on exit), all device arrays.
+ *   src_bufs[n_local], dst_bufs[n] (peer-mapped), ctrs[n] (peer-mapped pairs of
+ *   int32 arrival counters {pace, done}, zero on entry, left zero on exit), all
+ *   device arrays. The TMA engine signals `pace` as soon as a run's last store
+ *   is issued (the next run into that receiver may start; runs own disjoint
+ *   rows, so only pacing depends on it) and `done` once its stores completed;
+ *   the receiver's exit waits on `done`. The LSU engine signals both at once.
  *   ctas_per_rank copy CTAs per local rank; all must be co-resident.
  *   spin_limit bounds every flag wait (0 = unbounded); on expiry status = ETIMEOUT. */
 int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* counts,

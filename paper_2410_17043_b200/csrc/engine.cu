@@ -128,9 +128,11 @@ __device__ __forceinline__ void signal(int32_t* ctr, bool sys) {
   if (threadIdx.x == 0) {
     if (sys) {
       __threadfence_system();  // cumulative: orders the CTA's stores (observed via bar.sync)
-      red_release_sys_add(ctr, 1);
+      red_release_sys_add(ctr + 1, 1);  // done
+      red_release_sys_add(ctr, 1);      // pace
     } else {
       __threadfence();
+      red_release_gpu_add(ctr + 1, 1);
       red_release_gpu_add(ctr, 1);
     }
   }
@@ -247,10 +249,11 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
   if (c == 0 && threadIdx.x == 0) {
     const int expect = dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g]);
-    if (!wait_ge(p.ctrs[g], expect, p.spin_limit, sys)) {
+    if (!wait_ge(p.ctrs[g] + 1, expect, p.spin_limit, sys)) {
       atomicExch(p.status, AURORA_ETIMEOUT);
     } else {
-      *(volatile int32_t*)p.ctrs[g] = 0;
+      ((volatile int32_t*)p.ctrs[g])[0] = 0;
+      ((volatile int32_t*)p.ctrs[g])[1] = 0;
       __threadfence_system();
     }
   }
@@ -383,6 +386,7 @@ struct TmaShared {
   int nloc;
   int abort;
   long long issued, consumed;
+  int runs_to[AUR_MAXN];  // runs this CTA ended into each receiver (done signals owed)
 };
 
 __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p, int S, int slot_bytes) {
@@ -422,6 +426,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     sh.known = 0;
     sh.known_done = 0;
     sh.cons_k = 0;
+    for (int q = 0; q < AUR_MAXN; q++) sh.runs_to[q] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -526,13 +531,12 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
         // a run ends where this sender's entries stop continuing it
         const bool cont = more && e.x >= 0 && e.x == prev_peer && e.w < 0;
         if (prev_peer >= 0 && !cont) {
+          // the run's stores are all issued: the next run into prev_peer may start
+          // (pace); completion (done) is owed until this CTA's final drain
           if (lane == 0) {
-            bulk_wait_all();  // every store of the run has completed
-            release_upto(t);
-            // async-proxy writes -> generic release (cumulative) on the receiver's counter
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            if (sys) red_release_sys_add(sh.ctr[prev_peer], 1);
-            else red_release_gpu_add(sh.ctr[prev_peer], 1);
+            if (sys) red_relaxed_sys_add(sh.ctr[prev_peer], 1);
+            else red_relaxed_gpu_add(sh.ctr[prev_peer], 1);
+            sh.runs_to[prev_peer]++;
           }
           prev_peer = -1;
         }
@@ -581,15 +585,23 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       bulk_wait_all();
       release_upto(t);
       sh.consumed = t;
+      // every store of this CTA has completed: pay the done signals (release, cumulative)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      for (int j = 0; j < n; j++)
+        if (sh.runs_to[j]) {
+          if (sys) red_release_sys_add(sh.ctr[j] + 1, sh.runs_to[j]);
+          else red_release_gpu_add(sh.ctr[j] + 1, sh.runs_to[j]);
+        }
       if (g_engine_trace) g_engine_trace[blockIdx.x * 4 + 2] = eng_ns();
     }
     // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
     if (do_remote && !*abort && c == 0 && lane == 0) {
       const int expect = dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g]);
-      if (!wait_ge(sh.ctr[g], expect, p.spin_limit, sys)) {
+      if (!wait_ge(sh.ctr[g] + 1, expect, p.spin_limit, sys)) {
         atomicExch(p.status, AURORA_ETIMEOUT);
-      } else {
-        *(volatile int32_t*)sh.ctr[g] = 0;
+      } else {  // every pace signal precedes its sender's done signal (release): both are final
+        ((volatile int32_t*)sh.ctr[g])[0] = 0;
+        ((volatile int32_t*)sh.ctr[g])[1] = 0;
         __threadfence_system();
       }
     }

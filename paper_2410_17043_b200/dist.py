@@ -24,7 +24,7 @@ def _names(layer) -> tuple:
 def _strides(layer) -> Dict[str, int]:
     """Byte distance between consecutive ranks inside one process's buffer."""
     H = layer.cfg.hidden
-    return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 4, "ctr_c": 4,
+    return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 8, "ctr_c": 8,
             "meta_recv": layer.cap * layer.meta_bytes}
 
 

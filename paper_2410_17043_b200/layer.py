@@ -205,8 +205,10 @@ class AuroraMoELayer:
         self.ret_stride = Tr * k
         self.ret = torch.empty(self.n_local * self.ret_stride, H, **bf)
         self.out = torch.empty(self.T_local, H, **bf)
-        self.ctr_d = torch.zeros(n, **i32)
-        self.ctr_c = torch.zeros(n, **i32)
+        # per rank {pace, done} arrival counters (peer-visible): pace paces run starts, done
+        # counts runs whose stores have completed (the engine's exit condition)
+        self.ctr_d = torch.zeros(n, 2, **i32)
+        self.ctr_c = torch.zeros(n, 2, **i32)
         # several experts per rank: per-row expert metadata travels with the rows, the rows
         # are grouped by local expert for the GEMM and pre-reduced before the combine
         self.meta_bytes = ((k * 8 + 15) // 16) * 16
@@ -273,8 +275,8 @@ class AuroraMoELayer:
         if peers is None:
             recv_p = [self.recv.data_ptr() + r * self.cap * H * esz for r in range(self.n)]
             ret_p = [self.ret.data_ptr() + r * self.ret_stride * H * esz for r in range(self.n)]
-            ctr_d = [self.ctr_d.data_ptr() + 4 * r for r in range(self.n)]
-            ctr_c = [self.ctr_c.data_ptr() + 4 * r for r in range(self.n)]
+            ctr_d = [self.ctr_d.data_ptr() + 8 * r for r in range(self.n)]
+            ctr_c = [self.ctr_c.data_ptr() + 8 * r for r in range(self.n)]
         else:
             recv_p, ret_p, ctr_d, ctr_c = peers["recv"], peers["ret"], peers["ctr_d"], peers["ctr_c"]
         self.t_dst_d = self._ptr_table(recv_p)
