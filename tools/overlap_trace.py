@@ -54,3 +54,20 @@ for sync_before in (True, False):
         torch.cuda.synchronize()
         tt.append(ev[0].elapsed_time(ev[1]) * 1e3)
     print("events schedule+dispatch, sync before" if sync_before else "events schedule+dispatch, queued", [round(v, 1) for v in tt], flush=True)
+
+# K2's effective SM clock inside the queued layer sequence (cycles / ns)
+prof = torch.zeros(8, dtype=torch.int64, device="cuda")
+L.aurora_debug_set_schedule_profile(prof.data_ptr())
+L.aurora_debug_set_schedule_trace(st.data_ptr())
+for it in range(5):
+    st.zero_()
+    layer.route(x, s); layer.pack(s); layer.progress.zero_()
+    layer.schedule(s); layer.dispatch(s, overlap_schedule=True)
+    layer.experts(s); layer.combine(s); layer.aggregate(s)
+    torch.cuda.synchronize()
+    nph = int(layer.sched_i[0])
+    ns = int(st[nph].item() - st[0].item())
+    cyc = int(prof[6].item())
+    print(f"queued iter {it}: K2 {cyc} cycles in {ns / 1e3:.1f} us -> {cyc / ns * 1e3:.0f} MHz", flush=True)
+L.aurora_debug_set_schedule_profile(None)
+L.aurora_debug_set_schedule_trace(None)
