@@ -49,9 +49,12 @@ def parse():
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ranks", type=int, default=8, help="expert-parallel ranks (GPUs of the modelled cluster)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c5"],
-                    help="c2: Mixtral-8x7B layer (the headline); c5: DeepSeek-style 64 experts top-6, "
-                         "hidden 5120, FFN 1536 (DeepSeek-V2 expert size; the config leaves F open)")
+    ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2: Mixtral-8x7B layer (the headline); c4: C2 on an emulated heterogeneous "
+                         "cluster (bandwidths 100/80/50/40 x2, PAPER.md:666; placement by "
+                         "assign_exclusive_hetero; copy CTAs per rank follow bandwidth); c5: DeepSeek-style "
+                         "64 experts top-6, hidden 5120, FFN 1536 (DeepSeek-V2 expert size; the config "
+                         "leaves F open)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -62,11 +65,16 @@ def apply_preset(args):
     return args
 
 
+C4_BANDWIDTHS = (1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4)  # PAPER.md:666 ratios 100/80/50/40, two ranks each
+
+
 def workload(args):
-    name = ("C2 Mixtral-8x7B MoE layer" if args.config == "c2" else "C5 DeepSeek-style 64-expert top-6 MoE layer")
+    name = {"c2": "C2 Mixtral-8x7B MoE layer", "c4": "C4 Mixtral-8x7B MoE layer, heterogeneous emulation",
+            "c5": "C5 DeepSeek-style 64-expert top-6 MoE layer"}[args.config]
     return {"workload": f"{name} (EP over {args.ranks} ranks)", "hidden": args.hidden, "ffn": args.ffn,
             "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.ranks,
             "skew": args.skew, "seed": args.seed, "gpus": args.gpus,
+            **({"bandwidths": list(C4_BANDWIDTHS)} if args.config == "c4" else {}),
             "l2": "inputs larger than L2 (x >= 128 MiB, expert weights >= 2.6 GiB read every step)"}
 
 
@@ -203,6 +211,66 @@ def reference_arm(args):
 
 
 # ------------------------------------------------------------------ our arm
+def library_alltoall(layer, x, args, world, rank, stream, reps=5):
+    """Unscheduled library all-to-all of the same dispatch rows. N = 1 (all ranks on
+    one GPU): one torch.index_select gathering every rank's rows into receive order
+    (the single-GPU stand-in: NCCL cannot run several ranks on one GPU). N > 1, one
+    rank per GPU: the NCCL alltoallv the engine replaces -- pack by send list,
+    device-to-host read of the split sizes, dist.all_to_all_single."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2410_17043_b200 import _lib
+    sp = _lib.stream_ptr(stream)
+    layer.route(x, sp)
+    layer.exchange_counts()
+    layer.pack(sp)
+    torch.cuda.synchronize()
+    n, Tr = layer.n, layer.cfg.tokens_per_rank
+    counts = layer.counts.cpu().numpy()
+    soff = layer.soff.cpu().numpy()
+    sl = layer.send_list.cpu().numpy()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    if world == 1:
+        idx = []
+        for j in range(n):
+            for i in [j] + [q for q in range(n) if q != j]:
+                idx.append(sl[i, soff[i, j]:soff[i, j] + counts[i, j]] + i * Tr)
+        idx = torch.from_numpy(np.concatenate(idx).astype(np.int64)).to(x.device)
+        out = torch.empty(idx.numel(), x.shape[1], dtype=x.dtype, device=x.device)
+        torch.index_select(x, 0, idx, out=out)
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for _ in range(reps):
+            torch.index_select(x, 0, idx, out=out)
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        return {"torch_index_select_us": ev[0].elapsed_time(ev[1]) / reps * 1e3, "rows": int(idx.numel()),
+                "note": "one gather kernel moving every dispatched row into receive order (all ranks on one GPU)"}
+    if layer.n_local != 1:
+        return {"unavailable": "NCCL baseline needs one rank per GPU"}
+    g = layer.rank_base
+    nsend = int(counts[g].sum())
+    lst = layer.send_list[0, :nsend].long()
+    recv = torch.empty(int(counts[:, g].sum()), x.shape[1], dtype=x.dtype, device=x.device)
+    tot = 0.0
+    for r_ in range(reps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        send = torch.index_select(x, 0, lst)
+        c = layer.counts.cpu()  # alltoallv needs the split sizes on the host
+        dist.all_to_all_single(recv, send, output_split_sizes=c[:, g].tolist(), input_split_sizes=c[g].tolist())
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        if r_:
+            tot += ev[0].elapsed_time(ev[1])
+    t = torch.tensor([tot / reps * 1e3], dtype=torch.float64, device=x.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"nccl_alltoallv_us": float(t.item()),
+            "note": "pack (index_select) + D2H split sizes + dist.all_to_all_single, max over ranks"}
+
+
 def baseline_schedules(layer, x, sp, stream, reps=3):
     """SURVEY 8(f)3 / PAPER.md:747: the paper's SJF and RCS schedules of the same
     traffic matrix, executed by the same engine (host-built tables)."""
@@ -280,7 +348,22 @@ def main():
     n_local = n // world
     cfg = MoEConfig(hidden=args.hidden, ffn=args.ffn, experts=args.experts, top_k=args.topk, tokens=args.tokens,
                     ranks=n, skew=args.skew, seed=args.seed)
-    layer = AuroraMoELayer(cfg, rank_base=rank * n_local, n_local=n_local)
+    plan, bws = None, None
+    if args.config == "c4":
+        # deployment-time placement (placement.py:46-60) from a calibration pass of the router
+        from paper_2410_17043_b200 import ClusterSpec, GpuSpec, assign_exclusive_hetero
+        bws = C4_BANDWIDTHS[:n]
+        calib = AuroraMoELayer(cfg, rank_base=rank * n_local, n_local=n_local)
+        gc_ = torch.Generator(device=calib.dev).manual_seed(args.seed + 101 + rank)
+        xc = torch.randn(calib.T_local, cfg.hidden, device=calib.dev, generator=gc_).to(torch.bfloat16)
+        calib.route(xc, _lib.stream_ptr())  # the router alone gives the traffic matrix
+        calib.exchange_counts()
+        torch.cuda.synchronize()
+        loads = calib.counts.cpu().numpy().sum(axis=0)
+        plan = assign_exclusive_hetero(loads, ClusterSpec(tuple(GpuSpec(b, b) for b in bws)))
+        del calib
+        torch.cuda.empty_cache()
+    layer = AuroraMoELayer(cfg, plan, rank_base=rank * n_local, n_local=n_local, bandwidths=bws)
     if world > 1:
         from paper_2410_17043_b200 import dist as adist
         adist.connect_peers(layer)
@@ -379,6 +462,7 @@ def main():
     unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
     baseline_sched = baseline_schedules(layer, x, sp, stream) if world == 1 else {}
     sched_dispatch_us = a2a_overlapped(args.steps)
+    library_a2a = library_alltoall(layer, x, args, world, rank, stream)
 
     # ---- end to end through the public API with host buffers (pinned), copies timed.
     # Serving-style pipeline: the copy engines move step i+1's input in and step
@@ -448,9 +532,12 @@ def main():
     achieved_tf = gemm_flops / (stage_ms["experts"] * 1e-3) / 1e12
     off = counts.copy()
     np.fill_diagonal(off, 0)
+    bw_arr = np.asarray(bws if bws is not None else [1.0] * n, dtype=float)
+    tmat = off / np.minimum.outer(bw_arr, bw_arr)  # time_normalize (commsched.py:338-347); B = 1 <-> 900 GB/s
     bmax_tokens = int(max(off.sum(axis=1).max(), off.sum(axis=0).max()))
+    bmax_time = float(max(tmat.sum(axis=1).max(), tmat.sum(axis=0).max()))
     row_bytes = cfg.hidden * 2
-    bound_us = bmax_tokens * row_bytes / (NVLINK_GBS * 1e9) * 1e6
+    bound_us = bmax_time * row_bytes / (NVLINK_GBS * 1e9) * 1e6
     nph = int(layer.sched_i[0].item())
     line = {
         "metric": METRIC, "value": cfg.tokens / (ms_per_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
@@ -468,9 +555,11 @@ def main():
             "unscheduled_dispatch_us": unpaced_ms["dispatch"] * 1e3,
             "unscheduled_combine_us": unpaced_ms["combine"] * 1e3,
             "baseline_schedules_on_engine": baseline_sched,
+            "unscheduled_library": library_a2a,
             "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
-            "bound_basis": "b_max x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
+            "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:338-352; tokens when B = 1) "
+                           "x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
             "transport": "NVSwitch peer stores" if world > 1 else
                          "loopback: all 8 ranks on one GPU, peer stores land in local HBM (not NVLink)",
         },

@@ -89,8 +89,8 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  * (the buffer layout soff / roff the chunk offsets refer to comes from aurora_pack)
  * Heterogeneous durations (time units, commsched.py:338-347) are converted to
  * whole tokens per entry by rounding each pair's cumulative time x
- * min(B_i,B_j); the pair's last entry absorbs the rounding so per-pair totals
- * are exact (such schedules publish progress only when complete). */
+ * min(B_i,B_j) (the pair's final cumulative time lands on its exact count; a
+ * pair that would need a correction is reported as AURORA_EINVAL). */
 #define AURORA_PROGRESS_DONE (1 << 20)
 #define AURORA_SPLIT_EVEN 0
 #define AURORA_SPLIT_VOLUME 1

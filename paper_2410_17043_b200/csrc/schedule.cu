@@ -337,8 +337,14 @@ __device__ void chunk_step(const SchedParams& p, const ChunkCtx& c, ChunkLane& c
 
 // after the last phase: exact per-pair totals for fractional (heterogeneous)
 // durations, run counts, then the DONE word the engine waits for
-__device__ void chunk_finish(const SchedParams& p, const ChunkCtx& c, const ChunkLane& cl, int lane) {
+// Returns true (warp-uniform) if some pair needed the fix-up. With integer
+// tokens it never does; with fractional durations the pair's final cumulative
+// time x min(B_i, B_j) is within ~1e-9 of its integer count, so rint() already
+// lands on it -- a fix-up would mean an entry the engine may already have
+// consumed was short, which the streamed path reports as an error.
+__device__ bool chunk_finish(const SchedParams& p, const ChunkCtx& c, const ChunkLane& cl, int lane) {
   const int n = p.n;
+  bool fixed = false;
   if (lane < n) {
     for (int j = 0; j < n; j++) {
       const int q = lane * c.ld + j;
@@ -346,12 +352,14 @@ __device__ void chunk_finish(const SchedParams& p, const ChunkCtx& c, const Chun
       if (kl >= 0 && got != want) {
         p.chunks[kl * n + lane].z += want - got;
         p.rchunks[kl * n + j].z += want - got;
+        fixed = true;
       }
     }
     p.n_out[lane] = cl.scnt;
   }
   __syncwarp();
   if (lane < n) p.n_in[lane] = c.rcnt[lane];
+  return __any_sync(0xffffffffu, fixed);
 }
 
 // diagnostics: when set, every publication records %globaltimer (ns) at
@@ -587,7 +595,7 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
     p.prof[7] = clock64() - t_begin;
   }
   np_out = status == AURORA_OK ? np_ : 0;
-  if (p.chunks && status == AURORA_OK) chunk_finish(p, cc, cl, lane);
+  if (p.chunks && status == AURORA_OK && chunk_finish(p, cc, cl, lane) && stream) status = AURORA_EINVAL;
 }
 
 template <int NB, typename V>
@@ -751,9 +759,8 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   const bool run = status == AURORA_OK;
   if (status < 0) status = AURORA_OK;
   int np_ = 0;
-  // streaming publication: integer tokens only (fractional durations get a
-  // final fix-up of each pair's last entry, so they publish once at the end)
-  const bool stream = p.chunks && !p.bw;
+  // streaming publication (fractional durations too: see chunk_finish)
+  const bool stream = p.chunks != nullptr;
 
   if constexpr (TWO) {
     ChunkCtx cc{cd_s, cc_s, cum_s, tok_s, lastc_s, rcnt_s, rtmp_s, want_s, p.bw ? bw_s : nullptr, MAXN, MAXN};
