@@ -557,6 +557,7 @@ def main():
             "baseline_schedules_on_engine": baseline_sched,
             "unscheduled_library": library_a2a,
             "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
+            "traffic_matrix": counts.tolist(),
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
             "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:338-352; tokens when B = 1) "
                            "x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
