@@ -392,19 +392,116 @@ __device__ __forceinline__ void publish(int32_t* progress, int value, int lane) 
 // The strip only needs the raw phases produced so far, so warp 1 is never
 // ahead of warp 0 and never on its critical path.
 // ============================================================================
+// warp 0 -> warp 1 hand-off of raw phase r: mbarrier ready[r] completes once
+// (arrive has release, try_wait acquire semantics at CTA scope) -- cheaper than a
+// memory barrier per phase. Slots are never reused (R <= 226 for n <= 16).
+constexpr int RING_BARS = 232;
+__device__ __forceinline__ void ring_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ bool ring_test(uint64_t* bar) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], 0;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+  return ok != 0;
+}
+
 template <int NB>
 struct RawRing {  // the flags lead so every NB shares their offsets
   static constexpr int R = NB * NB - 2 * NB + 2;
-  volatile int published;  // raw phases ready
+  volatile int published;  // raw phases ready (informational; the barriers carry the hand-off)
   volatile int done;       // 1 + status once warp 0 has finished
   double dur[R];
   signed char perm[R * NB];
 };
 
 template <int NB, typename V>
-__device__ void decompose_warp(const SchedParams& p, const double* rem_in, const double* real_in, int ld,
+struct Row {
+  V v[NB];
+};
+
+// Integer-domain prologue (int32 counts on a uniform cluster, the in-layer
+// path): time_normalize is the identity, bmax / augment are exact in int32, so
+// the whole of commsched.py:338-391 runs in registers -- lane i holds row i.
+// augment's greedy fill of row i (j ascending, skipping j == i and exhausted
+// columns, stopping once the row is full) is a prefix over the eligible
+// columns: fill_j = clamp(rr_i - sum_{eligible j' < j} cr_j', 0, cr_j).
+// Returns b_max (0: empty schedule); bad = negative counts.
+template <int NB>
+__device__ int int_prologue(const SchedParams& p, int lane, Row<NB, int>& rem, Row<NB, int>& real, bool& bad) {
+  const int n = p.n;
+  const bool on = lane < n;
+  int d[NB];
+  bool neg = false;
+  int row = 0;
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    d[j] = (on && j < n && j != lane) ? p.d32[lane * n + j] : 0;  // TrafficMatrix zeroes the diagonal
+    neg |= d[j] < 0;
+    row += d[j];
+  }
+  bad = __any_sync(0xffffffffu, neg);
+  int col = 0;
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    const int c = (int)__reduce_add_sync(0xffffffffu, (unsigned)d[j]);
+    if (lane == j) col = c;
+  }
+  const int rmax = (int)__reduce_max_sync(0xffffffffu, on ? (unsigned)row : 0u);
+  const int cmax = (int)__reduce_max_sync(0xffffffffu, on ? (unsigned)col : 0u);
+  const int b_max = rmax > cmax ? rmax : cmax;
+  int x[NB];
+#pragma unroll
+  for (int j = 0; j < NB; j++) x[j] = 0;
+  int rr = b_max - row, cr = b_max - col;
+#pragma unroll
+  for (int i = 0; i < NB; i++) {
+    if (i >= n) break;
+    const int rri = __shfl_sync(0xffffffffu, rr, i);
+    if (rri <= 0) continue;
+    const bool elig = on && lane != i && cr > 0;
+    const int v = elig ? cr : 0;
+    int inc = v;  // inclusive scan of v over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int avail = rri - (inc - v);
+    const int fill = elig ? (avail <= 0 ? 0 : (avail < cr ? avail : cr)) : 0;
+    cr -= fill;
+    const int used = (int)__reduce_add_sync(0xffffffffu, (unsigned)fill);
+    if (lane == i) rr = rri - used;
+#pragma unroll
+    for (int j = 0; j < NB; j++) {
+      const int f = __shfl_sync(0xffffffffu, fill, j);
+      if (lane == i) x[j] = f;
+    }
+  }
+  if (on && rr > 0) {  // leftover on the diagonal (commsched.py:386-389)
+#pragma unroll
+    for (int j = 0; j < NB; j++)
+      if (j == lane) x[j] = rr;
+  }
+#pragma unroll
+  for (int j = 0; j < NB; j++) {
+    rem.v[j] = d[j] + x[j];  // d' = t + x
+    real.v[j] = d[j];        // clip(d' - x, 0) = t exactly
+  }
+  return b_max;
+}
+
+template <int NB, typename V>
+__device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V> real0,
                                uint32_t* pref_s, uint32_t* sup_s, int* perm_s, Dom<V> dom,
-                               RawRing<NB>& ring) {
+                               RawRing<NB>& ring, uint64_t* ready) {
   const int lane = threadIdx.x & 31, n = p.n;
   const bool on = lane < n;
   const V INF = Dom<V>::inf();
@@ -412,8 +509,8 @@ __device__ void decompose_warp(const SchedParams& p, const double* rem_in, const
   V rem[NB], real[NB];
 #pragma unroll
   for (int j = 0; j < NB; j++) {
-    rem[j] = (on && j < n) ? (V)rem_in[lane * ld + j] : (V)0;
-    real[j] = (on && j < n) ? (V)real_in[lane * ld + j] : (V)0;
+    rem[j] = rem0.v[j];
+    real[j] = real0.v[j];
   }
   int nr = 0, status = AURORA_OK;
   FastMatch<NB> fm;
@@ -489,12 +586,9 @@ __device__ void decompose_warp(const SchedParams& p, const double* rem_in, const
       ring.dur[nr] = (double)dur;
       if (p.raw_dur) p.raw_dur[nr] = (double)dur;
     }
-    nr++;
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      ring.published = nr;
-    }
+    if (lane == 0) ring_arrive(&ready[nr]);  // release: the ring entries above are visible to warp 1
+    nr++;
     const long long t3 = clock64();
     cy[0] += t1 - t0;
     cy[1] += t2 - t1;
@@ -504,6 +598,7 @@ __device__ void decompose_warp(const SchedParams& p, const double* rem_in, const
     if (p.n_raw) *p.n_raw = nr;
     if (p.prof)
       for (int q = 0; q < 3; q++) p.prof[q] = cy[q];
+    ring.published = nr;
     __threadfence_block();
     ring.done = 1 + status;
   }
@@ -511,6 +606,7 @@ __device__ void decompose_warp(const SchedParams& p, const double* rem_in, const
 
 template <int NB, typename V>
 __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom<V> dom, RawRing<NB>& ring,
+                           uint64_t* ready,
                            const ChunkCtx& cc, double bw_i, bool stream, int& np_out, int& status) {
   const int lane = threadIdx.x & 31, n = p.n;
   const bool on = lane < n;
@@ -518,7 +614,8 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   const int P_MAX = 2 * n * n - 3 * n + 2;
   V lr[NB];  // real demand not yet delivered (commsched.py:463)
 #pragma unroll
-  for (int j = 0; j < NB; j++) lr[j] = (on && j < n) ? (V)t_in[lane * ld + j] : (V)0;
+  for (int j = 0; j < NB; j++)
+    lr[j] = (on && j < n) ? (t_in ? (V)t_in[lane * ld + j] : (j == lane ? (V)0 : (V)p.d32[lane * n + j])) : (V)0;
   ChunkLane cl;
   int np_ = 0, last_recv = -2, r = 0, avail = 0;
   V cur_dur = 0;
@@ -537,22 +634,28 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   };
   for (;;) {
     int dn = 0;
-    if (r >= avail) {  // wait for warp 0
+    if (r >= avail) {  // wait for warp 0: raw phase r ready, or warp 0 finished
+      int got = 0;
       if (lane == 0) {
         for (;;) {
-          avail = ring.published;
+          if (ring_test(&ready[r])) { got = 1; break; }
           dn = ring.done;
-          if (avail > r || dn) break;
+          if (dn) {
+            __threadfence_block();
+            got = r < ring.published;  // finished after publishing r?
+            if (got) while (!ring_test(&ready[r])) {
+              }
+            break;
+          }
         }
-        if (dn) avail = ring.published;
       }
-      avail = __shfl_sync(0xffffffffu, avail, 0);
+      got = __shfl_sync(0xffffffffu, got, 0);
       dn = __shfl_sync(0xffffffffu, dn, 0);
-      __threadfence_block();
-      if (r >= avail) {
+      if (!got) {
         if (dn > 1) status = dn - 1;
         break;
       }
+      avail = r + 1;
     }
     const long long b0 = clock64();
     const int pj = on ? (int)ring.perm[r * NB + lane] : 0;
@@ -600,12 +703,25 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
 
 template <int NB, typename V>
 __device__ void schedule_two_warps(const SchedParams& p, const double* R, const double* Q, const double* Tt,
-                                   int ld, MatchState& ms, Dom<V> dom, RawRing<NB>& ring, const ChunkCtx& cc,
-                                   double bw_i, bool stream, int& np_, int& status) {
+                                   int ld, MatchState& ms, Dom<V> dom, RawRing<NB>& ring, uint64_t* ready,
+                                   const ChunkCtx& cc, double bw_i, bool stream, int& np_, int& status,
+                                   const Row<NB, V>* rem_regs = nullptr, const Row<NB, V>* real_regs = nullptr) {
   if (threadIdx.x < 32) {
-    decompose_warp<NB, V>(p, R, Q, ld, ms.pref, ms.sup, ms.ml, dom, ring);
+    const int lane = threadIdx.x, n = p.n;
+    Row<NB, V> r0, q0;
+    if (rem_regs) {  // rows already in registers (integer prologue)
+      r0 = *rem_regs;
+      q0 = *real_regs;
+    } else {
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        r0.v[j] = (lane < n && j < n) ? (V)R[lane * ld + j] : (V)0;
+        q0.v[j] = (lane < n && j < n) ? (V)Q[lane * ld + j] : (V)0;
+      }
+    }
+    decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
   } else {
-    strip_warp<NB, V>(p, Tt, ld, dom, ring, cc, bw_i, stream, np_, status);
+    strip_warp<NB, V>(p, Tt, ld, dom, ring, ready, cc, bw_i, stream, np_, status);
   }
 }
 
@@ -629,6 +745,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   __shared__ int cd_s[MAXN], cc_s[MAXN];
   // two-warp path only: raw ring, chunk state, pair totals
   __shared__ RawRing<TWO ? MAXN : 1> ring;
+  __shared__ uint64_t ready_s[TWO ? RING_BARS : 1];
   __shared__ double cum_s[TWO ? MAXN * MAXN : 1];
   __shared__ int tok_s[TWO ? MAXN * MAXN : 1], lastc_s[TWO ? MAXN * MAXN : 1], want_s[TWO ? MAXN * MAXN : 1];
 
@@ -651,6 +768,12 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
       ring.published = 0;
       ring.done = 0;
     }
+  }
+  if constexpr (TWO) {
+    for (int q = tid; q < RING_BARS; q += 64)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(&ready_s[q]))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && on) bw_s[lane] = p.bw ? p.bw[lane] : 1.0;
 
@@ -678,7 +801,20 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
   const double bw_i = on ? bw_s[lane] : 1.0;
 
   double b_max = 0.0, eps = 0.0, row = -INF, col = -INF;
-  if (warp == 0) {
+  // integer fast path: int32 counts on a uniform cluster, n <= 16
+  const bool int_fast = TWO && p.d32 && !p.bw;
+  Row<8, int> rem8, real8;
+  Row<16, int> rem16, real16;
+  if (warp == 0 && int_fast) {
+    bool bad = false;
+    const int bm = n <= 8 ? int_prologue<8>(p, lane, rem8, real8, bad) : int_prologue<16>(p, lane, rem16, real16, bad);
+    if (lane == 0) {
+      bmax_s = (double)bm;
+      if (p.b_max) *p.b_max = (double)bm;
+      status_s = bad ? AURORA_EINVAL : (bm > 0 ? AURORA_OK : -1);
+      if (p.prof) p.prof[5] = clock64() - k_start;
+    }
+  } else if (warp == 0) {
     // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
     bool bad = false;
     if (on) {
@@ -777,12 +913,12 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
       RawRing<MAXN>& rg = ring;
       if (n <= 8) {
         auto& r8 = reinterpret_cast<RawRing<8>&>(rg);  // fits: R_8 * 8 < R_16 * 16
-        if (int_dom) schedule_two_warps<8, int>(p, R, Q, Tt, MAXN + 1, ms, Dom<int>{}, r8, cc, bw_i, stream, np_, status);
-        else schedule_two_warps<8, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r8, cc, bw_i, stream, np_, status);
+        if (int_dom) schedule_two_warps<8, int>(p, R, Q, nullptr, MAXN + 1, ms, Dom<int>{}, r8, ready_s, cc, bw_i, stream, np_, status, &rem8, &real8);
+        else schedule_two_warps<8, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r8, ready_s, cc, bw_i, stream, np_, status);
       } else {
         auto& r16 = reinterpret_cast<RawRing<16>&>(rg);
-        if (int_dom) schedule_two_warps<16, int>(p, R, Q, Tt, MAXN + 1, ms, Dom<int>{}, r16, cc, bw_i, stream, np_, status);
-        else schedule_two_warps<16, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r16, cc, bw_i, stream, np_, status);
+        if (int_dom) schedule_two_warps<16, int>(p, R, Q, nullptr, MAXN + 1, ms, Dom<int>{}, r16, ready_s, cc, bw_i, stream, np_, status, &rem16, &real16);
+        else schedule_two_warps<16, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r16, ready_s, cc, bw_i, stream, np_, status);
       }
     } else if (warp == 1 && p.chunks && status == AURORA_OK) {
       ChunkLane cl;
