@@ -137,9 +137,9 @@ def schedule_tables(entries: np.ndarray, bandwidths: np.ndarray | None):
     if n > 32:
         raise ValueError(f"the device scheduler supports n <= 32 GPUs, got {n}")
     dev = torch.device("cuda", torch.cuda.current_device())
-    d = torch.as_tensor(np.ascontiguousarray(entries, dtype=np.float64), device=dev)
-    bw = None if bandwidths is None else torch.as_tensor(
-        np.ascontiguousarray(bandwidths, dtype=np.float64), device=dev)
+    # the reference's arrays are read-only (core.py:30-33): copy, never alias
+    d = torch.tensor(np.array(entries, dtype=np.float64), device=dev)
+    bw = None if bandwidths is None else torch.tensor(np.array(bandwidths, dtype=np.float64), device=dev)
     R, P = L.aurora_raw_phase_cap(n), L.aurora_phase_cap(n)
     i32 = dict(dtype=torch.int32, device=dev)
     f64 = dict(dtype=torch.float64, device=dev)

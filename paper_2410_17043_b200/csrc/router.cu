@@ -83,40 +83,14 @@ __device__ __forceinline__ float warp_logits(const int4* __restrict__ xrow[TG],
   return v[0];
 }
 
-template <int TG, int EP>
-__global__ void __launch_bounds__(WARPS * 32) route_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-    const float* __restrict__ bias, int T, int H, int E, int k,
-    const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
-    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
-    int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
-  __shared__ float logit_s[TILE][MAXE + 1];
-  __shared__ int hist_s[AUR_MAXN];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * TILE;
-  const int hv = H / 8;         // int4 per row
-  const int h_chunks = H / 256;
-  if (threadIdx.x < AUR_MAXN) hist_s[threadIdx.x] = 0;
-
-  // ---- logits: warp w owns tokens [t0 + 8w, t0 + 8w + 8)
-  for (int tg = 0; tg < 8; tg += TG) {
-    const int tb = t0 + warp * 8 + tg;
-    const int4* xrow[TG];
-#pragma unroll
-    for (int t = 0; t < TG; t++) {
-      int tt = min(tb + t, T - 1);
-      xrow[t] = reinterpret_cast<const int4*>(x + (size_t)tt * H);
-    }
-    for (int e0 = 0; e0 < E; e0 += EP) {
-      const int4* wrow = reinterpret_cast<const int4*>(wg + (size_t)e0 * H);
-      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv, min(EP, E - e0));
-      const int tq = lane / EP, eq = e0 + lane % EP;
-      if (eq < E) logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
-    }
-  }
-  __syncthreads();
-
-  // ---- top-k + softmax + destinations: thread per token (first 64 threads)
+// top-k + softmax + destinations (thread per token, first 64 threads) and the
+// tile's destination histogram (warp-aggregated), shared by both router kernels
+__device__ __forceinline__ void route_tail(const float (*logit_s)[MAXE + 1], int* hist_s, int t0, int T, int E,
+                                           int k, const int32_t* __restrict__ gpu_of_expert, int n,
+                                           int rank_base, int tokens_per_rank, int32_t* __restrict__ topk_idx,
+                                           float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
+                                           int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x < TILE) {
     const int tl = threadIdx.x, t = t0 + tl;
     const bool valid = t < T;
@@ -164,6 +138,135 @@ __global__ void __launch_bounds__(WARPS * 32) route_kernel(
     const int src = rank_base + t0 / tokens_per_rank;
     if (c) atomicAdd(&counts[src * n + threadIdx.x], c);
   }
+}
+
+template <int TG, int EP>
+__global__ void __launch_bounds__(WARPS * 32) route_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int T, int H, int E, int k,
+    const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
+    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
+    int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  __shared__ float logit_s[TILE][MAXE + 1];
+  __shared__ int hist_s[AUR_MAXN];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * TILE;
+  const int hv = H / 8;         // int4 per row
+  const int h_chunks = H / 256;
+  if (threadIdx.x < AUR_MAXN) hist_s[threadIdx.x] = 0;
+
+  // ---- logits: warp w owns tokens [t0 + 8w, t0 + 8w + 8)
+  for (int tg = 0; tg < 8; tg += TG) {
+    const int tb = t0 + warp * 8 + tg;
+    const int4* xrow[TG];
+#pragma unroll
+    for (int t = 0; t < TG; t++) {
+      int tt = min(tb + t, T - 1);
+      xrow[t] = reinterpret_cast<const int4*>(x + (size_t)tt * H);
+    }
+    for (int e0 = 0; e0 < E; e0 += EP) {
+      const int4* wrow = reinterpret_cast<const int4*>(wg + (size_t)e0 * H);
+      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv, min(EP, E - e0));
+      const int tq = lane / EP, eq = e0 + lane % EP;
+      if (eq < E) logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
+    }
+  }
+  __syncthreads();
+
+  route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
+             slot_dst, blk_cnt, counts);
+}
+
+// Many experts (E > 8): the gate no longer fits L1, and streaming it from L2
+// for every 4-token group makes the router L2-bound. Here each CTA stages, per
+// pass of 8 experts and per 256-wide h chunk, that gate slice once in shared
+// memory as fp32 (double-buffered; every warp of the CTA reuses it for its 8
+// tokens). The arithmetic is the defined one: lane l of the token's warp
+// accumulates h = 256 i + 8 l + jj (i asc, jj asc) with fmaf, then the xor tree.
+constexpr int SEP = 8;  // experts per pass
+__global__ void __launch_bounds__(WARPS * 32, 1) route_staged_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int T, int H, int E, int k,
+    const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
+    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
+    int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  __shared__ float logit_s[TILE][MAXE + 1];
+  __shared__ int hist_s[AUR_MAXN];
+  // [buffer][expert][plane][lane * 4 + q]: lane l's h = 8 l + 4 plane + q (conflict-free LDS.128)
+  __shared__ __align__(16) float w_s[2][SEP][2][128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t0 = blockIdx.x * TILE;
+  const int h_chunks = H / 256;
+  if (tid < AUR_MAXN) hist_s[tid] = 0;
+  const int4* xrow[8];
+#pragma unroll
+  for (int t = 0; t < 8; t++) xrow[t] = reinterpret_cast<const int4*>(x + (size_t)min(t0 + warp * 8 + t, T - 1) * H);
+  const int se = tid >> 5, sl = tid & 31;  // staging: expert se of the pass, lane slot sl (8 h values)
+
+  for (int e0 = 0; e0 < E; e0 += SEP) {
+    const int ev = min(SEP, E - e0);
+    const int4* wsrc = reinterpret_cast<const int4*>(wg + (size_t)(e0 + min(se, ev - 1)) * H) + sl;
+    auto stage = [&](int buf, int4 v) {
+      float f[8];
+      bf16x8_to_f32(v, f);
+      *reinterpret_cast<float4*>(&w_s[buf][se][0][sl * 4]) = make_float4(f[0], f[1], f[2], f[3]);
+      *reinterpret_cast<float4*>(&w_s[buf][se][1][sl * 4]) = make_float4(f[4], f[5], f[6], f[7]);
+    };
+    stage(0, __ldg(wsrc));
+    __syncthreads();
+    float acc[8][SEP];
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+#pragma unroll
+      for (int e = 0; e < SEP; e++) acc[t][e] = 0.0f;
+    for (int i = 0; i < h_chunks; i++) {
+      const int buf = i & 1;
+      int4 wn = make_int4(0, 0, 0, 0);
+      if (i + 1 < h_chunks) wn = __ldg(wsrc + 32 * (i + 1));  // next slice, in flight during the FMAs
+      float wf[SEP][8];
+#pragma unroll
+      for (int e = 0; e < SEP; e++) {
+        const float4 a = *reinterpret_cast<const float4*>(&w_s[buf][e][0][lane * 4]);
+        const float4 b = *reinterpret_cast<const float4*>(&w_s[buf][e][1][lane * 4]);
+        wf[e][0] = a.x; wf[e][1] = a.y; wf[e][2] = a.z; wf[e][3] = a.w;
+        wf[e][4] = b.x; wf[e][5] = b.y; wf[e][6] = b.z; wf[e][7] = b.w;
+      }
+#pragma unroll
+      for (int t = 0; t < 8; t++) {
+        float xf[8];
+        bf16x8_to_f32(ld_nc_v4(xrow[t] + 32 * i + lane), xf);
+#pragma unroll
+        for (int e = 0; e < SEP; e++)
+#pragma unroll
+          for (int jj = 0; jj < 8; jj++) acc[t][e] = fmaf(xf[jj], wf[e][jj], acc[t][e]);
+      }
+      if (i + 1 < h_chunks) stage(buf ^ 1, wn);
+      __syncthreads();
+    }
+    // xor tree over the lanes: reduce-scatter per group of 32 pairs (pair p = t * SEP + e)
+#pragma unroll
+    for (int g = 0; g < 2; g++) {
+      float v[32];
+#pragma unroll
+      for (int q = 0; q < 32; q++) v[q] = acc[(g * 32 + q) / SEP][(g * 32 + q) % SEP];
+#pragma unroll
+      for (int o = 16, sz = 32; o >= 1; o >>= 1, sz >>= 1) {
+        const bool upper = lane & o;
+#pragma unroll
+        for (int q = 0; q < sz / 2; q++) {
+          float mine = upper ? v[q + sz / 2] : v[q];
+          float send = upper ? v[q] : v[q + sz / 2];
+          float got = __shfl_xor_sync(0xffffffffu, send, o);
+          v[q] = mine + got;
+        }
+      }
+      const int pr = g * 32 + lane, tq = pr / SEP, eq = e0 + pr % SEP;
+      if (eq < E) logit_s[warp * 8 + tq][eq] = v[0] + bias[eq];
+    }
+  }
+  __syncthreads();
+  route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
+             slot_dst, blk_cnt, counts);
 }
 
 // K3: token permutation. CTA = 64 threads = the 64 tokens of one route tile.
@@ -269,8 +372,11 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
   if (E < 1 || E > MAXE) return AURORA_EUNSUPPORTED;
   if (E <= 4)
     LAUNCH(8, 4);
-  else
+  else if (E <= 8)
     LAUNCH(4, 8);
+  else
+    route_staged_kernel<<<blocks, WARPS * 32, 0, s>>>(xb, wb, bias, T, H, E, k, gpu_of_expert, n, rank_base,
+                                                     tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
 #undef LAUNCH
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

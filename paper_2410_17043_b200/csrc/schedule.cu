@@ -373,9 +373,8 @@ __device__ __forceinline__ long long global_ns() {
 }
 
 __device__ __forceinline__ void publish(int32_t* progress, int value, int lane) {
-  __syncwarp();
+  __syncwarp();  // the lanes' table stores happen-before lane 0's release (cumulative at gpu scope)
   if (lane == 0 && progress) {
-    __threadfence();
     st_release_gpu(progress, value);
     if (g_sched_trace) g_sched_trace[(value & AURORA_PROGRESS_COUNT) & 511] = global_ns();
   }
