@@ -128,12 +128,12 @@ __device__ __forceinline__ void signal(int32_t* ctr, bool sys) {
   if (threadIdx.x == 0) {
     if (sys) {
       __threadfence_system();  // cumulative: orders the CTA's stores (observed via bar.sync)
-      red_release_sys_add(ctr + 1, 1);  // done
       red_release_sys_add(ctr, 1);      // pace
+      red_release_sys_add(ctr + 1, 1);  // done last: once the receiver sees every done, every pace is in
     } else {
       __threadfence();
-      red_release_gpu_add(ctr + 1, 1);
       red_release_gpu_add(ctr, 1);
+      red_release_gpu_add(ctr + 1, 1);
     }
   }
 }

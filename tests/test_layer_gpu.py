@@ -306,3 +306,26 @@ def test_layer_edge_shapes(torch, shape):
     kw = dict(hidden=256, ffn=128, skew=1.0, seed=7)
     kw.update(shape)
     _check_layer(torch, MoEConfig(**kw))
+
+
+def test_engine_cta_splits_and_copy_paths_agree(torch):
+    """Every copy-CTA split (even / volume / bandwidth, csrc/apportion.cuh), the
+    LSU and TMA copy paths, K2 overlapped (PDL) or serial, and the unpaced
+    ablation deliver the same rows: identical output, counters rearmed."""
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=8, top_k=2, tokens=4096, ranks=8, skew=1.5, seed=4)
+    layer = AuroraMoELayer(cfg, bandwidths=[1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4])
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = layer(x).clone()
+    torch.cuda.synchronize()
+    layer.check_status()
+    for split in (0, 1, 2):
+        for lsu in (0, 64):
+            for stream_sched in (True, False):
+                for unpaced in (0, 16):
+                    layer.split, layer.engine_lsu, layer.stream_schedule, layer.unpaced = split, lsu, stream_sched, unpaced
+                    out = layer(x)
+                    torch.cuda.synchronize()
+                    layer.check_status()
+                    assert torch.equal(out, ref), (split, lsu, stream_sched, unpaced)
+    assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
