@@ -329,3 +329,57 @@ def test_engine_cta_splits_and_copy_paths_agree(torch):
                     layer.check_status()
                     assert torch.equal(out, ref), (split, lsu, stream_sched, unpaced)
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("experts,top_k", [(8, 2), (16, 4)])
+def test_two_rank_groups_in_one_context(torch, experts, top_k):
+    """The multi-GPU code path on one device: two layer instances, each driving
+    4 of the 8 ranks (what two processes on two GPUs do), with peer tables
+    pointing at each other's buffers, system-scope flags, the traffic matrix
+    summed from both halves (exchange_counts' all_reduce), K2 counting
+    hand-over thresholds over 4-rank groups, and the two engines running
+    concurrently on two streams, each waiting on the other's arrival counters.
+    Output identical to the single-instance (loopback) layer; with several
+    experts per rank the expert-metadata plane travels to the peers too."""
+    from paper_2410_17043_b200.dist import _names, _strides
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=experts, top_k=top_k, tokens=4096, ranks=8, skew=1.0, seed=6)
+    ref_layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = ref_layer(x).clone()
+    torch.cuda.synchronize()
+    halves = [AuroraMoELayer(cfg, rank_base=4 * p, n_local=4, spin_limit=1 << 24) for p in range(2)]
+    xs = [x[: cfg.tokens // 2].contiguous(), x[cfg.tokens // 2:].contiguous()]
+    for h, xi in zip(halves, xs):
+        h._use_input(xi)
+    tables = {}
+    for name in _names(halves[0]):
+        st = _strides(halves[0])[name]
+        tables[name] = [getattr(halves[r // 4], name).data_ptr() + (r % 4) * st for r in range(8)]
+    for h in halves:
+        h._peers = tables
+        h._tables_for(h.x, tables)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    sp = [int(s.cuda_stream) for s in streams]
+
+    def both(fn):
+        for h, s in zip(halves, sp):
+            fn(h, s)
+        torch.cuda.synchronize()
+
+    for _ in range(2):  # twice: counters must be rearmed across calls
+        both(lambda h, s: h.route(h.x, s))
+        total = halves[0].counts + halves[1].counts
+        for h in halves:
+            h.counts.copy_(total)
+        both(lambda h, s: h.pack(s))
+        both(lambda h, s: h.schedule(s))
+        both(lambda h, s: h.dispatch(s))   # concurrent: each waits on the other's flags
+        both(lambda h, s: h.experts(s))
+        both(lambda h, s: h.combine(s))
+        both(lambda h, s: h.aggregate(s))
+        for h in halves:
+            h.check_status()
+        assert torch.equal(torch.cat([halves[0].out, halves[1].out]), ref)
+    for h in halves:
+        assert int(h.ctr_d.abs().sum()) == 0 and int(h.ctr_c.abs().sum()) == 0
