@@ -462,7 +462,10 @@ def main():
     unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
     baseline_sched = baseline_schedules(layer, x, sp, stream) if world == 1 else {}
     sched_dispatch_us = a2a_overlapped(args.steps)
-    library_a2a = library_alltoall(layer, x, args, world, rank, stream)
+    try:  # a diagnostic beside the headline: never let it take the bench line down
+        library_a2a = library_alltoall(layer, x, args, world, rank, stream)
+    except Exception as e:  # noqa: BLE001
+        library_a2a = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
     # ---- end to end through the public API with host buffers (pinned), copies timed.
     # Serving-style pipeline: the copy engines move step i+1's input in and step
@@ -538,6 +541,15 @@ def main():
     bmax_time = float(max(tmat.sum(axis=1).max(), tmat.sum(axis=0).max()))
     row_bytes = cfg.hidden * 2
     bound_us = bmax_time * row_bytes / (NVLINK_GBS * 1e9) * 1e6
+    # loopback (all ranks on one GPU): every moved row is read and written once in this GPU's HBM
+    peak_hbm = None
+    try:
+        peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs")
+    except Exception:
+        pass
+    peak_hbm = float(peak_hbm or 6650.0)  # fallback: B200_PROFILING.md
+    moved_rows = float(counts.sum())
+    loopback_floor_us = 2 * moved_rows * row_bytes / (peak_hbm * 1e9) * 1e6
     nph = int(layer.sched_i[0].item())
     line = {
         "metric": METRIC, "value": cfg.tokens / (ms_per_step * 1e-3), "unit": "tokens/s", "n_gpus": world,
@@ -557,6 +569,7 @@ def main():
             "baseline_schedules_on_engine": baseline_sched,
             "unscheduled_library": library_a2a,
             "bound_us_per_direction": bound_us, "b_max_tokens": bmax_tokens, "phases": nph,
+            "loopback_hbm_floor_us": loopback_floor_us if world == 1 else None,
             "traffic_matrix": counts.tolist(),
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
             "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:338-352; tokens when B = 1) "
