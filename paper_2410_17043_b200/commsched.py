@@ -256,3 +256,22 @@ def validate_schedule(s, d, cluster, atol: float = TIME_ATOL) -> ScheduleReport:
     if abs(s.makespan - b_max) > atol:
         optimality.append(f"makespan {s.makespan:.12g} != minimum time {b_max:.12g}")
     return ScheduleReport(tuple(contention), tuple(conservation), tuple(optimality))
+
+
+# ---------------------------------------------------------------- wire format
+def schedule_payload(s, d, cluster) -> dict:
+    """One strategy's entry of ``moeplan schedule``'s JSON output
+    (cli.py:75-100): makespan, phases as {duration, transfers}, and the
+    validate_schedule verdicts (commsched.py:355-398)."""
+    rep = validate_schedule(s, d, cluster)
+    return {"makespan": s.makespan,
+            "phases": [{"duration": p.duration, "transfers": [list(t) for t in p.transfers]} for p in s.phases],
+            "contention_free": rep.contention_ok, "complete": rep.conservation_ok, "optimal": rep.optimal}
+
+
+def schedule_from_payload(payload: dict, n: int) -> CommSchedule:
+    """Inverse of :func:`schedule_payload`: a CommSchedule (e.g. one written by
+    the reference CLI) the engine can execute through ``AuroraMoELayer.load_schedule``."""
+    phases = tuple(Phase(tuple(sorted((int(a), int(b)) for a, b in ph["transfers"])), float(ph["duration"]))
+                   for ph in payload["phases"])
+    return CommSchedule(n, phases, float(payload["makespan"]))

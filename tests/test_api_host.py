@@ -155,3 +155,38 @@ def test_baseline_schedules_vs_reference(moeplan):
                          (moeplan.schedule_rcs(tm_ref, cl_ref, it), B.schedule_rcs(tm, cl, it))):
             assert [(p.transfers, p.duration) for p in ref.phases] == [(p.transfers, p.duration) for p in got.phases]
             assert ref.makespan == got.makespan
+
+
+def test_schedule_wire_format_matches_reference_cli():
+    """schedule_payload produces the reference CLI's JSON entry (cli.py:75-100)
+    and round-trips through schedule_from_payload (oracle-built schedule, so
+    no GPU is needed)."""
+    import json
+    import numpy as np
+    from oracle.oracle import build_schedule_oracle
+    import paper_2410_17043_b200 as A
+    from paper_2410_17043_b200.commsched import CommSchedule, Phase, schedule_from_payload, schedule_payload
+    rng = np.random.default_rng(5)
+    d = rng.integers(0, 400, size=(6, 6)).astype(float)
+    np.fill_diagonal(d, 0)
+    o = build_schedule_oracle(d)
+    phases = tuple(Phase(tuple(t), dur) for t, dur in o["phases"])
+    s = CommSchedule(6, phases, sum(p.duration for p in phases))
+    cl = A.ClusterSpec.uniform(6)
+    pay = schedule_payload(s, A.TrafficMatrix(d), cl)
+    assert pay["contention_free"] and pay["complete"] and pay["optimal"]
+    back = schedule_from_payload(json.loads(json.dumps(pay)), 6)
+    assert [(p.transfers, p.duration) for p in back.phases] == [(p.transfers, p.duration) for p in s.phases]
+    try:
+        import sys
+        sys.path.insert(0, "/root/reference/pkg/src")
+        from moeplan import commsched as RC
+        from moeplan.core import ClusterSpec as RCl, TrafficMatrix as RT
+    except Exception:
+        return
+    ref = RC.build_schedule(RT(d), RCl.uniform(6))
+    rep = RC.validate_schedule(ref, RT(d), RCl.uniform(6))
+    ref_pay = {"makespan": ref.makespan,
+               "phases": [{"duration": p.duration, "transfers": [list(t) for t in p.transfers]} for p in ref.phases],
+               "contention_free": rep.contention_ok, "complete": rep.conservation_ok, "optimal": rep.optimal}
+    assert json.dumps(pay) == json.dumps(ref_pay)
