@@ -202,6 +202,9 @@ int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_b
 
 /* ---------------------------------------------------------------- K7 ----
  * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret_i[soff[i][dst_s] + pos[t][s]]
+ * (with y_buf: slots whose expert lives on the token's own rank i are read from
+ * the expert output y_i[roff[i][i] + pos[t][s]] instead, so the combine can skip
+ * the local rows -- engine mode bit 3)
  * in fp32, bf16 out (pre_weighted = 0; every slot must have its own destination),
  * or the plain sum of the rows of the non-duplicate slots when the expert side
  * already applied the gate weights and pre-reduced its local experts
@@ -210,7 +213,8 @@ int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_b
 int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const int32_t* soff,
                      const int32_t* pos, const int32_t* slot_dst, const float* topk_w, int T,
                      int k, int H, int n, int rank_base, int tokens_per_rank, int pre_weighted,
-                     void* out, void* stream);
+                     void* out, const void* y_buf, int64_t y_rank_stride_rows,
+                     const int32_t* roff, void* stream);
 
 /* ---------------------------------------------------------------- K5 ----
  * aurora_expert_ffn: SwiGLU experts as tcgen05/TMEM grouped GEMMs fed by TMA

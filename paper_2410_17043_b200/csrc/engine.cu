@@ -617,12 +617,15 @@ __global__ void __launch_bounds__(THREADS) aggregate_kernel(
     const __nv_bfloat16* __restrict__ ret, long long ret_stride_rows, const int32_t* __restrict__ soff,
     const int32_t* __restrict__ pos, const int32_t* __restrict__ slot_dst,
     const float* __restrict__ topk_w, int T, int k, int H, int n, int rank_base,
-    int tokens_per_rank, int pre_weighted, __nv_bfloat16* __restrict__ out) {
+    int tokens_per_rank, int pre_weighted, __nv_bfloat16* __restrict__ out,
+    const __nv_bfloat16* __restrict__ ybuf, long long y_stride_rows, const int32_t* __restrict__ roff) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * WARPS + warp;
   if (t >= T) return;
   const int i_local = t / tokens_per_rank, i = rank_base + i_local;
   const __nv_bfloat16* base = ret + (size_t)i_local * ret_stride_rows * H;
+  // local slots (expert on the token's own rank): straight from the expert output
+  const __nv_bfloat16* ybase = ybuf ? ybuf + (size_t)i_local * y_stride_rows * H : nullptr;
   const int4* rows[8];
   float w[8];
   int ns = 0;
@@ -630,28 +633,48 @@ __global__ void __launch_bounds__(THREADS) aggregate_kernel(
     const int v = slot_dst[(size_t)t * k + s];
     if (pre_weighted && v < 0) continue;  // duplicate slot: row already pre-reduced
     const int j = v >= 0 ? v : -(v + 1);
-    rows[ns] = reinterpret_cast<const int4*>(base + (size_t)(soff[i * n + j] + pos[(size_t)t * k + s]) * H);
+    rows[ns] = (ybase && j == i)
+                   ? reinterpret_cast<const int4*>(ybase + (size_t)(roff[i * n + i] + pos[(size_t)t * k + s]) * H)
+                   : reinterpret_cast<const int4*>(base + (size_t)(soff[i * n + j] + pos[(size_t)t * k + s]) * H);
     w[ns] = pre_weighted ? 1.0f : topk_w[(size_t)t * k + s];
     ns++;
   }
   int4* o = reinterpret_cast<int4*>(out + (size_t)t * H);
-  for (int u = lane; u < H / 8; u += 32) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int q = 0; q < ns; q++) {
-      int4 v = ld_nc_v4(rows[q] + u);
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+  // U vectors per lane per step, every slot's loads issued before the math:
+  // up to U * k 16-byte loads in flight per lane (HBM latency x bandwidth)
+  constexpr int U = 4;
+  const int hv = H / 8;
+  for (int u0 = lane; u0 < hv; u0 += 32 * U) {
+    float acc[U][8];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        float2 f = __bfloat1622float2(b[e]);
-        acc[2 * e] = fmaf(w[q], f.x, acc[2 * e]);
-        acc[2 * e + 1] = fmaf(w[q], f.y, acc[2 * e + 1]);
+    for (int uu = 0; uu < U; uu++)
+#pragma unroll
+      for (int e = 0; e < 8; e++) acc[uu][e] = 0.0f;
+    for (int q = 0; q < ns; q++) {  // slot order fixed: fp32 sum in slot order
+      int4 v[U];
+#pragma unroll
+      for (int uu = 0; uu < U; uu++)
+        if (u0 + 32 * uu < hv) v[uu] = ld_nc_v4(rows[q] + u0 + 32 * uu);
+#pragma unroll
+      for (int uu = 0; uu < U; uu++) {
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[uu]);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float2 f = __bfloat1622float2(b[e]);
+          acc[uu][2 * e] = fmaf(w[q], f.x, acc[uu][2 * e]);
+          acc[uu][2 * e + 1] = fmaf(w[q], f.y, acc[uu][2 * e + 1]);
+        }
       }
     }
-    int4 r;
-    __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&r);
 #pragma unroll
-    for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
-    o[u] = r;
+    for (int uu = 0; uu < U; uu++) {
+      if (u0 + 32 * uu >= hv) break;
+      int4 r;
+      __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+      for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[uu][2 * e], acc[uu][2 * e + 1]);
+      st_na_v4(o + u0 + 32 * uu, r);
+    }
   }
 }
 
@@ -768,12 +791,16 @@ extern "C" int aurora_debug_set_engine_trace(long long* trace) {
 extern "C" int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows,
                                 const int32_t* soff, const int32_t* pos, const int32_t* slot_dst,
                                 const float* topk_w, int T, int k, int H, int n, int rank_base,
-                                int tokens_per_rank, int pre_weighted, void* out, void* stream) {
-  if (T <= 0 || k < 1 || k > 8 || H % 8 || n < 1 || n > AUR_MAXN || tokens_per_rank < 1)
+                                int tokens_per_rank, int pre_weighted, void* out,
+                                const void* y_buf, int64_t y_rank_stride_rows, const int32_t* roff,
+                                void* stream) {
+  if (T <= 0 || k < 1 || k > 8 || H % 8 || n < 1 || n > AUR_MAXN || tokens_per_rank < 1 ||
+      (y_buf && !roff))
     return AURORA_EINVAL;
   aggregate_kernel<<<(T + WARPS - 1) / WARPS, THREADS, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)ret_buf, ret_rank_stride_rows, soff, pos, slot_dst, topk_w, T, k, H,
-      n, rank_base, tokens_per_rank, pre_weighted, (__nv_bfloat16*)out);
+      n, rank_base, tokens_per_rank, pre_weighted, (__nv_bfloat16*)out, (const __nv_bfloat16*)y_buf,
+      y_rank_stride_rows, roff);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

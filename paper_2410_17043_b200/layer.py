@@ -180,6 +180,9 @@ class AuroraMoELayer:
             self.overlap = False
         self.C_overlap = int(os.environ.get("AURORA_C_OVERLAP", "0"))  # copy CTAs/rank beside the GEMM
         self.unpaced = 0  # 16: ablation -- run the all-to-all without the schedule's pacing
+        # the aggregation reads local (diagonal) rows straight from the expert output, so the
+        # combine only moves rows that cross the network
+        self.local_direct = os.environ.get("AURORA_LOCAL_DIRECT", "1") != "0"
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # how a process's copy CTAs are split among the ranks it drives (csrc/apportion.cuh):
@@ -429,7 +432,8 @@ class AuroraMoELayer:
                    "aurora_expert_reduce")
 
     def combine(self, stream: int) -> None:
-        self._engine(1 | self.unpaced, stream)
+        # local rows stay in the expert output; the aggregation reads them there
+        self._engine(1 | (8 if self.local_direct else 0) | self.unpaced, stream)
 
     def aggregate(self, stream: int, out: Optional[torch.Tensor] = None) -> None:
         cfg = self.cfg
@@ -438,7 +442,8 @@ class AuroraMoELayer:
                                            self.pos.data_ptr(), self.slot_dst.data_ptr(), self.topk_w.data_ptr(),
                                            self.T_local, cfg.top_k, cfg.hidden, self.n, self.rank_base,
                                            cfg.tokens_per_rank, 1 if self.G > 1 else 0, out.data_ptr(),
-                                           stream), "aurora_aggregate")
+                                           self.ybuf.data_ptr() if self.local_direct else None, self.cap,
+                                           self.roff.data_ptr(), stream), "aurora_aggregate")
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:

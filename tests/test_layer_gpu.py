@@ -310,8 +310,9 @@ def test_layer_edge_shapes(torch, shape):
 
 def test_engine_cta_splits_and_copy_paths_agree(torch):
     """Every copy-CTA split (even / volume / bandwidth, csrc/apportion.cuh), the
-    LSU and TMA copy paths, K2 overlapped (PDL) or serial, and the unpaced
-    ablation deliver the same rows: identical output, counters rearmed."""
+    LSU and TMA copy paths, K2 overlapped (PDL) or serial, the unpaced
+    ablation, and local rows read in place or combined deliver the same rows:
+    identical output, counters rearmed."""
     from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
     cfg = MoEConfig(hidden=512, ffn=256, experts=8, top_k=2, tokens=4096, ranks=8, skew=1.5, seed=4)
     layer = AuroraMoELayer(cfg, bandwidths=[1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4])
@@ -328,6 +329,12 @@ def test_engine_cta_splits_and_copy_paths_agree(torch):
                     torch.cuda.synchronize()
                     layer.check_status()
                     assert torch.equal(out, ref), (split, lsu, stream_sched, unpaced)
+    for local_direct in (False, True):  # combine moving the local rows too vs aggregation reading them in place
+        layer.local_direct = local_direct
+        out = layer(x)
+        torch.cuda.synchronize()
+        layer.check_status()
+        assert torch.equal(out, ref), local_direct
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
 
 
