@@ -134,8 +134,13 @@ struct TileIter {
 // stay L2-resident while every n-tile passes over them.
 __device__ __forceinline__ void tile_coords(const TileIter& it, int G, int gm, int t, int& g,
                                             int& mt, int& nt) {
-  g = 0;
-  while (g + 1 < G && it.prefix[g + 1] <= t) g++;
+  int lo = 0, hi = G - 1;  // the last g with prefix[g] <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (it.prefix[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  g = lo;
   const int local = t - it.prefix[g];
   const int per_block = gm * it.n_tiles_n;
   const int sb = local / per_block, rem = local - sb * per_block;

@@ -31,12 +31,19 @@ struct TileIter2 {
   int prefix[MAX_GROUPS + 1];
   int mt[MAX_GROUPS];
   int ms[MAX_GROUPS];
+  int rows[MAX_GROUPS];
 };
 
 __device__ __forceinline__ void tile_coords2(const TileIter2& it, int G, int gm, int t, int& g,
                                              int& mt, int& nt) {
-  g = 0;
-  while (g + 1 < G && it.prefix[g + 1] <= t) g++;
+  // group of tile t: the last g with prefix[g] <= t (binary search: up to 64 groups)
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (it.prefix[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  g = lo;
   const int local = t - it.prefix[g];
   const int per_block = gm * it.n_tiles_n;
   const int sb = local / per_block, rem = local - sb * per_block;
@@ -72,6 +79,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int acc = 0;
     for (int g = 0; g < G; g++) {
       const int m = m_rows[g];
+      it.rows[g] = m;
       it.mt[g] = (m + BMP - 1) / BMP;
       it.ms[g] = m_start ? m_start[g] : 0;
       it.prefix[g] = acc;
@@ -158,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc::mbar_wait(&tfull[acc], (local >> 1) & 1);
       tc::fence_after();
       const int row_in_group = mt * BMP + (int)rank * HALF + quarter * 32 + lane;
-      const bool live = row_in_group < m_rows[g];
+      const bool live = row_in_group < it.rows[g];
       const long long row = g * cap + it.ms[g] + row_in_group;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (epilogue == 1) {
