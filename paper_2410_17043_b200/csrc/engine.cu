@@ -512,7 +512,24 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
         if (++rs == S) rs = 0;
       }
     };
-    int prev_peer = -1;  // peer of the open run (-1: none)
+    int prev_peer = -1;    // peer of the open run (-1: none)
+    bool paced_out = false;  // this CTA already released the open run's receiver (early pace)
+    // early pace: release the receiver when this CTA has only EARLY rows of the
+    // run left to issue -- about the flag's round trip -- so the next sender's
+    // first stores follow this run's last ones instead of waiting a hand-over
+    const int EARLY = (p.mode & 128) ? 2 : 0;  // mode bit 7
+    auto pace = [&](int peer_) {
+      if (sys) red_relaxed_sys_add(sh.ctr[peer_], 1);
+      else red_relaxed_gpu_add(sh.ctr[peer_], 1);
+    };
+    // does entry k end the open run into `peer_`? 1 yes, 0 no, -1 not known yet
+    auto run_ends_at = [&](int k_, int peer_) -> int {
+      if (k_ + 1 < sh.known) {
+        const int4 nx = sh.ring[(k_ + 1) & (RING - 1)];
+        return (nx.x == peer_ && nx.w < 0) ? 0 : 1;
+      }
+      return sh.known_done ? 1 : -1;
+    };
     for (int k = do_local ? -1 : 0; do_remote || k < 0; k++) {
       int peer, first, ntok;
       if (k < 0) {
@@ -534,11 +551,11 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
           // the run's stores are all issued: the next run into prev_peer may start
           // (pace); completion (done) is owed until this CTA's final drain
           if (lane == 0) {
-            if (sys) red_relaxed_sys_add(sh.ctr[prev_peer], 1);
-            else red_relaxed_gpu_add(sh.ctr[prev_peer], 1);
+            if (!paced_out) pace(prev_peer);
             sh.runs_to[prev_peer]++;
           }
           prev_peer = -1;
+          paced_out = false;
         }
         if (!more) break;
         if (e.x < 0) continue;
@@ -559,7 +576,16 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       char* dst = sh.dst[peer];
       char* dst2 = sh.dst2[peer];
       if (lane == 0) {
+        const int early_at = r1 - EARLY;  // signal before issuing row early_at (or now)
+        if (EARLY && k >= 0 && paced && !paced_out && early_at <= r0 && run_ends_at(k, peer) == 1) {
+          pace(peer);
+          paced_out = true;
+        }
         for (int r = r0; r < r1; r++) {
+          if (EARLY && k >= 0 && paced && !paced_out && r == early_at && run_ends_at(k, peer) == 1) {
+            pace(peer);
+            paced_out = true;
+          }
           if (!mbar_wait_or_abort(&sh.full[s], u & 1, abort)) break;
           const uint32_t sp = slot0 + (uint32_t)(s * slot_bytes);
           bulk_store(dst + (drow0 + r) * rb, sp, rb);
@@ -723,7 +749,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, int split, const double* bw, void* stream) {
   if (split < 0 || split > 2) return AURORA_EINVAL;
-  if (mode < 0 || mode > 127 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+  if (mode < 0 || mode > 255 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !progress || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||

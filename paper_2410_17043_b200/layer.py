@@ -185,6 +185,8 @@ class AuroraMoELayer:
         self.local_direct = os.environ.get("AURORA_LOCAL_DIRECT", "1") != "0"
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
+        # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
+        self.early_pace = 128 if os.environ.get("AURORA_EARLY_PACE", "1") != "0" else 0
         # how a process's copy CTAs are split among the ranks it drives (csrc/apportion.cuh):
         # by bandwidth when the cluster is heterogeneous (C4: a rank's copy rate follows its
         # bandwidth), else by volume (one rank per GPU: identity; loopback: the hot rank gets the
@@ -374,7 +376,7 @@ class AuroraMoELayer:
         sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
         plane2 = self.G > 1 and not combine
         _lib.check(self.L.aurora_engine(
-            mode | sys_scope | self.engine_lsu, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            mode | sys_scope | self.engine_lsu | self.early_pace, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.progress.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,

@@ -19,6 +19,26 @@ for _ in range(2):
 torch.cuda.synchronize()
 layer.check_status()
 res = {}
+def a2a_only(reps=12):
+    """dispatch / combine medians without the GEMM in between (its power-capped clocks skew the copies)"""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    dd, cc = [], []
+    for _ in range(reps):
+        layer.route(x, s); layer.pack(s); layer.schedule(s)
+        ev[0].record(st); layer.dispatch(s); ev[1].record(st)
+        ev[2].record(st); layer.combine(s); ev[3].record(st)
+        torch.cuda.synchronize()
+        dd.append(ev[0].elapsed_time(ev[1]) * 1e3); cc.append(ev[2].elapsed_time(ev[3]) * 1e3)
+    layer.check_status()
+    return {"dispatch_us": round(sorted(dd)[reps // 2], 1), "combine_us": round(sorted(cc)[reps // 2], 1)}
+
+
+for early in (0, 128, 0, 128):  # A/B of the early pace release, interleaved
+    layer.early_pace = early
+    r = a2a_only()
+    res[f"tma/{'early' if early else 'end'}_pace_nogemm"] = r
+    print("early pace" if early else "pace at run end", r, flush=True)
+layer.early_pace = 128
 for eng in ("tma", "lsu"):
     layer.engine_lsu = 64 if eng == "lsu" else 0
     for paced in (True, False):
