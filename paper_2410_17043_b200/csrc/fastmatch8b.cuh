@@ -18,6 +18,7 @@ struct FastMatch8b {
   uint64_t P, S;      // pref / sup rows: byte u = right-vertex mask of left u
   uint64_t MR;        // byte v = left vertex matched to right v (index)
   uint64_t MRB;       // byte v = one-hot left vertex matched to v (0: free)
+  uint64_t MLB;       // byte u = one-hot right vertex matched to u (0: free)
   uint64_t ML;        // byte u = right vertex matched to u
   uint64_t LAY;       // byte d = BFS layer d (left vertices)
   uint32_t freeL, freeR, alive;
@@ -59,6 +60,7 @@ struct FastMatch8b {
     ML = set_byte(ML, u, v);
     MR = set_byte(MR, v, u);
     MRB = set_byte(MRB, v, 1u << u);
+    MLB = set_byte(MLB, u, 1u << v);
   }
   // path: U nibbles = us[top..0] (low = top), V nibbles = vs[top-1..0], final right vertex v
   AUR_HD void augment(uint32_t U, uint32_t V, uint32_t v, int top) {
@@ -71,12 +73,20 @@ struct FastMatch8b {
     // U now holds nothing; the root is the last u matched
   }
 
+  // hopcroft_karp dfs(root), matching.py:57-65, with masked candidates: at
+  // depth d only v that are free or whose partner sits on layer d+1 and is
+  // alive can be taken; every other v would be skipped by the loop with no
+  // side effect, and can never become viable again within this dfs (alive
+  // only shrinks, layers and the matching are fixed until it augments), so
+  // they are dropped up front. Viability is re-checked at every visit
+  // (partners may die while a sibling is explored).
   AUR_HD bool hk_dfs(uint32_t root) {
     uint64_t L = byte_of(P, root);  // candidate stack, top at the low byte
     uint32_t U = root, V = 0;       // vertex stack / chosen right vertices
     int top = 0;
     for (;;) {
-      const uint32_t m = (uint32_t)L & 0xFFu;
+      const uint32_t nl = top + 1 < 8 ? byte_of(LAY, top + 1) & alive : 0u;
+      const uint32_t m = (uint32_t)L & 0xFFu & (freeR | gather_or(MLB, nl));
       if (!m) {
         alive &= ~(1u << (U & 15u));  // dist[u] = _INF
         if (top == 0) return false;
@@ -87,7 +97,7 @@ struct FastMatch8b {
         continue;
       }
       const uint32_t b = m & (0u - m);
-      L ^= b;
+      L = (L & ~0xFFull) | (m ^ b);
       const uint32_t v = idx(b);
       if (freeR & b) {
         augment(U, V, v, top);
@@ -95,13 +105,11 @@ struct FastMatch8b {
         freeR &= ~b;
         return true;
       }
-      const uint32_t w = byte_of(MR, v);
-      if (top + 1 < 8 && ((byte_of(LAY, top + 1) & alive) >> w) & 1u) {
-        L = (L << 8) | byte_of(P, w);
-        U = (U << 4) | w;
-        V = (V << 4) | v;
-        top++;
-      }
+      const uint32_t w = byte_of(MR, v);  // on layer top+1 and alive, by the mask
+      L = (L << 8) | byte_of(P, w);
+      U = (U << 4) | w;
+      V = (V << 4) | v;
+      top++;
     }
   }
 
@@ -142,7 +150,7 @@ struct FastMatch8b {
   AUR_HD bool run(int n) {
     const uint32_t all = (1u << n) - 1;
     freeL = freeR = all;
-    ML = MR = MRB = 0;
+    ML = MR = MRB = MLB = 0;
     if (P) {
       // first Hopcroft-Karp phase: all left free -> greedy lowest free preferred
       // vertex. The chain through freeR is four ALU ops per row; the match
@@ -154,7 +162,7 @@ struct FastMatch8b {
         b[u] = m & (0u - m);
         freeR &= ~b[u];
       }
-      uint64_t mrb = 0;
+      uint64_t mrb = 0, mlb = 0;
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         if (b[u]) {
@@ -162,10 +170,12 @@ struct FastMatch8b {
           ML |= (uint64_t)v << (8 * u);
           MR |= (uint64_t)u << (8 * v);
           mrb |= (uint64_t)(1u << u) << (8 * v);
+          mlb |= (uint64_t)b[u] << (8 * u);
           freeL &= ~(1u << u);
         }
       }
       MRB = mrb;
+      MLB = mlb;
       for (;;) {
         uint32_t frontier = freeL, visited = freeL;
         LAY = frontier;
