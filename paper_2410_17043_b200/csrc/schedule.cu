@@ -622,13 +622,31 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   const long long t_begin = clock64();
   long long busy = 0;
   // close the open phase np_-1: outputs, chunk entries, progress
+  long long c_chunk = 0, c_pub = 0;
+  int closed = 0, published = 0;  // phases closed / announced to the engine
   auto close_phase = [&]() {
     const int k = np_ - 1;
+    const long long q0 = clock64();
     if (on) p.phase_recv[k * n + lane] = last_recv;
     if (lane == 0) p.phase_dur[k] = (double)cur_dur;
-    if (p.chunks) {
-      chunk_step(p, cc, cl, k, on ? last_recv : -1, (double)cur_dur, bw_i, lane);
-      if (stream) publish(p.progress, k + 1, lane);
+    if (p.chunks) chunk_step(p, cc, cl, k, on ? last_recv : -1, (double)cur_dur, bw_i, lane);
+    closed = k + 1;
+    c_chunk += clock64() - q0;
+  };
+  // A release store costs ~1k cycles: announce closed phases when this warp
+  // would otherwise wait for warp 0 (it has slack), or every 4 phases when it
+  // is behind, so the engine never lags far and this warp never becomes the
+  // kernel's critical path.
+  auto maybe_publish = [&](int next_r) {
+    if (!stream || closed == published) return;
+    int nxt = 0;
+    if (lane == 0) nxt = ring_test(&ready[next_r]) ? 1 : 0;
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+    if (!nxt || closed - published >= 4) {
+      const long long q1 = clock64();
+      publish(p.progress, closed, lane);
+      published = closed;
+      c_pub += clock64() - q1;
     }
   };
   for (;;) {
@@ -690,10 +708,12 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
     }
     busy += clock64() - b0;
     if (status != AURORA_OK) break;
+    maybe_publish(r);
   }
   if (status == AURORA_OK && np_ > 0 && closing_ok) close_phase();
   if (p.prof && lane == 0) {
     p.prof[3] = busy;
+    p.prof[4] = (c_chunk << 32) | (c_pub & 0xffffffffll);  // close-phase cycles (hi) / of which publish (lo)
     p.prof[7] = clock64() - t_begin;
   }
   np_out = status == AURORA_OK ? np_ : 0;

@@ -6,7 +6,7 @@ from paper_2410_17043_b200 import _lib
 from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
 
 L = _lib.load()
-names = ["w0:snap+mask", "w0:match", "w0:update+publish", "w1:strip+chunks busy", "-", "prologue", "kernel", "w1:total"]
+names = ["w0:snap+mask", "w0:match", "w0:update+publish", "w1:strip+chunks busy", "w1:", "prologue", "kernel", "w1:total"]
 for n, T in ((8, 16384), (16, 16384)):
     cfg = MoEConfig(hidden=256, ffn=256, experts=n, top_k=2, tokens=T, ranks=n, skew=1.0, seed=0)
     layer = AuroraMoELayer(cfg)
@@ -26,5 +26,7 @@ for n, T in ((8, 16384), (16, 16384)):
         layer.schedule(s)
     e1.record()
     torch.cuda.synchronize()
+    pv = prof.cpu().tolist()
+    pv[4] = f"close={pv[4] >> 32}/publish={pv[4] & 0xffffffff}"
     print(f"n={n}: {e0.elapsed_time(e1) / 20 * 1000:.1f} us/launch;",
-          " ".join(f"{k}={v}" for k, v in zip(names, prof.cpu().tolist())), flush=True)
+          " ".join(f"{k}={v}" for k, v in zip(names, pv)), flush=True)
