@@ -145,23 +145,40 @@ __global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
     }
   }
   int4* o = reinterpret_cast<int4*>(ybuf + row * H);
-  for (int u = lane; u < H / 8; u += 32) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int q = 0; q < ns; q++) {
-      int4 v = ld_nc_v4(src[q] + u);
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+  // U vectors per lane per step with every slot's loads issued before the math
+  constexpr int U = 4;
+  const int hv = H / 8;
+  for (int u0 = lane; u0 < hv; u0 += 32 * U) {
+    float acc[U][8];
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        float2 f = __bfloat1622float2(b[e]);
-        acc[2 * e] = fmaf(w[q], f.x, acc[2 * e]);
-        acc[2 * e + 1] = fmaf(w[q], f.y, acc[2 * e + 1]);
+    for (int uu = 0; uu < U; uu++)
+#pragma unroll
+      for (int e = 0; e < 8; e++) acc[uu][e] = 0.0f;
+    for (int q = 0; q < ns; q++) {  // slot order fixed: fp32 sum in slot order
+      int4 v[U];
+#pragma unroll
+      for (int uu = 0; uu < U; uu++)
+        if (u0 + 32 * uu < hv) v[uu] = ld_nc_v4(src[q] + u0 + 32 * uu);
+#pragma unroll
+      for (int uu = 0; uu < U; uu++) {
+        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v[uu]);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          float2 f = __bfloat1622float2(b[e]);
+          acc[uu][2 * e] = fmaf(w[q], f.x, acc[uu][2 * e]);
+          acc[uu][2 * e + 1] = fmaf(w[q], f.y, acc[uu][2 * e + 1]);
+        }
       }
     }
-    int4 res;
-    __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&res);
 #pragma unroll
-    for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[2 * e], acc[2 * e + 1]);
-    o[u] = res;
+    for (int uu = 0; uu < U; uu++) {
+      if (u0 + 32 * uu >= hv) break;
+      int4 res;
+      __nv_bfloat162* rb = reinterpret_cast<__nv_bfloat162*>(&res);
+#pragma unroll
+      for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[uu][2 * e], acc[uu][2 * e + 1]);
+      st_na_v4(o + u0 + 32 * uu, res);
+    }
   }
 }
 
