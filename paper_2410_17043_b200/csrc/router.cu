@@ -13,9 +13,13 @@
 // The tree is evaluated as a reduce-scatter (lane q ends with pair q), which
 // has the same tree shape, hence the same bits, as the butterfly.
 //
-// HBM-bound: x is streamed once with 16-byte non-allocating loads; w_gate
-// (E*H*2 bytes) stays L1/L2-resident.
+// x is streamed by TMA (2-D tiles of 64 tokens x 256 h into a 4-stage
+// shared-memory ring); the gate slice of each 8-expert pass is read from
+// L1/L2 into registers once per chunk and reused for the warp's 8 tokens.
+#include <cuda.h>
+
 #include "common.cuh"
+#include "tc_helpers.cuh"
 
 namespace {
 
@@ -31,56 +35,6 @@ __device__ __forceinline__ void bf16x8_to_f32(const int4& v, float* f) {
     f[2 * q] = __uint_as_float(w[q] << 16);
     f[2 * q + 1] = __uint_as_float(w[q] & 0xffff0000u);
   }
-}
-
-// One warp computes the logits of TG tokens x EP experts (TG*EP == 32) and
-// leaves pair q = lane (token q / EP, expert q % EP) in its return value.
-template <int TG, int EP>
-__device__ __forceinline__ float warp_logits(const int4* __restrict__ xrow[TG],
-                                             const int4* __restrict__ wrow, int h_chunks, int lane,
-                                             int hv, int e_valid) {
-  static_assert(TG * EP == 32, "tile");
-  float acc[TG][EP];
-#pragma unroll
-  for (int t = 0; t < TG; t++)
-#pragma unroll
-    for (int e = 0; e < EP; e++) acc[t][e] = 0.0f;
-  for (int i = 0; i < h_chunks; i++) {
-    const int c = 32 * i + lane;  // 16-byte chunk index within the row
-    float xf[TG][8];
-#pragma unroll
-    for (int t = 0; t < TG; t++) {
-      int4 v = ld_nc_v4(xrow[t] + c);
-      bf16x8_to_f32(v, xf[t]);
-    }
-#pragma unroll
-    for (int e = 0; e < EP; e++) {
-      // experts past the last one of this pass re-read a valid row; their sums are dropped
-      int4 wv = __ldg(wrow + (size_t)min(e, e_valid - 1) * hv + c);
-      float wf[8];
-      bf16x8_to_f32(wv, wf);
-#pragma unroll
-      for (int t = 0; t < TG; t++)
-#pragma unroll
-        for (int jj = 0; jj < 8; jj++) acc[t][e] = fmaf(xf[t][jj], wf[jj], acc[t][e]);
-    }
-  }
-  // reduce-scatter: 32 values per lane -> 1, keeping the upper half when (lane & o)
-  float v[32];
-#pragma unroll
-  for (int q = 0; q < 32; q++) v[q] = acc[q / EP][q % EP];
-#pragma unroll
-  for (int o = 16, s = 32; o >= 1; o >>= 1, s >>= 1) {
-    const bool upper = lane & o;
-#pragma unroll
-    for (int q = 0; q < s / 2; q++) {
-      float mine = upper ? v[q + s / 2] : v[q];
-      float send = upper ? v[q] : v[q + s / 2];
-      float got = __shfl_xor_sync(0xffffffffu, send, o);
-      v[q] = mine + got;
-    }
-  }
-  return v[0];
 }
 
 // top-k + softmax + destinations (thread per token, first 64 threads) and the
@@ -140,133 +94,131 @@ __device__ __forceinline__ void route_tail(const float (*logit_s)[MAXE + 1], int
   }
 }
 
-template <int TG, int EP>
-__global__ void __launch_bounds__(WARPS * 32) route_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-    const float* __restrict__ bias, int T, int H, int E, int k,
-    const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
-    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
-    int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
-  __shared__ float logit_s[TILE][MAXE + 1];
-  __shared__ int hist_s[AUR_MAXN];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * TILE;
-  const int hv = H / 8;         // int4 per row
-  const int h_chunks = H / 256;
-  if (threadIdx.x < AUR_MAXN) hist_s[threadIdx.x] = 0;
-
-  // ---- logits: warp w owns tokens [t0 + 8w, t0 + 8w + 8)
-  for (int tg = 0; tg < 8; tg += TG) {
-    const int tb = t0 + warp * 8 + tg;
-    const int4* xrow[TG];
-#pragma unroll
-    for (int t = 0; t < TG; t++) {
-      int tt = min(tb + t, T - 1);
-      xrow[t] = reinterpret_cast<const int4*>(x + (size_t)tt * H);
-    }
-    for (int e0 = 0; e0 < E; e0 += EP) {
-      const int4* wrow = reinterpret_cast<const int4*>(wg + (size_t)e0 * H);
-      float r = warp_logits<TG, EP>(xrow, wrow, h_chunks, lane, hv, min(EP, E - e0));
-      const int tq = lane / EP, eq = e0 + lane % EP;
-      if (eq < E) logit_s[warp * 8 + tg + tq][eq] = r + bias[eq];
-    }
-  }
-  __syncthreads();
-
-  route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
-             slot_dst, blk_cnt, counts);
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
 
-// Many experts (E > 8): the gate no longer fits L1, and streaming it from L2
-// for every 4-token group makes the router L2-bound. Here each CTA stages, per
-// pass of 8 experts and per 256-wide h chunk, that gate slice once in shared
-// memory as fp32 (double-buffered; every warp of the CTA reuses it for its 8
-// tokens). The arithmetic is the defined one: lane l of the token's warp
-// accumulates h = 256 i + 8 l + jj (i asc, jj asc) with fmaf, then the xor tree.
-constexpr int SEP = 8;  // experts per pass
-__global__ void __launch_bounds__(WARPS * 32, 1) route_staged_kernel(
-    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+constexpr int XS = 4;                      // x stages
+constexpr int XCHUNK = TILE * 256 * 2;     // bytes per stage
+constexpr int REP = 8;                     // experts per pass
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
     const float* __restrict__ bias, int T, int H, int E, int k,
     const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
     int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  extern __shared__ __align__(1024) uint8_t xs_raw[];
+  uint8_t* xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(xs_raw) + 1023) & ~uintptr_t(1023));
   __shared__ float logit_s[TILE][MAXE + 1];
   __shared__ int hist_s[AUR_MAXN];
-  // [buffer][expert][plane][lane * 4 + q]: lane l's h = 8 l + 4 plane + q (conflict-free LDS.128)
-  __shared__ __align__(16) float w_s[2][SEP][2][128];
+  __shared__ __align__(8) uint64_t full[XS], empty[XS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t0 = blockIdx.x * TILE;
-  const int h_chunks = H / 256;
+  const int h_chunks = H / 256, passes = (E + REP - 1) / REP, total = passes * h_chunks;
   if (tid < AUR_MAXN) hist_s[tid] = 0;
-  const int4* xrow[8];
-#pragma unroll
-  for (int t = 0; t < 8; t++) xrow[t] = reinterpret_cast<const int4*>(x + (size_t)min(t0 + warp * 8 + t, T - 1) * H);
-  const int se = tid >> 5, sl = tid & 31;  // staging: expert se of the pass, lane slot sl (8 h values)
+  if (tid == 0) {
+    for (int q = 0; q < XS; q++) {
+      tc::mbar_init(&full[q], 1);
+      tc::mbar_init(&empty[q], WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < XS && q < total; q++) {
+      tc::mbar_expect_tx(&full[q], XCHUNK);
+      tma_load_2d(xs + q * XCHUNK, &xmap, &full[q], 256 * (q % h_chunks), t0);
+    }
 
-  for (int e0 = 0; e0 < E; e0 += SEP) {
-    const int ev = min(SEP, E - e0);
-    const int4* wsrc = reinterpret_cast<const int4*>(wg + (size_t)(e0 + min(se, ev - 1)) * H) + sl;
-    auto stage = [&](int buf, int4 v) {
-      float f[8];
-      bf16x8_to_f32(v, f);
-      *reinterpret_cast<float4*>(&w_s[buf][se][0][sl * 4]) = make_float4(f[0], f[1], f[2], f[3]);
-      *reinterpret_cast<float4*>(&w_s[buf][se][1][sl * 4]) = make_float4(f[4], f[5], f[6], f[7]);
-    };
-    stage(0, __ldg(wsrc));
-    __syncthreads();
-    float acc[8][SEP];
+  for (int pass = 0; pass < passes; pass++) {
+    const int e0 = pass * REP, ev = min(REP, E - e0);
+    float acc[8][REP];
 #pragma unroll
     for (int t = 0; t < 8; t++)
 #pragma unroll
-      for (int e = 0; e < SEP; e++) acc[t][e] = 0.0f;
+      for (int e = 0; e < REP; e++) acc[t][e] = 0.0f;
     for (int i = 0; i < h_chunks; i++) {
-      const int buf = i & 1;
-      int4 wn = make_int4(0, 0, 0, 0);
-      if (i + 1 < h_chunks) wn = __ldg(wsrc + 32 * (i + 1));  // next slice, in flight during the FMAs
-      float wf[SEP][8];
+      const int q = pass * h_chunks + i, s = q % XS;
+      const uint32_t ph = (uint32_t)(q / XS) & 1u;
+      float wf[REP][8];
 #pragma unroll
-      for (int e = 0; e < SEP; e++) {
-        const float4 a = *reinterpret_cast<const float4*>(&w_s[buf][e][0][lane * 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&w_s[buf][e][1][lane * 4]);
-        wf[e][0] = a.x; wf[e][1] = a.y; wf[e][2] = a.z; wf[e][3] = a.w;
-        wf[e][4] = b.x; wf[e][5] = b.y; wf[e][6] = b.z; wf[e][7] = b.w;
-      }
+      for (int e = 0; e < REP; e++)  // experts past the pass's last re-read a valid row (dropped)
+        bf16x8_to_f32(__ldg(reinterpret_cast<const int4*>(wg + (size_t)(e0 + min(e, ev - 1)) * H + 256 * i) + lane),
+                      wf[e]);
+      tc::mbar_wait(&full[s], ph);
+      const uint8_t* xb = xs + s * XCHUNK + (warp * 8) * 512 + 16 * lane;
 #pragma unroll
       for (int t = 0; t < 8; t++) {
         float xf[8];
-        bf16x8_to_f32(ld_nc_v4(xrow[t] + 32 * i + lane), xf);
+        bf16x8_to_f32(*reinterpret_cast<const int4*>(xb + t * 512), xf);
 #pragma unroll
-        for (int e = 0; e < SEP; e++)
+        for (int e = 0; e < REP; e++)
 #pragma unroll
           for (int jj = 0; jj < 8; jj++) acc[t][e] = fmaf(xf[jj], wf[e][jj], acc[t][e]);
       }
-      if (i + 1 < h_chunks) stage(buf ^ 1, wn);
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
+      if (tid == 0 && q + XS < total) {  // refill this stage once every warp is done with it
+        tc::mbar_wait(&empty[s], ph);
+        tc::mbar_expect_tx(&full[s], XCHUNK);
+        tma_load_2d(xs + s * XCHUNK, &xmap, &full[s], 256 * ((q + XS) % h_chunks), t0);
+      }
     }
-    // xor tree over the lanes: reduce-scatter per group of 32 pairs (pair p = t * SEP + e)
+    // xor tree over the lanes: reduce-scatter per group of 32 pairs (pair p = t * REP + e)
 #pragma unroll
     for (int g = 0; g < 2; g++) {
       float v[32];
 #pragma unroll
-      for (int q = 0; q < 32; q++) v[q] = acc[(g * 32 + q) / SEP][(g * 32 + q) % SEP];
+      for (int qq = 0; qq < 32; qq++) v[qq] = acc[(g * 32 + qq) / REP][(g * 32 + qq) % REP];
 #pragma unroll
       for (int o = 16, sz = 32; o >= 1; o >>= 1, sz >>= 1) {
         const bool upper = lane & o;
 #pragma unroll
-        for (int q = 0; q < sz / 2; q++) {
-          float mine = upper ? v[q + sz / 2] : v[q];
-          float send = upper ? v[q] : v[q + sz / 2];
+        for (int qq = 0; qq < sz / 2; qq++) {
+          float mine = upper ? v[qq + sz / 2] : v[qq];
+          float send = upper ? v[qq] : v[qq + sz / 2];
           float got = __shfl_xor_sync(0xffffffffu, send, o);
-          v[q] = mine + got;
+          v[qq] = mine + got;
         }
       }
-      const int pr = g * 32 + lane, tq = pr / SEP, eq = e0 + pr % SEP;
+      const int pr = g * 32 + lane, tq = pr / REP, eq = e0 + pr % REP;
       if (eq < E) logit_s[warp * 8 + tq][eq] = v[0] + bias[eq];
     }
   }
   __syncthreads();
   route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
              slot_dst, blk_cnt, counts);
+}
+
+typedef CUresult (*EncodeTiledFnR)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_x_map(CUtensorMap* m, const void* x, uint64_t T, uint64_t H) {
+  static EncodeTiledFnR fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFnR>(p);
+  }
+  cuuint64_t dims[2] = {H, T};
+  cuuint64_t strides[1] = {H * 2};
+  cuuint32_t box[2] = {256, TILE};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // K3: token permutation. CTA = 64 threads = the 64 tokens of one route tile.
@@ -361,23 +313,19 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
     return AURORA_EINVAL;
   const int blocks = (T + TILE - 1) / TILE;
   cudaStream_t s = (cudaStream_t)stream;
-  const __nv_bfloat16* xb = (const __nv_bfloat16*)x;
   const __nv_bfloat16* wb = (const __nv_bfloat16*)w_gate;
-#define LAUNCH(TG, EP)                                                                          \
-  route_kernel<TG, EP><<<blocks, WARPS * 32, 0, s>>>(xb, wb, bias, T, H, E, k, gpu_of_expert, n, \
-                                                    rank_base, tokens_per_rank, topk_idx,        \
-                                                    topk_w, slot_dst, blk_cnt, counts)
-  // 4 tokens x 8 experts per warp pass: the gate matrix is streamed once per
-  // 4 tokens (ceil(E/8) passes), x re-read from L1 between passes; E <= 4 in one pass
   if (E < 1 || E > MAXE) return AURORA_EUNSUPPORTED;
-  if (E <= 4)
-    LAUNCH(8, 4);
-  else if (E <= 8)
-    LAUNCH(4, 8);
-  else
-    route_staged_kernel<<<blocks, WARPS * 32, 0, s>>>(xb, wb, bias, T, H, E, k, gpu_of_expert, n, rank_base,
-                                                     tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
-#undef LAUNCH
+  CUtensorMap xmap;
+  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H)) return AURORA_ECUDA;
+  constexpr int dyn = XS * XCHUNK + 1024;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(route_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
+      return AURORA_ECUDA;
+    attr = true;
+  }
+  route_tma_kernel<<<blocks, WARPS * 32, dyn, s>>>(xmap, wb, bias, T, H, E, k, gpu_of_expert, n, rank_base,
+                                                   tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
