@@ -6,8 +6,6 @@
 #include <cuda_runtime.h>
 #include "../../paper_2410_17043_b200/csrc/fastmatch.cuh"
 #include "../../paper_2410_17043_b200/csrc/fastmatch8b.cuh"
-#include "../../paper_2410_17043_b200/csrc/fastmatch8c.cuh"
-#include "fastmatch8d.cuh"
 #ifdef PROFILE
 #include "/tmp/k2/fm8p.cuh"
 #endif
@@ -37,18 +35,6 @@ __global__ void bench(const uint32_t* g, int ng, int reps, uint32_t* out_a, uint
       if (r == 0) out_b[i] = f.ML;
     }
   long long t2 = clock64();
-  for (int r = 0; r < reps; r++)
-    for (int i = 0; i < ng; i++) {
-      FastMatch8d f;
-      f.P = ((uint64_t)g[4 * i + 1] << 32) | (g[4 * i] ^ (acc & 0));
-      f.S = ((uint64_t)g[4 * i + 3] << 32) | g[4 * i + 2];
-      f.run(8);
-      uint32_t nb = 0;
-      for (int u = 0; u < 8; u++) nb |= (uint32_t)((f.ML >> (8 * u)) & 15) << (4 * u);
-      f.ML = nb;
-      acc += (uint32_t)f.ML;
-      if (r == 0) out_a[ng + i] = f.ML;
-    }
   long long t3 = clock64();
 #ifdef PROFILE
   long long cg = 0, ch = 0, ck = 0;
@@ -85,9 +71,9 @@ int main(int argc, char** argv) {
   for (int i = 0; i < ng; i++) {
     uint32_t nb = 0;
     for (int u = 0; u < 8; u++) nb |= (uint32_t)((rb[i] >> (8 * u)) & 15) << (4 * u);
-    if (nb != ra[i] || ra[ng + i] != ra[i]) bad++;
+    if (nb != ra[i]) bad++;
   }
-  printf("graphs %d  FastMatch8 %.0f  FastMatch8b %.0f  FastMatch8d %.0f cyc/match  mismatches %d\n", ng,
-         (double)hc[0] / (ng * reps), (double)hc[1] / (ng * reps), (double)hc[3] / (ng * reps), bad);
+  printf("graphs %d  FastMatch8 %.0f  FastMatch8b %.0f cyc/match  mismatches %d\n", ng,
+         (double)hc[0] / (ng * reps), (double)hc[1] / (ng * reps), bad);
   return bad != 0;
 }
