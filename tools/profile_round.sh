@@ -5,8 +5,13 @@ set -x
 mkdir -p gpurun_out/prof
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/prof/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/prof/bench_under_ncu.log 2>&1
-for k in aurora_schedule_kernel engine_tma_kernel route_kernel pack_kernel aggregate_kernel grouped_gemm_2sm_kernel; do
+for k in aurora_schedule_kernel engine_tma_kernel route_tma_kernel pack_kernel aggregate_kernel; do
   ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 -o gpurun_out/prof/$k \
     python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/prof/$k.log 2>&1
 done
+ls -la gpurun_out/prof
+# both expert GEMM launches of one step
+ncu --set full --import-source on --clock-control none -k regex:grouped_gemm_2sm_kernel -s 2 -c 2 \
+  -o gpurun_out/prof/grouped_gemm_2sm_kernel python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
+  > gpurun_out/prof/grouped_gemm_2sm_kernel.log 2>&1
 ls -la gpurun_out/prof
