@@ -117,9 +117,11 @@ class AuroraMoELayer:
         self.gpu_of = gpu_of
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
-        # copy CTAs per rank (two 256-thread CTAs fit per SM; all must be
-        # co-resident -- the engine clamps to the occupancy limit too)
-        self.C = ctas_per_rank or max(1, min(32, (2 * sms) // self.n_local))
+        # copy CTAs per rank: as many as stay co-resident (two TMA-engine CTAs per SM; the
+        # engine clamps to its occupancy limit), capped at 64 -- enough rows in flight for a
+        # GPU's NVLink when one rank owns the GPU (measured in loopback: 16 / 24 / 32 / 37 CTAs
+        # per rank -> paced dispatch 336 / 253 / 217 / 204 us, profiles/r01_engine_sweep.json)
+        self.C = ctas_per_rank or max(1, min(64, (2 * sms) // self.n_local))
         self.spin_limit = spin_limit
         H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
         Tr = cfg.tokens_per_rank
