@@ -198,7 +198,7 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
  * error. K2 needs n_local x this value to count hand-over thresholds. The
  * engine's grid (n_local x that value) is split among its ranks by `split`
  * (csrc/apportion.cuh; bw: rank bandwidths for AURORA_SPLIT_BANDWIDTH). */
-int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu);
+int aurora_engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu);
 
 /* ---------------------------------------------------------------- K7 ----
  * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret_i[soff[i][dst_s] + pos[t][s]]

@@ -379,7 +379,6 @@ struct TmaShared {
   volatile int known, known_done, cons_k;
   int32_t idx[32];
   // per-call metadata staged once: every per-entry lookup is a shared-memory read
-  int32_t soff[AUR_MAXN * AUR_MAXN], roff[AUR_MAXN * AUR_MAXN];
   char* dst[AUR_MAXN];
   char* dst2[AUR_MAXN];
   int32_t* ctr[AUR_MAXN];
@@ -392,6 +391,9 @@ struct TmaShared {
 __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p, int S, int slot_bytes) {
   extern __shared__ __align__(128) unsigned char slots[];
   __shared__ TmaShared sh;
+  // per-call buffer offsets behind the row slots (n x n each): every per-entry lookup is a shared read
+  int32_t* soff_s = reinterpret_cast<int32_t*>(slots + (size_t)S * slot_bytes);
+  int32_t* roff_s = soff_s + p.n * p.n;
   __shared__ int cs[AUR_MAXN];
   int r_local, c, C;
   cta_assign(p, cs, r_local, c, C);
@@ -407,8 +409,8 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
   const int4* table = dispatch ? p.chunks : p.rchunks;
   volatile int* abort = &sh.abort;
   for (int q = threadIdx.x; q < n * n; q += TMA_THREADS) {
-    sh.soff[q] = p.soff[q];
-    sh.roff[q] = p.roff[q];
+    soff_s[q] = p.soff[q];
+    roff_s[q] = p.roff[q];
   }
   for (int q = threadIdx.x; q < n; q += TMA_THREADS) {
     sh.dst[q] = p.dst_bufs[q];
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       slice(ntok, r0, r1);
       // source rows: dispatch gathers x rows through the send list (pair (g, peer)
       // starts at soff[g][peer]); combine reads expert outputs of pair (peer, g)
-      const int base = dispatch ? sh.soff[g * n + peer] + first : sh.roff[peer * n + g] + first;
+      const int base = dispatch ? soff_s[g * n + peer] + first : roff_s[peer * n + g] + first;
       for (int b = r0; b < r1; b += 32) {
         const int cnt = min(32, r1 - b);
         if (dispatch) {
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       }
       int r0, r1;
       slice(ntok, r0, r1);
-      const long long drow0 = dispatch ? (long long)sh.roff[g * n + peer] + first : (long long)sh.soff[peer * n + g] + first;
+      const long long drow0 = dispatch ? (long long)roff_s[g * n + peer] + first : (long long)soff_s[peer * n + g] + first;
       char* dst = sh.dst[peer];
       char* dst2 = sh.dst2[peer];
       if (lane == 0) {
@@ -710,14 +712,16 @@ __global__ void __launch_bounds__(THREADS) aggregate_kernel(
 // spins on flags written by others, so all must be resident); also the TMA
 // engine's slot geometry. Returns the clamped count, 0 if none fit, -1 on a
 // CUDA error. Deterministic: every process computes the same value.
-static int engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int rb2, bool lsu, int* S_out,
+static int engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int rb2, bool lsu, int* S_out,
                        int* slot_out, size_t* dyn_out) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int slot_bytes = ((row_bytes + rb2 + 127) / 128) * 128;
-  const int S = max(2, min(16, (96 * 1024) / slot_bytes));
-  const size_t dyn = lsu ? 0 : (size_t)S * slot_bytes;
+  // 48 KB of row slots: four TMA-engine CTAs fit per SM -- more copy CTAs beat deeper rings
+  // (loopback C2, paced dispatch: 2 CTAs/SM x 12 slots 204 us, 3 x 8 170 us, 4 x 6 155 us, 6 x 4 159 us)
+  const int S = max(2, min(16, (48 * 1024) / slot_bytes));
+  const size_t dyn = lsu ? 0 : (size_t)S * slot_bytes + 2 * (size_t)n * n * sizeof(int32_t);
   if (!lsu && dyn > 200 * 1024) return 0;
   if (!lsu && cudaFuncSetAttribute(engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
                   cudaSuccess)
@@ -729,13 +733,16 @@ static int engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int rb2, b
   if (S_out) *S_out = S;
   if (slot_out) *slot_out = slot_bytes;
   if (dyn_out) *dyn_out = dyn;
-  return min(ctas_per_rank, (occ * sms) / n_local);
+  // one SM stays free for K2, which runs beside the PDL-launched dispatch (it
+  // reserves most of its SM's shared memory); every copy CTA must be resident
+  return min(ctas_per_rank, (occ * (sms - 1)) / n_local);
 }
 
-extern "C" int aurora_engine_ctas(int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu) {
-  if (n_local < 1 || ctas_per_rank < 1 || row_bytes < 16 || row_bytes % 16 || row2_bytes < 0 || row2_bytes % 16)
+extern "C" int aurora_engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu) {
+  if (n < 1 || n > AUR_MAXN || n_local < 1 || n_local > n || ctas_per_rank < 1 || row_bytes < 16 ||
+      row_bytes % 16 || row2_bytes < 0 || row2_bytes % 16)
     return -AURORA_EINVAL;
-  const int c = engine_ctas(n_local, ctas_per_rank, row_bytes, row2_bytes, lsu != 0, nullptr, nullptr, nullptr);
+  const int c = engine_ctas(n, n_local, ctas_per_rank, row_bytes, row2_bytes, lsu != 0, nullptr, nullptr, nullptr);
   return c > 0 ? c : (c == 0 ? -AURORA_EINVAL : -AURORA_ECUDA);
 }
 
@@ -759,7 +766,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   const int rb2 = src2_bufs ? row2_bytes : 0;
   int S = 0, slot_bytes = 0;
   size_t dyn = 0;
-  const int c_clamped = engine_ctas(n_local, ctas_per_rank, row_bytes, rb2, lsu, &S, &slot_bytes, &dyn);
+  const int c_clamped = engine_ctas(n, n_local, ctas_per_rank, row_bytes, rb2, lsu, &S, &slot_bytes, &dyn);
   if (c_clamped < 1) return c_clamped == 0 ? AURORA_EINVAL : AURORA_ECUDA;
   ctas_per_rank = c_clamped;
   EngineParams p;

@@ -117,11 +117,11 @@ class AuroraMoELayer:
         self.gpu_of = gpu_of
         sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.num_sms = sms
-        # copy CTAs per rank: as many as stay co-resident (two TMA-engine CTAs per SM; the
-        # engine clamps to its occupancy limit), capped at 64 -- enough rows in flight for a
-        # GPU's NVLink when one rank owns the GPU (measured in loopback: 16 / 24 / 32 / 37 CTAs
-        # per rank -> paced dispatch 336 / 253 / 217 / 204 us, profiles/r01_engine_sweep.json)
-        self.C = ctas_per_rank or max(1, min(64, (2 * sms) // self.n_local))
+        # copy CTAs per rank: as many as stay co-resident (four TMA-engine CTAs per SM; the
+        # engine clamps to its occupancy limit), capped at 96. Measured in loopback (C2, paced
+        # dispatch): 16 / 24 / 32 / 37 / 55 / 74 CTAs per rank -> 336 / 253 / 217 / 204 / 170 /
+        # 155 us (profiles/r01_engine_sweep.json)
+        self.C = ctas_per_rank or max(1, min(96, (4 * sms) // self.n_local))
         self.spin_limit = spin_limit
         H, F, E, k = cfg.hidden, cfg.ffn, cfg.experts, cfg.top_k
         Tr = cfg.tokens_per_rank
@@ -336,7 +336,8 @@ class AuroraMoELayer:
     def engine_ctas(self, combine: bool) -> int:
         """Copy CTAs per local rank the engine launches (clamped to co-residency)."""
         row2 = self.meta_bytes if (self.G > 1 and not combine) else 0
-        c = self.L.aurora_engine_ctas(self.n_local, self.C, self.cfg.hidden * 2, row2, 1 if self.engine_lsu else 0)
+        c = self.L.aurora_engine_ctas(self.n, self.n_local, self.C, self.cfg.hidden * 2, row2,
+                                      1 if self.engine_lsu else 0)
         if c < 1:
             _lib.check(-c, "aurora_engine_ctas")
         return c

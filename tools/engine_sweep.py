@@ -14,7 +14,7 @@ res = {}
 layer = AuroraMoELayer(cfg)
 layer(x)
 torch.cuda.synchronize()
-for C in (16, 24, 32, 37, 16, 24, 32, 37):
+for C in (16, 24, 32, 37, 55, 74, 16, 24, 32, 37, 55, 74):
     layer.C = C
     for unpaced in (0, 16):
         layer.unpaced = unpaced
