@@ -99,8 +99,10 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
 }
 
 constexpr int XS = 4;                      // x stages
-constexpr int XCHUNK = TILE * 256 * 2;     // bytes per stage
 constexpr int REP = 8;                     // experts per pass
+constexpr int XBYTES = TILE * 256 * 2;     // x part of a stage: 64 tokens x 256 h
+constexpr int WBYTES = REP * 256 * 2;      // gate part: the pass's 8 experts x 256 h
+constexpr int XCHUNK = XBYTES + WBYTES;    // bytes per stage
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
@@ -110,7 +112,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 
 __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ wg,
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
     const float* __restrict__ bias, int T, int H, int E, int k,
     const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
@@ -132,11 +134,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // stage q holds x chunk (q % h_chunks) of the CTA's tokens and the gate slice of pass q / h_chunks
+  auto fill = [&](int q, int st) {
+    tc::mbar_expect_tx(&full[st], XCHUNK);
+    tma_load_2d(xs + st * XCHUNK, &xmap, &full[st], 256 * (q % h_chunks), t0);
+    tma_load_2d(xs + st * XCHUNK + XBYTES, &wmap, &full[st], 256 * (q % h_chunks), REP * (q / h_chunks));
+  };
   if (tid == 0)
-    for (int q = 0; q < XS && q < total; q++) {
-      tc::mbar_expect_tx(&full[q], XCHUNK);
-      tma_load_2d(xs + q * XCHUNK, &xmap, &full[q], 256 * (q % h_chunks), t0);
-    }
+    for (int q = 0; q < XS && q < total; q++) fill(q, q);
 
   for (int pass = 0; pass < passes; pass++) {
     const int e0 = pass * REP, ev = min(REP, E - e0);
@@ -148,12 +153,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
     for (int i = 0; i < h_chunks; i++) {
       const int q = pass * h_chunks + i, s = q % XS;
       const uint32_t ph = (uint32_t)(q / XS) & 1u;
-      float wf[REP][8];
-#pragma unroll
-      for (int e = 0; e < REP; e++)  // experts past the pass's last re-read a valid row (dropped)
-        bf16x8_to_f32(__ldg(reinterpret_cast<const int4*>(wg + (size_t)(e0 + min(e, ev - 1)) * H + 256 * i) + lane),
-                      wf[e]);
       tc::mbar_wait(&full[s], ph);
+      float wf[REP][8];  // experts past E read TMA's zero fill; their sums are dropped
+#pragma unroll
+      for (int e = 0; e < REP; e++)
+        bf16x8_to_f32(*reinterpret_cast<const int4*>(xs + s * XCHUNK + XBYTES + e * 512 + 16 * lane), wf[e]);
       const uint8_t* xb = xs + s * XCHUNK + (warp * 8) * 512 + 16 * lane;
 #pragma unroll
       for (int t = 0; t < 8; t++) {
@@ -168,8 +172,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
       if (lane == 0) mbar_arrive_cta(&empty[s]);
       if (tid == 0 && q + XS < total) {  // refill this stage once every warp is done with it
         tc::mbar_wait(&empty[s], ph);
-        tc::mbar_expect_tx(&full[s], XCHUNK);
-        tma_load_2d(xs + s * XCHUNK, &xmap, &full[s], 256 * ((q + XS) % h_chunks), t0);
+        fill(q + XS, s);
       }
     }
     // xor tree over the lanes: reduce-scatter per group of 32 pairs (pair p = t * REP + e)
@@ -202,7 +205,7 @@ typedef CUresult (*EncodeTiledFnR)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool make_x_map(CUtensorMap* m, const void* x, uint64_t T, uint64_t H) {
+bool make_x_map(CUtensorMap* m, const void* x, uint64_t T, uint64_t H, uint32_t box_rows = TILE) {
   static EncodeTiledFnR fn = nullptr;
   if (!fn) {
     cudaDriverEntryPointQueryResult q;
@@ -214,7 +217,7 @@ bool make_x_map(CUtensorMap* m, const void* x, uint64_t T, uint64_t H) {
   }
   cuuint64_t dims[2] = {H, T};
   cuuint64_t strides[1] = {H * 2};
-  cuuint32_t box[2] = {256, TILE};
+  cuuint32_t box[2] = {256, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -313,10 +316,10 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
     return AURORA_EINVAL;
   const int blocks = (T + TILE - 1) / TILE;
   cudaStream_t s = (cudaStream_t)stream;
-  const __nv_bfloat16* wb = (const __nv_bfloat16*)w_gate;
   if (E < 1 || E > MAXE) return AURORA_EUNSUPPORTED;
-  CUtensorMap xmap;
-  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H)) return AURORA_ECUDA;
+  CUtensorMap xmap, wmap;
+  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H) || !make_x_map(&wmap, w_gate, (uint64_t)E, (uint64_t)H, REP))
+    return AURORA_ECUDA;
   constexpr int dyn = XS * XCHUNK + 1024;
   static bool attr = false;
   if (!attr) {
@@ -324,7 +327,7 @@ extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias
       return AURORA_ECUDA;
     attr = true;
   }
-  route_tma_kernel<<<blocks, WARPS * 32, dyn, s>>>(xmap, wb, bias, T, H, E, k, gpu_of_expert, n, rank_base,
+  route_tma_kernel<<<blocks, WARPS * 32, dyn, s>>>(xmap, wmap, bias, T, H, E, k, gpu_of_expert, n, rank_base,
                                                    tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
