@@ -557,7 +557,11 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": workload(args),
         "stage_ms_serial": stage_ms, "serial_ms_per_step": serial_ms,
-        "overlap": "local rows' copy + expert GEMM on a side stream, concurrent with K2 and the network dispatch",
+        "overlap": ("K2 (on-device schedule) and the dispatch engine run concurrently: the engine is a programmatic "
+                    "dependent launch of K2 and executes phase k as soon as K2 publishes it"
+                    if layer.stream_schedule and not layer.overlap else f"AURORA_OVERLAP={layer.overlap}"),
+        "engine": {"copy": "lsu" if layer.engine_lsu else "tma", "ctas_per_rank": layer.engine_ctas(False),
+                   "cta_split": ["even", "volume", "bandwidth"][layer.split], "early_pace": bool(layer.early_pace)},
         "all_to_all": {
             "dispatch_us": stage_ms["dispatch"] * 1e3, "combine_us": stage_ms["combine"] * 1e3,
             "schedule_us": stage_ms["schedule"] * 1e3,
