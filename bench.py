@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ranks", type=int, default=8, help="expert-parallel ranks (GPUs of the modelled cluster)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c4", "c5"],
-                    help="c2: Mixtral-8x7B layer (the headline); c4: C2 on an emulated heterogeneous "
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="c2: Mixtral-8x7B layer (the headline); c3: C2's model colocated with a 16-expert "
+                         "top-2 model (hidden 4096, FFN 7168; the config leaves F open) on the same 8 ranks by "
+                         "Aurora's colocation plan (single GPU only); c4: C2 on an emulated heterogeneous "
                          "cluster (bandwidths 100/80/50/40 x2, PAPER.md:666; placement by "
                          "assign_exclusive_hetero; copy CTAs per rank follow bandwidth); c5: DeepSeek-style "
                          "64 experts top-6, hidden 5120, FFN 1536 (DeepSeek-V2 expert size; the config "
@@ -69,7 +71,8 @@ C4_BANDWIDTHS = (1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4)  # PAPER.md:666 ratios 
 
 
 def workload(args):
-    name = {"c2": "C2 Mixtral-8x7B MoE layer", "c4": "C4 Mixtral-8x7B MoE layer, heterogeneous emulation",
+    name = {"c2": "C2 Mixtral-8x7B MoE layer", "c3": "C3 Mixtral-8x7B + 16-expert top-2 layers colocated",
+            "c4": "C4 Mixtral-8x7B MoE layer, heterogeneous emulation",
             "c5": "C5 DeepSeek-style 64-expert top-6 MoE layer"}[args.config]
     return {"workload": f"{name} (EP over {args.ranks} ranks)", "hidden": args.hidden, "ffn": args.ffn,
             "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.ranks,
@@ -326,10 +329,108 @@ def gemm_traffic(args):
         return None
 
 
+def run_c3(args):
+    """C3: two models colocated on the same ranks by Aurora's plan (colocation.py:
+    Lina-style slots of model b, colocate_homogeneous pairing, placement.py:109-126).
+    A step = one layer of each model over its 16384 tokens; value = both models'
+    tokens per second. Single GPU (loopback)."""
+    import numpy as np
+    import torch
+    from paper_2410_17043_b200 import _lib
+    from paper_2410_17043_b200.colocation import ColocatedLayers, combined_bmax, lina_slots, plan_colocation
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--config c3 runs on one GPU")
+    n = args.ranks
+    cfg_a = MoEConfig(hidden=4096, ffn=14336, experts=n, top_k=2, tokens=args.tokens, ranks=n, skew=args.skew,
+                      seed=args.seed)
+    cfg_b = MoEConfig(hidden=4096, ffn=7168, experts=2 * n, top_k=2, tokens=args.tokens, ranks=n, skew=1.5,
+                      seed=args.seed + 1)
+    g = torch.Generator(device="cuda").manual_seed(args.seed + 101)
+    xa = torch.randn(cfg_a.tokens, cfg_a.hidden, device="cuda", generator=g).to(torch.bfloat16)
+    xb = torch.randn(cfg_b.tokens, cfg_b.hidden, device="cuda", generator=g).to(torch.bfloat16)
+    sp = _lib.stream_ptr()
+    # deployment-time calibration: the routers alone give the traffic matrices
+    cal_a = AuroraMoELayer(cfg_a)
+    cal_a.route(xa, sp)
+    cal_b = AuroraMoELayer(cfg_b)
+    cal_b.route(xb, sp)
+    torch.cuda.synchronize()
+    counts_a = cal_a.counts.cpu().numpy()
+    slots = lina_slots(np.bincount(cal_b.topk_idx.cpu().numpy().ravel(), minlength=2 * n))
+    slot_of = [0] * (2 * n)
+    for s_, (e1, e2) in enumerate(slots):
+        slot_of[e1] = slot_of[e2] = s_
+    cal_s = AuroraMoELayer(cfg_b, gpu_of_expert=slot_of, weights={"w_gate": cal_b.w_gate, "bias": cal_b.bias,
+                                                                   "w13": cal_b.w13, "w2": cal_b.w2})
+    cal_s.route(xb, sp)
+    torch.cuda.synchronize()
+    slot_counts = cal_s.counts.cpu().numpy()
+    del cal_a, cal_b, cal_s
+    torch.cuda.empty_cache()
+    cplan = plan_colocation(counts_a, slot_counts, slots)
+    pair = ColocatedLayers(cfg_a, cfg_b, cplan)
+    for _ in range(args.warmup):
+        pair(xa, xb)
+    torch.cuda.synchronize()
+    pair.check_status()
+    st = torch.cuda.current_stream()
+    clocks = ClockSampler(os.path.join(ROOT, "gpurun_out", "clocks_r0.csv")
+                          if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp/clocks_r0.csv")
+    with clocks:
+        time.sleep(0.3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            pair(xa, xb)
+        e1.record(st)
+        torch.cuda.synchronize()
+        time.sleep(0.2)
+    pair.check_status()
+    ms = e0.elapsed_time(e1) / args.steps
+    # end to end: both inputs in from pinned host memory, both outputs back, every step
+    xah, xbh = xa.cpu().pin_memory(), xb.cpu().pin_memory()
+    oah, obh = torch.empty_like(xah).pin_memory(), torch.empty_like(xbh).pin_memory()
+    xad, xbd = torch.empty_like(xa), torch.empty_like(xb)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    for _ in range(args.steps):
+        xad.copy_(xah, non_blocking=True)
+        xbd.copy_(xbh, non_blocking=True)
+        oa, ob = pair(xad, xbd)
+        oah.copy_(oa, non_blocking=True)
+        obh.copy_(ob, non_blocking=True)
+    e3.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3) / args.steps
+    rows = float(pair.a.counts.sum().item()) * 14336 + float(pair.b.g_rows.sum().item()) * 7168
+    flops = rows * 2 * 3 * 4096
+    tokens = cfg_a.tokens + cfg_b.tokens
+    line = {"metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload(args),
+            "colocation": {"pairing": list(cplan.plan.pairing),
+                           "combined_bmax_tokens": combined_bmax(counts_a, slot_counts, cplan.plan),
+                           "model_b": {"experts": 2 * n, "top_k": 2, "hidden": 4096, "ffn": 7168, "skew": 1.5}},
+            "roofline": {"bound": "tensor", "achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                         "note": "both models' expert FLOPs over the whole step (upper bound on the GEMM time)"},
+            "gpu_launches": 8 + 13,
+            "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int((xah.numel() + xbh.numel()) * 2),
+                    "d2h_bytes_per_step": int((oah.numel() + obh.numel()) * 2), "ms_per_step": e2e_ms,
+                    "path": "ColocatedLayers.__call__ on pinned host buffers (serial copies)"},
+            "clocks": clocks.summary(0),
+            "timeline_ms": {"a": pair.a.timeline(xa), "b": pair.b.timeline(xb)}}
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     args = apply_preset(parse())
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "c3":
+        return run_c3(args)
     import numpy as np
     import torch
     import torch.distributed as dist
