@@ -677,6 +677,10 @@ def main():
             "loopback_hbm_floor_us": loopback_floor_us if world == 1 else None,
             "traffic_matrix": counts.tolist(),
             "ratio_dispatch_to_bound": (stage_ms["dispatch"] * 1e3) / bound_us if bound_us else None,
+            # the bottleneck rank's traffic (b_max) over the measured time: comparable with the
+            # 900 GB/s per direction per GPU the bound assumes
+            "bottleneck_gbs_dispatch": bmax_tokens * row_bytes / (stage_ms["dispatch"] * 1e-3) / 1e9,
+            "bottleneck_gbs_combine": bmax_tokens * row_bytes / (stage_ms["combine"] * 1e-3) / 1e9,
             "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:338-352; tokens when B = 1) "
                            "x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
             "transport": "NVSwitch peer stores" if world > 1 else
