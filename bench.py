@@ -476,7 +476,7 @@ def main():
 
     stages = ["route", "pack", "schedule", "dispatch", "experts", "combine", "aggregate"]
 
-    def staged_step(ev):
+    def staged_step(ev, fused=False):
         """The same kernels run serially on one stream with events between
         stages: the per-stage breakdown (the timed steps overlap stages)."""
         ev[0].record(stream)
@@ -489,9 +489,14 @@ def main():
         ev[3].record(stream)
         layer.dispatch(sp)
         ev[4].record(stream)
-        layer.experts(sp)
-        ev[5].record(stream)
-        layer.combine(sp)
+        if fused:  # the combine inside GEMM2's epilogue; "combine" = the receivers' wait
+            layer.experts_combine(sp)
+            ev[5].record(stream)
+            layer.combine_wait(sp)
+        else:
+            layer.experts(sp)
+            ev[5].record(stream)
+            layer.combine(sp)
         ev[6].record(stream)
         layer.aggregate(sp)
         ev[7].record(stream)
@@ -546,12 +551,20 @@ def main():
     ms_per_step = float(ms.item()) / args.steps
 
     # ---- per-stage breakdown (serial pass, not the headline number)
+    # (with the combine fused into GEMM2, the fused and the engine step alternate so
+    # both see the same power / clock state)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    evf = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    fused = layer.combine_in_gemm
     for s_ in range(args.steps):
         staged_step(evs[s_])
+        if fused:
+            staged_step(evf[s_], fused=True)
     torch.cuda.synchronize()
     layer.check_status()
     stage_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
+    fused_ms = ({st: sum(e[i].elapsed_time(e[i + 1]) for e in evf) / args.steps for i, st in enumerate(stages)}
+                if fused else None)
     serial_ms = sum(stage_ms.values())
     # ablation: the same engine with the schedule's pacing switched off
     layer.unpaced = 16
@@ -658,6 +671,13 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": workload(args),
         "stage_ms_serial": stage_ms, "serial_ms_per_step": serial_ms,
+        "combine_fused": None if fused_ms is None else {
+            "experts_plus_combine_ms": fused_ms["experts"] + fused_ms["combine"],
+            "vs_engine_ms": stage_ms["experts"] + stage_ms["combine"],
+            "wait_ms": fused_ms["combine"],
+            "note": "the layer's default: GEMM2's epilogue stores every row straight into its sender's return "
+                    "buffer (peer memory) and the last CTA signals the senders; the engine rows above time the "
+                    "reversed-schedule combine all-to-all (AURORA_COMBINE=engine)"},
         "overlap": ("K2 (on-device schedule) and the dispatch engine run concurrently: the engine is a programmatic "
                     "dependent launch of K2 and executes phase k as soon as K2 publishes it"
                     if layer.stream_schedule and not layer.overlap else f"AURORA_OVERLAP={layer.overlap}"),

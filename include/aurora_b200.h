@@ -200,6 +200,16 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
  * (csrc/apportion.cuh; bw: rank bandwidths for AURORA_SPLIT_BANDWIDTH). */
 int aurora_engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu);
 
+/* aurora_combine_wait: the receiving side of the fused combine
+ * (aurora_expert_ffn_combine). One thread per local sender rank
+ * r in [rank_base, rank_base + n_local) waits until its {pace, done} pair
+ * ctrs[r] (the combine's peer-mapped counter table, device array [n]) has
+ * done >= expect arrivals (one per expert rank: n), then re-arms the pair to
+ * zero. spin_limit bounds the wait (0 = unbounded); on expiry status =
+ * ETIMEOUT. sys: peers on other GPUs. */
+int aurora_combine_wait(int32_t* const* ctrs, int rank_base, int n_local, int expect, int sys,
+                        int64_t spin_limit, int32_t* status, void* stream);
+
 /* ---------------------------------------------------------------- K7 ----
  * aurora_aggregate: out[t] = sum_s topk_w[t][s] * ret_i[soff[i][dst_s] + pos[t][s]]
  * (with y_buf: slots whose expert lives on the token's own rank i are read from
@@ -230,6 +240,24 @@ int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const in
 int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                       void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
                       int64_t cap, int H, int F, int num_sms, void* stream);
+
+/* aurora_expert_ffn_combine: the same FFN (one expert per rank: group g is
+ * expert rank rank_base + g, all received rows) with the combine fused into
+ * GEMM2's epilogue -- the K6 + K5 pair written as one kernel over peer memory:
+ * every output row of sender i's block (recv rows roff[i][j] + [0, counts[i][j]))
+ * is stored straight into ret_bufs[i] row soff[i][j] + offset (the row the
+ * combine engine would write; NVSwitch stores overlap the GEMM tile by tile),
+ * rows of the rank's own tokens (i == j) into y_buf as with local-direct
+ * aggregation. The last CTA to finish adds G arrivals (release) to the done
+ * slot of every sender's {pace, done} pair ctrs[i] (the combine table);
+ * aurora_combine_wait on the sender consumes them. ticket: one int32, zero
+ * on first use (re-armed by the kernel). counts/soff/roff [n][n], ret_bufs[n],
+ * ctrs[n]: device arrays. sys: peers on other GPUs. n, G <= 16. */
+int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2, void* h_buf,
+                              void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
+                              void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
+                              const int32_t* roff, int n, int rank_base, int32_t* const* ctrs,
+                              int32_t* ticket, int sys, int num_sms, void* stream);
 
 /* Same FFN with the groups packed back to back (a rank hosting several
  * experts): group g's rows are a_buf rows [g_off[g], g_off[g] + g_rows[g]);

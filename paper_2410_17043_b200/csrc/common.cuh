@@ -74,6 +74,18 @@ __device__ __forceinline__ void st_na_v4(int4* p, int4 v) {
                : "memory");
 }
 
+// internal (gemm.cu -> gemm2sm.cu): the fused combine's destinations, see
+// aurora_expert_ffn_combine in include/aurora_b200.h
+struct AuroraScatterArgs {
+  void* const* ret;
+  const int32_t* counts;
+  const int32_t* soff;
+  const int32_t* roff;
+  int32_t* const* ctrs;
+  int32_t* ticket;
+  int n, rank_base, sys;
+};
+
 #define AUR_CHECK_LAUNCH()                          \
   do {                                              \
     cudaError_t _e = cudaGetLastError();            \

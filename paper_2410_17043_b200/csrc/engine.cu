@@ -817,6 +817,31 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   return AURORA_OK;
 }
 
+// the fused combine's receiving side: wait for every expert rank's arrival on
+// this process's senders, then re-arm the counters for the next layer step
+__global__ void combine_wait_kernel(int32_t* const* ctrs, int rank_base, int n_local, int expect, int sys,
+                                    long long spin_limit, int32_t* status) {
+  const int r = threadIdx.x;
+  if (r >= n_local) return;
+  int32_t* c = ctrs[rank_base + r];
+  if (!wait_ge(c + 1, expect, spin_limit, sys)) {
+    atomicExch(status, AURORA_ETIMEOUT);
+    return;
+  }
+  ((volatile int32_t*)c)[0] = 0;
+  ((volatile int32_t*)c)[1] = 0;
+  __threadfence_system();
+}
+
+extern "C" int aurora_combine_wait(int32_t* const* ctrs, int rank_base, int n_local, int expect, int sys,
+                                   int64_t spin_limit, int32_t* status, void* stream) {
+  if (!ctrs || !status || n_local < 1 || n_local > AUR_MAXN || rank_base < 0 || expect < 1) return AURORA_EINVAL;
+  combine_wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ctrs, rank_base, n_local, expect, sys, spin_limit,
+                                                          status);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
 extern "C" int aurora_debug_set_engine_trace(long long* trace) {
   return cudaMemcpyToSymbol(g_engine_trace, &trace, sizeof(trace)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }

@@ -25,6 +25,23 @@ constexpr int TMEM_COLS = 512;                   // 2 accumulators x 256 columns
 constexpr int MAX_GROUPS = 64;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = tc::idesc_bf16(BMP, BN);
+constexpr int SC_MAXN = 16;                      // fused combine: ranks / local groups
+
+// Fused combine (epilogue 0 with n > 0): group g is expert rank rank_base + g;
+// its received rows come in per-sender blocks (roff / counts); the epilogue
+// stores each output row straight into the sender's return buffer (peer memory
+// over NVSwitch) at the row the combine engine would have written, local rows
+// into c. The last CTA to finish releases one arrival per local group on every
+// sender's {pace, done} counter (done slot).
+struct Scatter {
+  __nv_bfloat16* const* ret;  // [n] return buffers (peer addresses), rows of N
+  const int32_t* counts;      // [n][n]
+  const int32_t* soff;        // [n][n]
+  const int32_t* roff;        // [n][n]
+  int32_t* const* ctrs;       // [n] {pace, done} counters of the senders
+  int32_t* ticket;            // grid completion ticket (zero; re-armed by the last CTA)
+  int n, rank_base, sys;
+};
 
 struct TileIter2 {
   int n_tiles_n, total;
@@ -59,7 +76,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             const __grid_constant__ CUtensorMap map_b,
                             __nv_bfloat16* __restrict__ c, const int32_t* __restrict__ m_start,
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
-                            int epilogue, int group_m) {
+                            int epilogue, int group_m, const Scatter sc) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -68,6 +85,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ TileIter2 it;
+  __shared__ int sc_lo[SC_MAXN * SC_MAXN], sc_cnt[SC_MAXN * SC_MAXN], sc_dst[SC_MAXN * SC_MAXN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_rank();
@@ -87,6 +105,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     it.prefix[G] = acc;
     it.total = acc;
+    for (int q = 0; q < (sc.n ? G * sc.n : 0); q++) {  // (group, sender) -> row block
+      const int g = q / sc.n, src = q - g * sc.n, r = sc.rank_base + g;
+      sc_lo[q] = sc.roff[src * sc.n + r];
+      sc_cnt[q] = sc.counts[src * sc.n + r];
+      sc_dst[q] = sc.soff[src * sc.n + r];
+    }
     for (int s = 0; s < STAGES; s++) {
       tc::mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
       tc::mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
@@ -193,6 +217,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       } else {
         __nv_bfloat16* out = c + row * (long long)N + nt * BN;
+        if (sc.n && live) {  // fused combine: the row goes back to its sender
+          for (int src = 0; src < sc.n; src++) {
+            const int q = g * sc.n + src, off = row_in_group - sc_lo[q];
+            if (off >= 0 && off < sc_cnt[q]) {
+              if (src != sc.rank_base + g)
+                out = sc.ret[src] + (long long)(sc_dst[q] + off) * N + nt * BN;
+              break;
+            }
+          }
+        }
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t r[32];
           TC_TMEM_LD32(tbase + c0, r);
@@ -215,9 +249,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc::mbar_arrive_cluster(tempty0 + acc * 8);
     }
   }
+  if (sc.n) {
+    if (sc.sys) __threadfence_system();
+    else __threadfence();
+  }
   tc::fence_before();
   __syncthreads();
   tc::cluster_sync();
+  if (sc.n && threadIdx.x == 0) {  // grid completion -> one arrival per group on every sender
+    __threadfence();
+    if (atomicAdd(sc.ticket, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      *sc.ticket = 0;
+      for (int src = 0; src < sc.n; src++) {
+        if (sc.sys) red_release_sys_add(sc.ctrs[src] + 1, G);
+        else red_release_gpu_add(sc.ctrs[src] + 1, G);
+      }
+    }
+  }
   if (warp == 1) {
     __syncwarp();
     tc::fence_after();
@@ -256,7 +305,24 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 // C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
-                              int K, int epilogue, int num_sms, cudaStream_t stream) {
+                              int K, int epilogue, int num_sms, cudaStream_t stream,
+                              const AuroraScatterArgs* scatter) {
+  Scatter sc{};
+  if (scatter) {
+    if (epilogue != 0 || m_start || cap <= 0 || scatter->n < 1 || scatter->n > SC_MAXN || G > SC_MAXN ||
+        scatter->rank_base < 0 || scatter->rank_base + G > scatter->n || !scatter->ret || !scatter->counts ||
+        !scatter->soff || !scatter->roff || !scatter->ctrs || !scatter->ticket)
+      return AURORA_EINVAL;
+    sc.ret = reinterpret_cast<__nv_bfloat16* const*>(scatter->ret);
+    sc.counts = scatter->counts;
+    sc.soff = scatter->soff;
+    sc.roff = scatter->roff;
+    sc.ctrs = scatter->ctrs;
+    sc.ticket = scatter->ticket;
+    sc.n = scatter->n;
+    sc.rank_base = scatter->rank_base;
+    sc.sys = scatter->sys;
+  }
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
@@ -281,7 +347,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   }
   const int grid = num_sms & ~1;
   grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m);
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -171,6 +171,7 @@ class AuroraMoELayer:
         self.rloc = torch.empty(n, **i32)
         self.rrem = torch.empty(n, **i32)
         self.engine_status = torch.zeros(1, **i32)
+        self.gemm_ticket = torch.zeros(1, **i32)  # fused combine: GEMM2's grid completion ticket
         # overlap: the local rows' copy + expert GEMM run on a side stream while
         # K2 computes the schedule and the engine moves the network rows
         # Measured on B200 (profiles/r01_overlap_sweep.json): the expert GEMM runs
@@ -185,6 +186,11 @@ class AuroraMoELayer:
         # the aggregation reads local (diagonal) rows straight from the expert output, so the
         # combine only moves rows that cross the network
         self.local_direct = os.environ.get("AURORA_LOCAL_DIRECT", "1") != "0"
+        # the combine fused into GEMM2's epilogue (one expert per rank): output rows are stored
+        # straight into their senders' return buffers while the GEMM runs, so no combine
+        # all-to-all follows the experts; AURORA_COMBINE=engine runs the reversed-schedule
+        # combine engine instead (needs local-direct aggregation either way)
+        self.fused_combine = os.environ.get("AURORA_COMBINE", "fused") == "fused"
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
@@ -413,6 +419,32 @@ class AuroraMoELayer:
                                             self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
                    "aurora_expert_ffn")
 
+    @property
+    def combine_in_gemm(self) -> bool:
+        """The combine runs inside GEMM2 (one expert per rank, local rows read in place)."""
+        return self.fused_combine and self.G == 1 and self.local_direct and not self.overlap
+
+    def experts_combine(self, stream: int) -> None:
+        """The experts with the combine fused into GEMM2's epilogue: every output
+        row goes straight to its sender's return buffer (peer memory), local rows
+        stay in ybuf for the aggregation; see aurora_expert_ffn_combine."""
+        cfg = self.cfg
+        sys_scope = 1 if self.n_local != self.n else 0
+        _lib.check(self.L.aurora_expert_ffn_combine(
+            self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), self.hbuf.data_ptr(),
+            self.ybuf.data_ptr(), self.rtot[self.rank_base:].data_ptr(), self.n_local, self.cap, cfg.hidden,
+            cfg.ffn, self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
+            self.n, self.rank_base, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), sys_scope,
+            self.num_sms, stream), "aurora_expert_ffn_combine")
+
+    def combine_wait(self, stream: int) -> None:
+        """Receiving side of the fused combine: every expert rank's rows for this
+        process's senders have landed (then the counters are re-armed)."""
+        sys_scope = 1 if self.n_local != self.n else 0
+        _lib.check(self.L.aurora_combine_wait(self.t_ctr_c.data_ptr(), self.rank_base, self.n_local, self.n,
+                                              sys_scope, self.spin_limit, self.engine_status.data_ptr(), stream),
+                   "aurora_combine_wait")
+
     def _experts_grouped(self, stream: int) -> None:
         """Several experts per rank: group the received rows by local expert,
         run the packed grouped GEMMs, pre-reduce each row's expert outputs."""
@@ -490,11 +522,17 @@ class AuroraMoELayer:
                 self.schedule(s)
                 self.dispatch(s, overlap_schedule=True)
                 mark("dispatched", main)
-                self.experts(s)
+                if self.combine_in_gemm:
+                    self.experts_combine(s)
+                else:
+                    self.experts(s)
             else:
                 self.schedule(s)
                 self.dispatch(s)
-                self.experts(s)
+                if self.combine_in_gemm:
+                    self.experts_combine(s)
+                else:
+                    self.experts(s)
         else:
             self._ev_pack.record(main)
             self.side.wait_event(self._ev_pack)
@@ -525,7 +563,10 @@ class AuroraMoELayer:
                 mark("joined", main)
             self.experts(s, "remote")
         mark("experts_done", main)
-        self.combine(s)
+        if self.combine_in_gemm:
+            self.combine_wait(s)
+        else:
+            self.combine(s)
         mark("combined", main)
         self.aggregate(s, out)
         mark("end", main)

@@ -330,16 +330,17 @@ def test_engine_cta_splits_and_copy_paths_agree(torch):
                     layer.check_status()
                     assert torch.equal(out, ref), (split, lsu, stream_sched, unpaced)
     for local_direct in (False, True):  # combine moving the local rows too vs aggregation reading them in place
-        layer.local_direct = local_direct
-        out = layer(x)
-        torch.cuda.synchronize()
-        layer.check_status()
-        assert torch.equal(out, ref), local_direct
+        for fused in (False, True):  # combine engine vs the combine fused into GEMM2's epilogue
+            layer.local_direct, layer.fused_combine = local_direct, fused
+            out = layer(x)
+            torch.cuda.synchronize()
+            layer.check_status()
+            assert torch.equal(out, ref), (local_direct, fused)
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
 
 
-@pytest.mark.parametrize("experts,top_k", [(8, 2), (16, 4)])
-def test_two_rank_groups_in_one_context(torch, experts, top_k):
+@pytest.mark.parametrize("experts,top_k,fused", [(8, 2, False), (8, 2, True), (16, 4, False)])
+def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
     """The multi-GPU code path on one device: two layer instances, each driving
     4 of the 8 ranks (what two processes on two GPUs do), with peer tables
     pointing at each other's buffers, system-scope flags, the traffic matrix
@@ -347,7 +348,9 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k):
     hand-over thresholds over 4-rank groups, and the two engines running
     concurrently on two streams, each waiting on the other's arrival counters.
     Output identical to the single-instance (loopback) layer; with several
-    experts per rank the expert-metadata plane travels to the peers too."""
+    experts per rank the expert-metadata plane travels to the peers too. fused:
+    GEMM2 stores each half's rows straight into the other half's return buffers
+    and signals its counters (aurora_expert_ffn_combine / aurora_combine_wait)."""
     from paper_2410_17043_b200.dist import _names, _strides
     from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
     cfg = MoEConfig(hidden=512, ffn=256, experts=experts, top_k=top_k, tokens=4096, ranks=8, skew=1.0, seed=6)
@@ -382,8 +385,13 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k):
         both(lambda h, s: h.pack(s))
         both(lambda h, s: h.schedule(s))
         both(lambda h, s: h.dispatch(s))   # concurrent: each waits on the other's flags
-        both(lambda h, s: h.experts(s))
-        both(lambda h, s: h.combine(s))
+        if fused:
+            assert all(h.combine_in_gemm for h in halves)
+            both(lambda h, s: h.experts_combine(s))
+            both(lambda h, s: h.combine_wait(s))
+        else:
+            both(lambda h, s: h.experts(s))
+            both(lambda h, s: h.combine(s))
         both(lambda h, s: h.aggregate(s))
         for h in halves:
             h.check_status()
