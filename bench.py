@@ -675,8 +675,9 @@ def main():
             "experts_plus_combine_ms": fused_ms["experts"] + fused_ms["combine"],
             "vs_engine_ms": stage_ms["experts"] + stage_ms["combine"],
             "wait_ms": fused_ms["combine"],
-            "note": "the layer's default: GEMM2's epilogue stores every row straight into its sender's return "
-                    "buffer (peer memory) and the last CTA signals the senders; the engine rows above time the "
+            "note": "the layer's default: the expert stage's last kernel (GEMM2's epilogue; the pre-reduction "
+                    "when a rank hosts several experts) stores every row straight into its sender's return "
+                    "buffer (peer memory) and its last CTA signals the senders; the engine rows above time the "
                     "reversed-schedule combine all-to-all (AURORA_COMBINE=engine)"},
         "overlap": ("K2 (on-device schedule) and the dispatch engine run concurrently: the engine is a programmatic "
                     "dependent launch of K2 and executes phase k as soon as K2 publishes it"

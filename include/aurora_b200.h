@@ -285,6 +285,16 @@ int aurora_gather_rows(const void* src, void* dst, const int32_t* idx, const int
 int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap,
                          int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k,
                          int H, void* ybuf, void* stream);
+/* aurora_expert_reduce_combine: the pre-reduction with the combine fused into it
+ * (several experts per rank): each reduced row of sender i's block is stored
+ * straight into ret_bufs[i] row soff[i][j] + offset (rows of the rank's own tokens
+ * into ybuf), then the last CTA adds n_local arrivals to every sender's combine
+ * counter; same contract as aurora_expert_ffn_combine's scatter / signal half. */
+int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void* meta, int64_t cap,
+                                 int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k,
+                                 int H, void* ybuf, void* const* ret_bufs, const int32_t* counts,
+                                 const int32_t* soff, const int32_t* roff, int n, int32_t* const* ctrs,
+                                 int32_t* ticket, int sys, void* stream);
 
 /* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
  * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */

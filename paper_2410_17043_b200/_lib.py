@@ -44,6 +44,8 @@ _SIGNATURES = {
                            _vp, _c_int, _vp],
     "aurora_gather_rows": [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp],
     "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp],
+    "aurora_expert_reduce_combine": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp,
+                                     _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "aurora_debug_set_schedule_profile": [_vp],
     "aurora_debug_set_schedule_trace": [_vp],

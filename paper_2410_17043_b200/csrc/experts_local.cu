@@ -121,17 +121,13 @@ __global__ void gather_rows_kernel(const char* __restrict__ src, char* __restric
   }
 }
 
-// y_row = sum_s w_s * yg[inv[row][s]] (fp32) -> bf16, warp per received row
-__global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
-                                     const int32_t* __restrict__ inv,
-                                     const uint8_t* __restrict__ meta, long long cap,
-                                     int meta_bytes, const int32_t* __restrict__ rtot, int n_local,
-                                     int rank_base, int k, int H, __nv_bfloat16* __restrict__ ybuf) {
-  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= (long long)n_local * cap) return;
-  int r, i;
-  if (!row_valid(row, cap, rtot, rank_base, r, i)) return;
+// one received row: the pre-reduction over its local experts; with the fused
+// combine the row is stored straight into its sender's return buffer
+__device__ __forceinline__ void reduce_row(const __nv_bfloat16* __restrict__ yg, const int32_t* __restrict__ inv,
+                                           const uint8_t* __restrict__ meta, long long row, int r, int i,
+                                           int meta_bytes, int rank_base, int k, int H,
+                                           __nv_bfloat16* __restrict__ ybuf, const AuroraScatterArgs& sc,
+                                           int lane) {
   const int2* m = reinterpret_cast<const int2*>(meta + row * meta_bytes);
   const int4* src[MAX_SLOTS];
   float w[MAX_SLOTS];
@@ -145,6 +141,15 @@ __global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
     }
   }
   int4* o = reinterpret_cast<int4*>(ybuf + row * H);
+  if (sc.n) {  // sender of this row: lane q tests sender q's block of rank r's receive buffer
+    const int rr = rank_base + r;
+    const int lo = lane < sc.n ? sc.roff[lane * sc.n + rr] : 0;
+    const bool hit = lane < sc.n && i >= lo && i < lo + sc.counts[lane * sc.n + rr];
+    const int src = __ffs(__ballot_sync(0xffffffffu, hit)) - 1;
+    const int dst_row = __shfl_sync(0xffffffffu, lane < sc.n ? sc.soff[lane * sc.n + rr] + i - lo : 0, src);
+    if (src != rr)
+      o = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16* const*>(sc.ret)[src] + (long long)dst_row * H);
+  }
   // U vectors per lane per step with every slot's loads issued before the math
   constexpr int U = 4;
   const int hv = H / 8;
@@ -178,6 +183,36 @@ __global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
 #pragma unroll
       for (int e = 0; e < 4; e++) rb[e] = __floats2bfloat162_rn(acc[uu][2 * e], acc[uu][2 * e + 1]);
       st_na_v4(o + u0 + 32 * uu, res);
+    }
+  }
+}
+
+// y_row = sum_s w_s * yg[inv[row][s]] (fp32) -> bf16, warp per received row
+__global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
+                                     const int32_t* __restrict__ inv,
+                                     const uint8_t* __restrict__ meta, long long cap,
+                                     int meta_bytes, const int32_t* __restrict__ rtot, int n_local,
+                                     int rank_base, int k, int H, __nv_bfloat16* __restrict__ ybuf,
+                                     const AuroraScatterArgs sc) {
+  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  int r, i;
+  if (row < (long long)n_local * cap && row_valid(row, cap, rtot, rank_base, r, i))
+    reduce_row(yg, inv, meta, row, r, i, meta_bytes, rank_base, k, H, ybuf, sc, lane);
+  if (sc.n) {  // fused combine: grid completion -> one arrival per local rank on every sender
+    if (sc.sys) __threadfence_system();
+    else __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(sc.ticket, 1) == (int)gridDim.x - 1) {
+        __threadfence();
+        *sc.ticket = 0;
+        for (int src = 0; src < sc.n; src++) {
+          if (sc.sys) red_release_sys_add(sc.ctrs[src] + 1, n_local);
+          else red_release_gpu_add(sc.ctrs[src] + 1, n_local);
+        }
+      }
     }
   }
 }
@@ -221,16 +256,40 @@ extern "C" int aurora_gather_rows(const void* src, void* dst, const int32_t* idx
   return AURORA_OK;
 }
 
-extern "C" int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta,
-                                    int64_t cap, int meta_bytes, const int32_t* rtot, int n_local,
-                                    int rank_base, int k, int H, void* ybuf, void* stream) {
+namespace {
+int launch_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap, int meta_bytes,
+                  const int32_t* rtot, int n_local, int rank_base, int k, int H, void* ybuf,
+                  const AuroraScatterArgs& sc, void* stream) {
   if (!yg || !inv || !meta || cap < 1 || !rtot || k < 1 || k > MAX_SLOTS || H % 8 || !ybuf)
     return AURORA_EINVAL;
   const long long rows = (long long)n_local * cap;
   const int blocks = (int)((rows * 32 + 255) / 256);
   expert_reduce_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)yg, inv, (const uint8_t*)meta, cap, meta_bytes, rtot, n_local,
-      rank_base, k, H, (__nv_bfloat16*)ybuf);
+      rank_base, k, H, (__nv_bfloat16*)ybuf, sc);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
+}
+}  // namespace
+
+extern "C" int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta,
+                                    int64_t cap, int meta_bytes, const int32_t* rtot, int n_local,
+                                    int rank_base, int k, int H, void* ybuf, void* stream) {
+  return launch_reduce(yg, inv, meta, cap, meta_bytes, rtot, n_local, rank_base, k, H, ybuf,
+                       AuroraScatterArgs{}, stream);
+}
+
+extern "C" int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void* meta,
+                                            int64_t cap, int meta_bytes, const int32_t* rtot,
+                                            int n_local, int rank_base, int k, int H, void* ybuf,
+                                            void* const* ret_bufs, const int32_t* counts,
+                                            const int32_t* soff, const int32_t* roff, int n,
+                                            int32_t* const* ctrs, int32_t* ticket, int sys,
+                                            void* stream) {
+  if (!ret_bufs || !counts || !soff || !roff || !ctrs || !ticket || n < 1 || n > 32 || n_local < 1 ||
+      rank_base < 0 || rank_base + n_local > n)
+    return AURORA_EINVAL;
+  const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
+  return launch_reduce(yg, inv, meta, cap, meta_bytes, rtot, n_local, rank_base, k, H, ybuf, sc,
+                       stream);
 }

@@ -421,14 +421,20 @@ class AuroraMoELayer:
 
     @property
     def combine_in_gemm(self) -> bool:
-        """The combine runs inside GEMM2 (one expert per rank, local rows read in place)."""
-        return self.fused_combine and self.G == 1 and self.local_direct and not self.overlap
+        """The combine runs inside the expert stage's last kernel (GEMM2's epilogue,
+        or the pre-reduction when a rank hosts several experts); local rows are read
+        in place by the aggregation."""
+        return self.fused_combine and self.local_direct and not self.overlap
 
     def experts_combine(self, stream: int) -> None:
-        """The experts with the combine fused into GEMM2's epilogue: every output
+        """The experts with the combine fused into their last kernel: every output
         row goes straight to its sender's return buffer (peer memory), local rows
-        stay in ybuf for the aggregation; see aurora_expert_ffn_combine."""
+        stay in ybuf for the aggregation; see aurora_expert_ffn_combine /
+        aurora_expert_reduce_combine."""
         cfg = self.cfg
+        if self.G > 1:
+            self._experts_grouped(stream, fused=True)
+            return
         sys_scope = 1 if self.n_local != self.n else 0
         _lib.check(self.L.aurora_expert_ffn_combine(
             self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), self.hbuf.data_ptr(),
@@ -445,7 +451,7 @@ class AuroraMoELayer:
                                               sys_scope, self.spin_limit, self.engine_status.data_ptr(), stream),
                    "aurora_combine_wait")
 
-    def _experts_grouped(self, stream: int) -> None:
+    def _experts_grouped(self, stream: int, fused: bool = False) -> None:
         """Several experts per rank: group the received rows by local expert,
         run the packed grouped GEMMs, pre-reduce each row's expert outputs."""
         cfg = self.cfg
@@ -463,6 +469,14 @@ class AuroraMoELayer:
                                               self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                               self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
                                               self.num_sms, stream), "aurora_expert_ffn_packed")
+        if fused:
+            _lib.check(L.aurora_expert_reduce_combine(
+                self.y_g.data_ptr(), self.inv.data_ptr(), self.meta_recv.data_ptr(), self.cap, self.meta_bytes,
+                self.rtot.data_ptr(), self.n_local, self.rank_base, k, H, self.ybuf.data_ptr(),
+                self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
+                self.n, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), 1 if self.n_local != self.n else 0,
+                stream), "aurora_expert_reduce_combine")
+            return
         _lib.check(L.aurora_expert_reduce(self.y_g.data_ptr(), self.inv.data_ptr(), self.meta_recv.data_ptr(),
                                           self.cap, self.meta_bytes, self.rtot.data_ptr(), self.n_local,
                                           self.rank_base, k, H, self.ybuf.data_ptr(), stream),

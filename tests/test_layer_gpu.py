@@ -215,6 +215,25 @@ def test_layer_deepseek_shape_small(torch):
                                    seed=4))
 
 
+def test_fused_and_engine_combine_agree_several_experts(torch):
+    """E > n: the combine fused into the pre-reduction (rows stored straight
+    into the senders' return buffers) and the reversed-schedule combine engine
+    give identical outputs, repeatedly (counters and ticket rearmed)."""
+    from paper_2410_17043_b200.layer import AuroraMoELayer
+    cfg = MoEConfig_(hidden=512, ffn=256, experts=64, top_k=6, tokens=2048, ranks=8, skew=1.0, seed=9)
+    layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    layer.fused_combine = False
+    ref = layer(x).clone()
+    for fused in (True, False, True, True):
+        layer.fused_combine = fused
+        out = layer(x)
+        torch.cuda.synchronize()
+        layer.check_status()
+        assert torch.equal(out, ref), fused
+    assert int(layer.ctr_c.abs().sum()) == 0 and int(layer.gemm_ticket.item()) == 0
+
+
 def MoEConfig_(**kw):
     from paper_2410_17043_b200.layer import MoEConfig
     return MoEConfig(**kw)
@@ -339,7 +358,7 @@ def test_engine_cta_splits_and_copy_paths_agree(torch):
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
 
 
-@pytest.mark.parametrize("experts,top_k,fused", [(8, 2, False), (8, 2, True), (16, 4, False)])
+@pytest.mark.parametrize("experts,top_k,fused", [(8, 2, False), (8, 2, True), (16, 4, False), (16, 4, True)])
 def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
     """The multi-GPU code path on one device: two layer instances, each driving
     4 of the 8 ranks (what two processes on two GPUs do), with peer tables
