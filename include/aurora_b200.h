@@ -107,7 +107,8 @@ int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32
  * function: the reference models the gate as LayerProfile.gate_work
  * (core.py:194-221) and consumes its output as TrafficMatrix (core.py:75-117)
  * relabelled by deploy_to_gpus (core.py:337-345).
- *   x[T][H] bf16, w_gate[E][H] bf16, bias[E] f32; H % 256 == 0, E <= 64, k <= 8
+ *   x[T][H] bf16; gate_prep = the bf16 gate w_gate[E][H] prepared once by
+ *   aurora_route_prepare_gate; bias[E] f32; H % 256 == 0, E <= 64, k <= 8
  *   gpu_of_expert[E]  rank hosting expert e (DeploymentPlan.assignment_a, core.py:253-304)
  *   tokens are grouped by rank: token t (local index) lives on rank
  *   rank_base + t / tokens_per_rank (workload.py:59-61)
@@ -115,11 +116,20 @@ int aurora_schedule_counts(const int32_t* counts, const double* bw, int n, int32
  *   slot_dst[T][k] (destination rank g of the slot, or -(g+1) when an earlier
  *   slot of the same token already goes to g: a token crosses the network
  *   once per destination), blk_cnt[T/64][n] per-64-token-block histogram,
- *   counts[n][n] += this call's rows (must be zeroed by the caller). */
-int aurora_route(const void* x, const void* w_gate, const float* bias, int T, int H, int E,
+ *   counts[n][n] += this call's rows (must be zeroed by the caller).
+ * logits (nullable): [T][E] fp32 workspace; with E > 8 the (64-token tile,
+ *   8-expert pass) units are balanced over a persistent grid and the logits
+ *   (+ bias) are left there; NULL (or E <= 8) = one CTA per tile, all passes. */
+int aurora_route(const void* x, const float* gate_prep, const float* bias, int T, int H, int E,
                  int k, const int32_t* gpu_of_expert, int n, int rank_base, int tokens_per_rank,
                  int32_t* topk_idx, float* topk_w, int32_t* slot_dst, int32_t* blk_cnt,
-                 int32_t* counts, void* stream);
+                 int32_t* counts, float* logits, void* stream);
+/* aurora_route_gate_floats: floats of the prepared gate (ceil(E/8) * 8 * H), or -AURORA_E*.
+ * aurora_route_prepare_gate: w_gate[E][H] bf16 -> gate_prep: widened to fp32 (exact) in the
+ *   router's shared-memory order (per 8-expert pass and 256-h chunk, lane-major expert pairs;
+ *   experts past E zero). Once per layer (the gate is a weight). */
+int aurora_route_gate_floats(int E, int H);
+int aurora_route_prepare_gate(const void* w_gate, int E, int H, float* gate_prep, void* stream);
 
 /* ---------------------------------------------------------------- K3 ----
  * aurora_pack: the token permutation. For each local source rank i and

@@ -26,7 +26,9 @@ _SIGNATURES = {
     "aurora_schedule_counts": [_vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int,
                                _c_int, _c_int, _vp],
     "aurora_route": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
-                     _vp, _vp, _vp, _vp, _vp, _vp],
+                     _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "aurora_route_gate_floats": [_c_int, _c_int],
+    "aurora_route_prepare_gate": [_vp, _c_int, _c_int, _vp, _vp],
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,

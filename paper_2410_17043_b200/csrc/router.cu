@@ -14,8 +14,9 @@
 // has the same tree shape, hence the same bits, as the butterfly.
 //
 // x is streamed by TMA (2-D tiles of 64 tokens x 256 h into a 4-stage
-// shared-memory ring); the gate slice of each 8-expert pass is read from
-// L1/L2 into registers once per chunk and reused for the warp's 8 tokens.
+// shared-memory ring) beside the matching block of the gate, prepared once
+// per layer as fp32 in a lane-major expert-pair layout; the FMAs run as
+// fp32x2 (FFMA2) over expert pairs -- two independent RN fmas, same bits.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -37,33 +38,51 @@ __device__ __forceinline__ void bf16x8_to_f32(const int4& v, float* f) {
   }
 }
 
+// 16-byte shared-memory load by 32-bit shared address (a generic load of the
+// realigned dynamic smem pointer would go through the long-scoreboard path)
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
 // top-k + softmax + destinations (thread per token, first 64 threads) and the
 // tile's destination histogram (warp-aggregated), shared by both router kernels
+// presel (sel_s / sv_s non-null): the selection was made by warp_topk, read it from shared memory
+template <bool PRESEL = false>
 __device__ __forceinline__ void route_tail(const float (*logit_s)[MAXE + 1], int* hist_s, int t0, int T, int E,
                                            int k, const int32_t* __restrict__ gpu_of_expert, int n,
                                            int rank_base, int tokens_per_rank, int32_t* __restrict__ topk_idx,
                                            float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
-                                           int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+                                           int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts,
+                                           const int (*sel_s)[MAXK] = nullptr, const float (*sv_s)[MAXK] = nullptr) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x < TILE) {
     const int tl = threadIdx.x, t = t0 + tl;
     const bool valid = t < T;
     int dst[MAXK];
     if (valid) {
-      uint64_t taken = 0;
       int sel[MAXK];
       float sv[MAXK];
-      for (int s = 0; s < k; s++) {
-        int best = -1;
-        float bv = 0.0f;
-        for (int e = 0; e < E; e++) {
-          if ((taken >> e) & 1) continue;
-          float l = logit_s[tl][e];
-          if (best < 0 || l > bv) { best = e; bv = l; }
+      if (PRESEL) {
+        for (int s = 0; s < k; s++) {
+          sel[s] = sel_s[tl][s];
+          sv[s] = sv_s[tl][s];
         }
-        taken |= 1ull << best;
-        sel[s] = best;
-        sv[s] = bv;
+      } else {
+        uint64_t taken = 0;
+        for (int s = 0; s < k; s++) {
+          int best = -1;
+          float bv = 0.0f;
+          for (int e = 0; e < E; e++) {
+            if ((taken >> e) & 1) continue;
+            float l = logit_s[tl][e];
+            if (best < 0 || l > bv) { best = e; bv = l; }
+          }
+          taken |= 1ull << best;
+          sel[s] = best;
+          sv[s] = bv;
+        }
       }
       float z = 0.0f, ex[MAXK];
       for (int s = 0; s < k; s++) { ex[s] = expf(sv[s] - sv[0]); z += ex[s]; }
@@ -98,10 +117,10 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
 }
 
-constexpr int XS = 4;                      // x stages
+constexpr int XS = 4;                      // stages
 constexpr int REP = 8;                     // experts per pass
-constexpr int XBYTES = TILE * 256 * 2;     // x part of a stage: 64 tokens x 256 h
-constexpr int WBYTES = REP * 256 * 2;      // gate part: the pass's 8 experts x 256 h
+constexpr int XBYTES = TILE * 256 * 2;     // x part of a stage: 64 tokens x 256 h (bf16)
+constexpr int WBYTES = REP * 256 * 4;      // gate part: the pass's 8 experts x 256 h (fp32, lane-major pairs)
 constexpr int XCHUNK = XBYTES + WBYTES;    // bytes per stage
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -110,9 +129,98 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       ::"r"(tc::smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)), "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
 
+// The gate, prepared once per layer (aurora_route_prepare_gate): widened to
+// fp32 (exact) and laid out per (8-expert pass, 256-h chunk) block of 2048
+// floats so that one 16-byte shared load per lane yields two expert pairs:
+//   float index ((p * 4 + jp) * 32 + l) * 4 + q,  q = 2 * (jj & 1) + (e & 1)
+//   for expert e = 8 pass + 2 p + (q & 1), h = 256 chunk + 8 l + 2 jp + (q >> 1)
+// (experts past E are zero). Lane l's accumulation order is unchanged.
+__global__ void prepare_gate_kernel(const __nv_bfloat16* __restrict__ w, int E, int H, float* __restrict__ wp) {
+  const int h_chunks = H / 256, passes = (E + REP - 1) / REP;
+  const long long total = (long long)passes * h_chunks * 2048;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (long long)gridDim.x * blockDim.x) {
+    const int blk = (int)(o >> 11), f = (int)(o & 2047);
+    const int pass = blk / h_chunks, c = blk - pass * h_chunks;
+    const int q = f & 3, l = (f >> 2) & 31, jp = (f >> 7) & 3, p = f >> 9;
+    const int e = pass * REP + 2 * p + (q & 1), h = c * 256 + 8 * l + 2 * jp + (q >> 1);
+    wp[o] = e < E ? __bfloat162float(w[(size_t)e * H + h]) : 0.0f;
+  }
+}
+
+// one 256-h chunk of the warp's 8 tokens x 8 experts: fp32x2 FMAs (FFMA2) over
+// expert pairs, x broadcast into both halves; per (token, expert) the same
+// sequential fmaf chain over h = 256 i + 8 l + jj as the scalar definition
+__device__ __forceinline__ void gate_chunk(float2 (&acc)[8][REP / 2], uint32_t stage_u, int warp, int lane) {
+  float2 wp[REP / 2][8];
+#pragma unroll
+  for (int p = 0; p < REP / 2; p++)
+#pragma unroll
+    for (int jp = 0; jp < 4; jp++) {
+      const int4 v = lds128(stage_u + XBYTES + ((p * 4 + jp) * 32 + lane) * 16);
+      wp[p][2 * jp] = make_float2(__int_as_float(v.x), __int_as_float(v.y));
+      wp[p][2 * jp + 1] = make_float2(__int_as_float(v.z), __int_as_float(v.w));
+    }
+  const uint32_t xb = stage_u + (warp * 8) * 512 + 16 * lane;
+  // tokens in groups of TG, jj outer: TG * 4 independent accumulator chains per step
+  constexpr int TG = 4;
+#pragma unroll
+  for (int t0 = 0; t0 < 8; t0 += TG) {
+    float xf[TG][8];
+#pragma unroll
+    for (int t = 0; t < TG; t++) bf16x8_to_f32(lds128(xb + (t0 + t) * 512), xf[t]);
+#pragma unroll
+    for (int jj = 0; jj < 8; jj++)
+#pragma unroll
+      for (int t = 0; t < TG; t++) {
+        const float2 xx = make_float2(xf[t][jj], xf[t][jj]);
+#pragma unroll
+        for (int p = 0; p < REP / 2; p++) acc[t0 + t][p] = __ffma2_rn(xx, wp[p][jj], acc[t0 + t][p]);
+      }
+  }
+}
+
+// xor tree over the lanes: reduce-scatter per group of 32 (token, expert) pairs;
+// lane q ends with pair g * 32 + q (t = pair / 8, e = pair % 8)
+__device__ __forceinline__ float gate_reduce(const float2 (&acc)[8][REP / 2], int g, int lane) {
+  float v[32];
+#pragma unroll
+  for (int qq = 0; qq < 32; qq++) {
+    const int pr = g * 32 + qq, t = pr / REP, e = pr % REP;
+    v[qq] = (e & 1) ? acc[t][e >> 1].y : acc[t][e >> 1].x;
+  }
+#pragma unroll
+  for (int o = 16, sz = 32; o >= 1; o >>= 1, sz >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int qq = 0; qq < sz / 2; qq++) {
+      float mine = upper ? v[qq + sz / 2] : v[qq];
+      float send = upper ? v[qq] : v[qq + sz / 2];
+      float got = __shfl_xor_sync(0xffffffffu, send, o);
+      v[qq] = mine + got;
+    }
+  }
+  return v[0];
+}
+
+__device__ __forceinline__ void init_ring(uint64_t* full, uint64_t* empty) {
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < XS; q++) {
+      tc::mbar_init(&full[q], 1);
+      tc::mbar_init(&empty[q], WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
+// E <= 8 (one pass) or no logits workspace: one CTA per 64-token tile, every pass, then the tail
 __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+    const __grid_constant__ CUtensorMap xmap, const float* __restrict__ wperm,
     const float* __restrict__ bias, int T, int H, int E, int k,
     const int32_t* __restrict__ gpu_of_expert, int n, int rank_base, int tokens_per_rank,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, int32_t* __restrict__ slot_dst,
@@ -123,51 +231,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
   __shared__ int hist_s[AUR_MAXN];
   __shared__ __align__(8) uint64_t full[XS], empty[XS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t xs_u = tc::smem_u32(xs);
   const int t0 = blockIdx.x * TILE;
   const int h_chunks = H / 256, passes = (E + REP - 1) / REP, total = passes * h_chunks;
   if (tid < AUR_MAXN) hist_s[tid] = 0;
-  if (tid == 0) {
-    for (int q = 0; q < XS; q++) {
-      tc::mbar_init(&full[q], 1);
-      tc::mbar_init(&empty[q], WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
+  init_ring(full, empty);
   __syncthreads();
-  // stage q holds x chunk (q % h_chunks) of the CTA's tokens and the gate slice of pass q / h_chunks
+  // stage q: x chunk (q % h_chunks) of the CTA's tokens + gate block q (pass q / h_chunks)
   auto fill = [&](int q, int st) {
     tc::mbar_expect_tx(&full[st], XCHUNK);
     tma_load_2d(xs + st * XCHUNK, &xmap, &full[st], 256 * (q % h_chunks), t0);
-    tma_load_2d(xs + st * XCHUNK + XBYTES, &wmap, &full[st], 256 * (q % h_chunks), REP * (q / h_chunks));
+    bulk_load(xs + st * XCHUNK + XBYTES, wperm + (size_t)q * 2048, WBYTES, &full[st]);
   };
   if (tid == 0)
     for (int q = 0; q < XS && q < total; q++) fill(q, q);
 
   for (int pass = 0; pass < passes; pass++) {
-    const int e0 = pass * REP, ev = min(REP, E - e0);
-    float acc[8][REP];
+    const int e0 = pass * REP;
+    float2 acc[8][REP / 2];
 #pragma unroll
     for (int t = 0; t < 8; t++)
 #pragma unroll
-      for (int e = 0; e < REP; e++) acc[t][e] = 0.0f;
+      for (int p = 0; p < REP / 2; p++) acc[t][p] = make_float2(0.0f, 0.0f);
     for (int i = 0; i < h_chunks; i++) {
       const int q = pass * h_chunks + i, s = q % XS;
       const uint32_t ph = (uint32_t)(q / XS) & 1u;
       tc::mbar_wait(&full[s], ph);
-      float wf[REP][8];  // experts past E read TMA's zero fill; their sums are dropped
-#pragma unroll
-      for (int e = 0; e < REP; e++)
-        bf16x8_to_f32(*reinterpret_cast<const int4*>(xs + s * XCHUNK + XBYTES + e * 512 + 16 * lane), wf[e]);
-      const uint8_t* xb = xs + s * XCHUNK + (warp * 8) * 512 + 16 * lane;
-#pragma unroll
-      for (int t = 0; t < 8; t++) {
-        float xf[8];
-        bf16x8_to_f32(*reinterpret_cast<const int4*>(xb + t * 512), xf);
-#pragma unroll
-        for (int e = 0; e < REP; e++)
-#pragma unroll
-          for (int jj = 0; jj < 8; jj++) acc[t][e] = fmaf(xf[jj], wf[e][jj], acc[t][e]);
-      }
+      gate_chunk(acc, xs_u + s * XCHUNK, warp, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[s]);
       if (tid == 0 && q + XS < total) {  // refill this stage once every warp is done with it
@@ -175,30 +265,124 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
         fill(q + XS, s);
       }
     }
-    // xor tree over the lanes: reduce-scatter per group of 32 pairs (pair p = t * REP + e)
 #pragma unroll
     for (int g = 0; g < 2; g++) {
-      float v[32];
-#pragma unroll
-      for (int qq = 0; qq < 32; qq++) v[qq] = acc[(g * 32 + qq) / REP][(g * 32 + qq) % REP];
-#pragma unroll
-      for (int o = 16, sz = 32; o >= 1; o >>= 1, sz >>= 1) {
-        const bool upper = lane & o;
-#pragma unroll
-        for (int qq = 0; qq < sz / 2; qq++) {
-          float mine = upper ? v[qq + sz / 2] : v[qq];
-          float send = upper ? v[qq] : v[qq + sz / 2];
-          float got = __shfl_xor_sync(0xffffffffu, send, o);
-          v[qq] = mine + got;
-        }
-      }
+      const float v = gate_reduce(acc, g, lane);
       const int pr = g * 32 + lane, tq = pr / REP, eq = e0 + pr % REP;
-      if (eq < E) logit_s[warp * 8 + tq][eq] = v[0] + bias[eq];
+      if (eq < E) logit_s[warp * 8 + tq][eq] = v + bias[eq];
     }
   }
   __syncthreads();
   route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
              slot_dst, blk_cnt, counts);
+}
+
+// E > 8: the (64-token tile, 8-expert pass) units of the gate are spread over a
+// persistent grid (C5: 256 tiles x 8 passes = 2048 units over 148 CTAs, so the
+// FMA-bound work balances across the SMs instead of running 256 whole tiles in
+// 1.7 waves). The x / gate stages stream through one TMA ring across units;
+// each unit stores its 64 x 8 logits (+ bias) and route_tail_kernel finishes
+// every tile. Same per-lane order and xor tree as route_tma_kernel: same bits.
+__global__ void __launch_bounds__(WARPS * 32, 1) route_units_kernel(
+    const __grid_constant__ CUtensorMap xmap, const float* __restrict__ wperm,
+    const float* __restrict__ bias, int T, int H, int E, float* __restrict__ logits) {
+  extern __shared__ __align__(1024) uint8_t xs_raw[];
+  uint8_t* xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(xs_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[XS], empty[XS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t xs_u = tc::smem_u32(xs);
+  const int h_chunks = H / 256, passes = (E + REP - 1) / REP, tiles = (T + TILE - 1) / TILE;
+  const int units = tiles * passes;
+  const int my_units = units > (int)blockIdx.x ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_units * h_chunks;
+  init_ring(full, empty);
+  __syncthreads();
+  // stage q: chunk q % h_chunks of this CTA's unit q / h_chunks (unit u = tile * passes + pass)
+  auto fill = [&](int q, int st) {
+    const int u = (int)blockIdx.x + (q / h_chunks) * (int)gridDim.x, c = q % h_chunks;
+    tc::mbar_expect_tx(&full[st], XCHUNK);
+    tma_load_2d(xs + st * XCHUNK, &xmap, &full[st], 256 * c, (u / passes) * TILE);
+    bulk_load(xs + st * XCHUNK + XBYTES, wperm + ((size_t)(u % passes) * h_chunks + c) * 2048, WBYTES, &full[st]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < XS && q < total; q++) fill(q, q);
+  for (int ui = 0; ui < my_units; ui++) {
+    const int u = (int)blockIdx.x + ui * (int)gridDim.x;
+    const int t0 = (u / passes) * TILE, e0 = (u % passes) * REP;
+    float2 acc[8][REP / 2];
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+#pragma unroll
+      for (int p = 0; p < REP / 2; p++) acc[t][p] = make_float2(0.0f, 0.0f);
+    for (int i = 0; i < h_chunks; i++) {
+      const int q = ui * h_chunks + i, s = q % XS;
+      const uint32_t ph = (uint32_t)(q / XS) & 1u;
+      tc::mbar_wait(&full[s], ph);
+      gate_chunk(acc, xs_u + s * XCHUNK, warp, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
+      if (tid == 0 && q + XS < total) {
+        tc::mbar_wait(&empty[s], ph);
+        fill(q + XS, s);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 2; g++) {
+      const float v = gate_reduce(acc, g, lane);
+      const int pr = g * 32 + lane, t = t0 + warp * 8 + pr / REP, eq = e0 + pr % REP;
+      if (eq < E && t < T) logits[(size_t)t * E + eq] = v + bias[eq];
+    }
+  }
+}
+
+// the tail of the split router: one CTA per 64-token tile (blk_cnt row = blockIdx.x)
+__global__ void __launch_bounds__(WARPS * 32) route_tail_kernel(
+    const float* __restrict__ logits, int T, int E, int k, const int32_t* __restrict__ gpu_of_expert, int n,
+    int rank_base, int tokens_per_rank, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+    int32_t* __restrict__ slot_dst, int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  __shared__ int hist_s[AUR_MAXN];
+  __shared__ int sel_s[TILE][MAXK];
+  __shared__ float sv_s[TILE][MAXK];
+  const int t0 = blockIdx.x * TILE;
+  if (threadIdx.x < AUR_MAXN) hist_s[threadIdx.x] = 0;
+  // 4 threads per token (all 256 threads: the tile's 64 tokens at once); thread
+  // sub holds experts e = sub + 4 j. Each of the k rounds takes the larger logit,
+  // the lower index on ties -- the sequential scan's choice.
+  {
+    const int tl = threadIdx.x >> 2, sub = threadIdx.x & 3, t = t0 + tl;
+    float v[16];
+    uint32_t live = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const int e = sub + 4 * j;
+      v[j] = 0.0f;
+      if (t < T && e < E) {
+        v[j] = logits[(size_t)t * E + e];
+        live |= 1u << j;
+      }
+    }
+    for (int s = 0; s < k; s++) {
+      float bv = 0.0f;
+      int bi = 1 << 30;
+#pragma unroll
+      for (int j = 0; j < 16; j++)
+        if (((live >> j) & 1) && (bi == (1 << 30) || v[j] > bv)) { bv = v[j]; bi = sub + 4 * j; }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi != (1 << 30) && (bi == (1 << 30) || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+      }
+      if (sub == 0 && t < T) {
+        sel_s[tl][s] = bi;
+        sv_s[tl][s] = bv;
+      }
+      if (bi != (1 << 30) && (bi & 3) == sub) live &= ~(1u << (bi >> 2));
+    }
+  }
+  __syncthreads();
+  route_tail<true>(nullptr, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
+                   slot_dst, blk_cnt, counts, sel_s, sv_s);
 }
 
 typedef CUresult (*EncodeTiledFnR)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -307,27 +491,51 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
 
 }  // namespace
 
-extern "C" int aurora_route(const void* x, const void* w_gate, const float* bias, int T, int H,
+extern "C" int aurora_route_gate_floats(int E, int H) {
+  if (E < 1 || E > MAXE || H <= 0 || H % 256) return -AURORA_EINVAL;
+  return ((E + REP - 1) / REP) * H * REP;
+}
+
+extern "C" int aurora_route_prepare_gate(const void* w_gate, int E, int H, float* gate_prep, void* stream) {
+  if (!w_gate || !gate_prep || E < 1 || E > MAXE || H <= 0 || H % 256) return AURORA_EINVAL;
+  prepare_gate_kernel<<<256, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)w_gate, E, H, gate_prep);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_route(const void* x, const float* gate_prep, const float* bias, int T, int H,
                             int E, int k, const int32_t* gpu_of_expert, int n, int rank_base,
                             int tokens_per_rank, int32_t* topk_idx, float* topk_w,
-                            int32_t* slot_dst, int32_t* blk_cnt, int32_t* counts, void* stream) {
+                            int32_t* slot_dst, int32_t* blk_cnt, int32_t* counts, float* logits,
+                            void* stream) {
   if (T <= 0 || H % 256 || k < 1 || k > MAXK || k > E || n < 1 || n > AUR_MAXN ||
-      tokens_per_rank % TILE || T % tokens_per_rank)
+      tokens_per_rank % TILE || T % tokens_per_rank || !x || !gate_prep || !bias)
     return AURORA_EINVAL;
   const int blocks = (T + TILE - 1) / TILE;
   cudaStream_t s = (cudaStream_t)stream;
   if (E < 1 || E > MAXE) return AURORA_EUNSUPPORTED;
-  CUtensorMap xmap, wmap;
-  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H) || !make_x_map(&wmap, w_gate, (uint64_t)E, (uint64_t)H, REP))
-    return AURORA_ECUDA;
+  CUtensorMap xmap;
+  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H)) return AURORA_ECUDA;
   constexpr int dyn = XS * XCHUNK + 1024;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(route_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
+    if (cudaFuncSetAttribute(route_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess ||
+        cudaFuncSetAttribute(route_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
       return AURORA_ECUDA;
     attr = true;
   }
-  route_tma_kernel<<<blocks, WARPS * 32, dyn, s>>>(xmap, wmap, bias, T, H, E, k, gpu_of_expert, n, rank_base,
+  if (logits && E > REP) {  // several 8-expert passes: balance (tile, pass) units over a persistent grid
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int units = blocks * ((E + REP - 1) / REP);
+    route_units_kernel<<<units < sms ? units : sms, WARPS * 32, dyn, s>>>(xmap, gate_prep, bias, T, H, E, logits);
+    route_tail_kernel<<<blocks, WARPS * 32, 0, s>>>(logits, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank,
+                                                     topk_idx, topk_w, slot_dst, blk_cnt, counts);
+    AUR_CHECK_LAUNCH();
+    return AURORA_OK;
+  }
+  route_tma_kernel<<<blocks, WARPS * 32, dyn, s>>>(xmap, gate_prep, bias, T, H, E, k, gpu_of_expert, n, rank_base,
                                                    tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;

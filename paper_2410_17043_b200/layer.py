@@ -134,6 +134,14 @@ class AuroraMoELayer:
         if weights is None:
             weights = self.synthetic_weights(cfg, dev, [e for r in self.local_ranks for e in self.experts_of_rank(r)])
         self.w_gate = weights["w_gate"].to(dev, torch.bfloat16).contiguous()
+        # the router's copy of the gate: fp32 (exact) in its shared-memory order, prepared once
+        nf = self.L.aurora_route_gate_floats(cfg.experts, cfg.hidden)
+        if nf < 0:
+            raise ValueError(f"router: unsupported experts={cfg.experts} / hidden={cfg.hidden}")
+        self.gate_prep = torch.empty(nf, dtype=torch.float32, device=dev)
+        _lib.check(self.L.aurora_route_prepare_gate(self.w_gate.data_ptr(), cfg.experts, cfg.hidden,
+                                                    self.gate_prep.data_ptr(), _lib.stream_ptr()),
+                   "aurora_route_prepare_gate")
         self.bias = weights["bias"].to(dev, torch.float32).contiguous()
         self.w13 = weights["w13"].to(dev, torch.bfloat16).contiguous()   # [n_local, 2F, H] interleaved
         self.w2 = weights["w2"].to(dev, torch.bfloat16).contiguous()     # [n_local, H, F]
@@ -150,6 +158,9 @@ class AuroraMoELayer:
         self.counts = torch.zeros(n, n, **i32)
         self.send_list = torch.empty(self.n_local, Tr * k, **i32)
         self.pos = torch.empty(self.T_local, k, **i32)
+        # E > 8: router logits workspace (the (tile, 8-expert pass) units run on a balanced grid)
+        self.logits = (torch.empty(self.T_local, cfg.experts, dtype=torch.float32, device=dev)
+                       if cfg.experts > 8 else None)
 
         # ---- schedule tables (written by K2 on the device)
         P = self.L.aurora_phase_cap(n)
@@ -326,11 +337,12 @@ class AuroraMoELayer:
     def route(self, x: torch.Tensor, stream: int) -> None:
         cfg = self.cfg
         self.counts.zero_()
-        _lib.check(self.L.aurora_route(x.data_ptr(), self.w_gate.data_ptr(), self.bias.data_ptr(), self.T_local,
+        _lib.check(self.L.aurora_route(x.data_ptr(), self.gate_prep.data_ptr(), self.bias.data_ptr(), self.T_local,
                                        cfg.hidden, cfg.experts, cfg.top_k, self.gpu_of_expert.data_ptr(), self.n,
                                        self.rank_base, cfg.tokens_per_rank, self.topk_idx.data_ptr(),
                                        self.topk_w.data_ptr(), self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
-                                       self.counts.data_ptr(), stream), "aurora_route")
+                                       self.counts.data_ptr(), None if self.logits is None else self.logits.data_ptr(),
+                                       stream), "aurora_route")
 
     def exchange_counts(self) -> None:
         """Multi-GPU: complete the traffic matrix (each process owns its rows).

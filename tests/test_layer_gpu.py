@@ -34,6 +34,8 @@ def _check_layer(torch, cfg, plan=None, out_tol=3e-2):
     # router: bit-exact expert choice
     logits, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), k)
     assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
+    if layer.logits is not None:  # E > 8: the balanced split router leaves its logits: same bits as the oracle
+        assert np.array_equal(layer.logits.cpu().numpy().view(np.uint32), np.asarray(logits, np.float32).view(np.uint32))
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-5)
     # traffic matrix + token permutation
     counts, lists, pos = pack_oracle(idx, layer.gpu_of, n)
@@ -130,6 +132,8 @@ def test_layer_c2_full_size(torch):
     n, k = cfg.ranks, cfg.top_k
     _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), k)
     assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
+    if layer.logits is not None:  # E > 8: the balanced split router leaves its logits: same bits as the oracle
+        assert np.array_equal(layer.logits.cpu().numpy().view(np.uint32), np.asarray(logits, np.float32).view(np.uint32))
     counts, lists, pos = pack_oracle(idx, layer.gpu_of, n)
     assert np.array_equal(layer.counts.cpu().numpy(), counts)
     assert np.array_equal(layer.pos.cpu().numpy(), pos)
@@ -273,6 +277,8 @@ def test_colocated_models(torch):
     for layer, x, out in ((pair.a, xa, out_a), (pair.b, xb, out_b)):
         _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), 2)
         assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
+    if layer.logits is not None:  # E > 8: the balanced split router leaves its logits: same bits as the oracle
+        assert np.array_equal(layer.logits.cpu().numpy().view(np.uint32), np.asarray(logits, np.float32).view(np.uint32))
         counts, _, _ = pack_oracle(idx, layer.gpu_of, 4)
         assert np.array_equal(layer.counts.cpu().numpy(), counts)
         F = layer.cfg.ffn
@@ -417,3 +423,29 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
         assert torch.equal(torch.cat([halves[0].out, halves[1].out]), ref)
     for h in halves:
         assert int(h.ctr_d.abs().sum()) == 0 and int(h.ctr_c.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("experts,top_k", [(8, 2), (16, 4), (64, 6)])
+def test_router_ties_pick_lower_index(torch, experts, top_k):
+    """Duplicate gate rows with equal bias give bit-identical logits: both
+    router paths (one CTA per tile for E <= 8; balanced (tile, pass) units +
+    the 4-threads-per-token top-k tail for E > 8) must choose the lower expert
+    index on every tie, as the oracle's sequential scan does."""
+    from oracle.oracle import bf16_bits, router_oracle
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=experts, top_k=top_k, tokens=2048, ranks=8, skew=0.0, seed=12)
+    gpu_of = [e * 8 // experts for e in range(experts)]
+    w = AuroraMoELayer.synthetic_weights(cfg, torch.device("cuda"),
+                                         [e for r in range(8) for e in range(experts) if gpu_of[e] == r])
+    for e in range(1, experts, 2):  # every odd expert duplicates its even neighbour
+        w["w_gate"][e] = w["w_gate"][e - 1]
+        w["bias"][e] = w["bias"][e - 1]
+    layer = AuroraMoELayer(cfg, gpu_of_expert=gpu_of, weights=w)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    layer.route(x, int(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), top_k)
+    got = layer.topk_idx.cpu().numpy()
+    assert np.array_equal(got, idx)
+    assert (got[:, 0] % 2 == 0).all()  # the first choice is always the lower twin
+    assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-6)
