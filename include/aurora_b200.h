@@ -253,7 +253,9 @@ int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* 
 
 /* aurora_expert_ffn_combine: the same FFN (one expert per rank: group g is
  * expert rank rank_base + g, all received rows) with the combine fused into
- * GEMM2's epilogue -- the K6 + K5 pair written as one kernel over peer memory:
+ * GEMM2's epilogue -- the K6 + K5 pair written as one kernel over peer memory
+ * (reference: ffn_work_per_token, core.py:194-221, then the reversed all-to-all,
+ * CommSchedule.reversed commsched.py:310-319, as sequenced by sim.py:130-154):
  * every output row of sender i's block (recv rows roff[i][j] + [0, counts[i][j]))
  * is stored straight into ret_bufs[i] row soff[i][j] + offset (the row the
  * combine engine would write; NVSwitch stores overlap the GEMM tile by tile),
