@@ -458,7 +458,8 @@ def main():
         gc_ = torch.Generator(device=calib.dev).manual_seed(args.seed + 101 + rank)
         xc = torch.randn(calib.T_local, cfg.hidden, device=calib.dev, generator=gc_).to(torch.bfloat16)
         calib.route(xc, _lib.stream_ptr())  # the router alone gives the traffic matrix
-        calib.exchange_counts()
+        if world > 1:  # calibration pass (host side, once): plain all-reduce of the rows
+            dist.all_reduce(calib.counts)
         torch.cuda.synchronize()
         loads = calib.counts.cpu().numpy().sum(axis=0)
         plan = assign_exclusive_hetero(loads, ClusterSpec(tuple(GpuSpec(b, b) for b in bws)))

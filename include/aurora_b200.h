@@ -210,6 +210,22 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
  * (csrc/apportion.cuh; bw: rank bandwidths for AURORA_SPLIT_BANDWIDTH). */
 int aurora_engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int row2_bytes, int lsu);
 
+/* aurora_exchange_counts: the traffic-matrix all-gather over peer memory (SURVEY
+ * 8(e) pre-step; the reference has one process and a complete TrafficMatrix,
+ * core.py:75-117). counts2 [2][n][n] int32 (this process; buffer (epoch-1) & 1 of
+ * the call is used, its rows [rank_base, rank_base + n_local) filled by
+ * aurora_route); peer_counts2[n] = base of the [2][n][n] buffer of rank q's
+ * process, xflag[n] (this process, zero-initialised, monotonic), peer_xflag[n] =
+ * base of rank q's process's xflag, epoch: one int32 of this process (zero at
+ * first call; every process must make the same sequence of calls). Stores this
+ * process's rows into every peer's buffer, releases xflag[r] = epoch for its
+ * ranks, and completes once every other rank's flag has arrived (system scope).
+ * The caller alternates the counts buffer it passes to the other kernels with
+ * the same parity. spin_limit bounds the wait; on expiry status = ETIMEOUT. */
+int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+                           int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base, int n_local,
+                           int64_t spin_limit, int32_t* status, void* stream);
+
 /* aurora_combine_wait: the receiving side of the fused combine
  * (aurora_expert_ffn_combine). One thread per local sender rank
  * r in [rank_base, rank_base + n_local) waits until its {pace, done} pair

@@ -817,6 +817,50 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   return AURORA_OK;
 }
 
+// Traffic-matrix exchange over peer memory (SURVEY 8(e) pre-step): every process
+// stores its ranks' rows of counts into every peer's copy, then releases one flag
+// per local rank (value = the call's epoch); it returns once every other rank's
+// flag reached the epoch. counts are double-buffered by epoch parity, so a peer
+// one step ahead never overwrites rows this process may still read.
+__global__ void exchange_counts_kernel(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+                                       int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base,
+                                       int n_local, long long spin_limit, int32_t* status) {
+  __shared__ int e_s;
+  const int q = threadIdx.x;
+  if (q == 0) {
+    const int e = *epoch + 1;
+    *epoch = e;
+    e_s = e;
+  }
+  __syncthreads();
+  const int e = e_s, par = (e - 1) & 1;
+  const bool local_q = q >= rank_base && q < rank_base + n_local;
+  // one writer per peer process: the lowest non-local rank of that process
+  bool first = q < n && !local_q;
+  for (int q2 = 0; first && q2 < q; q2++)
+    if (!(q2 >= rank_base && q2 < rank_base + n_local) && peer_counts2[q2] == peer_counts2[q]) first = false;
+  if (first) {
+    const int32_t* src = counts2 + (size_t)par * n * n + (size_t)rank_base * n;
+    int32_t* dst = peer_counts2[q] + (size_t)par * n * n + (size_t)rank_base * n;
+    for (int v = 0; v < n_local * n; v++) dst[v] = src[v];
+    __threadfence_system();
+    for (int r = 0; r < n_local; r++) st_release_sys(peer_xflag[q] + rank_base + r, e);
+  }
+  if (q < n && !local_q && !wait_ge(xflag + q, e, spin_limit, true)) atomicExch(status, AURORA_ETIMEOUT);
+}
+
+extern "C" int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+                                      int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base,
+                                      int n_local, int64_t spin_limit, int32_t* status, void* stream) {
+  if (!counts2 || !peer_counts2 || !xflag || !peer_xflag || !epoch || !status || n < 1 || n > AUR_MAXN ||
+      n_local < 1 || rank_base < 0 || rank_base + n_local > n)
+    return AURORA_EINVAL;
+  exchange_counts_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(counts2, peer_counts2, xflag, peer_xflag, epoch, n,
+                                                             rank_base, n_local, spin_limit, status);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
 // the fused combine's receiving side: wait for every expert rank's arrival on
 // this process's senders, then re-arm the counters for the next layer step
 __global__ void combine_wait_kernel(int32_t* const* ctrs, int rank_base, int n_local, int expect, int sys,

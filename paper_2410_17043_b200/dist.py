@@ -13,7 +13,7 @@ from typing import Callable, Dict, List
 
 from . import _lib
 
-BUFFERS = ("recv", "ret", "ctr_d", "ctr_c")
+BUFFERS = ("recv", "ret", "ctr_d", "ctr_c", "counts2", "xflag")
 OPTIONAL = ("meta_recv",)  # present when ranks host several experts
 
 
@@ -24,7 +24,9 @@ def _names(layer) -> tuple:
 def _strides(layer) -> Dict[str, int]:
     """Byte distance between consecutive ranks inside one process's buffer."""
     H = layer.cfg.hidden
+    # counts2 / xflag: one per process (every rank of a process maps to its base)
     return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 8, "ctr_c": 8,
+            "counts2": 0, "xflag": 0,
             "meta_recv": layer.cap * layer.meta_bytes}
 
 

@@ -155,7 +155,13 @@ class AuroraMoELayer:
         self.topk_w = torch.empty(self.T_local, k, dtype=torch.float32, device=dev)
         self.slot_dst = torch.empty(self.T_local, k, **i32)
         self.blk_cnt = torch.empty(self.T_local // 64, n, **i32)
-        self.counts = torch.zeros(n, n, **i32)
+        # traffic matrix, double-buffered by exchange step parity (aurora_exchange_counts): a peer
+        # one step ahead writes its rows into the other buffer
+        self.counts2 = torch.zeros(2, n, n, **i32)
+        self.counts = self.counts2[0]
+        self.xflag = torch.zeros(n, **i32)    # peer-visible: epoch of the last row received per rank
+        self.xepoch = torch.zeros(1, **i32)   # exchange calls made (device side)
+        self._xstep = 0
         self.send_list = torch.empty(self.n_local, Tr * k, **i32)
         self.pos = torch.empty(self.T_local, k, **i32)
         # E > 8: router logits workspace (the (tile, 8-expert pass) units run on a balanced grid)
@@ -303,6 +309,8 @@ class AuroraMoELayer:
             ctr_c = [self.ctr_c.data_ptr() + 8 * r for r in range(self.n)]
         else:
             recv_p, ret_p, ctr_d, ctr_c = peers["recv"], peers["ret"], peers["ctr_d"], peers["ctr_c"]
+            self.t_counts2 = self._ptr_table(peers["counts2"])
+            self.t_xflag = self._ptr_table(peers["xflag"])
         self.t_dst_d = self._ptr_table(recv_p)
         self.t_dst_c = self._ptr_table(ret_p)
         self.t_ctr_d = self._ptr_table(ctr_d)
@@ -336,7 +344,9 @@ class AuroraMoELayer:
     # ------------------------------------------------------------ stages
     def route(self, x: torch.Tensor, stream: int) -> None:
         cfg = self.cfg
-        self.counts.zero_()
+        self.counts = self.counts2[self._xstep & 1]
+        # only this process's rows: a peer may already have stored its rows for this step
+        self.counts[self.rank_base:self.rank_base + self.n_local].zero_()
         _lib.check(self.L.aurora_route(x.data_ptr(), self.gate_prep.data_ptr(), self.bias.data_ptr(), self.T_local,
                                        cfg.hidden, cfg.experts, cfg.top_k, self.gpu_of_expert.data_ptr(), self.n,
                                        self.rank_base, cfg.tokens_per_rank, self.topk_idx.data_ptr(),
@@ -344,12 +354,21 @@ class AuroraMoELayer:
                                        self.counts.data_ptr(), None if self.logits is None else self.logits.data_ptr(),
                                        stream), "aurora_route")
 
-    def exchange_counts(self) -> None:
-        """Multi-GPU: complete the traffic matrix (each process owns its rows).
-        Loopback: nothing to do, every row was produced here."""
-        if self.n_local != self.n:
-            import torch.distributed as dist
-            dist.all_reduce(self.counts)
+    def exchange_counts(self, stream: Optional[int] = None) -> None:
+        """Multi-GPU: complete the traffic matrix (each process owns its rows) with
+        peer stores + flags on the stream (aurora_exchange_counts; no NCCL, no host
+        sync). Loopback: nothing to do, every row was produced here."""
+        if self.n_local == self.n:
+            return
+        if getattr(self, "t_counts2", None) is None:
+            raise RuntimeError("multi-process layer: call dist.connect_peers(layer) first")
+        s = _lib.stream_ptr() if stream is None else stream
+        _lib.check(self.L.aurora_exchange_counts(self.counts2.data_ptr(), self.t_counts2.data_ptr(),
+                                                 self.xflag.data_ptr(), self.t_xflag.data_ptr(),
+                                                 self.xepoch.data_ptr(), self.n, self.rank_base, self.n_local,
+                                                 self.spin_limit, self.engine_status.data_ptr(), s),
+                   "aurora_exchange_counts")
+        self._xstep += 1
 
     def engine_ctas(self, combine: bool) -> int:
         """Copy CTAs per local rank the engine launches (clamped to co-residency)."""
@@ -539,7 +558,7 @@ class AuroraMoELayer:
         self._marked = set()
         mark("start", main)
         self.route(x, s)
-        self.exchange_counts()
+        self.exchange_counts(s)
         self.pack(s)
         mark("packed", main)
         if not self.overlap:

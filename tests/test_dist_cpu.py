@@ -27,7 +27,7 @@ def _worker(rank, world, port, n, q):
         mine[name] = (bytes([rank, b]) * 32, 64 * (b + 1))
     exports = [None] * world
     dist.all_gather_object(exports, mine)
-    strides = {"recv": 1 << 20, "ret": 1 << 16, "ctr_d": 4, "ctr_c": 4}
+    strides = {"recv": 1 << 20, "ret": 1 << 16, "ctr_d": 4, "ctr_c": 4, "counts2": 0, "xflag": 0}
     local = {name: 0x7000_0000 + rank * 0x100_0000 + b * 0x10_0000 for b, name in enumerate(BUFFERS)}
 
     def opener(handle, off):
@@ -53,7 +53,7 @@ def test_peer_tables_two_processes():
         p.join(timeout=60)
         assert p.exitcode == 0
     from paper_2410_17043_b200.dist import BUFFERS
-    strides = {"recv": 1 << 20, "ret": 1 << 16, "ctr_d": 4, "ctr_c": 4}
+    strides = {"recv": 1 << 20, "ret": 1 << 16, "ctr_d": 4, "ctr_c": 4, "counts2": 0, "xflag": 0}
     for me in range(world):
         t = got[me]
         for b, name in enumerate(BUFFERS):

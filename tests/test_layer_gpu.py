@@ -369,7 +369,8 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
     """The multi-GPU code path on one device: two layer instances, each driving
     4 of the 8 ranks (what two processes on two GPUs do), with peer tables
     pointing at each other's buffers, system-scope flags, the traffic matrix
-    summed from both halves (exchange_counts' all_reduce), K2 counting
+    exchanged between the halves by peer stores + flags (aurora_exchange_counts,
+    double-buffered by step parity), K2 counting
     hand-over thresholds over 4-rank groups, and the two engines running
     concurrently on two streams, each waiting on the other's arrival counters.
     Output identical to the single-instance (loopback) layer; with several
@@ -404,9 +405,9 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
 
     for _ in range(2):  # twice: counters must be rearmed across calls
         both(lambda h, s: h.route(h.x, s))
-        total = halves[0].counts + halves[1].counts
-        for h in halves:
-            h.counts.copy_(total)
+        both(lambda h, s: h.exchange_counts(s))  # peer stores + flags, concurrently on both streams
+        assert torch.equal(halves[0].counts, halves[1].counts)
+        assert torch.equal(halves[0].counts, ref_layer.counts)
         both(lambda h, s: h.pack(s))
         both(lambda h, s: h.schedule(s))
         both(lambda h, s: h.dispatch(s))   # concurrent: each waits on the other's flags
