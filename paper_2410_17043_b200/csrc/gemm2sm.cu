@@ -11,6 +11,10 @@
 // full barrier), warp 1 TMEM allocator (both, cta_group::2) and MMA issuer
 // (leader only), warps 2-5 epilogue (both; arrive on the leader's tmem_empty).
 // Same grouped tiling, rasterisation, epilogues and C ABI as gemm.cu.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "tc_helpers.cuh"
 
 namespace {
@@ -25,7 +29,11 @@ constexpr int TMEM_COLS = 512;                   // 2 accumulators x 256 columns
 constexpr int MAX_GROUPS = 64;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t IDESC = tc::idesc_bf16(BMP, BN);
-constexpr int SC_MAXN = 16;                      // fused combine: ranks / local groups
+constexpr int SC_MAXN = 16;
+constexpr int TRING = 8;                         // tile-index ring (dynamic schedule)
+// readers of a ring slot that arrive on the leader's tr_empty: the peer's
+// producer, the MMA issuer and the 4 epilogue warps of each CTA
+constexpr int TR_READERS = 1 + 1 + 8;                      // fused combine: ranks / local groups
 
 // Fused combine (epilogue 0 with n > 0): group g is expert rank rank_base + g;
 // its received rows come in per-sender blocks (roff / counts); the epilogue
@@ -76,7 +84,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             const __grid_constant__ CUtensorMap map_b,
                             __nv_bfloat16* __restrict__ c, const int32_t* __restrict__ m_start,
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
-                            int epilogue, int group_m, const Scatter sc) {
+                            int epilogue, int group_m, const Scatter sc,
+                            int32_t* __restrict__ tile_ctr) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -85,6 +94,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + 2);
   __shared__ TileIter2 it;
+  // dynamic tile order (tile_ctr != NULL): the leader's producer takes the next
+  // tile index from a global counter and publishes it to both CTAs' rings
+  __shared__ int tile_ring[TRING];
+  __shared__ __align__(8) uint64_t tr_full[TRING], tr_empty[TRING];
   __shared__ int sc_lo[SC_MAXN * SC_MAXN], sc_cnt[SC_MAXN * SC_MAXN], sc_dst[SC_MAXN * SC_MAXN];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -115,6 +128,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc::mbar_init(&full[s], 1);   // leader: its expect_tx arrive + both CTAs' bytes
       tc::mbar_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
     }
+    for (int q = 0; q < TRING; q++) {
+      tc::mbar_init(&tr_full[q], 1);
+      tc::mbar_init(&tr_empty[q], TR_READERS);
+    }
     for (int a = 0; a < 2; a++) {
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 2 * 128);  // every epilogue thread of both CTAs
@@ -133,13 +150,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc::fence_after();
   const uint32_t tmem_base = *tmem_base_s;
   const int k_blocks = K / BK;
+  const bool dyn = tile_ctr != nullptr;
+  // i-th tile of this cluster (-1: done). Static: round robin over clusters.
+  // Dynamic: ring slot i % TRING, published by the leader's producer.
+  auto next_tile = [&](int i, bool arrive) -> int {
+    if (!dyn) {
+      const int t = cluster_id + i * n_clusters;
+      return t < it.total ? t : -1;
+    }
+    const int q = i % TRING;
+    tc::mbar_wait_cluster(&tr_full[q], (uint32_t)(i / TRING) & 1u);
+    const int t = *(volatile int*)&tile_ring[q];
+    if (arrive) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tr_empty[q]), 0));
+    return t;
+  };
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       const uint32_t full0 = tc::mapa(tc::smem_u32(&full[0]), 0);
       int s = 0;
       uint32_t ph = 0;
-      for (int t = cluster_id; t < it.total; t += n_clusters) {
+      bool ended = false;
+      // leader: publish tile j (index t from the global counter) to both CTAs' rings
+      auto publish = [&](int j, int t) {
+        const int q = j % TRING;
+        if (j >= TRING) tc::mbar_wait_cluster(&tr_empty[q], (uint32_t)(j / TRING - 1) & 1u);
+        if (ended || t >= it.total) t = -1;
+        ended = ended || t < 0;
+        tile_ring[q] = t;
+        const uint32_t peer_slot = tc::mapa(tc::smem_u32(&tile_ring[q]), 1);
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_slot), "r"(t) : "memory");
+        tc::mbar_arrive_cluster(tc::smem_u32(&tr_full[q]));
+        tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tr_full[q]), 1));
+      };
+      if (dyn && leader) {
+        publish(0, atomicAdd(tile_ctr, 1));
+        publish(1, atomicAdd(tile_ctr, 1));
+      }
+      for (int i = 0;; i++) {
+        int t, ahead = -1;
+        if (dyn && leader) {
+          // two tiles of lookahead: tile i + 2's counter fetch is issued now and its
+          // result consumed after this tile's loads, so neither CTA waits on it
+          ahead = ended ? -1 : atomicAdd(tile_ctr, 1);
+          t = tile_ring[i % TRING];
+        } else {
+          t = next_tile(i, dyn);
+        }
+        if (t < 0) break;
         int g, mt, nt;
         tile_coords2(it, G, group_m, t, g, mt, nt);
         const int a_row = (int)(g * cap) + it.ms[g] + mt * BMP + (int)rank * HALF;
@@ -153,14 +211,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tc::tma_load_2d_pair(sa + A_BYTES, &map_b, fb, kb * BK, b_row);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
+        if (dyn && leader) publish(i + 2, ahead);
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
       int s = 0;
       uint32_t ph = 0;
-      int local = 0;
-      for (int t = cluster_id; t < it.total; t += n_clusters, local++) {
+      for (int local = 0;; local++) {
+        if (next_tile(local, true) < 0) break;
         const int acc = local & 1;
         tc::mbar_wait_cluster(&tempty[acc], ((local >> 1) & 1) ^ 1);
         tc::fence_after();
@@ -182,8 +241,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else {  // ---------------- epilogue warps 2..5 (both CTAs)
     const int quarter = warp & 3;
     const uint32_t tempty0 = tc::mapa(tc::smem_u32(&tempty[0]), 0);
-    int local = 0;
-    for (int t = cluster_id; t < it.total; t += n_clusters, local++) {
+    for (int local = 0;; local++) {
+      // one reader arrival per epilogue warp: lane 0 after the warp has the index
+      int t = 0;
+      if (lane == 0) t = next_tile(local, false);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (dyn && lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tr_empty[local % TRING]), 0));
+      if (t < 0) break;
       int g, mt, nt;
       tile_coords2(it, G, group_m, t, g, mt, nt);
       const int acc = local & 1;
@@ -256,6 +320,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc::fence_before();
   __syncthreads();
   tc::cluster_sync();
+  if (dyn && leader && threadIdx.x == 0) {  // last cluster out re-arms the tile counter
+    if (atomicAdd(tile_ctr + 1, 1) == n_clusters - 1) {
+      tile_ctr[0] = 0;
+      tile_ctr[1] = 0;
+      __threadfence();
+    }
+  }
   if (sc.n && threadIdx.x == 0) {  // grid completion -> one arrival per group on every sender
     __threadfence();
     if (atomicAdd(sc.ticket, 1) == (int)gridDim.x - 1) {
@@ -300,6 +371,25 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// One {next tile, clusters done} counter pair per stream (launches on one stream
+// are ordered; the kernel's last cluster re-arms the pair to zero).
+int32_t* tile_counter_for(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int32_t*> ctrs;  // (device, stream)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  const auto key = std::make_pair(dev, stream);
+  std::lock_guard<std::mutex> lock(mu);
+  auto f = ctrs.find(key);
+  if (f != ctrs.end()) return f->second;
+  int32_t* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(int32_t)) != cudaSuccess) return nullptr;
+  if (cudaMemset(p, 0, 2 * sizeof(int32_t)) != cudaSuccess) return nullptr;
+  if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+  ctrs[key] = p;
+  return p;
+}
+
 }  // namespace
 
 // C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
@@ -339,6 +429,17 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
       return AURORA_ECUDA;
     attr_set = true;
   }
+  // dynamic tile order (default): clusters take tiles from a global counter, so the
+  // tiles in flight stay a window of consecutive indices and each operand tile is
+  // read from DRAM about once (8-expert C2 GEMM1: 8.1 -> 2.2 GB for 2.15 GB of
+  // operands); AURORA_GEMM_STATIC=1: round robin (clusters drift apart over the
+  // persistent loop and the window -- the L2 working set -- grows with the drift)
+  static const bool dyn_sched = !getenv("AURORA_GEMM_STATIC") || atoi(getenv("AURORA_GEMM_STATIC")) == 0;
+  int32_t* tile_ctr = nullptr;
+  if (dyn_sched) {
+    tile_ctr = tile_counter_for(stream);
+    if (!tile_ctr) return AURORA_ECUDA;
+  }
   const int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BMP * K * 2)));
   if (num_sms <= 0) {
     int dev = 0;
@@ -347,7 +448,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   }
   const int grid = num_sms & ~1;
   grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc);
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
