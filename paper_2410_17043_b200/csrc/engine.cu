@@ -874,7 +874,7 @@ __global__ void combine_wait_kernel(int32_t* const* ctrs, int rank_base, int n_l
   }
   ((volatile int32_t*)c)[0] = 0;
   ((volatile int32_t*)c)[1] = 0;
-  __threadfence_system();
+  if (sys) __threadfence_system();  // peers on other GPUs see the re-arm before our next exchange
 }
 
 extern "C" int aurora_combine_wait(int32_t* const* ctrs, int rank_base, int n_local, int expect, int sys,
