@@ -325,6 +325,9 @@ def test_engine_runs_baseline_schedules(torch):
     dict(experts=6, top_k=2, ranks=2, tokens=512),           # E not a power of two, 3 experts per rank
     dict(experts=8, top_k=2, ranks=8, tokens=2048, skew=30.0),  # nearly every token to two experts
     dict(experts=4, top_k=4, ranks=4, tokens=1024),          # every token to every rank
+    dict(experts=16, top_k=2, ranks=16, tokens=4096),        # the most ranks (K2's n <= 16 kernel)
+    dict(experts=64, top_k=6, ranks=16, tokens=4096),        # 16 ranks x 4 experts, C5 routing
+    dict(experts=8, top_k=1, ranks=8, tokens=2048, skew=60.0),  # one hot expert, most ranks idle
 ])
 def test_layer_edge_shapes(torch, shape):
     from paper_2410_17043_b200.layer import MoEConfig
