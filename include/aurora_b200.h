@@ -354,6 +354,9 @@ int aurora_debug_set_schedule_profile(long long* prof);
  * per copy CTA {start, local rows done, end, -} at trace[4 * cta]. */
 int aurora_debug_set_schedule_trace(long long* trace);
 int aurora_debug_set_engine_trace(long long* trace);
+/* aurora_debug_set_early_rows: rows before the end of a CTA's share of a run at
+ * which the TMA engine sends the run's pace signal (engine mode bit 7; default 2). */
+int aurora_debug_set_early_rows(int rows);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ _SIGNATURES = {
     "aurora_debug_set_schedule_profile": [_vp],
     "aurora_debug_set_schedule_trace": [_vp],
     "aurora_debug_set_engine_trace": [_vp],
+    "aurora_debug_set_early_rows": [_c_int],
     "aurora_ipc_handle_bytes": [],
     "aurora_ipc_get": [_vp, _vp, _vp],
     "aurora_ipc_open": [_vp, _c_i64, _vp],

@@ -366,6 +366,7 @@ constexpr int RING = 128;
 
 // diagnostics: per copy CTA {start, local rows done, end} in %globaltimer ns
 __device__ long long* g_engine_trace = nullptr;
+__device__ int g_early_rows = 2;  // rows before a run's end at which its pace signal goes out
 __device__ __forceinline__ long long eng_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     // early pace: release the receiver when this CTA has only EARLY rows of the
     // run left to issue -- about the flag's round trip -- so the next sender's
     // first stores follow this run's last ones instead of waiting a hand-over
-    const int EARLY = (p.mode & 128) ? 2 : 0;  // mode bit 7
+    const int EARLY = (p.mode & 128) ? g_early_rows : 0;  // mode bit 7
     auto pace = [&](int peer_) {
       if (sys) red_relaxed_sys_add(sh.ctr[peer_], 1);
       else red_relaxed_gpu_add(sh.ctr[peer_], 1);
@@ -884,6 +885,11 @@ extern "C" int aurora_combine_wait(int32_t* const* ctrs, int rank_base, int n_lo
                                                           status);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
+}
+
+extern "C" int aurora_debug_set_early_rows(int rows) {
+  if (rows < 0) return AURORA_EINVAL;
+  return cudaMemcpyToSymbol(g_early_rows, &rows, sizeof(rows)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }
 
 extern "C" int aurora_debug_set_engine_trace(long long* trace) {

@@ -72,8 +72,11 @@ int main() {
   cudaMemcpy(perm, h.data(), rows * 4, cudaMemcpyHostToDevice);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   auto report = [&](const char* name, float ms) { printf("%-28s %8.1f us  %7.0f GB/s (r+w)\n", name, ms * 1e3, 2.0 * rows * rb / (ms * 1e-3) / 1e9); };
-  for (int grid : {128, 148, 256, 296}) {
-    for (int S : {4, 8, 12, 16, 24}) {
+  // per-CTA rate = (r+w)/2 / grid
+  for (int grid : {37, 74, 148, 296, 592}) {
+    for (int S : {6, 12, 24}) {
+      if ((size_t)S * rb * (grid > 148 ? (grid + 147) / 148 : 1) > 200 * 1024) continue;
+      const int rows_used = rows / grid * grid;
       int rpc = rows / grid; size_t sm = (size_t)S * rb;
       auto run = [&](auto kern, const char* tag) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
