@@ -147,6 +147,27 @@ int aurora_route_prepare_gate(const void* w_gate, int E, int H, float* gate_prep
  * a record of k {int32 local expert on the destination or -1, float gate
  * weight}, padded to a multiple of 16 bytes (meta_bytes = roundup(8k, 16));
  * [n_local][T/n * k] records. local_of_expert[E] = expert index within its rank. */
+/* Grouped placement (several experts per rank, engine mode bit 8): the receiver
+ * keeps its rows grouped by local expert -- the packed layout aurora_expert_ffn_packed
+ * runs on: groups (r_local, local expert) of a process back to back, each ordered
+ * by (sender rank, token) -- and every dispatched row lands directly at its position
+ * in each local-expert group it belongs to, so no receiver-side sort / gather runs.
+ *   aurora_expert_hist: blk_cnt_e[T/64][E] tokens of each 64-token tile choosing each
+ *     expert; cnt_e[n][E] += per sender rank (rows of the caller's ranks zeroed by the
+ *     caller; exchanged like counts).
+ *   aurora_pack_grouped: aurora_pack, plus (cnt_e complete) meta records whose x field
+ *     is the row's position in its process's packed group buffer (-1: not on that
+ *     rank; padding records -1), and this process's g_off[n_local*G + 1] / g_rows[n_local*G]
+ *     (group g = r_local*G + local expert). Experts e live on gpu_of_expert[e]; every
+ *     process drives n_local consecutive ranks; E = n*G. */
+int aurora_expert_hist(const int32_t* topk_idx, int T, int k, int E, int rank_base, int tokens_per_rank,
+                       int32_t* blk_cnt_e, int32_t* cnt_e, void* stream);
+int aurora_pack_grouped(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T, int k,
+                        int n, int rank_base, int tokens_per_rank, int32_t* send_list, int32_t* pos,
+                        int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc, int32_t* rrem,
+                        const int32_t* topk_idx, const float* topk_w, const int32_t* local_of_expert, void* meta,
+                        const int32_t* blk_cnt_e, const int32_t* cnt_e, const int32_t* gpu_of_expert, int E,
+                        int G, int n_local, int32_t* g_off, int32_t* g_rows, void* stream);
 int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T,
                 int k, int n, int rank_base, int tokens_per_rank, int32_t* send_list,
                 int32_t* pos, int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc,
@@ -165,6 +186,9 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * while K2 is still computing; mode bit 3: scheduled remote chunks only;
  * mode bit 4: ablation -- no pacing, every sender pushes all of its chunks at
  * once (the unscheduled all-pairs-concurrent all-to-all);
+ * mode bit 8 (dispatch, TMA engine, meta plane required): grouped placement -- dst_bufs[j]
+ * is the base of rank j's process's packed group buffer and every row is stored at
+ * the positions in its meta record (aurora_pack_grouped), one store per local expert;
  * mode bit 5: launch as a programmatic dependent (PDL) of the immediately
  * preceding aurora_schedule_counts on the same stream -- the engine starts
  * while K2 runs (K2 triggers its dependents on entry, so it is resident first)
@@ -222,9 +246,12 @@ int aurora_engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int
  * ranks, and completes once every other rank's flag has arrived (system scope).
  * The caller alternates the counts buffer it passes to the other kernels with
  * the same parity. spin_limit bounds the wait; on expiry status = ETIMEOUT. */
-int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* rows2,
+                           int32_t* const* peer_rows2, int w2, int32_t* xflag,
                            int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base, int n_local,
                            int64_t spin_limit, int32_t* status, void* stream);
+/* (rows2 / peer_rows2 / w2, nullable: a second [2][n][w2] matrix exchanged the same way --
+ * the per-expert token counts of aurora_expert_hist for the grouped dispatch.) */
 
 /* aurora_combine_wait: the receiving side of the fused combine
  * (aurora_expert_ffn_combine). One thread per local sender rank
@@ -302,7 +329,8 @@ int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
  *     received row of grouped position p, inv[row][slot] = p or -1.
  *     scratch >= ceil(n_local*cap/256) * n_local*G ints.
  *   aurora_gather_rows: dst[p] = src[idx[p]] for p < *count (device count).
- *   aurora_expert_reduce: ybuf[row] = sum_slots w * yg[inv[row][slot]] (fp32 -> bf16),
+ *   aurora_expert_reduce: ybuf[row] = sum_slots w * yg[inv[row][slot]] (fp32 -> bf16)
+ *     (inv NULL: the position is the meta record's x field -- grouped dispatch),
  *     the pre-reduction that returns one row per (token, rank) to the combine. */
 int aurora_expert_sort(const void* meta, int64_t cap, int meta_bytes, const int32_t* rtot,
                        int n_local, int rank_base, int k, int G, int32_t* g_off, int32_t* g_rows,

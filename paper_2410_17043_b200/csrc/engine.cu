@@ -54,6 +54,7 @@ struct EngineParams {
   int max_phases;
   long long spin_limit;
   int32_t* status;
+  int meta_k;            // grouped dispatch (mode bit 8): expert records per meta row
 };
 
 // This CTA's rank (local index), its index among the rank's CTAs and the
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
   const bool do_local = (p.mode & 8) == 0;
   const bool paced = (p.mode & 16) == 0;
   const int rb = p.row_bytes, rb2 = p.src2_bufs ? p.row2_bytes : 0;
+  const bool grouped = (p.mode & 256) && rb2 && !(p.mode & 1);  // dispatch with the meta plane only
   const int4* table = dispatch ? p.chunks : p.rchunks;
   volatile int* abort = &sh.abort;
   for (int q = threadIdx.x; q < n * n; q += TMA_THREADS) {
@@ -591,7 +593,17 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
           }
           if (!mbar_wait_or_abort(&sh.full[s], u & 1, abort)) break;
           const uint32_t sp = slot0 + (uint32_t)(s * slot_bytes);
-          bulk_store(dst + (drow0 + r) * rb, sp, rb);
+          if (grouped) {
+            // the row goes to its position in every local-expert group it belongs to:
+            // the positions are the x fields of its meta records, landed in this slot
+            for (int q = 0; q < p.meta_k; q++) {
+              int gp;
+              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(gp) : "r"(sp + rb + 8 * q) : "memory");
+              if (gp >= 0) bulk_store(dst + (long long)gp * rb, sp, rb);
+            }
+          } else {
+            bulk_store(dst + (drow0 + r) * rb, sp, rb);
+          }
           if (rb2) bulk_store(dst2 + (drow0 + r) * rb2, sp + rb, rb2);
           bulk_commit();
           t++;
@@ -757,7 +769,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, int split, const double* bw, void* stream) {
   if (split < 0 || split > 2) return AURORA_EINVAL;
-  if (mode < 0 || mode > 255 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+  if (mode < 0 || mode > 511 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
+      ((mode & 256) && ((mode & 65) || !src2_bufs || !dst2_bufs || row2_bytes < 8)) ||
       rank_base < 0 ||
       rank_base + n_local > n || row_bytes % 16 || ctas_per_rank < 1 || !counts || !chunks ||
       !rchunks || !progress || !soff || !roff || !src_bufs || !dst_bufs || !ctrs || !status ||
@@ -775,6 +788,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.n = n;
   p.n_local = n_local;
   p.rank_base = rank_base;
+  p.meta_k = row2_bytes / 8;
   p.counts = counts;
   p.chunks = reinterpret_cast<const int4*>(chunks);
   p.rchunks = reinterpret_cast<const int4*>(rchunks);
@@ -823,7 +837,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
 // per local rank (value = the call's epoch); it returns once every other rank's
 // flag reached the epoch. counts are double-buffered by epoch parity, so a peer
 // one step ahead never overwrites rows this process may still read.
-__global__ void exchange_counts_kernel(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+__global__ void exchange_counts_kernel(int32_t* counts2, int32_t* const* peer_counts2, int32_t* rows2,
+                                       int32_t* const* peer_rows2, int w2, int32_t* xflag,
                                        int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base,
                                        int n_local, long long spin_limit, int32_t* status) {
   __shared__ int e_s;
@@ -844,20 +859,27 @@ __global__ void exchange_counts_kernel(int32_t* counts2, int32_t* const* peer_co
     const int32_t* src = counts2 + (size_t)par * n * n + (size_t)rank_base * n;
     int32_t* dst = peer_counts2[q] + (size_t)par * n * n + (size_t)rank_base * n;
     for (int v = 0; v < n_local * n; v++) dst[v] = src[v];
+    if (rows2) {  // second matrix [2][n][w2] (per-expert token counts), same rows
+      const int32_t* src2 = rows2 + (size_t)par * n * w2 + (size_t)rank_base * w2;
+      int32_t* dst2 = peer_rows2[q] + (size_t)par * n * w2 + (size_t)rank_base * w2;
+      for (int v = 0; v < n_local * w2; v++) dst2[v] = src2[v];
+    }
     __threadfence_system();
     for (int r = 0; r < n_local; r++) st_release_sys(peer_xflag[q] + rank_base + r, e);
   }
   if (q < n && !local_q && !wait_ge(xflag + q, e, spin_limit, true)) atomicExch(status, AURORA_ETIMEOUT);
 }
 
-extern "C" int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* xflag,
+extern "C" int aurora_exchange_counts(int32_t* counts2, int32_t* const* peer_counts2, int32_t* rows2,
+                                      int32_t* const* peer_rows2, int w2, int32_t* xflag,
                                       int32_t* const* peer_xflag, int32_t* epoch, int n, int rank_base,
                                       int n_local, int64_t spin_limit, int32_t* status, void* stream) {
   if (!counts2 || !peer_counts2 || !xflag || !peer_xflag || !epoch || !status || n < 1 || n > AUR_MAXN ||
-      n_local < 1 || rank_base < 0 || rank_base + n_local > n)
+      n_local < 1 || rank_base < 0 || rank_base + n_local > n || (rows2 && (!peer_rows2 || w2 < 1)))
     return AURORA_EINVAL;
-  exchange_counts_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(counts2, peer_counts2, xflag, peer_xflag, epoch, n,
-                                                             rank_base, n_local, spin_limit, status);
+  exchange_counts_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(counts2, peer_counts2, rows2, peer_rows2, w2, xflag,
+                                                             peer_xflag, epoch, n, rank_base, n_local, spin_limit,
+                                                             status);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -133,7 +133,7 @@ __device__ __forceinline__ void reduce_row(const __nv_bfloat16* __restrict__ yg,
   float w[MAX_SLOTS];
   int ns = 0;
   for (int s = 0; s < k; s++) {
-    const int p = inv[row * k + s];
+    const int p = inv ? inv[row * k + s] : m[s].x;  // grouped dispatch: the position is in the record
     if (p >= 0) {
       src[ns] = reinterpret_cast<const int4*>(yg + (long long)p * H);
       w[ns] = __int_as_float(m[s].y);
@@ -260,7 +260,7 @@ namespace {
 int launch_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap, int meta_bytes,
                   const int32_t* rtot, int n_local, int rank_base, int k, int H, void* ybuf,
                   const AuroraScatterArgs& sc, void* stream) {
-  if (!yg || !inv || !meta || cap < 1 || !rtot || k < 1 || k > MAX_SLOTS || H % 8 || !ybuf)
+  if (!yg || !meta || cap < 1 || !rtot || k < 1 || k > MAX_SLOTS || H % 8 || !ybuf)
     return AURORA_EINVAL;
   const long long rows = (long long)n_local * cap;
   const int blocks = (int)((rows * 32 + 255) / 256);

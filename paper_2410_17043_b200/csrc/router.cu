@@ -412,6 +412,21 @@ bool make_x_map(CUtensorMap* m, const void* x, uint64_t T, uint64_t H, uint32_t 
 // list(i, j) = rank i's tokens bound for j in ascending order; the entry for
 // token t lands at soff[i][j] + (entries of earlier tiles of rank i, from
 // blk_cnt) + (entries of earlier tokens in this tile, from warp ballots).
+// Grouped placement (several experts per rank, GROUPED): the receiver keeps its
+// rows grouped by local expert -- group (r_local, local expert) of a process,
+// rows ordered by (sender, token) -- and each dispatched row lands straight at
+// its position in every group it belongs to (the engine reads the positions from
+// the row's meta record), so no receiver-side sort or gather is needed.
+struct GroupedArgs {
+  const int32_t* blk_cnt_e;       // [T/64][E] tokens of each tile choosing each expert
+  const int32_t* cnt_e;           // [n][E] tokens of each sender rank choosing each expert (all senders)
+  const int32_t* gpu_of_expert;   // [E]
+  int E, G, n_local;              // experts, experts per rank, ranks per process (uniform)
+  int32_t* g_off;                 // [n_local * G + 1] this process's packed group offsets
+  int32_t* g_rows;                // [n_local * G]
+};
+
+template <bool GROUPED>
 __global__ void __launch_bounds__(TILE) pack_kernel(
     const int32_t* __restrict__ slot_dst, const int32_t* __restrict__ blk_cnt,
     const int32_t* __restrict__ counts, int T, int k, int n, int rank_base, int tokens_per_rank,
@@ -419,10 +434,12 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
     int32_t* __restrict__ roff, int32_t* __restrict__ rtot, int32_t* __restrict__ rloc,
     int32_t* __restrict__ rrem, const int32_t* __restrict__ topk_idx,
     const float* __restrict__ topk_w, const int32_t* __restrict__ local_of_expert,
-    uint8_t* __restrict__ meta, int meta_bytes) {
+    uint8_t* __restrict__ meta, int meta_bytes, const GroupedArgs ga) {
   __shared__ int base_s[AUR_MAXN];   // entries of earlier tiles of rank i, per destination
   __shared__ int soff_s[AUR_MAXN];   // start of list(i, j) in rank i's send list
   __shared__ int warp0_s[AUR_MAXN];  // entries of warp 0 per destination
+  __shared__ int gbase_s[GROUPED ? MAXE : 1];                 // grouped position of this tile's first row per expert
+  __shared__ unsigned long long tmask_s[GROUPED ? MAXE : 1];  // tokens of the tile choosing each expert
   const int tl = threadIdx.x, warp = tl >> 5, lane = tl & 31;
   const int t0 = blockIdx.x * TILE, t = t0 + tl;
   if (blockIdx.x == 0 && tl < n) {  // buffer layout of every rank (thread tl: sender row / receiver column tl)
@@ -452,6 +469,49 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
     base_s[tl] = acc;
     soff_s[tl] = so;
   }
+  if (GROUPED) {
+    const int E = ga.E;
+    __shared__ int rows_s[MAXE], key_s[MAXE];
+    int rows_e = 0, earlier_senders = 0, key = 0, proc = 0;
+    if (tl < E) {  // expert tl: rows of its group (all senders), rows from senders before i
+      const int e = tl, j = ga.gpu_of_expert[e];
+      proc = j / ga.n_local;
+      key = j * ga.G + local_of_expert[e];  // group order: (rank, local expert)
+      for (int i2 = 0; i2 < n; i2++) {
+        const int c = ga.cnt_e[i2 * E + e];
+        rows_e += c;
+        if (i2 < i) earlier_senders += c;
+      }
+      rows_s[e] = rows_e;
+      key_s[e] = key;
+    }
+    __syncthreads();
+    if (tl < E) {  // the group's offset in its process's packed buffer, this tile's base
+      const int e = tl;
+      int before = 0;
+      for (int e2 = 0; e2 < E; e2++)
+        if (key_s[e2] < key && key_s[e2] / (ga.n_local * ga.G) == proc) before += rows_s[e2];
+      key = key - proc * ga.n_local * ga.G;  // the group's index inside its process
+      int acc = 0;
+      for (int b = b_first; b < (int)blockIdx.x; b++) acc += ga.blk_cnt_e[(size_t)b * E + e];
+      gbase_s[e] = before + earlier_senders + acc;
+      tmask_s[e] = 0ull;
+      if (blockIdx.x == 0 && proc * ga.n_local == rank_base) {  // this process's packed groups
+        const int g = key;
+        ga.g_rows[g] = rows_e;
+        ga.g_off[g] = before;
+      }
+    }
+    if (blockIdx.x == 0 && tl == 0) {  // total rows of this process
+      int tot = 0;
+      for (int e2 = 0; e2 < E; e2++)
+        if (key_s[e2] / (ga.n_local * ga.G) == rank_base / ga.n_local) tot += rows_s[e2];
+      ga.g_off[ga.n_local * ga.G] = tot;
+    }
+    __syncthreads();
+    if (t < T)
+      for (int s2 = 0; s2 < k; s2++) atomicOr(&tmask_s[topk_idx[(size_t)t * k + s2]], 1ull << tl);
+  }
   const bool valid = t < T;
   int full[MAXK];  // destination rank of every slot (duplicates decoded)
   uint32_t mine = 0;
@@ -475,14 +535,24 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
       pos[(size_t)t * k + s] = p;
       if (slot_dst[(size_t)t * k + s] >= 0) {
         list[soff_s[j] + p] = t - i_local * tokens_per_rank;
-        if (meta) {  // the row's expert slots on rank j: {local expert, gate weight} or {-1, 0}
+        if (meta) {  // the row's expert slots on rank j: {local expert (grouped: the
+                     // row's position in that expert's group), gate weight} or {-1, 0}
           int2* m = reinterpret_cast<int2*>(meta + ((size_t)i_local * tokens_per_rank * k +
                                                     soff_s[j] + p) * meta_bytes);
           for (int q = 0; q < k; q++) {
             const bool here = full[q] == j;
-            const int e = here ? local_of_expert[topk_idx[(size_t)t * k + q]] : -1;
+            const int eg = topk_idx[(size_t)t * k + q];
+            int e = -1;
+            if (here) {
+              if (GROUPED)
+                e = gbase_s[eg] + __popcll(tmask_s[eg] & ((1ull << tl) - 1ull));
+              else
+                e = local_of_expert[eg];
+            }
             m[q] = make_int2(e, here ? __float_as_int(topk_w[(size_t)t * k + q]) : 0);
           }
+          if (GROUPED)  // padding records: no position (the engine reads meta_bytes / 8 records)
+            for (int q = k; q < meta_bytes / 8; q++) m[q] = make_int2(-1, 0);
         }
       }
     }
@@ -541,6 +611,56 @@ extern "C" int aurora_route(const void* x, const float* gate_prep, const float* 
   return AURORA_OK;
 }
 
+// per 64-token tile and expert: tokens choosing the expert (+ per sender rank totals)
+__global__ void __launch_bounds__(TILE) expert_hist_kernel(const int32_t* __restrict__ topk_idx, int T, int k, int E,
+                                                         int rank_base, int tokens_per_rank,
+                                                         int32_t* __restrict__ blk_cnt_e, int32_t* __restrict__ cnt_e) {
+  __shared__ int h[MAXE];
+  const int tl = threadIdx.x, t = blockIdx.x * TILE + tl;
+  if (tl < E) h[tl] = 0;
+  __syncthreads();
+  if (t < T)
+    for (int s = 0; s < k; s++) atomicAdd(&h[topk_idx[(size_t)t * k + s]], 1);
+  __syncthreads();
+  if (tl < E) {
+    blk_cnt_e[(size_t)blockIdx.x * E + tl] = h[tl];
+    const int src = rank_base + (blockIdx.x * TILE) / tokens_per_rank;
+    if (h[tl]) atomicAdd(&cnt_e[src * E + tl], h[tl]);
+  }
+}
+
+extern "C" int aurora_expert_hist(const int32_t* topk_idx, int T, int k, int E, int rank_base, int tokens_per_rank,
+                                  int32_t* blk_cnt_e, int32_t* cnt_e, void* stream) {
+  if (!topk_idx || !blk_cnt_e || !cnt_e || T <= 0 || k < 1 || k > MAXK || E < 1 || E > MAXE ||
+      tokens_per_rank % TILE || T % tokens_per_rank)
+    return AURORA_EINVAL;
+  expert_hist_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(topk_idx, T, k, E, rank_base, tokens_per_rank,
+                                                                   blk_cnt_e, cnt_e);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_pack_grouped(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts,
+                                   int T, int k, int n, int rank_base, int tokens_per_rank,
+                                   int32_t* send_list, int32_t* pos, int32_t* soff, int32_t* roff,
+                                   int32_t* rtot, int32_t* rloc, int32_t* rrem,
+                                   const int32_t* topk_idx, const float* topk_w,
+                                   const int32_t* local_of_expert, void* meta,
+                                   const int32_t* blk_cnt_e, const int32_t* cnt_e, const int32_t* gpu_of_expert,
+                                   int E, int G, int n_local, int32_t* g_off, int32_t* g_rows, void* stream) {
+  if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
+      T % tokens_per_rank || !soff || !roff || !rtot || !rloc || !rrem || !meta || !blk_cnt_e || !cnt_e ||
+      !gpu_of_expert || !local_of_expert || !g_off || !g_rows || E < 1 || E > MAXE || G < 1 || n_local < 1 ||
+      n % n_local || rank_base % n_local || E != n * G)
+    return AURORA_EINVAL;
+  const GroupedArgs ga{blk_cnt_e, cnt_e, gpu_of_expert, E, G, n_local, g_off, g_rows};
+  pack_kernel<true><<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
+      slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
+      rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16, ga);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
 extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts,
                            int T, int k, int n, int rank_base, int tokens_per_rank,
                            int32_t* send_list, int32_t* pos, int32_t* soff, int32_t* roff,
@@ -550,9 +670,10 @@ extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, cons
   if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
       T % tokens_per_rank || !soff || !roff || !rtot || !rloc || !rrem)
     return AURORA_EINVAL;
-  pack_kernel<<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
+  pack_kernel<false><<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
       slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
-      rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16);
+      rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16,
+      GroupedArgs{});
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

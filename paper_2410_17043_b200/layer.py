@@ -208,6 +208,9 @@ class AuroraMoELayer:
         # all-to-all follows the experts; AURORA_COMBINE=engine runs the reversed-schedule
         # combine engine instead (needs local-direct aggregation either way)
         self.fused_combine = os.environ.get("AURORA_COMBINE", "fused") == "fused"
+        # several experts per rank: dispatch rows straight into the packed per-expert groups
+        # (engine mode bit 8; AURORA_GROUPED_DISPATCH=0: receive, sort, gather)
+        self.grouped_dispatch = os.environ.get("AURORA_GROUPED_DISPATCH", "1") != "0"
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
@@ -254,6 +257,10 @@ class AuroraMoELayer:
             blocks = (self.n_local * self.cap + 255) // 256
             self.sort_scratch = torch.empty(blocks * E_loc, **i32)
             self.a_g = torch.empty(self.max_entries, H, **bf)
+            # grouped dispatch (default): rows land straight at their packed-group positions
+            self.blk_cnt_e = torch.zeros(self.T_local // 64, E, **i32)
+            self.cnt_e2 = torch.zeros(2, n, E, **i32)   # tokens per (sender rank, expert), parity-buffered
+            self.cnt_e = self.cnt_e2[0]
             self.h_g = torch.empty(self.max_entries, F, **bf)
             self.y_g = torch.empty(self.max_entries, H, **bf)
             self.overlap = False  # the local/network GEMM split assumes one expert per rank
@@ -322,6 +329,11 @@ class AuroraMoELayer:
             meta_p = (peers["meta_recv"] if peers is not None else
                       [self.meta_recv.data_ptr() + r * self.cap * mb for r in range(self.n)])
             self.t_dst2 = self._ptr_table(meta_p)
+            # grouped dispatch: every rank's rows go to its process's packed group buffer
+            ag_p = peers["a_g"] if peers is not None else [self.a_g.data_ptr()] * self.n
+            self.t_dst_g = self._ptr_table(ag_p)
+            if peers is not None:
+                self.t_cnt_e2 = self._ptr_table(peers["cnt_e2"])
         self._src_tables = {}
         if x is not None:
             self._use_input(x)
@@ -353,6 +365,12 @@ class AuroraMoELayer:
                                        self.topk_w.data_ptr(), self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
                                        self.counts.data_ptr(), None if self.logits is None else self.logits.data_ptr(),
                                        stream), "aurora_route")
+        if self.grouped:
+            self.cnt_e = self.cnt_e2[self._xstep & 1]
+            self.cnt_e[self.rank_base:self.rank_base + self.n_local].zero_()
+            _lib.check(self.L.aurora_expert_hist(self.topk_idx.data_ptr(), self.T_local, cfg.top_k, cfg.experts,
+                                                 self.rank_base, cfg.tokens_per_rank, self.blk_cnt_e.data_ptr(),
+                                                 self.cnt_e.data_ptr(), stream), "aurora_expert_hist")
 
     def exchange_counts(self, stream: Optional[int] = None) -> None:
         """Multi-GPU: complete the traffic matrix (each process owns its rows) with
@@ -363,8 +381,11 @@ class AuroraMoELayer:
         if getattr(self, "t_counts2", None) is None:
             raise RuntimeError("multi-process layer: call dist.connect_peers(layer) first")
         s = _lib.stream_ptr() if stream is None else stream
+        grouped = self.grouped
         _lib.check(self.L.aurora_exchange_counts(self.counts2.data_ptr(), self.t_counts2.data_ptr(),
-                                                 self.xflag.data_ptr(), self.t_xflag.data_ptr(),
+                                                 self.cnt_e2.data_ptr() if grouped else None,
+                                                 self.t_cnt_e2.data_ptr() if grouped else None,
+                                                 self.cfg.experts, self.xflag.data_ptr(), self.t_xflag.data_ptr(),
                                                  self.xepoch.data_ptr(), self.n, self.rank_base, self.n_local,
                                                  self.spin_limit, self.engine_status.data_ptr(), s),
                    "aurora_exchange_counts")
@@ -397,6 +418,16 @@ class AuroraMoELayer:
 
     def pack(self, stream: int) -> None:
         cfg = self.cfg
+        if self.grouped:
+            _lib.check(self.L.aurora_pack_grouped(
+                self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(), self.counts.data_ptr(), self.T_local, cfg.top_k,
+                self.n, self.rank_base, cfg.tokens_per_rank, self.send_list.data_ptr(), self.pos.data_ptr(),
+                self.soff.data_ptr(), self.roff.data_ptr(), self.rtot.data_ptr(), self.rloc.data_ptr(),
+                self.rrem.data_ptr(), self.topk_idx.data_ptr(), self.topk_w.data_ptr(),
+                self.local_of_expert.data_ptr(), self.meta_send.data_ptr(), self.blk_cnt_e.data_ptr(),
+                self.cnt_e.data_ptr(), self.gpu_of_expert.data_ptr(), cfg.experts, self.G, self.n_local,
+                self.g_off.data_ptr(), self.g_rows.data_ptr(), stream), "aurora_pack_grouped")
+            return
         _lib.check(self.L.aurora_pack(self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(), self.counts.data_ptr(),
                                       self.T_local, cfg.top_k, self.n, self.rank_base, cfg.tokens_per_rank,
                                       self.send_list.data_ptr(), self.pos.data_ptr(), self.soff.data_ptr(),
@@ -411,12 +442,13 @@ class AuroraMoELayer:
         cfg = self.cfg
         combine = mode & 1
         src = self.t_src_c if combine else self.t_src_d
-        dst = self.t_dst_c if combine else self.t_dst_d
+        dst = self.t_dst_c if combine else (self.t_dst_g if self.grouped else self.t_dst_d)
         ctr = self.t_ctr_c if combine else self.t_ctr_d
         sys_scope = 2 if self.n_local != self.n else 0  # peers on other GPUs
         plane2 = self.G > 1 and not combine
+        grouped = 256 if (self.grouped and not combine) else 0
         _lib.check(self.L.aurora_engine(
-            mode | sys_scope | self.engine_lsu | self.early_pace, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            mode | sys_scope | self.engine_lsu | self.early_pace | grouped, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.progress.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
@@ -449,6 +481,11 @@ class AuroraMoELayer:
                                             self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_start or None, m_rows,
                                             self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
                    "aurora_expert_ffn")
+
+    @property
+    def grouped(self) -> bool:
+        """Rows are dispatched straight into the packed per-expert groups (needs the TMA engine)."""
+        return self.G > 1 and self.grouped_dispatch and not self.engine_lsu
 
     @property
     def combine_in_gemm(self) -> bool:
@@ -487,6 +524,34 @@ class AuroraMoELayer:
         run the packed grouped GEMMs, pre-reduce each row's expert outputs."""
         cfg = self.cfg
         L, k, H = self.L, cfg.top_k, cfg.hidden
+        E_loc = self.n_local * self.G
+        if self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack)
+            _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+                                                  self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
+                                                  self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
+                                                  self.num_sms, stream), "aurora_expert_ffn_packed")
+            inv = None
+        else:
+            self._sort_and_gather(stream)
+            inv = self.inv.data_ptr()
+        if fused:
+            _lib.check(L.aurora_expert_reduce_combine(
+                self.y_g.data_ptr(), inv, self.meta_recv.data_ptr(), self.cap, self.meta_bytes,
+                self.rtot.data_ptr(), self.n_local, self.rank_base, k, H, self.ybuf.data_ptr(),
+                self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
+                self.n, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), 1 if self.n_local != self.n else 0,
+                stream), "aurora_expert_reduce_combine")
+            return
+        _lib.check(L.aurora_expert_reduce(self.y_g.data_ptr(), inv, self.meta_recv.data_ptr(),
+                                          self.cap, self.meta_bytes, self.rtot.data_ptr(), self.n_local,
+                                          self.rank_base, k, H, self.ybuf.data_ptr(), stream),
+                   "aurora_expert_reduce")
+
+    def _sort_and_gather(self, stream: int) -> None:
+        """Ungrouped receive: sort the received rows by local expert, then gather them
+        into the packed group buffer and run the packed GEMMs."""
+        cfg = self.cfg
+        L, k, H = self.L, cfg.top_k, cfg.hidden
         _lib.check(L.aurora_expert_sort(self.meta_recv.data_ptr(), self.cap, self.meta_bytes, self.rtot.data_ptr(),
                                         self.n_local, self.rank_base, k, self.G, self.g_off.data_ptr(),
                                         self.g_rows.data_ptr(), self.g_src.data_ptr(), self.inv.data_ptr(),
@@ -500,18 +565,6 @@ class AuroraMoELayer:
                                               self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                               self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
                                               self.num_sms, stream), "aurora_expert_ffn_packed")
-        if fused:
-            _lib.check(L.aurora_expert_reduce_combine(
-                self.y_g.data_ptr(), self.inv.data_ptr(), self.meta_recv.data_ptr(), self.cap, self.meta_bytes,
-                self.rtot.data_ptr(), self.n_local, self.rank_base, k, H, self.ybuf.data_ptr(),
-                self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
-                self.n, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), 1 if self.n_local != self.n else 0,
-                stream), "aurora_expert_reduce_combine")
-            return
-        _lib.check(L.aurora_expert_reduce(self.y_g.data_ptr(), self.inv.data_ptr(), self.meta_recv.data_ptr(),
-                                          self.cap, self.meta_bytes, self.rtot.data_ptr(), self.n_local,
-                                          self.rank_base, k, H, self.ybuf.data_ptr(), stream),
-                   "aurora_expert_reduce")
 
     def combine(self, stream: int) -> None:
         # local rows stay in the expert output; the aggregation reads them there

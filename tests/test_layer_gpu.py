@@ -55,11 +55,22 @@ def _check_layer(torch, cfg, plan=None, out_tol=3e-2):
     # dispatched rows: receiver j holds its local rows list(j,j) first, then
     # list(i,j) for the other senders in index order -- bit-exact copies of x
     xb = x.view(torch.int16)
-    recv = layer.recv.view(torch.int16)
-    for j in range(n):
-        rows = list(lists[j][j]) + [t for i in range(n) if i != j for t in lists[i][j]]
-        if rows:
-            assert torch.equal(recv[j * layer.cap: j * layer.cap + len(rows)], xb[rows])
+    if getattr(layer, "grouped", False):
+        # grouped dispatch: the packed group buffer holds, per (rank, local expert) in
+        # that order, x of every token choosing the expert in token order
+        gl = layer.gpu_of_expert.cpu().numpy()
+        lo = layer.local_of_expert.cpu().numpy()
+        rows = [t for e in sorted(range(cfg.experts), key=lambda e: (gl[e], lo[e]))
+                for t in np.where((idx == e).any(axis=1))[0]]
+        ag = layer.a_g.view(torch.int16)
+        assert int(layer.g_off[-1].item()) == len(rows)
+        assert torch.equal(ag[:len(rows)], xb[torch.tensor(rows, device=xb.device)])
+    else:
+        recv = layer.recv.view(torch.int16)
+        for j in range(n):
+            rows = list(lists[j][j]) + [t for i in range(n) if i != j for t in lists[i][j]]
+            if rows:
+                assert torch.equal(recv[j * layer.cap: j * layer.cap + len(rows)], xb[rows])
     # combined output vs fp32 oracle
     F = cfg.ffn
     w1, w3 = _deinterleave(layer.w13, F)
@@ -221,20 +232,21 @@ def test_layer_deepseek_shape_small(torch):
 
 def test_fused_and_engine_combine_agree_several_experts(torch):
     """E > n: the combine fused into the pre-reduction (rows stored straight
-    into the senders' return buffers) and the reversed-schedule combine engine
-    give identical outputs, repeatedly (counters and ticket rearmed)."""
+    into the senders' return buffers) and the reversed-schedule combine engine,
+    rows dispatched straight into their expert groups or received, sorted and
+    gathered, all give identical outputs, repeatedly (counters / ticket rearmed)."""
     from paper_2410_17043_b200.layer import AuroraMoELayer
     cfg = MoEConfig_(hidden=512, ffn=256, experts=64, top_k=6, tokens=2048, ranks=8, skew=1.0, seed=9)
     layer = AuroraMoELayer(cfg)
     x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
-    layer.fused_combine = False
+    layer.fused_combine, layer.grouped_dispatch = False, False
     ref = layer(x).clone()
-    for fused in (True, False, True, True):
-        layer.fused_combine = fused
+    for fused, grouped in ((True, True), (False, True), (True, False), (False, False), (True, True)):
+        layer.fused_combine, layer.grouped_dispatch = fused, grouped
         out = layer(x)
         torch.cuda.synchronize()
         layer.check_status()
-        assert torch.equal(out, ref), fused
+        assert torch.equal(out, ref), (fused, grouped)
     assert int(layer.ctr_c.abs().sum()) == 0 and int(layer.gemm_ticket.item()) == 0
 
 
