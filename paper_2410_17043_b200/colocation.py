@@ -88,8 +88,8 @@ class ColocatedLayers:
         self.a = AuroraMoELayer(cfg_a, DeploymentPlan(cplan.gpu_of_a), **kw)
         self.b = AuroraMoELayer(cfg_b, None, gpu_of_expert=cplan.gpu_of_b, **kw)
 
-    def forward(self, x_a, x_b):
-        return self.a(x_a), self.b(x_b)
+    def forward(self, x_a, x_b, out_a=None, out_b=None):
+        return self.a(x_a, out=out_a), self.b(x_b, out=out_b)
 
     __call__ = forward
 
