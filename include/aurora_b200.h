@@ -226,7 +226,11 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
                   const void* const* src_bufs, void* const* dst_bufs, int row_bytes,
                   const void* const* src2_bufs, void* const* dst2_bufs, int row2_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
-                  int32_t* status, int split, const double* bw, void* stream);
+                  int32_t* status, int split, const double* bw, void* const* ginfo_bufs, void* stream);
+/* ginfo_bufs (mode bit 8, nullable): per rank the base of its process's [rows] int4
+ * array; every grouped store of a row also writes {receiver-layout row, gate weight,
+ * single (the row's only local expert), 0} at the row's group position
+ * (aurora_expert_ffn_packed_scatter). */
 /* aurora_engine_ctas: copy CTAs per local rank the engine will actually use
  * (ctas_per_rank clamped so every copy CTA is co-resident), or -AURORA_E* on
  * error. K2 needs n_local x this value to count hand-over thresholds. The
@@ -314,6 +318,22 @@ int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2
                               const int32_t* roff, int n, int rank_base, int32_t* const* ctrs,
                               int32_t* ticket, int sys, int num_sms, void* stream);
 
+/* aurora_expert_ffn_packed_scatter: the packed FFN of the grouped dispatch with the
+ * pre-reduction of single-expert rows folded into GEMM2's epilogue. ginfo [a_rows]
+ * int4 per packed row = {receiver-layout row, gate weight bits, single, -} (written by
+ * the grouped dispatch, engine mode bit 8). A single row's output is w * y (the
+ * pre-reduction's fp32 arithmetic on the bf16 y) stored into ybuf row
+ * r_local * ycap + recv row, or with to_ret (fused combine) straight into its
+ * sender's return buffer (ret_bufs / counts / soff / roff as in
+ * aurora_expert_ffn_combine; rank = rank_base + group / experts_per_rank). Other
+ * rows go to y_buf for aurora_expert_reduce(_combine) with skip_single = 1. */
+int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const void* w2, void* h_buf,
+                                     void* y_buf, const int32_t* g_off, const int32_t* g_rows, int G,
+                                     int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
+                                     void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
+                                     const int32_t* roff, int n, int rank_base, void* ybuf, int64_t ycap,
+                                     int to_ret, int sys, int num_sms, void* stream);
+
 /* Same FFN with the groups packed back to back (a rank hosting several
  * experts): group g's rows are a_buf rows [g_off[g], g_off[g] + g_rows[g]);
  * a_rows = rows allocated in a_buf / h_buf / y_buf. */
@@ -339,8 +359,8 @@ int aurora_expert_sort(const void* meta, int64_t cap, int meta_bytes, const int3
 int aurora_gather_rows(const void* src, void* dst, const int32_t* idx, const int32_t* count,
                        int64_t max_rows, int row_bytes, void* stream);
 int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap,
-                         int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k,
-                         int H, void* ybuf, void* stream);
+                         int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k, int H,
+                         void* ybuf, int skip_single, void* stream);
 /* aurora_expert_reduce_combine: the pre-reduction with the combine fused into it
  * (several experts per rank): each reduced row of sender i's block is stored
  * straight into ret_bufs[i] row soff[i][j] + offset (rows of the rank's own tokens
@@ -350,7 +370,9 @@ int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void*
                                  int meta_bytes, const int32_t* rtot, int n_local, int rank_base, int k,
                                  int H, void* ybuf, void* const* ret_bufs, const int32_t* counts,
                                  const int32_t* soff, const int32_t* roff, int n, int32_t* const* ctrs,
-                                 int32_t* ticket, int sys, void* stream);
+                                 int32_t* ticket, int sys, int skip_single, void* stream);
+/* skip_single (both): rows whose (token, rank) has exactly one local expert were
+ * finished by aurora_expert_ffn_packed_scatter; only the others are reduced. */
 
 /* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
  * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */

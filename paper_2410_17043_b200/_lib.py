@@ -32,7 +32,7 @@ _SIGNATURES = {
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
-                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp],
+                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp, _vp],
     "aurora_engine_ctas": [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp, _c_i64, _vp, _vp],
@@ -49,9 +49,12 @@ _SIGNATURES = {
     "aurora_expert_sort": [_vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
                            _vp, _c_int, _vp],
     "aurora_gather_rows": [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp],
-    "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp],
+    "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
+    "aurora_expert_ffn_packed_scatter": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp,
+                                         _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_i64, _c_int, _c_int,
+                                         _c_int, _vp],
     "aurora_expert_reduce_combine": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp,
-                                     _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp],
+                                     _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "aurora_debug_set_schedule_profile": [_vp],
     "aurora_debug_set_schedule_trace": [_vp],

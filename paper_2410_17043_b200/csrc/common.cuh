@@ -84,6 +84,11 @@ struct AuroraScatterArgs {
   int32_t* const* ctrs;
   int32_t* ticket;
   int n, rank_base, sys;
+  const void* ginfo;  // packed groups: per-row {recv row, weight, single, -} (nullptr: one expert per rank)
+  int G;
+  void* ybuf;
+  long long ycap;
+  int to_ret;
 };
 
 #define AUR_CHECK_LAUNCH()                          \

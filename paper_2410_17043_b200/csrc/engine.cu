@@ -55,6 +55,7 @@ struct EngineParams {
   long long spin_limit;
   int32_t* status;
   int meta_k;            // grouped dispatch (mode bit 8): expert records per meta row
+  int4* const* ginfo;    // grouped dispatch: per-rank {recv row, weight, single, 0} arrays (nullable)
 };
 
 // This CTA's rank (local index), its index among the rank's CTAs and the
@@ -596,10 +597,20 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
           if (grouped) {
             // the row goes to its position in every local-expert group it belongs to:
             // the positions are the x fields of its meta records, landed in this slot
+            int nq = 0;
+            if (p.ginfo)
+              for (int q = 0; q < p.meta_k; q++) {
+                int gp;
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(gp) : "r"(sp + rb + 8 * q) : "memory");
+                nq += gp >= 0;
+              }
             for (int q = 0; q < p.meta_k; q++) {
-              int gp;
-              asm volatile("ld.shared.b32 %0, [%1];" : "=r"(gp) : "r"(sp + rb + 8 * q) : "memory");
-              if (gp >= 0) bulk_store(dst + (long long)gp * rb, sp, rb);
+              int gp, wb;
+              asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(gp), "=r"(wb) : "r"(sp + rb + 8 * q) : "memory");
+              if (gp >= 0) {
+                bulk_store(dst + (long long)gp * rb, sp, rb);
+                if (p.ginfo) p.ginfo[peer][gp] = make_int4((int)(drow0 + r), wb, nq == 1 ? 1 : 0, 0);
+              }
             }
           } else {
             bulk_store(dst + (drow0 + r) * rb, sp, rb);
@@ -767,7 +778,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst_bufs, int row_bytes, const void* const* src2_bufs,
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
-                             int32_t* status, int split, const double* bw, void* stream) {
+                             int32_t* status, int split, const double* bw, void* const* ginfo_bufs,
+                             void* stream) {
   if (split < 0 || split > 2) return AURORA_EINVAL;
   if (mode < 0 || mode > 511 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       ((mode & 256) && ((mode & 65) || !src2_bufs || !dst2_bufs || row2_bytes < 8)) ||
@@ -789,6 +801,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.n_local = n_local;
   p.rank_base = rank_base;
   p.meta_k = row2_bytes / 8;
+  p.ginfo = reinterpret_cast<int4* const*>(ginfo_bufs);
   p.counts = counts;
   p.chunks = reinterpret_cast<const int4*>(chunks);
   p.rchunks = reinterpret_cast<const int4*>(rchunks);

@@ -127,7 +127,7 @@ __device__ __forceinline__ void reduce_row(const __nv_bfloat16* __restrict__ yg,
                                            const uint8_t* __restrict__ meta, long long row, int r, int i,
                                            int meta_bytes, int rank_base, int k, int H,
                                            __nv_bfloat16* __restrict__ ybuf, const AuroraScatterArgs& sc,
-                                           int lane) {
+                                           int lane, bool skip_single) {
   const int2* m = reinterpret_cast<const int2*>(meta + row * meta_bytes);
   const int4* src[MAX_SLOTS];
   float w[MAX_SLOTS];
@@ -140,6 +140,7 @@ __device__ __forceinline__ void reduce_row(const __nv_bfloat16* __restrict__ yg,
       ns++;
     }
   }
+  if (skip_single && ns == 1) return;  // finished by GEMM2's epilogue (packed scatter)
   int4* o = reinterpret_cast<int4*>(ybuf + row * H);
   if (sc.n) {  // sender of this row: lane q tests sender q's block of rank r's receive buffer
     const int rr = rank_base + r;
@@ -193,12 +194,12 @@ __global__ void expert_reduce_kernel(const __nv_bfloat16* __restrict__ yg,
                                      const uint8_t* __restrict__ meta, long long cap,
                                      int meta_bytes, const int32_t* __restrict__ rtot, int n_local,
                                      int rank_base, int k, int H, __nv_bfloat16* __restrict__ ybuf,
-                                     const AuroraScatterArgs sc) {
+                                     const AuroraScatterArgs sc, int skip_single) {
   const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   int r, i;
   if (row < (long long)n_local * cap && row_valid(row, cap, rtot, rank_base, r, i))
-    reduce_row(yg, inv, meta, row, r, i, meta_bytes, rank_base, k, H, ybuf, sc, lane);
+    reduce_row(yg, inv, meta, row, r, i, meta_bytes, rank_base, k, H, ybuf, sc, lane, skip_single != 0);
   if (sc.n) {  // fused combine: grid completion -> one arrival per local rank on every sender
     if (sc.sys) __threadfence_system();
     else __threadfence();
@@ -259,14 +260,14 @@ extern "C" int aurora_gather_rows(const void* src, void* dst, const int32_t* idx
 namespace {
 int launch_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t cap, int meta_bytes,
                   const int32_t* rtot, int n_local, int rank_base, int k, int H, void* ybuf,
-                  const AuroraScatterArgs& sc, void* stream) {
+                  const AuroraScatterArgs& sc, int skip_single, void* stream) {
   if (!yg || !meta || cap < 1 || !rtot || k < 1 || k > MAX_SLOTS || H % 8 || !ybuf)
     return AURORA_EINVAL;
   const long long rows = (long long)n_local * cap;
   const int blocks = (int)((rows * 32 + 255) / 256);
   expert_reduce_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)yg, inv, (const uint8_t*)meta, cap, meta_bytes, rtot, n_local,
-      rank_base, k, H, (__nv_bfloat16*)ybuf, sc);
+      rank_base, k, H, (__nv_bfloat16*)ybuf, sc, skip_single);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
@@ -274,9 +275,9 @@ int launch_reduce(const void* yg, const int32_t* inv, const void* meta, int64_t 
 
 extern "C" int aurora_expert_reduce(const void* yg, const int32_t* inv, const void* meta,
                                     int64_t cap, int meta_bytes, const int32_t* rtot, int n_local,
-                                    int rank_base, int k, int H, void* ybuf, void* stream) {
+                                    int rank_base, int k, int H, void* ybuf, int skip_single, void* stream) {
   return launch_reduce(yg, inv, meta, cap, meta_bytes, rtot, n_local, rank_base, k, H, ybuf,
-                       AuroraScatterArgs{}, stream);
+                       AuroraScatterArgs{}, skip_single, stream);
 }
 
 extern "C" int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void* meta,
@@ -285,11 +286,11 @@ extern "C" int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, 
                                             void* const* ret_bufs, const int32_t* counts,
                                             const int32_t* soff, const int32_t* roff, int n,
                                             int32_t* const* ctrs, int32_t* ticket, int sys,
-                                            void* stream) {
+                                            int skip_single, void* stream) {
   if (!ret_bufs || !counts || !soff || !roff || !ctrs || !ticket || n < 1 || n > 32 || n_local < 1 ||
       rank_base < 0 || rank_base + n_local > n)
     return AURORA_EINVAL;
   const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
   return launch_reduce(yg, inv, meta, cap, meta_bytes, rtot, n_local, rank_base, k, H, ybuf, sc,
-                       stream);
+                       skip_single, stream);
 }

@@ -435,6 +435,26 @@ extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, con
                         (cudaStream_t)stream, &sc);
 }
 
+extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const void* w2, void* h_buf,
+                                                void* y_buf, const int32_t* g_off, const int32_t* g_rows, int G,
+                                                int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
+                                                void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
+                                                const int32_t* roff, int n, int rank_base, void* ybuf,
+                                                int64_t ycap, int to_ret, int sys, int num_sms, void* stream) {
+  if (!ginfo || !ret_bufs || !counts || !soff || !roff || !ybuf || experts_per_rank < 1) return AURORA_EINVAL;
+  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, num_sms,
+                          (cudaStream_t)stream);
+  if (rc != AURORA_OK) return rc;
+  AuroraScatterArgs sc{ret_bufs, counts, soff, roff, nullptr, nullptr, n, rank_base, sys ? 1 : 0};
+  sc.ginfo = ginfo;
+  sc.G = experts_per_rank;
+  sc.ybuf = ybuf;
+  sc.ycap = ycap;
+  sc.to_ret = to_ret ? 1 : 0;
+  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, num_sms,
+                        (cudaStream_t)stream, &sc);
+}
+
 extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
                                         void* h_buf, void* y_buf, const int32_t* g_off,
                                         const int32_t* g_rows, int G, int64_t a_rows, int H, int F,

@@ -49,6 +49,16 @@ struct Scatter {
   int32_t* const* ctrs;       // [n] {pace, done} counters of the senders
   int32_t* ticket;            // grid completion ticket (zero; re-armed by the last CTA)
   int n, rank_base, sys;
+  // packed groups (several experts per rank): ginfo[row] = {recv row, weight bits, single, -}
+  // per packed row (written by the grouped dispatch). A row whose (token, rank) has one
+  // local expert is finished here -- w * y, stored into its sender's return buffer (to_ret,
+  // other ranks) or into ybuf -- instead of going through the pre-reduction. No arrivals:
+  // the pre-reduction that follows signals the senders.
+  const int4* ginfo;
+  int G;                      // experts per rank (groups per local rank)
+  __nv_bfloat16* ybuf;        // [n_local][ycap] rows of N
+  long long ycap;
+  int to_ret;
 };
 
 struct TileIter2 {
@@ -118,7 +128,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     it.prefix[G] = acc;
     it.total = acc;
-    for (int q = 0; q < (sc.n ? G * sc.n : 0); q++) {  // (group, sender) -> row block
+    const int sc_ranks = sc.ginfo ? G / sc.G : G;   // local ranks the table covers
+    for (int q = 0; q < (sc.n ? sc_ranks * sc.n : 0); q++) {  // (local rank, sender) -> row block
       const int g = q / sc.n, src = q - g * sc.n, r = sc.rank_base + g;
       sc_lo[q] = sc.roff[src * sc.n + r];
       sc_cnt[q] = sc.counts[src * sc.n + r];
@@ -281,7 +292,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       } else {
         __nv_bfloat16* out = c + row * (long long)N + nt * BN;
-        if (sc.n && live) {  // fused combine: the row goes back to its sender
+        bool weighted = false;
+        float wsc = 0.0f;
+        if (sc.n && live && sc.ginfo) {  // packed groups: single-expert rows are finished here
+          const int4 rec = sc.ginfo[row];
+          if (rec.z) {
+            weighted = true;
+            wsc = __int_as_float(rec.y);
+            const int rl = g / sc.G, rr = sc.rank_base + rl, recv_row = rec.x;
+            out = sc.ybuf + ((long long)rl * sc.ycap + recv_row) * N + nt * BN;
+            if (sc.to_ret)
+              for (int src = 0; src < sc.n; src++) {
+                const int q = rl * sc.n + src, off = recv_row - sc_lo[q];
+                if (off >= 0 && off < sc_cnt[q]) {
+                  if (src != rr) out = sc.ret[src] + (long long)(sc_dst[q] + off) * N + nt * BN;
+                  break;
+                }
+              }
+          }
+        } else if (sc.n && live) {  // fused combine: the row goes back to its sender
           for (int src = 0; src < sc.n; src++) {
             const int q = g * sc.n + src, off = row_in_group - sc_lo[q];
             if (off >= 0 && off < sc_cnt[q]) {
@@ -300,6 +329,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 16; q++) {
               __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+              if (weighted) {  // the pre-reduction's arithmetic: fmaf(w, bf16(y), 0) in fp32, then bf16
+                const float2 f = __bfloat1622float2(h2);
+                h2 = __floats2bfloat162_rn(fmaf(wsc, f.x, 0.0f), fmaf(wsc, f.y, 0.0f));
+              }
               packed[q] = *reinterpret_cast<uint32_t*>(&h2);
             }
             int4* o = reinterpret_cast<int4*>(out + c0);
@@ -327,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       __threadfence();
     }
   }
-  if (sc.n && threadIdx.x == 0) {  // grid completion -> one arrival per group on every sender
+  if (sc.n && !sc.ginfo && threadIdx.x == 0) {  // grid completion -> one arrival per group on every sender
     __threadfence();
     if (atomicAdd(sc.ticket, 1) == (int)gridDim.x - 1) {
       __threadfence();
@@ -399,10 +432,19 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
                               const AuroraScatterArgs* scatter) {
   Scatter sc{};
   if (scatter) {
-    if (epilogue != 0 || m_start || cap <= 0 || scatter->n < 1 || scatter->n > SC_MAXN || G > SC_MAXN ||
-        scatter->rank_base < 0 || scatter->rank_base + G > scatter->n || !scatter->ret || !scatter->counts ||
-        !scatter->soff || !scatter->roff || !scatter->ctrs || !scatter->ticket)
+    const bool packed = scatter->ginfo != nullptr;
+    const int ranks = packed ? (scatter->G > 0 ? G / scatter->G : 0) : G;
+    if (epilogue != 0 || scatter->n < 1 || scatter->n > SC_MAXN || ranks < 1 || ranks > SC_MAXN ||
+        scatter->rank_base < 0 || scatter->rank_base + ranks > scatter->n || !scatter->ret || !scatter->counts ||
+        !scatter->soff || !scatter->roff ||
+        (packed ? (cap != 0 || !m_start || G % scatter->G || !scatter->ybuf || scatter->ycap < 1)
+                : (m_start || cap <= 0 || !scatter->ctrs || !scatter->ticket)))
       return AURORA_EINVAL;
+    sc.ginfo = reinterpret_cast<const int4*>(scatter->ginfo);
+    sc.G = scatter->G;
+    sc.ybuf = reinterpret_cast<__nv_bfloat16*>(scatter->ybuf);
+    sc.ycap = scatter->ycap;
+    sc.to_ret = scatter->to_ret;
     sc.ret = reinterpret_cast<__nv_bfloat16* const*>(scatter->ret);
     sc.counts = scatter->counts;
     sc.soff = scatter->soff;

@@ -261,6 +261,9 @@ class AuroraMoELayer:
             self.blk_cnt_e = torch.zeros(self.T_local // 64, E, **i32)
             self.cnt_e2 = torch.zeros(2, n, E, **i32)   # tokens per (sender rank, expert), parity-buffered
             self.cnt_e = self.cnt_e2[0]
+            # per packed row {receiver-layout row, weight, single, 0} (grouped dispatch): rows with
+            # one local expert are finished in GEMM2's epilogue instead of the pre-reduction
+            self.ginfo = torch.zeros(self.max_entries, 4, **i32)
             self.h_g = torch.empty(self.max_entries, F, **bf)
             self.y_g = torch.empty(self.max_entries, H, **bf)
             self.overlap = False  # the local/network GEMM split assumes one expert per rank
@@ -332,6 +335,7 @@ class AuroraMoELayer:
             # grouped dispatch: every rank's rows go to its process's packed group buffer
             ag_p = peers["a_g"] if peers is not None else [self.a_g.data_ptr()] * self.n
             self.t_dst_g = self._ptr_table(ag_p)
+            self.t_ginfo = self._ptr_table(peers["ginfo"] if peers is not None else [self.ginfo.data_ptr()] * self.n)
             if peers is not None:
                 self.t_cnt_e2 = self._ptr_table(peers["cnt_e2"])
         self._src_tables = {}
@@ -455,7 +459,8 @@ class AuroraMoELayer:
             self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
             self.meta_bytes if plane2 else 0,
             ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
-            None if self.bw is None else self.bw.data_ptr(), stream), "aurora_engine")
+            None if self.bw is None else self.bw.data_ptr(), self.t_ginfo.data_ptr() if grouped else None, stream),
+            "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
         """``overlap_schedule``: launched right after :meth:`schedule` on the same
@@ -525,12 +530,17 @@ class AuroraMoELayer:
         cfg = self.cfg
         L, k, H = self.L, cfg.top_k, cfg.hidden
         E_loc = self.n_local * self.G
-        if self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack)
-            _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
-                                                  self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
-                                                  self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
-                                                  self.num_sms, stream), "aurora_expert_ffn_packed")
-            inv = None
+        skip = 0
+        if self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack);
+            # single-expert rows are finished (w * y -> sender or ybuf) in GEMM2's epilogue
+            _lib.check(L.aurora_expert_ffn_packed_scatter(
+                self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), self.h_g.data_ptr(),
+                self.y_g.data_ptr(), self.g_off.data_ptr(), self.g_rows.data_ptr(), E_loc, self.max_entries, H,
+                cfg.ffn, self.ginfo.data_ptr(), self.G, self.t_dst_c.data_ptr(), self.counts.data_ptr(),
+                self.soff.data_ptr(), self.roff.data_ptr(), self.n, self.rank_base, self.ybuf.data_ptr(), self.cap,
+                1 if fused else 0, 1 if self.n_local != self.n else 0, self.num_sms, stream),
+                "aurora_expert_ffn_packed_scatter")
+            inv, skip = None, 1
         else:
             self._sort_and_gather(stream)
             inv = self.inv.data_ptr()
@@ -540,11 +550,11 @@ class AuroraMoELayer:
                 self.rtot.data_ptr(), self.n_local, self.rank_base, k, H, self.ybuf.data_ptr(),
                 self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
                 self.n, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), 1 if self.n_local != self.n else 0,
-                stream), "aurora_expert_reduce_combine")
+                skip, stream), "aurora_expert_reduce_combine")
             return
         _lib.check(L.aurora_expert_reduce(self.y_g.data_ptr(), inv, self.meta_recv.data_ptr(),
                                           self.cap, self.meta_bytes, self.rtot.data_ptr(), self.n_local,
-                                          self.rank_base, k, H, self.ybuf.data_ptr(), stream),
+                                          self.rank_base, k, H, self.ybuf.data_ptr(), skip, stream),
                    "aurora_expert_reduce")
 
     def _sort_and_gather(self, stream: int) -> None:

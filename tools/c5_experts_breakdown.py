@@ -8,6 +8,7 @@ from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
 
 cfg = MoEConfig(hidden=5120, ffn=1536, experts=64, top_k=6, tokens=16384, ranks=8, skew=1.0, seed=0)
 layer = AuroraMoELayer(cfg)
+layer.grouped_dispatch = False  # this breakdown times the receive / sort / gather path
 x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
 s = _lib.stream_ptr()
 st = torch.cuda.current_stream()
@@ -38,7 +39,7 @@ for _ in range(R):
     ev[3].record(st)
     L.aurora_expert_reduce(layer.y_g.data_ptr(), layer.inv.data_ptr(), layer.meta_recv.data_ptr(), layer.cap,
                            layer.meta_bytes, layer.rtot.data_ptr(), layer.n_local, layer.rank_base, k, H,
-                           layer.ybuf.data_ptr(), s)
+                           layer.ybuf.data_ptr(), 0, s)
     ev[4].record(st)
     layer.combine(s); layer.aggregate(s)
     torch.cuda.synchronize()
