@@ -257,7 +257,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int t = 0;
       if (lane == 0) t = next_tile(local, false);
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (dyn && lane == 0) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tr_empty[local % TRING]), 0));
+      if (dyn && lane == 0)  // t is consumed (shuffled) above: the slot has been read
+        tc::mbar_arrive_cluster_relaxed(tc::mapa(tc::smem_u32(&tr_empty[local % TRING]), 0));
       if (t < 0) break;
       int g, mt, nt;
       tile_coords2(it, G, group_m, t, g, mt, nt);
@@ -342,8 +343,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
       }
+      // the accumulator may be overwritten once every tcgen05.ld of it has completed
+      // (tmem_ld_wait above); the epilogue's global stores need no ordering here
       tc::fence_before();
-      tc::mbar_arrive_cluster(tempty0 + acc * 8);
+      tc::mbar_arrive_cluster_relaxed(tempty0 + acc * 8);
     }
   }
   if (sc.n) {
