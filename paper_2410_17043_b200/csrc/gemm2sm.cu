@@ -27,7 +27,9 @@ constexpr int B_BYTES = HALF * BK * 2;           // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 32 KB per CTA
 constexpr int TMEM_COLS = 512;                   // 2 accumulators x 256 columns
 constexpr int MAX_GROUPS = 64;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int OUT_CHUNK = 32 * 32 * 2;              // epilogue staging: 32 rows x 32 columns bf16
+constexpr int OUT_BYTES = 4 * 2 * OUT_CHUNK;         // 4 epilogue warps x 2 buffers
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024 + OUT_BYTES;
 constexpr uint32_t IDESC = tc::idesc_bf16(BMP, BN);
 constexpr int SC_MAXN = 16;
 constexpr int TRING = 8;                         // tile-index ring (dynamic schedule)
@@ -95,7 +97,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             __nv_bfloat16* __restrict__ c, const int32_t* __restrict__ m_start,
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
                             int epilogue, int group_m, const Scatter sc,
-                            int32_t* __restrict__ tile_ctr) {
+                            int32_t* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_c,
+                            int tma_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -103,6 +106,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tempty + 2);
+  // epilogue staging for the TMA stores (1 KB-aligned, 64-byte swizzle)
+  uint8_t* out_stage = smem + STAGES * STAGE_BYTES + 1024;
   __shared__ TileIter2 it;
   // dynamic tile order (tile_ctr != NULL): the leader's producer takes the next
   // tile index from a global counter and publishes it to both CTAs' rings
@@ -252,6 +257,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   } else {  // ---------------- epilogue warps 2..5 (both CTAs)
     const int quarter = warp & 3;
     const uint32_t tempty0 = tc::mapa(tc::smem_u32(&tempty[0]), 0);
+    // Output of one 32-column chunk of the warp's 32 rows (lane = row, 64 B each). With
+    // tma_out and every row live: staged in shared memory (64-byte swizzle, two buffers)
+    // and written by one TMA store of the 32 x 32 box -- whole 64-byte row segments
+    // instead of 32 rows x 16 B per store instruction. Otherwise plain stores.
+    const uint32_t stage_w = tc::smem_u32(out_stage) + quarter * 2 * OUT_CHUNK;
+    int chunk_no = 0;
+    auto emit = [&](const uint32_t (&packed)[16], bool live, __nv_bfloat16* out_row, int col, long long row0) {
+      if (tma_out && __all_sync(0xffffffffu, live)) {
+        const uint32_t buf = stage_w + (chunk_no & 1) * OUT_CHUNK;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const uint32_t a = buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(packed[4 * q]),
+                       "r"(packed[4 * q + 1]), "r"(packed[4 * q + 2]), "r"(packed[4 * q + 3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&map_c)),
+              "r"(col), "r"((int)row0), "r"(buf)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        chunk_no++;
+      } else if (live) {
+        int4* o = reinterpret_cast<int4*>(out_row);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          o[q] = make_int4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+      }
+    };
     for (int local = 0;; local++) {
       // one reader arrival per epilogue warp: lane 0 after the warp has the index
       int t = 0;
@@ -269,6 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const bool live = row_in_group < it.rows[g];
       const long long row = g * cap + it.ms[g] + row_in_group;
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      const long long row0 = row - lane;  // the warp's first row
       if (epilogue == 1) {
         __nv_bfloat16* out = c + row * (long long)(N / 2) + nt * (BN / 2);
         for (int c0 = 0; c0 < BN / 2; c0 += 32) {
@@ -276,20 +318,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           TC_TMEM_LD32(tbase + c0, gr);
           TC_TMEM_LD32(tbase + BN / 2 + c0, ur);
           tc::tmem_ld_wait();
-          if (live) {
-            uint32_t packed[16];
+          uint32_t packed[16];
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
-              float a0 = silu_mul(__uint_as_float(gr[2 * q]), __uint_as_float(ur[2 * q]));
-              float a1 = silu_mul(__uint_as_float(gr[2 * q + 1]), __uint_as_float(ur[2 * q + 1]));
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
-              packed[q] = *reinterpret_cast<uint32_t*>(&h2);
-            }
-            int4* o = reinterpret_cast<int4*>(out + c0);
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-              o[q] = make_int4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          for (int q = 0; q < 16; q++) {
+            float a0 = silu_mul(__uint_as_float(gr[2 * q]), __uint_as_float(ur[2 * q]));
+            float a1 = silu_mul(__uint_as_float(gr[2 * q + 1]), __uint_as_float(ur[2 * q + 1]));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(a0, a1);
+            packed[q] = *reinterpret_cast<uint32_t*>(&h2);
           }
+          emit(packed, live, out + c0, nt * (BN / 2) + c0, row0);
         }
       } else {
         __nv_bfloat16* out = c + row * (long long)N + nt * BN;
@@ -325,22 +362,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           uint32_t r[32];
           TC_TMEM_LD32(tbase + c0, r);
           tc::tmem_ld_wait();
-          if (live) {
-            uint32_t packed[16];
+          uint32_t packed[16];
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
-              if (weighted) {  // the pre-reduction's arithmetic: fmaf(w, bf16(y), 0) in fp32, then bf16
-                const float2 f = __bfloat1622float2(h2);
-                h2 = __floats2bfloat162_rn(fmaf(wsc, f.x, 0.0f), fmaf(wsc, f.y, 0.0f));
-              }
-              packed[q] = *reinterpret_cast<uint32_t*>(&h2);
+          for (int q = 0; q < 16; q++) {
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+            if (weighted) {  // the pre-reduction's arithmetic: fmaf(w, bf16(y), 0) in fp32, then bf16
+              const float2 f = __bfloat1622float2(h2);
+              h2 = __floats2bfloat162_rn(fmaf(wsc, f.x, 0.0f), fmaf(wsc, f.y, 0.0f));
             }
-            int4* o = reinterpret_cast<int4*>(out + c0);
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-              o[q] = make_int4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            packed[q] = *reinterpret_cast<uint32_t*>(&h2);
           }
+          emit(packed, live, out + c0, nt * BN + c0, row0);
         }
       }
       // the accumulator may be overwritten once every tcgen05.ld of it has completed
@@ -348,6 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc::fence_before();
       tc::mbar_arrive_cluster_relaxed(tempty0 + acc * 8);
     }
+    if (tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   if (sc.n) {
     if (sc.sys) __threadfence_system();
@@ -426,6 +459,26 @@ int32_t* tile_counter_for(cudaStream_t stream) {
   return p;
 }
 
+// output map for the epilogue's TMA stores: 32 x 32 boxes, 64-byte swizzle
+bool make_map_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 // C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
@@ -463,10 +516,16 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
     return AURORA_EINVAL;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   if (!make_map_2d(&ma, a, (uint64_t)map_rows, K, HALF) ||
       !make_map_2d(&mb, b, (uint64_t)G * N, K, HALF))
     return AURORA_ECUDA;
+  // TMA-stored epilogue for plain outputs (rows go where the tile is); scattered
+  // outputs (fused combine, packed scatter) keep per-row stores
+  static const bool tma_env = !getenv("AURORA_GEMM_TMA_STORE") || atoi(getenv("AURORA_GEMM_TMA_STORE")) != 0;
+  const int n_out = epilogue == 1 ? N / 2 : N;
+  const int tma_out = (tma_env && !scatter) ? 1 : 0;
+  if (!make_map_out(&mc, c, (uint64_t)map_rows, (uint64_t)n_out)) return AURORA_ECUDA;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -493,7 +552,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   }
   const int grid = num_sms & ~1;
   grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr);
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

@@ -211,6 +211,9 @@ class AuroraMoELayer:
         # several experts per rank: dispatch rows straight into the packed per-expert groups
         # (engine mode bit 8; AURORA_GROUPED_DISPATCH=0: receive, sort, gather)
         self.grouped_dispatch = os.environ.get("AURORA_GROUPED_DISPATCH", "1") != "0"
+        # grouped: finish single-expert rows in GEMM2's epilogue (per-row scattered stores)
+        # instead of TMA-storing every row for the pre-reduction (AURORA_PACKED_SCATTER=0)
+        self.packed_scatter = os.environ.get("AURORA_PACKED_SCATTER", "1") != "0"
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
@@ -531,7 +534,13 @@ class AuroraMoELayer:
         L, k, H = self.L, cfg.top_k, cfg.hidden
         E_loc = self.n_local * self.G
         skip = 0
-        if self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack);
+        if self.grouped and not self.packed_scatter:
+            _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+                                                  self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
+                                                  self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
+                                                  self.num_sms, stream), "aurora_expert_ffn_packed")
+            inv = None
+        elif self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack);
             # single-expert rows are finished (w * y -> sender or ybuf) in GEMM2's epilogue
             _lib.check(L.aurora_expert_ffn_packed_scatter(
                 self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), self.h_g.data_ptr(),
