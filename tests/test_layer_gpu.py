@@ -465,3 +465,27 @@ def test_router_ties_pick_lower_index(torch, experts, top_k):
     assert np.array_equal(got, idx)
     assert (got[:, 0] % 2 == 0).all()  # the first choice is always the lower twin
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-6)
+
+
+@pytest.mark.parametrize("experts,top_k", [(8, 2), (32, 4)])
+def test_layer_cuda_graph_replay(torch, experts, top_k):
+    """The whole forward captured as one CUDA graph: replays with new inputs
+    written into the captured buffer match the eager forward bit for bit (the
+    kernels read counts, schedule and group sizes from device memory)."""
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=256, experts=experts, top_k=top_k, tokens=4096, ranks=8, skew=1.0, seed=21)
+    layer = AuroraMoELayer(cfg)
+    xs = [torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    refs = [layer(x).clone() for x in xs]
+    torch.cuda.synchronize()
+    xbuf = xs[0].clone()
+    obuf = torch.empty_like(xbuf)
+    g, y = layer.capture(xbuf, obuf)
+    for rep in range(2):
+        for x, ref in zip(xs, refs):
+            xbuf.copy_(x)
+            g.replay()
+            torch.cuda.synchronize()
+            layer.check_status()
+            assert torch.equal(y, ref), rep
+    assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
