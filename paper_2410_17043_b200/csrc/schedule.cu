@@ -204,6 +204,7 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 
 #include "fastmatch.cuh"
 #include "fastmatch8b.cuh"
+#include "fastmatch16.cuh"
 #include "apportion.cuh"
 
 // Value domain of the fast path. Homogeneous integer traffic (the in-layer
@@ -554,6 +555,36 @@ __device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V>
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (!ok) { status = AURORA_ENOMATCH; break; }
       pj = on ? (int)(((lane < 4 ? mlo : mhi) >> (8 * (lane & 3))) & 15u) : 0;
+    } else if constexpr (NB == 16) {
+      // rows -> lane 0 as 16-bit lanes of eight words (warp OR-reductions: word k
+      // holds rows 2k, 2k+1), the matching back as nibbles of two words
+      uint32_t pw[8], sw[8];
+      const uint32_t sh = 16u * (lane & 1);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        pw[k] = __reduce_or_sync(0xffffffffu, (on && (lane >> 1) == k) ? pref << sh : 0u);
+        sw[k] = __reduce_or_sync(0xffffffffu, (on && (lane >> 1) == k) ? sup << sh : 0u);
+      }
+      uint32_t mlo = 0, mhi = 0, ok = 0;
+      if (lane == 0) {
+        FastMatch16 f;
+        f.P.w0 = ((uint64_t)pw[1] << 32) | pw[0];
+        f.P.w1 = ((uint64_t)pw[3] << 32) | pw[2];
+        f.P.w2 = ((uint64_t)pw[5] << 32) | pw[4];
+        f.P.w3 = ((uint64_t)pw[7] << 32) | pw[6];
+        f.S.w0 = ((uint64_t)sw[1] << 32) | sw[0];
+        f.S.w1 = ((uint64_t)sw[3] << 32) | sw[2];
+        f.S.w2 = ((uint64_t)sw[5] << 32) | sw[4];
+        f.S.w3 = ((uint64_t)sw[7] << 32) | sw[6];
+        ok = f.run(n) ? 1u : 0u;
+        mlo = (uint32_t)f.ML;
+        mhi = (uint32_t)(f.ML >> 32);
+      }
+      mlo = __shfl_sync(0xffffffffu, mlo, 0);
+      mhi = __shfl_sync(0xffffffffu, mhi, 0);
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) { status = AURORA_ENOMATCH; break; }
+      pj = on ? (int)(((lane < 8 ? mlo : mhi) >> (4 * (lane & 7))) & 15u) : 0;
     } else {
       if (on) { pref_s[lane] = pref; sup_s[lane] = sup; }
       __syncwarp();

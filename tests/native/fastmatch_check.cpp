@@ -6,6 +6,7 @@
 
 #include "../../paper_2410_17043_b200/csrc/fastmatch.cuh"
 #include "../../paper_2410_17043_b200/csrc/fastmatch8b.cuh"
+#include "../../paper_2410_17043_b200/csrc/fastmatch16.cuh"
 
 extern "C" int oracle_perfect_matching_masks(int n, const uint32_t* sup, const uint32_t* pref, int* perm);
 
@@ -90,9 +91,44 @@ static int check8(std::mt19937& rng, int iters) {
   return bad;
 }
 
+// the n <= 16 K2 matcher (16-bit lanes, shift-register stacks)
+static int check16(std::mt19937& rng, int iters) {
+  int bad = 0;
+  for (int it = 0; it < iters; it++) {
+    const int n = 1 + (int)(rng() % 16);
+    uint32_t sup[32], pref[32];
+    const double ps = 0.2 + 0.8 * (rng() % 1000) / 1000.0, pp = (rng() % 1000) / 1000.0;
+    for (int i = 0; i < n; i++) {
+      sup[i] = pref[i] = 0;
+      for (int j = 0; j < n; j++)
+        if ((rng() % 1000) / 1000.0 < ps) {
+          sup[i] |= 1u << j;
+          if ((rng() % 1000) / 1000.0 < pp) pref[i] |= 1u << j;
+        }
+    }
+    if (it % 3 == 0)
+      for (int i = 0; i < n; i++) sup[i] |= 1u << ((i + it) % n);
+    int ref[32];
+    const int ok_ref = oracle_perfect_matching_masks(n, sup, pref, ref);
+    FastMatch16 f;
+    f.P.clear();
+    f.S.clear();
+    for (int u = 0; u < n; u++) {
+      FastMatch16::set_lane(f.P, (uint32_t)u, pref[u]);
+      FastMatch16::set_lane(f.S, (uint32_t)u, sup[u]);
+    }
+    const bool ok = f.run(n);
+    bool same = ok == (bool)ok_ref;
+    if (same && ok)
+      for (int u = 0; u < n; u++) same &= (int)FastMatch16::nib(f.ML, u) == ref[u];
+    if (!same && bad++ < 5) std::printf("mismatch FastMatch16 n=%d ok=%d/%d\n", n, (int)ok, ok_ref);
+  }
+  return bad;
+}
+
 int main() {
   std::mt19937 rng(12345);
-  int bad = check<8>(rng, 200000) + check<16>(rng, 100000) + check8(rng, 300000);
+  int bad = check<8>(rng, 200000) + check<16>(rng, 100000) + check8(rng, 300000) + check16(rng, 300000);
   std::printf("fastmatch mismatches: %d\n", bad);
   return bad != 0;
 }
