@@ -475,9 +475,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
+    # AURORA_BENCH_SAME_GPU=1 (testing the multi-process path on a one-GPU box): every rank on
+    # cuda:0, gloo for the host-side collectives (NCCL refuses two ranks on one device); the
+    # data path is the same peer-memory engine over CUDA IPC
+    same_gpu = os.environ.get("AURORA_BENCH_SAME_GPU", "0") == "1"
+    torch.cuda.set_device(0 if same_gpu else local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n = args.ranks
     if n % world:
         raise SystemExit(f"{n} ranks do not split over {world} GPUs")
