@@ -418,7 +418,7 @@ def test_two_rank_groups_in_one_context(torch, experts, top_k, fused):
             fn(h, s)
         torch.cuda.synchronize()
 
-    for _ in range(2):  # twice: counters must be rearmed across calls
+    for _ in range(3):  # counters rearmed, counts buffers alternating (step parity) across calls
         both(lambda h, s: h.route(h.x, s))
         both(lambda h, s: h.exchange_counts(s))  # peer stores + flags, concurrently on both streams
         assert torch.equal(halves[0].counts, halves[1].counts)
