@@ -447,7 +447,7 @@ def run_c3(args):
                            "model_b": {"experts": 2 * n, "top_k": 2, "hidden": 4096, "ffn": 7168, "skew": 1.5}},
             "roofline": {"bound": "tensor", "achieved": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                          "note": "both models' expert FLOPs over the whole step (upper bound on the GEMM time)"},
-            "gpu_launches": 8 + 13,
+            "gpu_launches": (pair.a.kernels_per_step() + pair.b.kernels_per_step()) * args.steps,
             "e2e": {"value": tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int((xah[0].numel() + xbh[0].numel()) * 2),
                     "d2h_bytes_per_step": int((oah[0].numel() + obh[0].numel()) * 2), "ms_per_step": e2e_ms,
@@ -758,7 +758,7 @@ def main():
                      "flops_per_step": gemm_flops},
         # route, pack, K2, engine, 2 GEMM, engine, aggregate (+ sort x3, gather, reduce with G > 1;
         # + local engine / GEMM pair when overlapped)
-        "gpu_launches": (8 + (5 if layer.G > 1 else 0) + (3 if layer.overlap else 0)) * args.steps,
+        "gpu_launches": layer.kernels_per_step() * args.steps,
         "e2e": {"value": cfg.tokens / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": int(xh[0].numel() * 2), "d2h_bytes_per_step": int(outh[0].numel() * 2),
                 "ms_per_step": e2e_ms, "path": "AuroraMoELayer.__call__ on pinned host buffers",

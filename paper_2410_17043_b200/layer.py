@@ -705,6 +705,21 @@ class AuroraMoELayer:
 
     __call__ = forward
 
+    def kernels_per_step(self) -> int:
+        """Launches of this library's kernels in one forward (bench's gpu_launches)."""
+        n = 2 if self.logits is not None else 1          # router (+ top-k tail when E > 8)
+        n += 1 if self.grouped else 0                      # per-expert histogram
+        n += 3                                             # pack, K2, dispatch engine
+        if self.overlap:
+            n += 3                                         # local dispatch + local GEMMs split off
+        if self.G == 1:
+            n += 2                                         # GEMM1 (+SwiGLU), GEMM2
+        else:
+            n += (0 if self.grouped else 4) + 2 + 1        # [sort x3, gather], GEMMs, pre-reduction
+        n += 1                                             # combine engine or the fused combine's wait
+        n += 1                                             # aggregate
+        return n
+
     def capture(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, warmup: int = 2):
         """CUDA graph of one forward on these exact input / output buffers (serving
         loops with fixed buffers: one graph launch instead of ~15 kernel launches
