@@ -79,3 +79,11 @@ def test_expert_ffn_matches_fp32(env):
         got = y[gi * cap: gi * cap + m_rows[gi]].float()
         err = (got - ref).abs().max().item()
         assert err <= 2e-2 * ref.abs().max().item() + 1e-2, (gi, err)
+
+
+@pytest.mark.parametrize("epilogue", [0, 1])
+def test_grouped_gemm_half_tile_boundaries(env, epilogue):
+    """Group tails of exactly 128 / 129 / 64 / 1 rows next to full tiles (the
+    epilogue masks the padding rows of every partial 256-row tile)."""
+    torch, L, _lib = env
+    _run(torch, L, _lib, G=5, cap=512, m_rows=[128, 384, 385, 64, 257], N=768, K=512, epilogue=epilogue, seed=3)
