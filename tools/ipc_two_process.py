@@ -40,7 +40,9 @@ def worker(rank, world, port, q, stream_schedule):
         torch.cuda.synchronize()
         layer.check_status()
     assert torch.equal(outs[0], outs[1])
-    q.put((rank, outs[1].cpu(), time.time() - t0))
+    # by value (numpy bytes): a shared-memory tensor handle would need this process alive
+    # until the parent has opened it
+    q.put((rank, outs[1].cpu().view(torch.int16).numpy().tobytes(), time.time() - t0))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -63,7 +65,10 @@ if __name__ == "__main__":
         res = dict((r, (o, t)) for r, o, t in (q.get(timeout=300) for _ in range(2)))
         for p_ in ps:
             p_.join(timeout=60)
-        out = torch.cat([res[0][0], res[1][0]])
+        import numpy as np
+        half = [torch.from_numpy(np.frombuffer(res[r][0], dtype=np.int16).copy()).view(torch.bfloat16)
+                .view(cfg.tokens // 2, cfg.hidden) for r in (0, 1)]
+        out = torch.cat(half)
         same = torch.equal(out, ref)
         ok &= same
         print(f"two processes via CUDA IPC (K2 {'overlapped' if stream_schedule else 'serial'}, E={cfg.experts}): "
