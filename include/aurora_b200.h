@@ -167,7 +167,12 @@ int aurora_pack_grouped(const int32_t* slot_dst, const int32_t* blk_cnt, const i
                         int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc, int32_t* rrem,
                         const int32_t* topk_idx, const float* topk_w, const int32_t* local_of_expert, void* meta,
                         const int32_t* blk_cnt_e, const int32_t* cnt_e, const int32_t* gpu_of_expert, int E,
-                        int G, int n_local, int32_t* g_off, int32_t* g_rows, void* stream);
+                        int G, int n_local, int32_t* g_off, int32_t* g_rows, void* const* ginfo_bufs,
+                        void* stream);
+/* ginfo_bufs (nullable): per rank the base of its process's [rows] int4 array; every row
+ * position also gets {receiver-layout row, gate weight bits, single (the token's only
+ * expert on that rank), 0} (aurora_expert_ffn_packed_scatter). Peer stores: the
+ * receiver reads them after its dispatch completes (the senders' done signals follow). */
 int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* counts, int T,
                 int k, int n, int rank_base, int tokens_per_rank, int32_t* send_list,
                 int32_t* pos, int32_t* soff, int32_t* roff, int32_t* rtot, int32_t* rloc,
@@ -188,7 +193,8 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * once (the unscheduled all-pairs-concurrent all-to-all);
  * mode bit 8 (dispatch, TMA engine, meta plane required): grouped placement -- dst_bufs[j]
  * is the base of rank j's process's packed group buffer and every row is stored at
- * the positions in its meta record (aurora_pack_grouped), one store per local expert;
+ * the positions in its meta record (aurora_pack_grouped), one store per local expert
+ * (ginfo_bufs below: optional, the records can come from aurora_pack_grouped instead);
  * mode bit 5: launch as a programmatic dependent (PDL) of the immediately
  * preceding aurora_schedule_counts on the same stream -- the engine starts
  * while K2 runs (K2 triggers its dependents on entry, so it is resident first)

@@ -43,7 +43,7 @@ _SIGNATURES = {
     "aurora_exchange_counts": [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp, _vp],
     "aurora_expert_hist": [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp],
     "aurora_pack_grouped": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
+                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
     "aurora_combine_wait": [_vp, _c_int, _c_int, _c_int, _c_int, _c_i64, _vp, _vp],
     "aurora_expert_ffn_packed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp],
     "aurora_expert_sort": [_vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,

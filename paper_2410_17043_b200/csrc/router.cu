@@ -424,6 +424,7 @@ struct GroupedArgs {
   int E, G, n_local;              // experts, experts per rank, ranks per process (uniform)
   int32_t* g_off;                 // [n_local * G + 1] this process's packed group offsets
   int32_t* g_rows;                // [n_local * G]
+  int4* const* ginfo;             // [n] per rank: its process's {recv row, weight, single, 0} per packed row (nullable)
 };
 
 template <bool GROUPED>
@@ -440,6 +441,7 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
   __shared__ int warp0_s[AUR_MAXN];  // entries of warp 0 per destination
   __shared__ int gbase_s[GROUPED ? MAXE : 1];                 // grouped position of this tile's first row per expert
   __shared__ unsigned long long tmask_s[GROUPED ? MAXE : 1];  // tokens of the tile choosing each expert
+  __shared__ int roffi_s[GROUPED ? AUR_MAXN : 1];               // roff[i][j] of this tile's sender i
   const int tl = threadIdx.x, warp = tl >> 5, lane = tl & 31;
   const int t0 = blockIdx.x * TILE, t = t0 + tl;
   if (blockIdx.x == 0 && tl < n) {  // buffer layout of every rank (thread tl: sender row / receiver column tl)
@@ -471,6 +473,16 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
   }
   if (GROUPED) {
     const int E = ga.E;
+    if (tl < n) {  // receiver j = tl: local rows first, then the other senders in index order
+      const int j = tl;
+      int ro = 0;
+      if (i != j) {
+        ro = counts[j * n + j];
+        for (int i2 = 0; i2 < i; i2++)
+          if (i2 != j) ro += counts[i2 * n + j];
+      }
+      roffi_s[j] = ro;
+    }
     __shared__ int rows_s[MAXE], key_s[MAXE];
     int rows_e = 0, earlier_senders = 0, key = 0, proc = 0;
     if (tl < E) {  // expert tl: rows of its group (all senders), rows from senders before i
@@ -539,6 +551,8 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
                      // row's position in that expert's group), gate weight} or {-1, 0}
           int2* m = reinterpret_cast<int2*>(meta + ((size_t)i_local * tokens_per_rank * k +
                                                     soff_s[j] + p) * meta_bytes);
+          int nhere = 0;
+          for (int q = 0; q < k; q++) nhere += full[q] == j;
           for (int q = 0; q < k; q++) {
             const bool here = full[q] == j;
             const int eg = topk_idx[(size_t)t * k + q];
@@ -549,7 +563,10 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
               else
                 e = local_of_expert[eg];
             }
-            m[q] = make_int2(e, here ? __float_as_int(topk_w[(size_t)t * k + q]) : 0);
+            const int wb = here ? __float_as_int(topk_w[(size_t)t * k + q]) : 0;
+            m[q] = make_int2(e, wb);
+            // grouped: the receiver's per-position record for GEMM2's single-row epilogue
+            if (GROUPED && here && ga.ginfo) ga.ginfo[j][e] = make_int4(roffi_s[j] + p, wb, nhere == 1 ? 1 : 0, 0);
           }
           if (GROUPED)  // padding records: no position (the engine reads meta_bytes / 8 records)
             for (int q = k; q < meta_bytes / 8; q++) m[q] = make_int2(-1, 0);
@@ -647,13 +664,15 @@ extern "C" int aurora_pack_grouped(const int32_t* slot_dst, const int32_t* blk_c
                                    const int32_t* topk_idx, const float* topk_w,
                                    const int32_t* local_of_expert, void* meta,
                                    const int32_t* blk_cnt_e, const int32_t* cnt_e, const int32_t* gpu_of_expert,
-                                   int E, int G, int n_local, int32_t* g_off, int32_t* g_rows, void* stream) {
+                                   int E, int G, int n_local, int32_t* g_off, int32_t* g_rows,
+                                   void* const* ginfo_bufs, void* stream) {
   if (T <= 0 || k < 1 || k > MAXK || n < 1 || n > AUR_MAXN || tokens_per_rank % TILE ||
       T % tokens_per_rank || !soff || !roff || !rtot || !rloc || !rrem || !meta || !blk_cnt_e || !cnt_e ||
       !gpu_of_expert || !local_of_expert || !g_off || !g_rows || E < 1 || E > MAXE || G < 1 || n_local < 1 ||
       n % n_local || rank_base % n_local || E != n * G)
     return AURORA_EINVAL;
-  const GroupedArgs ga{blk_cnt_e, cnt_e, gpu_of_expert, E, G, n_local, g_off, g_rows};
+  const GroupedArgs ga{blk_cnt_e, cnt_e, gpu_of_expert, E, G, n_local, g_off, g_rows,
+                       reinterpret_cast<int4* const*>(ginfo_bufs)};
   pack_kernel<true><<<T / TILE, TILE, 0, (cudaStream_t)stream>>>(
       slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
       rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16, ga);

@@ -433,7 +433,8 @@ class AuroraMoELayer:
                 self.rrem.data_ptr(), self.topk_idx.data_ptr(), self.topk_w.data_ptr(),
                 self.local_of_expert.data_ptr(), self.meta_send.data_ptr(), self.blk_cnt_e.data_ptr(),
                 self.cnt_e.data_ptr(), self.gpu_of_expert.data_ptr(), cfg.experts, self.G, self.n_local,
-                self.g_off.data_ptr(), self.g_rows.data_ptr(), stream), "aurora_pack_grouped")
+                self.g_off.data_ptr(), self.g_rows.data_ptr(), self.t_ginfo.data_ptr(), stream),
+                "aurora_pack_grouped")
             return
         _lib.check(self.L.aurora_pack(self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(), self.counts.data_ptr(),
                                       self.T_local, cfg.top_k, self.n, self.rank_base, cfg.tokens_per_rank,
@@ -462,7 +463,7 @@ class AuroraMoELayer:
             self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
             self.meta_bytes if plane2 else 0,
             ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
-            None if self.bw is None else self.bw.data_ptr(), self.t_ginfo.data_ptr() if grouped else None, stream),
+            None if self.bw is None else self.bw.data_ptr(), None, stream),
             "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
