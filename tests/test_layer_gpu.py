@@ -241,12 +241,14 @@ def test_fused_and_engine_combine_agree_several_experts(torch):
     x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
     layer.fused_combine, layer.grouped_dispatch = False, False
     ref = layer(x).clone()
-    for fused, grouped in ((True, True), (False, True), (True, False), (False, False), (True, True)):
-        layer.fused_combine, layer.grouped_dispatch = fused, grouped
+    for fused, grouped, lsu in ((True, True, 0), (False, True, 0), (True, False, 0), (False, False, 0),
+                                (True, True, 64), (True, True, 0)):
+        # (the LSU copy engine has no grouped mode: it falls back to receive / sort / gather)
+        layer.fused_combine, layer.grouped_dispatch, layer.engine_lsu = fused, grouped, lsu
         out = layer(x)
         torch.cuda.synchronize()
         layer.check_status()
-        assert torch.equal(out, ref), (fused, grouped)
+        assert torch.equal(out, ref), (fused, grouped, lsu)
     assert int(layer.ctr_c.abs().sum()) == 0 and int(layer.gemm_ticket.item()) == 0
 
 
