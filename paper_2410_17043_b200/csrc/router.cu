@@ -156,13 +156,14 @@ __global__ void prepare_gate_kernel(const __nv_bfloat16* __restrict__ w, int E, 
 // one 256-h chunk of the warp's 8 tokens x 8 experts: fp32x2 FMAs (FFMA2) over
 // expert pairs, x broadcast into both halves; per (token, expert) the same
 // sequential fmaf chain over h = 256 i + 8 l + jj as the scalar definition
+template <int XB = XBYTES>
 __device__ __forceinline__ void gate_chunk(float2 (&acc)[8][REP / 2], uint32_t stage_u, int warp, int lane) {
   float2 wp[REP / 2][8];
 #pragma unroll
   for (int p = 0; p < REP / 2; p++)
 #pragma unroll
     for (int jp = 0; jp < 4; jp++) {
-      const int4 v = lds128(stage_u + XBYTES + ((p * 4 + jp) * 32 + lane) * 16);
+      const int4 v = lds128(stage_u + XB + ((p * 4 + jp) * 32 + lane) * 16);
       wp[p][2 * jp] = make_float2(__int_as_float(v.x), __int_as_float(v.y));
       wp[p][2 * jp + 1] = make_float2(__int_as_float(v.z), __int_as_float(v.w));
     }
@@ -208,11 +209,12 @@ __device__ __forceinline__ float gate_reduce(const float2 (&acc)[8][REP / 2], in
   return v[0];
 }
 
+template <int NS = XS, int NW = WARPS>
 __device__ __forceinline__ void init_ring(uint64_t* full, uint64_t* empty) {
   if (threadIdx.x == 0) {
-    for (int q = 0; q < XS; q++) {
+    for (int q = 0; q < NS; q++) {
       tc::mbar_init(&full[q], 1);
-      tc::mbar_init(&empty[q], WARPS);
+      tc::mbar_init(&empty[q], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -283,47 +285,52 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
 // 1.7 waves). The x / gate stages stream through one TMA ring across units;
 // each unit stores its 64 x 8 logits (+ bias) and route_tail_kernel finishes
 // every tile. Same per-lane order and xor tree as route_tma_kernel: same bits.
-__global__ void __launch_bounds__(WARPS * 32, 1) route_units_kernel(
+// NW warps x 8 tokens per unit, NS stages. 16 warps (four per scheduler: the FFMA2
+// chains need more than two warps to keep the FMA pipe busy) with two stages beat
+// 12 x 3 and 8 x 4 (C5: 247 / 258 / 277 us)
+template <int NW, int NS>
+__global__ void __launch_bounds__(NW * 32, 1) route_units_kernel(
     const __grid_constant__ CUtensorMap xmap, const float* __restrict__ wperm,
     const float* __restrict__ bias, int T, int H, int E, float* __restrict__ logits) {
   extern __shared__ __align__(1024) uint8_t xs_raw[];
   uint8_t* xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(xs_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[XS], empty[XS];
+  constexpr int UT = NW * 8, UXB = UT * 512, UCH = UXB + WBYTES;  // unit tokens, x bytes, stage bytes
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t xs_u = tc::smem_u32(xs);
-  const int h_chunks = H / 256, passes = (E + REP - 1) / REP, tiles = (T + TILE - 1) / TILE;
+  const int h_chunks = H / 256, passes = (E + REP - 1) / REP, tiles = (T + UT - 1) / UT;
   const int units = tiles * passes;
   const int my_units = units > (int)blockIdx.x ? (units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int total = my_units * h_chunks;
-  init_ring(full, empty);
+  init_ring<NS, NW>(full, empty);
   __syncthreads();
   // stage q: chunk q % h_chunks of this CTA's unit q / h_chunks (unit u = tile * passes + pass)
   auto fill = [&](int q, int st) {
     const int u = (int)blockIdx.x + (q / h_chunks) * (int)gridDim.x, c = q % h_chunks;
-    tc::mbar_expect_tx(&full[st], XCHUNK);
-    tma_load_2d(xs + st * XCHUNK, &xmap, &full[st], 256 * c, (u / passes) * TILE);
-    bulk_load(xs + st * XCHUNK + XBYTES, wperm + ((size_t)(u % passes) * h_chunks + c) * 2048, WBYTES, &full[st]);
+    tc::mbar_expect_tx(&full[st], UCH);
+    tma_load_2d(xs + st * UCH, &xmap, &full[st], 256 * c, (u / passes) * UT);
+    bulk_load(xs + st * UCH + UXB, wperm + ((size_t)(u % passes) * h_chunks + c) * 2048, WBYTES, &full[st]);
   };
   if (tid == 0)
-    for (int q = 0; q < XS && q < total; q++) fill(q, q);
+    for (int q = 0; q < NS && q < total; q++) fill(q, q);
   for (int ui = 0; ui < my_units; ui++) {
     const int u = (int)blockIdx.x + ui * (int)gridDim.x;
-    const int t0 = (u / passes) * TILE, e0 = (u % passes) * REP;
+    const int t0 = (u / passes) * UT, e0 = (u % passes) * REP;
     float2 acc[8][REP / 2];
 #pragma unroll
     for (int t = 0; t < 8; t++)
 #pragma unroll
       for (int p = 0; p < REP / 2; p++) acc[t][p] = make_float2(0.0f, 0.0f);
     for (int i = 0; i < h_chunks; i++) {
-      const int q = ui * h_chunks + i, s = q % XS;
-      const uint32_t ph = (uint32_t)(q / XS) & 1u;
+      const int q = ui * h_chunks + i, s = q % NS;
+      const uint32_t ph = (uint32_t)(q / NS) & 1u;
       tc::mbar_wait(&full[s], ph);
-      gate_chunk(acc, xs_u + s * XCHUNK, warp, lane);
+      gate_chunk<UXB>(acc, xs_u + s * UCH, warp, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[s]);
-      if (tid == 0 && q + XS < total) {
+      if (tid == 0 && q + NS < total) {
         tc::mbar_wait(&empty[s], ph);
-        fill(q + XS, s);
+        fill(q + NS, s);
       }
     }
 #pragma unroll
@@ -604,10 +611,13 @@ extern "C" int aurora_route(const void* x, const float* gate_prep, const float* 
   CUtensorMap xmap;
   if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H)) return AURORA_ECUDA;
   constexpr int dyn = XS * XCHUNK + 1024;
+  constexpr int UNW = 16, UNS = 2;  // balanced units: 16 warps x 8 tokens, 2 stages
+  constexpr int udyn = UNS * (UNW * 8 * 512 + WBYTES) + 1024;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(route_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess ||
-        cudaFuncSetAttribute(route_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) != cudaSuccess)
+        cudaFuncSetAttribute(route_units_kernel<UNW, UNS>, cudaFuncAttributeMaxDynamicSharedMemorySize, udyn) !=
+            cudaSuccess)
       return AURORA_ECUDA;
     attr = true;
   }
@@ -615,8 +625,11 @@ extern "C" int aurora_route(const void* x, const float* gate_prep, const float* 
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int units = blocks * ((E + REP - 1) / REP);
-    route_units_kernel<<<units < sms ? units : sms, WARPS * 32, dyn, s>>>(xmap, gate_prep, bias, T, H, E, logits);
+    CUtensorMap umap;
+    if (!make_x_map(&umap, x, (uint64_t)T, (uint64_t)H, UNW * 8)) return AURORA_ECUDA;
+    const int units = ((T + UNW * 8 - 1) / (UNW * 8)) * ((E + REP - 1) / REP);
+    route_units_kernel<UNW, UNS><<<units < sms ? units : sms, UNW * 32, udyn, s>>>(umap, gate_prep, bias, T, H, E,
+                                                                                   logits);
     route_tail_kernel<<<blocks, WARPS * 32, 0, s>>>(logits, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank,
                                                      topk_idx, topk_w, slot_dst, blk_cnt, counts);
     AUR_CHECK_LAUNCH();
