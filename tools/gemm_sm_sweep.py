@@ -1,6 +1,7 @@
 """Expert GEMM time vs the number of SMs it may use (C2 GEMM1 shape): what reserving SMs for
 overlapped work (C3 interleaving) would cost. Usage: python tools/gemm_sm_sweep.py"""
-sys.path.insert(0, os.getcwd())
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2410_17043_b200 import _lib
 L = _lib.load()
