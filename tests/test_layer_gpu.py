@@ -342,6 +342,8 @@ def test_engine_runs_baseline_schedules(torch):
     dict(experts=16, top_k=2, ranks=16, tokens=4096),        # the most ranks (K2's n <= 16 kernel)
     dict(experts=64, top_k=6, ranks=16, tokens=4096),        # 16 ranks x 4 experts, C5 routing
     dict(experts=8, top_k=1, ranks=8, tokens=2048, skew=60.0),  # one hot expert, most ranks idle
+    dict(experts=16, top_k=3, ranks=8, tokens=512),          # 64 tokens per rank: one router tile, partial units
+    dict(experts=40, top_k=5, ranks=8, tokens=1536),         # E = 5 x 8: a partial 8-expert pass
 ])
 def test_layer_edge_shapes(torch, shape):
     from paper_2410_17043_b200.layer import MoEConfig
