@@ -214,6 +214,9 @@ class AuroraMoELayer:
         # grouped: finish single-expert rows in GEMM2's epilogue (per-row scattered stores)
         # instead of TMA-storing every row for the pre-reduction (AURORA_PACKED_SCATTER=0)
         self.packed_scatter = os.environ.get("AURORA_PACKED_SCATTER", "1") != "0"
+        if os.environ.get("AURORA_GEMM") == "1sm":  # the single-CTA GEMM (ablation) has no scatter epilogue
+            self.fused_combine = False
+            self.packed_scatter = False
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
