@@ -707,7 +707,7 @@ def main():
     off = counts.copy()
     np.fill_diagonal(off, 0)
     bw_arr = np.asarray(bws if bws is not None else [1.0] * n, dtype=float)
-    tmat = off / np.minimum.outer(bw_arr, bw_arr)  # time_normalize (commsched.py:338-347); B = 1 <-> 900 GB/s
+    tmat = off / np.minimum.outer(bw_arr, bw_arr)  # time_normalize (commsched.py:181-190); B = 1 <-> 900 GB/s
     bmax_tokens = int(max(off.sum(axis=1).max(), off.sum(axis=0).max()))
     bmax_time = float(max(tmat.sum(axis=1).max(), tmat.sum(axis=0).max()))
     row_bytes = cfg.hidden * 2
@@ -761,7 +761,7 @@ def main():
             # 900 GB/s per direction per GPU the bound assumes
             "bottleneck_gbs_dispatch": bmax_tokens * row_bytes / (stage_ms["dispatch"] * 1e-3) / 1e9,
             "bottleneck_gbs_combine": bmax_tokens * row_bytes / (stage_ms["combine"] * 1e-3) / 1e9,
-            "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:338-352; tokens when B = 1) "
+            "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:181-195; tokens when B = 1) "
                            "x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
             "transport": "NVSwitch peer stores" if world > 1 else
                          "loopback: all 8 ranks on one GPU, peer stores land in local HBM (not NVLink)",

@@ -24,9 +24,9 @@ extern "C" {
 #endif
 
 /* Return / status codes. Map to the reference's exception types:
- *   AURORA_EINVAL    -> ValueError           (core.py:88-94, commsched.py:213-216, 252-258)
- *   AURORA_EOVERFLOW -> DecompositionError   (commsched.py:417-421, phase bound n^2-2n+2)
- *   AURORA_ENOMATCH  -> DecompositionError   (commsched.py:424-429, no perfect matching)   */
+ *   AURORA_EINVAL    -> ValueError           (core.py:88-94, commsched.py:56-59, 95-101)
+ *   AURORA_EOVERFLOW -> DecompositionError   (commsched.py:260-264, phase bound n^2-2n+2)
+ *   AURORA_ENOMATCH  -> DecompositionError   (commsched.py:267-272, no perfect matching)   */
 #define AURORA_OK 0
 #define AURORA_EINVAL 1
 #define AURORA_EOVERFLOW 2
@@ -39,7 +39,7 @@ extern "C" {
 
 int aurora_version(void);
 
-/* Table capacities: raw permutation phases (commsched.py:410, n^2-2n+2) and
+/* Table capacities: raw permutation phases (commsched.py:253, n^2-2n+2) and
  * stripped phases (each of the <= n(n-1) real pairs can split one raw phase:
  * 2n^2-3n+2). */
 int aurora_raw_phase_cap(int n);
@@ -47,15 +47,15 @@ int aurora_phase_cap(int n);
 
 /* ---------------------------------------------------------------- K2 ----
  * aurora_schedule_f64: replaces moeplan.commsched.build_schedule
- * (commsched.py:448-481) including decompose's raw permutations
- * (commsched.py:394-435). Bit-exact with the reference for n <= 32.
+ * (commsched.py:291-324) including decompose's raw permutations
+ * (commsched.py:237-278). Bit-exact with the reference for n <= 32.
  *   d[n*n]   traffic matrix, row-major, float64 (TrafficMatrix.entries, core.py:75-97)
  *   bw[n]    ClusterSpec.bandwidths (core.py:179-181); NULL == all 1.0
  *   raw_perm[(n^2-2n+2)*n], raw_dur[n^2-2n+2], n_raw[1]       (decompose output)
  *   phase_recv[(2n^2-3n+2)*n]  receiver of sender i in phase k, or -1
  *   phase_dur[2n^2-3n+2], n_phases[1], b_max[1] (bmax_heterogeneous)
  *   status[1] AURORA_OK / EINVAL / EOVERFLOW / ENOMATCH
- * The makespan is math.fsum(phase_dur) (commsched.py:480), done by the shim. */
+ * The makespan is math.fsum(phase_dur) (commsched.py:323), done by the shim. */
 int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_perm,
                         double* raw_dur, int32_t* n_raw, int32_t* phase_recv, double* phase_dur,
                         int32_t* n_phases, double* b_max, int32_t* status, void* stream);
@@ -73,7 +73,7 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  *                     sends to j in between).
  *   rchunks[P][n][4]  the same entries indexed by receiver j: {sender, first,
  *                     count, run code of the reversed run into the sender} (the
- *                     combine runs CommSchedule.reversed(), commsched.py:310-319)
+ *                     combine runs CommSchedule.reversed(), commsched.py:153-162)
  *   n_in[n], n_out[n] arrival signals each rank receives in the dispatch / combine
  *   Hand-over thresholds and n_in / n_out count arrival signals: every copy CTA of
  *   the sending rank signals once per run. The copy CTAs are the engine's
@@ -87,7 +87,7 @@ int aurora_schedule_f64(const double* d, const double* bw, int n, int32_t* raw_p
  *                     phase 0 while later phases are still being computed. The
  *                     caller zeroes it (stream-ordered) before the launch.
  * (the buffer layout soff / roff the chunk offsets refer to comes from aurora_pack)
- * Heterogeneous durations (time units, commsched.py:338-347) are converted to
+ * Heterogeneous durations (time units, commsched.py:181-190) are converted to
  * whole tokens per entry by rounding each pair's cumulative time x
  * min(B_i,B_j) (the pair's final cumulative time lands on its exact count; a
  * pair that would need a correction is reported as AURORA_EINVAL). */
@@ -183,8 +183,8 @@ int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, const int32_t* 
  * aurora_engine: executes the schedule as in-kernel stores into peer
  * memory, self-timed per run (a run i->j starts once every earlier run into j
  * has landed), replacing a single NCCL alltoallv. mode bit 0: 0 =
- * dispatch (CommSchedule phases, commsched.py:112-132), 1 = combine (the
- * reversed schedule, commsched.py:310-319: same phases, directions flipped);
+ * dispatch (CommSchedule phases, commsched.py:113-132), 1 = combine (the
+ * reversed schedule, commsched.py:153-162: same phases, directions flipped);
  * mode bit 1: peers live on other GPUs (system-scope flag ordering) -- clear
  * when every rank of the call shares this GPU (gpu scope suffices);
  * mode bit 2: local (diagonal) rows only -- no schedule needed, so it can run
@@ -308,7 +308,7 @@ int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* 
  * expert rank rank_base + g, all received rows) with the combine fused into
  * GEMM2's epilogue -- the K6 + K5 pair written as one kernel over peer memory
  * (reference: ffn_work_per_token, core.py:194-221, then the reversed all-to-all,
- * CommSchedule.reversed commsched.py:310-319, as sequenced by sim.py:130-154):
+ * CommSchedule.reversed commsched.py:153-162, as sequenced by sim.py:130-154):
  * every output row of sender i's block (recv rows roff[i][j] + [0, counts[i][j]))
  * is stored straight into ret_bufs[i] row soff[i][j] + offset (the row the
  * combine engine would write; NVSwitch stores overlap the GEMM tile by tile),

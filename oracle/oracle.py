@@ -5,7 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (the
 The product package never does; it fails loudly without its CUDA library.
 
 * ``build_schedule_oracle``: ctypes over ``sched_oracle.c``, the C restatement
-  of ``moeplan.build_schedule`` (reference ``pkg/src/moeplan/commsched.py:448-481``),
+  of ``moeplan.build_schedule`` (reference ``pkg/src/moeplan/commsched.py:291-324``),
   pinned bit-exact against fixtures produced by the reference itself
   (``tests/golden/gen_golden.py``).
 * ``router_oracle`` / ``pack_oracle``: the router, traffic matrix
@@ -78,7 +78,7 @@ class OracleDecompositionError(RuntimeError):
 def build_schedule_oracle(d, bandwidths=None) -> dict:
     """Restated build_schedule. Returns a plain dict:
     ``raw``: list of (perm tuple, duration); ``phases``: list of
-    (transfers tuple, duration); ``makespan`` (math.fsum, commsched.py:480);
+    (transfers tuple, duration); ``makespan`` (math.fsum, commsched.py:323);
     ``b_max``; ``t`` (the time-normalised matrix)."""
     d = np.ascontiguousarray(np.asarray(d, dtype=np.float64))
     n = d.shape[0]

@@ -39,7 +39,7 @@ TIME_ATOL = 1e-9  # commsched.py:40
 
 @dataclass(frozen=True)
 class Phase:
-    """Concurrent transfers, distinct senders and receivers (commsched.py:112-123)."""
+    """Concurrent transfers, distinct senders and receivers (commsched.py:113-123)."""
 
     transfers: tuple
     duration: float
@@ -196,14 +196,14 @@ def build_schedule(d, cluster) -> CommSchedule:
 
 def decompose_raw(d, cluster) -> list:
     """The raw permutation phases ``decompose(augment(time_normalize(d)))``
-    returns (commsched.py:394-435), computed by the same kernel."""
+    returns (commsched.py:237-278), computed by the same kernel."""
     _, raw_perm, raw_dur, _, _, _ = _run(d, cluster)
     return [(tuple(int(v) for v in perm), float(dur)) for perm, dur in zip(raw_perm, raw_dur)]
 
 
 @dataclass(frozen=True)
 class ScheduleReport:
-    """Violations found by validate_schedule (commsched.py:327-352)."""
+    """Violations found by validate_schedule (commsched.py:169-195)."""
 
     contention: tuple = ()
     conservation: tuple = ()

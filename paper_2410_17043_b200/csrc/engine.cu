@@ -1,7 +1,7 @@
 // K4 dispatch / K6 combine: the Aurora schedule executed as in-kernel stores
 // into peer memory (NVSwitch is the paper's big switch).
 //
-// Schedule semantics (reference pkg/src/moeplan/commsched.py:112-162): in
+// Schedule semantics (reference pkg/src/moeplan/commsched.py:113-162): in
 // phase k sender i transmits `duration` tokens of its pair (i, j) while no
 // other sender targets j and i targets nobody else. Instead of a global
 // barrier per phase, every copy CTA runs its sender's entries in phase order
@@ -18,7 +18,7 @@
 // scheduler's latency hides behind the first phases' copies.
 //
 // Combine (mode 1) replays the same phases with directions flipped -- the
-// reference's CommSchedule.reversed() (commsched.py:310-319) -- from the
+// reference's CommSchedule.reversed() (commsched.py:153-162) -- from the
 // rchunks table, sending expert outputs back to the token owners.
 #include "common.cuh"
 #include "tc_helpers.cuh"

@@ -1,16 +1,16 @@
 // K2: Aurora's contention-free all-to-all schedule, computed on the device.
 //
 // Bit-exact restatement of moeplan.build_schedule (reference
-// pkg/src/moeplan/commsched.py:448-481) for n <= 32 GPUs, run by ONE warp:
-//   time_normalize        commsched.py:338-347   lane i divides row i
-//   bmax_heterogeneous    commsched.py:350-352   numpy pairwise row sums / sequential col sums
-//   augment               commsched.py:355-391   greedy fill, lane 0 (sequential by definition)
-//   AugmentedMatrix check commsched.py:247-262
-//   decompose             commsched.py:394-435   lane-parallel snap/min/update
+// pkg/src/moeplan/commsched.py:291-324) for n <= 32 GPUs, run by ONE warp:
+//   time_normalize        commsched.py:181-190   lane i divides row i
+//   bmax_heterogeneous    commsched.py:193-195   numpy pairwise row sums / sequential col sums
+//   augment               commsched.py:198-234   greedy fill, lane 0 (sequential by definition)
+//   AugmentedMatrix check commsched.py:90-105
+//   decompose             commsched.py:237-278   lane-parallel snap/min/update
 //   perfect_matching      matching.py:75-112     lane 0, bitmask rows, explicit DFS stacks
 //   hopcroft_karp         matching.py:20-72      level-synchronous bitmask BFS (distances are
 //                                                order-independent), exact-order DFS
-//   strip/_coalesce       commsched.py:463-479   interleaved with decompose (it only needs the
+//   strip/_coalesce       commsched.py:306-322   interleaved with decompose (it only needs the
 //                                                raw phases produced so far)
 // Compiled with -fmad=false so every double operation rounds exactly like numpy.
 //
@@ -258,13 +258,13 @@ __device__ __forceinline__ void row_put(V (&a)[NB], int j, V v) {
 //
 // Entry (phase k, sender i) = {receiver j, first token of pair (i, j) in this
 // phase, token count, run code}. A run is a maximal stretch of consecutive
-// phases in which i sends to j (commsched.py:463-479 splits and coalesces
+// phases in which i sends to j (commsched.py:306-322 splits and coalesces
 // phases, so a pair often stays matched across several of them); inside a run
 // no other sender touches j, so only the first entry of a run needs the
 // receiver's hand-over. Run code = r (the run's index among the runs into j)
 // on the first entry, -1 - r on continuation entries. rchunks holds the same
 // entries indexed by receiver with the run's index among the sender's runs
-// (the combine replays CommSchedule.reversed(), commsched.py:310-319).
+// (the combine replays CommSchedule.reversed(), commsched.py:153-162).
 // n_in[j] / n_out[i] = runs into j / out of i.
 // ============================================================================
 struct ChunkCtx {
@@ -383,10 +383,10 @@ __device__ __forceinline__ void publish(int32_t* progress, int value, int lane) 
 
 // ============================================================================
 // n <= 16: two warps.
-//   warp 0 -- decompose (commsched.py:406-435): snap / min / masks per lane row
+//   warp 0 -- decompose (commsched.py:249-278): snap / min / masks per lane row
 //             in registers, the matching (FastMatch8 / FastMatch<16>, lane 0),
 //             the update; every raw (perm, duration) goes to a shared ring.
-//   warp 1 -- strip + _coalesce (commsched.py:463-479) of each raw phase as
+//   warp 1 -- strip + _coalesce (commsched.py:306-322) of each raw phase as
 //             soon as it is published, the chunk entries of every phase that
 //             closes, and the progress word the engine polls.
 // The strip only needs the raw phases produced so far, so warp 1 is never
@@ -429,7 +429,7 @@ struct Row {
 
 // Integer-domain prologue (int32 counts on a uniform cluster, the in-layer
 // path): time_normalize is the identity, bmax / augment are exact in int32, so
-// the whole of commsched.py:338-391 runs in registers -- lane i holds row i.
+// the whole of commsched.py:181-234 runs in registers -- lane i holds row i.
 // augment's greedy fill of row i (j ascending, skipping j == i and exhausted
 // columns, stopping once the row is full) is a prefix over the eligible
 // columns: fill_j = clamp(rr_i - sum_{eligible j' < j} cr_j', 0, cr_j).
@@ -485,7 +485,7 @@ __device__ int int_prologue(const SchedParams& p, int lane, Row<NB, int>& rem, R
       if (lane == i) x[j] = f;
     }
   }
-  if (on && rr > 0) {  // leftover on the diagonal (commsched.py:386-389)
+  if (on && rr > 0) {  // leftover on the diagonal (commsched.py:229-232)
 #pragma unroll
     for (int j = 0; j < NB; j++)
       if (j == lane) x[j] = rr;
@@ -642,7 +642,7 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   const bool on = lane < n;
   const V INF = Dom<V>::inf();
   const int P_MAX = 2 * n * n - 3 * n + 2;
-  V lr[NB];  // real demand not yet delivered (commsched.py:463)
+  V lr[NB];  // real demand not yet delivered (commsched.py:306)
 #pragma unroll
   for (int j = 0; j < NB; j++)
     lr[j] = (on && j < n) ? (t_in ? (V)t_in[lane * ld + j] : (j == lane ? (V)0 : (V)p.d32[lane * n + j])) : (V)0;
@@ -715,7 +715,7 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
       const unsigned amask = __ballot_sync(0xffffffffu, act);
       V step;
       if (amask == 0) {
-        step = left;  // idle Phase((), left) (commsched.py:469-473)
+        step = left;  // idle Phase((), left) (commsched.py:312-316)
       } else {
         const V m = Dom<V>::warp_min(act ? lv : INF);
         step = m < left ? m : left;
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
       if (p.prof) p.prof[5] = clock64() - k_start;
     }
   } else if (warp == 0) {
-    // ---- time_normalize (commsched.py:338-347) + TimeMatrix checks (211-219)
+    // ---- time_normalize (commsched.py:181-190) + TimeMatrix checks (211-219)
     bool bad = false;
     if (on) {
       for (int j = 0; j < n; j++) {
@@ -880,7 +880,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
     int status = __any_sync(0xffffffffu, bad) ? AURORA_EINVAL : AURORA_OK;
     __syncwarp();
 
-    // ---- bmax_heterogeneous (commsched.py:350-352): numpy-order row/col sums
+    // ---- bmax_heterogeneous (commsched.py:193-195): numpy-order row/col sums
     if (on) {
       row = np_pairwise_row(&t_s[lane][0], n);
       col = 0.0;
@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
     if (lane == 0) bmax_s = b_max;
 
     if (status == AURORA_OK && b_max > 0) {
-      // ---- augment (commsched.py:367-391): greedy transportation fill on lane 0
+      // ---- augment (commsched.py:210-234): greedy transportation fill on lane 0
       if (on) { rr_s[lane] = b_max - row; cr_s[lane] = b_max - col; }
       if (on) for (int j = 0; j < n; j++) real_s[lane][j] = 0.0;  // x
       __syncwarp();
@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
         }
       }
       __syncwarp();
-      // AugmentedMatrix.__post_init__ balance check (commsched.py:252-258)
+      // AugmentedMatrix.__post_init__ balance check (commsched.py:95-101)
       const double tol = 1e-9 * (b_max > 1.0 ? b_max : 1.0);
       bool unbal = false;
       if (on) {

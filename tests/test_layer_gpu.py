@@ -177,7 +177,7 @@ def test_layer_c2_full_size(torch):
 def test_layer_heterogeneous_cluster(torch):
     """C4 (heterogeneous emulation): placement by assign_exclusive_hetero
     (placement.py:46-60) from a calibration pass, schedule on the fp64
-    time-normalised matrix (commsched.py:338-347) bit-exact with the oracle,
+    time-normalised matrix (commsched.py:181-190) bit-exact with the oracle,
     fractional durations turned into whole-token chunks whose per-pair totals
     equal the traffic matrix, and a correct layer output."""
     import paper_2410_17043_b200 as A
