@@ -302,7 +302,7 @@ int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const in
  *   y = (silu(x W1^T) * (x W3^T)) W2^T, fp32 accumulate. */
 int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                       void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
-                      int64_t cap, int H, int F, int num_sms, void* stream);
+                      int64_t cap, int H, int F, int32_t* tile_ctr, int num_sms, void* stream);
 
 /* aurora_expert_ffn_combine: the same FFN (one expert per rank: group g is
  * expert rank rank_base + g, all received rows) with the combine fused into
@@ -322,7 +322,7 @@ int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2
                               void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
                               void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                               const int32_t* roff, int n, int rank_base, int32_t* const* ctrs,
-                              int32_t* ticket, int sys, int num_sms, void* stream);
+                              int32_t* ticket, int sys, int32_t* tile_ctr, int num_sms, void* stream);
 
 /* aurora_expert_ffn_packed_scatter: the packed FFN of the grouped dispatch with the
  * pre-reduction of single-expert rows folded into GEMM2's epilogue. ginfo [a_rows]
@@ -338,14 +338,14 @@ int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const v
                                      int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
                                      void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                                      const int32_t* roff, int n, int rank_base, void* ybuf, int64_t ycap,
-                                     int to_ret, int sys, int num_sms, void* stream);
+                                     int to_ret, int sys, int32_t* tile_ctr, int num_sms, void* stream);
 
 /* Same FFN with the groups packed back to back (a rank hosting several
  * experts): group g's rows are a_buf rows [g_off[g], g_off[g] + g_rows[g]);
  * a_rows = rows allocated in a_buf / h_buf / y_buf. */
 int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                              void* y_buf, const int32_t* g_off, const int32_t* g_rows, int G,
-                             int64_t a_rows, int H, int F, int num_sms, void* stream);
+                             int64_t a_rows, int H, int F, int32_t* tile_ctr, int num_sms, void* stream);
 
 /* Several experts per rank (E > n). After the dispatch, receiver rows of the
  * local ranks (rank r_local: rows r_local*cap + [0, rtot[rank_base+r_local]))
@@ -380,11 +380,17 @@ int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void*
 /* skip_single (both): rows whose (token, rank) has exactly one local expert were
  * finished by aurora_expert_ffn_packed_scatter; only the others are reduced. */
 
+/* tile_ctr (every expert FFN / grouped GEMM entry point): two int32 owned by the caller,
+ * zero before first use and re-armed by each launch's last cluster -- the dynamic tile
+ * order's {next tile, clusters done} pair. One per stream whose GEMM launches may run
+ * concurrently with another's (a layer keeps one per stream it launches on); NULL
+ * selects the static round-robin tile order. No allocation or host sync happens inside. */
+
 /* Plain grouped GEMM (tests / building block): C[g] = A[g] B[g]^T, bf16 in,
  * fp32 accumulate, bf16 out; epilogue 0 = store, 1 = SwiGLU pairs (N/2 cols). */
 int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_start,
                         const int32_t* m_rows, int G, int64_t cap, int N, int K, int epilogue,
-                        int num_sms, void* stream);
+                        int32_t* tile_ctr, int num_sms, void* stream);
 
 /* ------------------------------------------------------- peer memory ----
  * CUDA IPC for the multi-GPU layer (one process per GPU). aurora_ipc_get

@@ -180,12 +180,31 @@ def _f32(w):
     return np.asarray(w, dtype=np.float32)
 
 
-def moe_layer_oracle(x: np.ndarray, topk_idx, topk_w, w1, w3, w2) -> np.ndarray:
+def bf16_round(a) -> np.ndarray:
+    """fp32 -> nearest bf16 (ties to even), returned as fp32: the rounding the
+    kernels apply when they store h and y (``__float2bfloat16_rn``)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    out = r.astype(np.uint32).view(np.float32)
+    return np.where(np.isnan(a), a, out)
+
+
+def moe_layer_oracle(x: np.ndarray, topk_idx, topk_w, w1, w3, w2, emulate_bf16: bool = False,
+                     gpu_of_expert=None) -> np.ndarray:
     """fp32 SwiGLU MoE: out[t] = sum_s w[t,s] * W2_e (silu(W1_e x) * W3_e x).
     x [T,H] float32; w1/w3 [E][F,H], w2 [E][H,F]: arrays or per-expert
-    sequences (numpy or torch, converted to fp32 one expert at a time)."""
+    sequences (numpy or torch, converted to fp32 one expert at a time).
+
+    ``emulate_bf16``: round where the device path stores bf16 -- the SwiGLU
+    intermediate h, the expert output y, and (with ``gpu_of_expert`` and
+    several experts per rank) the per-(token, rank) pre-reduced row
+    ``bf16(sum_s w_s y_s)`` the expert rank returns (arithmetic
+    contracts); the final sum stays fp32 in slot order, rounded to bf16."""
     T, H = x.shape
     E = len(w1)
+    k = topk_idx.shape[1]
+    y_slot = np.zeros((T, k, H), dtype=np.float32) if emulate_bf16 else None
     out = np.zeros((T, H), dtype=np.float32)
     for e in range(E):
         rows, slots = np.nonzero(topk_idx == e)
@@ -195,6 +214,49 @@ def moe_layer_oracle(x: np.ndarray, topk_idx, topk_w, w1, w3, w2) -> np.ndarray:
         g = xe @ _f32(w1[e]).T
         u = xe @ _f32(w3[e]).T
         h = (g / (1.0 + np.exp(-g))) * u
-        y = h @ _f32(w2[e]).T
-        out[rows] += topk_w[rows, slots][:, None] * y
-    return out
+        if emulate_bf16:
+            y_slot[rows, slots] = bf16_round(bf16_round(h) @ _f32(w2[e]).T)
+        else:
+            out[rows] += topk_w[rows, slots][:, None] * (h @ _f32(w2[e]).T)
+    if not emulate_bf16:
+        return out
+    return aggregate_oracle(y_slot, topk_idx, topk_w, gpu_of_expert)
+
+
+def aggregate_oracle(y_slot, topk_idx, topk_w, gpu_of_expert=None) -> np.ndarray:
+    """Combine + aggregation of bf16 expert outputs ``y_slot[T,k,H]`` (one per
+    (token, slot)) in the device path's order: one expert per rank -> fp32
+    ``sum_s w_s y_s`` in slot order; several experts per rank -> each expert
+    rank first pre-reduces its slots to ``bf16(sum w_s y_s)``, the sender sums
+    those rows (first-slot order). Rounded to bf16."""
+    y_slot = np.asarray(y_slot, dtype=np.float32)
+    T, k, H = y_slot.shape
+    w = np.asarray(topk_w, dtype=np.float32)
+    out = np.zeros((T, H), dtype=np.float32)
+    E = None if gpu_of_expert is None else len(gpu_of_expert)
+    G = 1 if gpu_of_expert is None else E // len(set(int(g) for g in gpu_of_expert))
+    if G == 1:
+        for s in range(k):
+            out += w[:, s:s + 1] * y_slot[:, s]
+        return bf16_round(out)
+    rank = np.asarray(gpu_of_expert)[np.asarray(topk_idx)]   # [T, k]
+    for t in range(T):
+        acc = np.zeros(H, dtype=np.float32)
+        for r in dict.fromkeys(rank[t].tolist()):             # ranks in first-slot order
+            part = np.zeros(H, dtype=np.float32)
+            for s in range(k):
+                if rank[t, s] == r:
+                    part += w[t, s] * y_slot[t, s]
+            acc += bf16_round(part)
+        out[t] = acc
+    return bf16_round(out)
+
+
+def row_errors(got, ref):
+    """Per-row relative L2 error ||got_t - ref_t|| / ||ref_t|| and the max
+    elementwise error over max|ref| (the two bounds the layer tests assert)."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    num = np.linalg.norm(got - ref, axis=1)
+    den = np.maximum(np.linalg.norm(ref, axis=1), 1e-30)
+    return num / den, float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))

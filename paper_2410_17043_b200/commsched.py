@@ -132,10 +132,9 @@ def schedule_tables(entries: np.ndarray, bandwidths: np.ndarray | None):
     phase_dur[P], b_max) as host numpy arrays."""
     import torch
 
-    L = _lib.load()
     n = int(entries.shape[0])
-    if n > 32:
-        raise ValueError(f"the device scheduler supports n <= 32 GPUs, got {n}")
+    _check_n(n)
+    L = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device())
     # the reference's arrays are read-only (core.py:30-33): copy, never alias
     d = torch.tensor(np.array(entries, dtype=np.float64), device=dev)
@@ -161,10 +160,23 @@ def schedule_tables(entries: np.ndarray, bandwidths: np.ndarray | None):
             float(bmax.item()))
 
 
+MAX_RANKS = 32  # K2 keeps one matrix row per lane of a warp (include/aurora_b200.h)
+
+
+def _check_n(n: int) -> None:
+    """The reference schedules any n; the device scheduler stops at a warp's
+    32 lanes. Larger clusters are refused at the boundary (ValueError, the
+    reference's class for inputs it cannot take) instead of falling back to a
+    host scheduler -- see INTEGRATION.md."""
+    if n > MAX_RANKS:
+        raise ValueError(f"the device scheduler supports n <= {MAX_RANKS} GPUs, got {n}")
+
+
 def _run(d, cluster):
     ref = _reference_flavour(d)
     if cluster.n != d.n:
         raise ValueError(f"cluster has {cluster.n} GPUs, matrix has {d.n}")
+    _check_n(d.n)
     entries = np.asarray(d.entries, dtype=float)
     bw = np.asarray(cluster.bandwidths, dtype=float)
     status, raw_perm, raw_dur, phase_recv, phase_dur, b_max = schedule_tables(entries, bw)

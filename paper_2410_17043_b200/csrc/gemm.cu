@@ -26,7 +26,7 @@
 // the CTA-pair variant (gemm2sm.cu)
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
-                              int K, int epilogue, int num_sms, cudaStream_t stream,
+                              int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
                               const AuroraScatterArgs* scatter);
 
 namespace {
@@ -359,14 +359,14 @@ bool use_pair_kernel() {
 
 int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start,
                    const int32_t* m_rows, int G,
-                   int64_t cap, int64_t map_rows, int N, int K, int epilogue, int num_sms,
+                   int64_t cap, int64_t map_rows, int N, int K, int epilogue, int32_t* tile_ctr, int num_sms,
                    cudaStream_t stream, const AuroraScatterArgs* scatter = nullptr) {
   // cap > 0: group g owns rows [g*cap, (g+1)*cap); cap == 0: groups packed,
   // m_start[g] absolute, map_rows = rows of the A buffer
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (use_pair_kernel())
-    return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, num_sms,
+    return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, tile_ctr, num_sms,
                                      stream, scatter);
   if (scatter) return AURORA_EINVAL;  // the fused combine lives in the CTA-pair kernel
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
@@ -400,22 +400,22 @@ int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start
 
 extern "C" int aurora_grouped_gemm(const void* a, const void* b, void* c, const int32_t* m_start,
                                    const int32_t* m_rows,
-                                   int G, int64_t cap, int N, int K, int epilogue, int num_sms,
+                                   int G, int64_t cap, int N, int K, int epilogue, int32_t* tile_ctr, int num_sms,
                                    void* stream) {
-  return launch_grouped(a, b, c, m_start, m_rows, G, cap, 0, N, K, epilogue, num_sms,
+  return launch_grouped(a, b, c, m_start, m_rows, G, cap, 0, N, K, epilogue, tile_ctr, num_sms,
                         (cudaStream_t)stream);
 }
 
 extern "C" int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                                  void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
                                  int64_t cap, int H,
-                                 int F, int num_sms, void* stream) {
+                                 int F, int32_t* tile_ctr, int num_sms, void* stream) {
   // h = silu(x W1^T) * (x W3^T): N = 2F interleaved, K = H
-  int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 0, 2 * F, H, 1, num_sms,
+  int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 0, 2 * F, H, 1, tile_ctr, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
   // y = h W2^T: N = H, K = F
-  return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, 0, H, F, 0, num_sms,
+  return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
                         (cudaStream_t)stream);
 }
 
@@ -425,13 +425,13 @@ extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, con
                                          const int32_t* counts, const int32_t* soff,
                                          const int32_t* roff, int n, int rank_base,
                                          int32_t* const* ctrs, int32_t* ticket, int sys,
-                                         int num_sms, void* stream) {
+                                         int32_t* tile_ctr, int num_sms, void* stream) {
   if (!ret_bufs || !counts || !soff || !roff || !ctrs || !ticket) return AURORA_EINVAL;
-  int rc = launch_grouped(a_buf, w13, h_buf, nullptr, m_rows, G, cap, 0, 2 * F, H, 1, num_sms,
+  int rc = launch_grouped(a_buf, w13, h_buf, nullptr, m_rows, G, cap, 0, 2 * F, H, 1, tile_ctr, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
   const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
-  return launch_grouped(h_buf, w2, y_buf, nullptr, m_rows, G, cap, 0, H, F, 0, num_sms,
+  return launch_grouped(h_buf, w2, y_buf, nullptr, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
                         (cudaStream_t)stream, &sc);
 }
 
@@ -440,9 +440,9 @@ extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w
                                                 int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
                                                 void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                                                 const int32_t* roff, int n, int rank_base, void* ybuf,
-                                                int64_t ycap, int to_ret, int sys, int num_sms, void* stream) {
+                                                int64_t ycap, int to_ret, int sys, int32_t* tile_ctr, int num_sms, void* stream) {
   if (!ginfo || !ret_bufs || !counts || !soff || !roff || !ybuf || experts_per_rank < 1) return AURORA_EINVAL;
-  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, num_sms,
+  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, tile_ctr, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
   AuroraScatterArgs sc{ret_bufs, counts, soff, roff, nullptr, nullptr, n, rank_base, sys ? 1 : 0};
@@ -451,17 +451,17 @@ extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w
   sc.ybuf = ybuf;
   sc.ycap = ycap;
   sc.to_ret = to_ret ? 1 : 0;
-  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, num_sms,
+  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
                         (cudaStream_t)stream, &sc);
 }
 
 extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
                                         void* h_buf, void* y_buf, const int32_t* g_off,
                                         const int32_t* g_rows, int G, int64_t a_rows, int H, int F,
-                                        int num_sms, void* stream) {
-  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, num_sms,
+                                        int32_t* tile_ctr, int num_sms, void* stream) {
+  int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, tile_ctr, num_sms,
                           (cudaStream_t)stream);
   if (rc != AURORA_OK) return rc;
-  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, num_sms,
+  return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
                         (cudaStream_t)stream);
 }

@@ -440,25 +440,6 @@ bool make_map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// One {next tile, clusters done} counter pair per stream (launches on one stream
-// are ordered; the kernel's last cluster re-arms the pair to zero).
-int32_t* tile_counter_for(cudaStream_t stream) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, int32_t*> ctrs;  // (device, stream)
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  const auto key = std::make_pair(dev, stream);
-  std::lock_guard<std::mutex> lock(mu);
-  auto f = ctrs.find(key);
-  if (f != ctrs.end()) return f->second;
-  int32_t* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(int32_t)) != cudaSuccess) return nullptr;
-  if (cudaMemset(p, 0, 2 * sizeof(int32_t)) != cudaSuccess) return nullptr;
-  if (cudaDeviceSynchronize() != cudaSuccess) return nullptr;
-  ctrs[key] = p;
-  return p;
-}
-
 // output map for the epilogue's TMA stores: 32 x 32 boxes, 64-byte swizzle
 bool make_map_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
   static EncodeTiledFn fn = nullptr;
@@ -484,7 +465,7 @@ bool make_map_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 // C-ABI-internal launcher used by gemm.cu when the pair kernel is selected.
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
-                              int K, int epilogue, int num_sms, cudaStream_t stream,
+                              int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
                               const AuroraScatterArgs* scatter) {
   Scatter sc{};
   if (scatter) {
@@ -538,12 +519,10 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   // read from DRAM about once (8-expert C2 GEMM1: 8.1 -> 2.2 GB for 2.15 GB of
   // operands); AURORA_GEMM_STATIC=1: round robin (clusters drift apart over the
   // persistent loop and the window -- the L2 working set -- grows with the drift)
+  // The counter pair {next tile, clusters done} is the caller's (zero before first use, re-armed by
+  // the kernel's last cluster): one per stream of launches that may run concurrently. NULL = round robin.
   static const bool dyn_sched = !getenv("AURORA_GEMM_STATIC") || atoi(getenv("AURORA_GEMM_STATIC")) == 0;
-  int32_t* tile_ctr = nullptr;
-  if (dyn_sched) {
-    tile_ctr = tile_counter_for(stream);
-    if (!tile_ctr) return AURORA_ECUDA;
-  }
+  if (!dyn_sched) tile_ctr = nullptr;
   const int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BMP * K * 2)));
   if (num_sms <= 0) {
     int dev = 0;

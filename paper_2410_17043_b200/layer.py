@@ -60,6 +60,8 @@ class MoEConfig:
             raise ValueError("experts must be a multiple of ranks (contiguous expert blocks per rank), <= 64")
         if not (1 <= self.top_k <= min(8, self.experts)):
             raise ValueError("top_k out of range")
+        if not 1 <= self.ranks <= 32:
+            raise ValueError("ranks must be 1..32 (the device scheduler keeps one matrix row per lane)")
 
 
 def zipf_bias(experts: int, skew: float, gen: torch.Generator) -> torch.Tensor:
@@ -83,6 +85,8 @@ class AuroraMoELayer:
     (default: all of them, on the current device). ``peer_bufs`` is filled
     by :mod:`paper_2410_17043_b200.dist` for multi-GPU runs.
     """
+
+    SCATTER_MAX_RANKS = 16  # gemm2sm.cu SC_MAXN
 
     def __init__(self, cfg: MoEConfig, plan: Optional[DeploymentPlan] = None, *, rank_base: int = 0,
                  n_local: Optional[int] = None, bandwidths=None, device=None, ctas_per_rank: Optional[int] = None,
@@ -189,6 +193,9 @@ class AuroraMoELayer:
         self.rrem = torch.empty(n, **i32)
         self.engine_status = torch.zeros(1, **i32)
         self.gemm_ticket = torch.zeros(1, **i32)  # fused combine: GEMM2's grid completion ticket
+        # the expert GEMMs' dynamic tile order: one {next tile, clusters done} pair per stream the
+        # layer launches GEMMs on (main, side), owned here -- no allocation inside a forward
+        self.tile_ctrs = torch.zeros(2, 2, **i32)
         # overlap: the local rows' copy + expert GEMM run on a side stream while
         # K2 computes the schedule and the engine moves the network rows
         # Measured on B200 (profiles/r01_overlap_sweep.json): the expert GEMM runs
@@ -214,7 +221,10 @@ class AuroraMoELayer:
         # grouped: finish single-expert rows in GEMM2's epilogue (per-row scattered stores)
         # instead of TMA-storing every row for the pre-reduction (AURORA_PACKED_SCATTER=0)
         self.packed_scatter = os.environ.get("AURORA_PACKED_SCATTER", "1") != "0"
-        if os.environ.get("AURORA_GEMM") == "1sm":  # the single-CTA GEMM (ablation) has no scatter epilogue
+        # the single-CTA GEMM (ablation; gemm.cu selects it for any AURORA_GEMM starting with '1') has no
+        # scatter epilogue, and the pair kernel's scatter tables stop at 16 ranks (gemm2sm.cu SC_MAXN):
+        # beyond that the combine runs on the reversed-schedule engine (up to 32 ranks)
+        if os.environ.get("AURORA_GEMM", "").startswith("1") or n > self.SCATTER_MAX_RANKS:
             self.fused_combine = False
             self.packed_scatter = False
         # the engine's copy path: TMA bulk copies (default) or LSU 16-byte vectors (ablation)
@@ -401,10 +411,10 @@ class AuroraMoELayer:
                    "aurora_exchange_counts")
         self._xstep += 1
 
-    def engine_ctas(self, combine: bool) -> int:
+    def engine_ctas(self, combine: bool, C: Optional[int] = None) -> int:
         """Copy CTAs per local rank the engine launches (clamped to co-residency)."""
         row2 = self.meta_bytes if (self.G > 1 and not combine) else 0
-        c = self.L.aurora_engine_ctas(self.n, self.n_local, self.C, self.cfg.hidden * 2, row2,
+        c = self.L.aurora_engine_ctas(self.n, self.n_local, C or self.C, self.cfg.hidden * 2, row2,
                                       1 if self.engine_lsu else 0)
         if c < 1:
             _lib.check(-c, "aurora_engine_ctas")
@@ -417,13 +427,17 @@ class AuroraMoELayer:
         return apportion(self.counts.cpu().numpy(), self.n, self.n_local, self.n_local * self.engine_ctas(combine),
                          self.split, combine, bw)
 
-    def schedule(self, stream: int) -> None:
+    def schedule(self, stream: int, dispatch_ctas: Optional[int] = None) -> None:
+        """K2. ``dispatch_ctas``: copy CTAs per rank the dispatch will run with when it
+        differs from ``self.C`` (the combine always runs with ``self.C``); the hand-over
+        thresholds count one signal per copy CTA, so K2 and the engine must agree."""
         _lib.check(self.L.aurora_schedule_counts(
             self.counts.data_ptr(), None if self.bw is None else self.bw.data_ptr(), self.n,
             self.phase_recv.data_ptr(), self.phase_dur.data_ptr(), self.sched_i.data_ptr(),
             self.chunks.data_ptr(), self.rchunks.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.sched_i[1:].data_ptr(), self.progress.data_ptr(), self.n_local,
-            self.n_local * self.engine_ctas(False), self.n_local * self.engine_ctas(True), self.split, stream),
+            self.n_local * self.engine_ctas(False, dispatch_ctas), self.n_local * self.engine_ctas(True), self.split,
+            stream),
             "aurora_schedule_counts")
 
     def pack(self, stream: int) -> None:
@@ -491,8 +505,13 @@ class AuroraMoELayer:
             m_start, m_rows = self.rloc[rb:].data_ptr(), self.rrem[rb:].data_ptr()
         _lib.check(self.L.aurora_expert_ffn(self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                             self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_start or None, m_rows,
-                                            self.n_local, self.cap, cfg.hidden, cfg.ffn, self.num_sms, stream),
+                                            self.n_local, self.cap, cfg.hidden, cfg.ffn, self._tctr(stream),
+                                            self.num_sms, stream),
                    "aurora_expert_ffn")
+
+    def _tctr(self, stream: int) -> int:
+        """The GEMM tile-counter pair of the stream a launch goes to."""
+        return self.tile_ctrs[1 if stream == int(self.side.cuda_stream) else 0].data_ptr()
 
     @property
     def grouped(self) -> bool:
@@ -521,7 +540,7 @@ class AuroraMoELayer:
             self.ybuf.data_ptr(), self.rtot[self.rank_base:].data_ptr(), self.n_local, self.cap, cfg.hidden,
             cfg.ffn, self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
             self.n, self.rank_base, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), sys_scope,
-            self.num_sms, stream), "aurora_expert_ffn_combine")
+            self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_combine")
 
     def combine_wait(self, stream: int) -> None:
         """Receiving side of the fused combine: every expert rank's rows for this
@@ -542,7 +561,8 @@ class AuroraMoELayer:
             _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                                   self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                                   self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
-                                                  self.num_sms, stream), "aurora_expert_ffn_packed")
+                                                  self._tctr(stream), self.num_sms, stream),
+                       "aurora_expert_ffn_packed")
             inv = None
         elif self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack);
             # single-expert rows are finished (w * y -> sender or ybuf) in GEMM2's epilogue
@@ -551,7 +571,7 @@ class AuroraMoELayer:
                 self.y_g.data_ptr(), self.g_off.data_ptr(), self.g_rows.data_ptr(), E_loc, self.max_entries, H,
                 cfg.ffn, self.ginfo.data_ptr(), self.G, self.t_dst_c.data_ptr(), self.counts.data_ptr(),
                 self.soff.data_ptr(), self.roff.data_ptr(), self.n, self.rank_base, self.ybuf.data_ptr(), self.cap,
-                1 if fused else 0, 1 if self.n_local != self.n else 0, self.num_sms, stream),
+                1 if fused else 0, 1 if self.n_local != self.n else 0, self._tctr(stream), self.num_sms, stream),
                 "aurora_expert_ffn_packed_scatter")
             inv, skip = None, 1
         else:
@@ -587,7 +607,7 @@ class AuroraMoELayer:
         _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                               self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                               self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
-                                              self.num_sms, stream), "aurora_expert_ffn_packed")
+                                              self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_packed")
 
     def combine(self, stream: int) -> None:
         # local rows stay in the expert output; the aggregation reads them there
@@ -663,7 +683,11 @@ class AuroraMoELayer:
             self.experts(ss, "local")
             mark("local_gemm_done", self.side)
             self._ev_local.record(self.side)
-            self.schedule(s)
+            # the remote dispatch may run with fewer copy CTAs beside the local GEMM
+            # (AURORA_C_OVERLAP): K2 counts its hand-over thresholds for the CTAs the
+            # dispatch will actually launch
+            c_disp = (self.C_overlap or self.C) if self.overlap != "schedule" else self.C
+            self.schedule(s, dispatch_ctas=c_disp)
             mark("scheduled", main)
             if self.overlap == "schedule":
                 # only the (latency-bound) scheduler hides under the local GEMM;
@@ -674,7 +698,7 @@ class AuroraMoELayer:
                 mark("dispatched", main)
             else:
                 c_full = self.C
-                self.C = self.C_overlap or self.C
+                self.C = c_disp
                 try:
                     self.dispatch(s, "remote")
                 finally:

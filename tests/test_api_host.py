@@ -190,3 +190,31 @@ def test_schedule_wire_format_matches_reference_cli():
                "phases": [{"duration": p.duration, "transfers": [list(t) for t in p.transfers]} for p in ref.phases],
                "contention_free": rep.contention_ok, "complete": rep.conservation_ok, "optimal": rep.optimal}
     assert json.dumps(pay) == json.dumps(ref_pay)
+
+
+def test_reference_error_classes_host(moeplan, monkeypatch):
+    """Errors map to the reference's classes with the device result faked (no
+    GPU): a cluster / matrix size mismatch is ValueError (commsched.py:181-190),
+    a device status of phase overflow or no perfect matching is moeplan's own
+    DecompositionError (commsched.py:165-166, 260-272) when the caller passed
+    moeplan objects, and this package's DecompositionError otherwise."""
+    import numpy as np
+    import pytest
+    import paper_2410_17043_b200 as A
+    from paper_2410_17043_b200 import _lib, commsched as C
+    tm = moeplan.TrafficMatrix(np.ones((4, 4)))
+    with pytest.raises(ValueError):
+        A.build_schedule(tm, moeplan.ClusterSpec.uniform(3))
+    empty = (np.zeros((0, 4), np.int32), np.zeros(0), np.zeros((0, 4), np.int32), np.zeros(0), 3.0)
+    for status in (_lib.AURORA_EOVERFLOW, _lib.AURORA_ENOMATCH):
+        monkeypatch.setattr(C, "schedule_tables", lambda e, b, s=status: (s,) + empty)
+        with pytest.raises(moeplan.commsched.DecompositionError):
+            A.build_schedule(tm, moeplan.ClusterSpec.uniform(4))
+        with pytest.raises(A.DecompositionError):
+            A.build_schedule(A.TrafficMatrix(np.ones((4, 4))), A.ClusterSpec.uniform(4))
+    monkeypatch.setattr(C, "schedule_tables", lambda e, b: (_lib.AURORA_EINVAL,) + empty)
+    with pytest.raises(ValueError):
+        A.build_schedule(tm, moeplan.ClusterSpec.uniform(4))
+    monkeypatch.undo()
+    with pytest.raises(ValueError, match="n <= 32"):  # beyond the device scheduler: a clear error, no fallback
+        A.build_schedule(A.TrafficMatrix(np.ones((33, 33))), A.ClusterSpec.uniform(33))

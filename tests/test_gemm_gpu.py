@@ -13,6 +13,16 @@ def env():
     return torch, _lib.load(), _lib
 
 
+_CTR = []
+
+
+def _ctr(torch):
+    """The caller-owned tile-counter pair of the GEMM's dynamic tile order."""
+    if not _CTR:
+        _CTR.append(torch.zeros(2, dtype=torch.int32, device="cuda"))
+    return _CTR[0].data_ptr()
+
+
 def _run(torch, L, _lib, G, cap, m_rows, N, K, epilogue, seed=0):
     g = torch.Generator(device="cuda").manual_seed(seed)
     a = (torch.randn(G * cap, K, device="cuda", generator=g)).to(torch.bfloat16)
@@ -21,7 +31,7 @@ def _run(torch, L, _lib, G, cap, m_rows, N, K, epilogue, seed=0):
     c = torch.full((G * cap, out_cols), float("nan"), device="cuda", dtype=torch.bfloat16)
     m = torch.tensor(m_rows, dtype=torch.int32, device="cuda")
     rc = L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, m.data_ptr(), G, cap, N, K, epilogue,
-                               0, _lib.stream_ptr())
+                               _ctr(torch), 0, _lib.stream_ptr())
     assert rc == 0
     torch.cuda.synchronize()
     for gi in range(G):
@@ -70,7 +80,7 @@ def test_expert_ffn_matches_fp32(env):
     m_rows = [cap, 100]
     m = torch.tensor(m_rows, dtype=torch.int32, device="cuda")
     rc = L.aurora_expert_ffn(x.data_ptr(), w13.contiguous().data_ptr(), w2.data_ptr(), h.data_ptr(), y.data_ptr(),
-                             None, m.data_ptr(), G, cap, H, F, 0, _lib.stream_ptr())
+                             None, m.data_ptr(), G, cap, H, F, _ctr(torch), 0, _lib.stream_ptr())
     assert rc == 0
     torch.cuda.synchronize()
     for gi in range(G):

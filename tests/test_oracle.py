@@ -96,3 +96,26 @@ def test_pack_oracle_small():
     assert lists[0][0] == [0, 1] and lists[0][1] == [2]
     assert lists[1][0] == [4, 5] and lists[1][1] == [3, 4, 5]
     assert pos[0].tolist() == [0, 0] and pos[4].tolist() == [0, 1] and pos[5].tolist() == [1, 2]
+
+
+def test_bf16_emulation_helpers():
+    """bf16_round is torch's round-to-nearest-even; aggregate_oracle follows
+    the device order (one expert per rank: fp32 slot sum; several: per-rank
+    bf16 pre-reduction first)."""
+    import torch
+    from oracle.oracle import aggregate_oracle, bf16_round, row_errors
+    rng = np.random.default_rng(0)
+    a = (rng.standard_normal(1 << 16) * np.exp(rng.uniform(-20, 20, 1 << 16))).astype(np.float32)
+    assert np.array_equal(bf16_round(a), torch.from_numpy(a).bfloat16().float().numpy())
+    y = bf16_round(rng.standard_normal((3, 4, 8)).astype(np.float32))
+    w = rng.random((3, 4)).astype(np.float32)
+    idx = np.array([[0, 1, 2, 3], [3, 2, 1, 0], [0, 2, 4, 6]])
+    one = aggregate_oracle(y, idx, w)
+    assert np.array_equal(one, bf16_round(sum(w[:, s:s + 1] * y[:, s] for s in range(4))))
+    gpu_of = [0, 0, 1, 1, 2, 2, 3, 3]  # two experts per rank
+    two = aggregate_oracle(y, idx, w, gpu_of)
+    t = 0  # experts 0,1 -> rank 0; 2,3 -> rank 1
+    exp0 = bf16_round(bf16_round(w[t, 0] * y[t, 0] + w[t, 1] * y[t, 1]) + bf16_round(w[t, 2] * y[t, 2] + w[t, 3] * y[t, 3]))
+    assert np.array_equal(two[0], exp0)
+    rel, glob = row_errors(two, two)
+    assert rel.max() == 0 and glob == 0

@@ -16,8 +16,9 @@ for name, (G, m, N, K, ep) in cases.items():
     b = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
     c = torch.empty(G * m, N // 2 if ep else N, device="cuda", dtype=torch.bfloat16)
     rows = torch.full((G,), m, dtype=torch.int32, device="cuda")
+    ctr = torch.zeros(2, dtype=torch.int32, device="cuda")
     run = lambda: L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, rows.data_ptr(), G, m, N,
-                                        K, ep, 0, _lib.stream_ptr())
+                                        K, ep, ctr.data_ptr(), 0, _lib.stream_ptr())
     for _ in range(3):
         run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -10,9 +10,10 @@ a = torch.randn(G * m, K, device="cuda").to(torch.bfloat16)
 b = (torch.randn(G * N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
 c = torch.empty(G * m, N // 2, device="cuda", dtype=torch.bfloat16)
 rows = torch.full((G,), m, dtype=torch.int32, device="cuda")
+ctr = torch.zeros(2, dtype=torch.int32, device="cuda")
 for rep in range(2):
   for sms in (148, 140, 132, 116):
-    run = lambda: L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, rows.data_ptr(), G, m, N, K, ep, sms, _lib.stream_ptr())
+    run = lambda: L.aurora_grouped_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), None, rows.data_ptr(), G, m, N, K, ep, ctr.data_ptr(), sms, _lib.stream_ptr())
     for _ in range(3): run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
