@@ -86,6 +86,7 @@ def test_experiment_with_build_schedule_rebound(A, moeplan, monkeypatch):
     reference imports (sim.py:23, experiment.py:19, cli.py:19) to the device
     scheduler and run the reference's own experiment driver
     (experiment.run_experiment, experiment.py:293-311): identical result rows."""
+    import moeplan.cli as mcli
     import moeplan.experiment as mexp
     cfg_kw = dict(strategies=("aurora", "sjf"), seed=3)
     prof = moeplan.generate_workload(moeplan.SyntheticWorkloadSpec(n=8, skew=1.2, total_tokens=4096.0,
@@ -104,7 +105,7 @@ def test_experiment_with_build_schedule_rebound(A, moeplan, monkeypatch):
         calls.append(d.n)
         return A.build_schedule(d, cluster)
 
-    for mod in (moeplan.commsched, moeplan.sim, mexp, moeplan.cli):
+    for mod in (moeplan.commsched, moeplan.sim, mexp, mcli):
         if hasattr(mod, "build_schedule"):
             monkeypatch.setattr(mod, "build_schedule", device_schedule)
     dev_rows = [mexp.run_experiment(c) for c in configs]
