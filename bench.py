@@ -133,9 +133,73 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm / cpu baseline
+def host_cores() -> int:
+    """Host threads this process may use (the CPU legs run on all of them)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_package():
+    """The reference package ``moeplan`` from its offline install (baseline/_ref, made by
+    ``pip install --target baseline/_ref``; it travels to the GPU box with the snapshot),
+    or None. /root/reference itself is never read at run time."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "moeplan")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import moeplan
+        return moeplan
+    except Exception:
+        return None
+
+
+def reference_schedule_timing(counts, bandwidths=None, reps=30):
+    """The reference's own CPU hot path on a traffic matrix: moeplan.build_schedule
+    (commsched.py:291-324) and simulate_exclusive (sim.py:130-154), timed with
+    time.perf_counter (median of ``reps``; single-threaded Python, 1 core), next to
+    the C restatement (oracle/sched_oracle.c); plus whether both give the same phases."""
+    import numpy as np
+    from oracle.oracle import build_schedule_oracle
+    d = np.asarray(counts, dtype=float).copy()
+    np.fill_diagonal(d, 0)
+    n = d.shape[0]
+
+    def med(fn):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = fn()
+            ts.append(time.perf_counter() - t0)
+        return 1e3 * sorted(ts)[len(ts) // 2], r
+
+    port_ms, o = med(lambda: build_schedule_oracle(d, bandwidths))
+    out = {"on": "this run's traffic matrix (off-diagonal token counts)", "n": n, "reps": reps, "cores": 1,
+           "port_build_schedule_ms": port_ms, "port": "oracle/sched_oracle.c (C restatement, 1 thread)"}
+    m = reference_package()
+    if m is None:
+        out["moeplan"] = "unavailable: baseline/_ref not installed"
+        return out
+    tm = m.TrafficMatrix(d)
+    cl = (m.ClusterSpec.uniform(n) if bandwidths is None else
+          m.ClusterSpec(tuple(m.GpuSpec(float(b), float(b)) for b in bandwidths)))
+    ref_ms, sched = med(lambda: m.build_schedule(tm, cl))
+    prof = m.LayerProfile(0.0, 0.0, 0.0, 0.0, tm)
+    sim_ms, _ = med(lambda: m.simulate_exclusive(prof, m.DeploymentPlan.identity(n), cl))
+    out.update({"moeplan_build_schedule_ms": ref_ms, "moeplan_simulate_exclusive_ms": sim_ms,
+                "moeplan": "baseline/_ref (the reference itself, unmodified)",
+                "phases": len(sched.phases),
+                "port_identical": [(p.transfers, p.duration) for p in sched.phases] == o["phases"]})
+    return out
+
+
 def cpu_reference_step(x_bits, w_gate_bits, bias, w1, w3, w2, k, n, gpu_of_expert):
-    """One pass of the oracle port over a token sample: router (C), traffic
-    matrix + permutation, build_schedule restatement (C), fp32 SwiGLU experts
+    """One pass of the CPU path over a token sample: router (oracle C), traffic
+    matrix + permutation, the schedule by the reference itself (moeplan.build_schedule
+    from baseline/_ref; the C restatement if it is not installed), fp32 SwiGLU experts
     (numpy BLAS, all threads), gate-weighted aggregation."""
     from oracle.oracle import build_schedule_oracle, moe_layer_oracle, pack_oracle, router_oracle
     import numpy as np
@@ -144,30 +208,41 @@ def cpu_reference_step(x_bits, w_gate_bits, bias, w1, w3, w2, k, n, gpu_of_exper
     counts, _, _ = pack_oracle(idx, gpu_of_expert, n)
     d = counts.astype(float)
     np.fill_diagonal(d, 0)
-    build_schedule_oracle(d)
+    m = reference_package()
+    if m is not None:
+        m.build_schedule(m.TrafficMatrix(d), m.ClusterSpec.uniform(n))
+    else:
+        build_schedule_oracle(d)
     x = torch.from_numpy(x_bits.astype(np.int32) << 16).view(torch.float32).numpy()
     return moe_layer_oracle(x, idx, wts, w1, w3, w2)
 
 
-def run_cpu(args, sample_tokens, reps, seed=0):
-    """Times the oracle port on `sample_tokens` tokens of the workload. Returns
-    (tokens/s, schedule ms on the full C2-size traffic matrix, seconds per rep)."""
-    import numpy as np
+def cpu_weights(args, seed=0):
     import torch
-    from oracle.oracle import build_schedule_oracle
-    torch.set_num_threads(os.cpu_count() or 1)
-    H, F, E, k, n = args.hidden, args.ffn, args.experts, args.topk, args.ranks
-    g = torch.Generator().manual_seed(seed)
     from paper_2410_17043_b200.layer import zipf_bias
+    H, F, E = args.hidden, args.ffn, args.experts
+    g = torch.Generator().manual_seed(seed)
     w_gate = (torch.randn(E, H, generator=g) / math.sqrt(H)).to(torch.bfloat16)
     bias = zipf_bias(E, args.skew, g).numpy()
-    gx = torch.Generator().manual_seed(seed + 5)
-    x = torch.randn(sample_tokens, H, generator=gx).to(torch.bfloat16)
     ge = torch.Generator().manual_seed(seed + 7)
     # bf16 on the host (2.6 GiB at C2); the oracle widens one expert at a time
     w1 = [(torch.randn(F, H, generator=ge) / math.sqrt(H)).to(torch.bfloat16) for _ in range(E)]
     w3 = [(torch.randn(F, H, generator=ge) / math.sqrt(H)).to(torch.bfloat16) for _ in range(E)]
     w2 = [(torch.randn(H, F, generator=ge) / math.sqrt(F)).to(torch.bfloat16) for _ in range(E)]
+    return w_gate, bias, w1, w3, w2
+
+
+def run_cpu(args, sample_tokens, reps, seed=0, weights=None):
+    """Times the CPU path (cpu_reference_step) on `sample_tokens` tokens of the
+    workload with every host thread. Returns (tokens/s, seconds per rep, threads)."""
+    import numpy as np
+    import torch
+    cores = host_cores()
+    torch.set_num_threads(cores)
+    E, k, n = args.experts, args.topk, args.ranks
+    w_gate, bias, w1, w3, w2 = weights or cpu_weights(args, seed)
+    gx = torch.Generator().manual_seed(seed + 5)
+    x = torch.randn(sample_tokens, args.hidden, generator=gx).to(torch.bfloat16)
     xb = x.view(torch.int16).numpy().view(np.uint16)
     wb = w_gate.view(torch.int16).numpy().view(np.uint16)
     times = []
@@ -176,17 +251,23 @@ def run_cpu(args, sample_tokens, reps, seed=0):
         cpu_reference_step(xb, wb, bias, w1, w3, w2, k, n, [e // (E // n) for e in range(E)])
         times.append(time.perf_counter() - t0)
     med = sorted(times)[len(times) // 2]
-    # the schedule on a full-size (16384-token) traffic matrix: the reference's own hot path
-    rng = np.random.default_rng(seed)
-    pop = 1.0 / (rng.permutation(n) + 1.0) ** args.skew
-    d = np.round(np.outer(np.full(n, args.tokens * k / n), pop / pop.sum()))
-    np.fill_diagonal(d, 0)
-    st = []
-    for _ in range(30):
-        t0 = time.perf_counter()
-        build_schedule_oracle(d)
-        st.append(time.perf_counter() - t0)
-    return sample_tokens / med, 1e3 * sorted(st)[len(st) // 2], med
+    return sample_tokens / med, med, cores
+
+
+def cpu_full_counts(args, weights, seed=0):
+    """The full workload's traffic matrix computed on the host (oracle router over
+    all T tokens of a CPU-generated input): what the reference arm schedules."""
+    import numpy as np
+    import torch
+    from oracle.oracle import pack_oracle, router_oracle
+    w_gate, bias = weights[0], weights[1]
+    gx = torch.Generator().manual_seed(seed + 9)
+    x = torch.randn(args.tokens, args.hidden, generator=gx).to(torch.bfloat16)
+    _, idx, _ = router_oracle(x.view(torch.int16).numpy().view(np.uint16),
+                              w_gate.view(torch.int16).numpy().view(np.uint16), bias, args.topk)
+    E, n = args.experts, args.ranks
+    counts, _, _ = pack_oracle(idx, [e // (E // n) for e in range(E)], n)
+    return counts
 
 
 def reference_arm(args):
@@ -196,18 +277,26 @@ def reference_arm(args):
         return 0
     sample = 256
     reps = max(1, args.steps)
+    weights = cpu_weights(args)
     for _ in range(min(args.warmup, 1)):
-        run_cpu(args, sample, 1)
-    tps, sched_ms, sec = run_cpu(args, sample, reps)
-    cores = os.cpu_count() or 1
+        run_cpu(args, sample, 1, weights=weights)
+    tps, sec, cores = run_cpu(args, sample, reps, weights=weights)
+    sched = reference_schedule_timing(cpu_full_counts(args, weights),
+                                      list(C4_BANDWIDTHS[:args.ranks]) if args.config == "c4" else None)
+    # the layer figure is the port (the reference has no token path); its schedule is the reference's own
+    kind = "port"
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": reps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload(args),
-            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": f"{sample} tokens of the C2 layer per step (router + traffic matrix + "
-                                       f"build_schedule restatement + fp32 SwiGLU experts + aggregation)",
-                             "build_schedule_ms_n8": sched_ms},
+            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": kind,
+                             "cpu_count": os.cpu_count(), "affinity": host_cores(),
+                             "sample": f"{sample} tokens of the layer per step: oracle router + traffic matrix, "
+                                       f"the schedule by moeplan.build_schedule (baseline/_ref), fp32 numpy "
+                                       f"SwiGLU experts + aggregation on {cores} threads",
+                             "schedule": sched,
+                             "schedule_impl": ("reference: moeplan.build_schedule from baseline/_ref"
+                                               if reference_package() is not None else "port")},
             "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -250,28 +339,42 @@ def library_alltoall(layer, x, args, world, rank, stream, reps=5):
         torch.cuda.synchronize()
         return {"torch_index_select_us": ev[0].elapsed_time(ev[1]) / reps * 1e3, "rows": int(idx.numel()),
                 "note": "one gather kernel moving every dispatched row into receive order (all ranks on one GPU)"}
-    if layer.n_local != 1:
-        return {"unavailable": "NCCL baseline needs one rank per GPU"}
-    g = layer.rank_base
-    nsend = int(counts[g].sum())
-    lst = layer.send_list[0, :nsend].long()
-    recv = torch.empty(int(counts[:, g].sum()), x.shape[1], dtype=x.dtype, device=x.device)
+    if os.environ.get("AURORA_BENCH_SAME_GPU", "0") == "1":
+        return {"unavailable": "processes share one GPU (gloo host collectives): no NCCL"}
+    # one process per GPU driving n_local ranks: the unscheduled NCCL alltoallv at process
+    # granularity -- every row from this process's ranks to process q's ranks in one split
+    # (rank order, then send-list order), rows between ranks of the same process included
+    nl, rb, P = layer.n_local, layer.rank_base, n // layer.n_local
+    idx, in_split, out_split = [], [], []
+    for q in range(P):
+        dst = range(q * nl, (q + 1) * nl)
+        for i in range(rb, rb + nl):
+            for j in dst:
+                idx.append(sl[i - rb, soff[i, j]:soff[i, j] + counts[i, j]] + (i - rb) * Tr)
+        in_split.append(int(sum(counts[i, j] for i in range(rb, rb + nl) for j in dst)))
+        out_split.append(int(sum(counts[i, j] for i in range(q * nl, (q + 1) * nl) for j in range(rb, rb + nl))))
+    lst = torch.from_numpy(np.concatenate(idx).astype(np.int64)).to(x.device)
+    recv = torch.empty(sum(out_split), x.shape[1], dtype=x.dtype, device=x.device)
     tot = 0.0
     for r_ in range(reps + 1):
         dist.barrier()
         torch.cuda.synchronize()
         ev[0].record(stream)
         send = torch.index_select(x, 0, lst)
-        c = layer.counts.cpu()  # alltoallv needs the split sizes on the host
-        dist.all_to_all_single(recv, send, output_split_sizes=c[:, g].tolist(), input_split_sizes=c[g].tolist())
+        c = layer.counts.cpu()  # alltoallv needs the split sizes on the host (a D2H sync every step)
+        ins = [int(c[rb:rb + nl, q * nl:(q + 1) * nl].sum()) for q in range(P)]
+        outs = [int(c[q * nl:(q + 1) * nl, rb:rb + nl].sum()) for q in range(P)]
+        dist.all_to_all_single(recv, send, output_split_sizes=outs, input_split_sizes=ins)
         ev[1].record(stream)
         torch.cuda.synchronize()
         if r_:
             tot += ev[0].elapsed_time(ev[1])
     t = torch.tensor([tot / reps * 1e3], dtype=torch.float64, device=x.device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"nccl_alltoallv_us": float(t.item()),
-            "note": "pack (index_select) + D2H split sizes + dist.all_to_all_single, max over ranks"}
+    return {"nccl_alltoallv_us": float(t.item()), "ranks_per_gpu": nl,
+            "note": "pack (index_select) + D2H split sizes + dist.all_to_all_single between processes "
+                    "(one split per GPU, its ranks' rows back to back), max over ranks",
+            "symm_mem_all_to_all_vdev": "unavailable: needs NVSHMEM (not in this image)"}
 
 
 def baseline_schedules(layer, x, sp, stream, reps=3):
@@ -311,13 +414,16 @@ def baseline_schedules(layer, x, sp, stream, reps=3):
     return out
 
 
+GEMM_CAPTURE = "profiles/r02_ncu_gemm.json"
+
+
 def gemm_traffic(args):
     """DRAM bytes (read + write) of the expert GEMM launches of one C2 step,
     from the committed ncu --set full capture; None for other workloads."""
     if args.config != "c2":
         return None
     try:
-        rec = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full.json")))["grouped_gemm_2sm_kernel"]
+        rec = json.load(open(os.path.join(ROOT, GEMM_CAPTURE)))["grouped_gemm_2sm_kernel"]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = 0.0
         for launch in rec:
@@ -484,6 +590,9 @@ def main():
         if same_gpu:
             dist.init_process_group("gloo")
         else:
+            # NCCL INIT lines on stderr: which ranks / GPUs / transports the run used
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     n = args.ranks
     if n % world:
@@ -578,9 +687,16 @@ def main():
         time.sleep(0.3)
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
+        # the dominant kernels' window inside every timed step: the layer records these two
+        # events on its stream right after the dispatch launch and after GEMM2 (GEMM1 with the
+        # SwiGLU epilogue, then GEMM2 with the fused combine) -- no extra sync, same launches
+        gemm_ev = [{"dispatched": torch.cuda.Event(enable_timing=True),
+                    "experts_done": torch.cuda.Event(enable_timing=True)} for _ in range(args.steps)]
         t_start.record(stream)
-        for _ in range(args.steps):
+        for i_ in range(args.steps):
+            layer.trace = gemm_ev[i_]
             layer(x)  # the public forward: overlapped streams, no host sync
+        layer.trace = None
         t_end.record(stream)
         torch.cuda.synchronize()
         time.sleep(0.2)
@@ -588,6 +704,8 @@ def main():
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
     layer.check_status()
+    gemm_ms_steps = [e["dispatched"].elapsed_time(e["experts_done"]) for e in gemm_ev]
+    gemm_ms = sum(gemm_ms_steps) / len(gemm_ms_steps)
     ms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -699,11 +817,16 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peak_tf = peaks.get("bf16_tflops_sustained")
-    peak_src = "measured (MEASURED_PEAKS.json bf16_tflops_sustained)"
+    # peak: the timed region is a short burst right after the warm-up (< 1 s of GEMMs), so the
+    # burst figure applies; a window long enough for the 1 kW limiter to settle would use the
+    # sustained one (B200_PROFILING.md)
+    window_s = gemm_ms * args.steps * 1e-3
+    regime = "burst" if window_s < 1.0 else "sustained"
+    peak_tf = peaks.get("bf16_tflops" if regime == "burst" else "bf16_tflops_sustained")
+    peak_src = f"measured (MEASURED_PEAKS.json {'bf16_tflops' if regime == 'burst' else 'bf16_tflops_sustained'})"
     if peak_tf is None:
-        peak_tf, peak_src = 1400.0, "fallback (B200_PROFILING.md sustained)"
-    achieved_tf = gemm_flops / (stage_ms["experts"] * 1e-3) / 1e12
+        peak_tf, peak_src = (1650.0 if regime == "burst" else 1400.0), f"fallback (B200_PROFILING.md {regime})"
+    achieved_tf = gemm_flops / (gemm_ms * 1e-3) / 1e12
     off = counts.copy()
     np.fill_diagonal(off, 0)
     bw_arr = np.asarray(bws if bws is not None else [1.0] * n, dtype=float)
@@ -763,14 +886,23 @@ def main():
             "bottleneck_gbs_combine": bmax_tokens * row_bytes / (stage_ms["combine"] * 1e-3) / 1e9,
             "bound_basis": "max row / column sum of d_ij / min(B_i, B_j) (commsched.py:181-195; tokens when B = 1) "
                            "x hidden x 2 B / 900 GB/s NVLink per direction (the paper's big switch)",
-            "transport": "NVSwitch peer stores" if world > 1 else
+            "transport": ("CUDA IPC between processes sharing one GPU (AURORA_BENCH_SAME_GPU=1: not NVLink)"
+                          if same_gpu else "NVSwitch peer stores (CUDA IPC mappings of the peers' HBM)")
+                         if world > 1 else
                          "loopback: all 8 ranks on one GPU, peer stores land in local HBM (not NVLink)",
         },
         "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved_tf / peak_tf, "traffic": gemm_traffic(args),
-                     "traffic_source": "profiles/r01_ncu_full.json (ncu --set full, both GEMM launches, C2)",
-                     "kernel": "aurora grouped_gemm_2sm_kernel (GEMM1 SwiGLU + GEMM2), "
-                     "FLOPs = sum over (token, expert) rows of 2 * 3 * H * F", "peak_source": peak_src,
+                     "traffic_source": "not measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of "
+                                       "both GEMM launches from the committed ncu --set full capture ("
+                                       + GEMM_CAPTURE + ", C2)",
+                     "kernel": "aurora grouped_gemm_2sm_kernel x2 (GEMM1 + SwiGLU, GEMM2 + fused combine), "
+                     "FLOPs = sum over (token, expert) rows of 2 * 3 * H * F",
+                     "timing": "CUDA events on the layer's stream around the two GEMM launches inside every timed "
+                               "step (mean over the timed steps)",
+                     "gemm_ms_per_step": gemm_ms, "gemm_share_of_step": gemm_ms / ms_per_step,
+                     "regime": regime, "peak_source": peak_src,
+                     "frac_of_sustained": achieved_tf / float(peaks.get("bf16_tflops_sustained") or 1400.0),
                      "flops_per_step": gemm_flops},
         # route, pack, K2, engine, 2 GEMM, engine, aggregate (+ sort x3, gather, reduce with G > 1;
         # + local engine / GEMM pair when overlapped)
@@ -784,11 +916,16 @@ def main():
         "timeline_ms": layer.timeline(x),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, sched_ms, sec = run_cpu(args, 256, 3)
-        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": os.cpu_count() or 1, "kind": "port",
-                                "sample": "256 tokens of the C2 layer per rep, median of 3 (oracle router + "
-                                          "build_schedule restatement + fp32 numpy experts + aggregation)",
-                                "build_schedule_ms_n8": sched_ms}
+        weights = cpu_weights(args)
+        tps, sec, cores = run_cpu(args, 256, 3, weights=weights)
+        line["cpu_baseline"] = {
+            "value": tps, "unit": "tokens/s", "cores": cores, "cpu_count": os.cpu_count(), "affinity": host_cores(),
+            "kind": "port",
+            "sample": "256 tokens of the layer per rep, median of 3: oracle router + traffic matrix, the schedule by "
+                      "moeplan.build_schedule (baseline/_ref), fp32 numpy SwiGLU experts + aggregation",
+            "schedule": reference_schedule_timing(counts, list(bws) if bws is not None else None),
+            "schedule_impl": ("reference: moeplan.build_schedule from baseline/_ref"
+                              if reference_package() is not None else "port")}
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

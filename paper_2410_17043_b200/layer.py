@@ -648,7 +648,7 @@ class AuroraMoELayer:
         s = int(main.cuda_stream)
         tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
         def mark(k, st):
-            if tr:
+            if tr and k in tr:
                 tr[k].record(st)
                 self._marked.add(k)
         self._marked = set()
