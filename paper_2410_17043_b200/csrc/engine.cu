@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     // does entry k end the open run into `peer_`? 1 yes, 0 no, -1 not known yet
     auto run_ends_at = [&](int k_, int peer_) -> int {
       if (k_ + 1 < sh.known) {
+        __threadfence_block();  // acquire side of the producer's fence + `known` store
         const int4 nx = sh.ring[(k_ + 1) & (RING - 1)];
         return (nx.x == peer_ && nx.w < 0) ? 0 : 1;
       }

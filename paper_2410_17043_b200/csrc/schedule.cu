@@ -414,11 +414,11 @@ __device__ __forceinline__ bool ring_test(uint64_t* bar) {
 }
 
 template <int NB>
-struct RawRing {  // the flags lead so every NB shares their offsets
+struct RawRing {
   static constexpr int R = NB * NB - 2 * NB + 2;
-  volatile int published;  // raw phases ready (informational; the barriers carry the hand-off)
-  volatile int done;       // 1 + status once warp 0 has finished
-  double dur[R];
+  // dur[r] < 0 ends the stream: warp 0 finished after r raw phases with status -1 - dur[r].
+  // Every hand-off, the final one included, goes through the mbarrier of its slot.
+  double dur[R + 1];
   signed char perm[R * NB];
 };
 
@@ -628,9 +628,8 @@ __device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V>
     if (p.n_raw) *p.n_raw = nr;
     if (p.prof)
       for (int q = 0; q < 3; q++) p.prof[q] = cy[q];
-    ring.published = nr;
-    __threadfence_block();
-    ring.done = 1 + status;
+    ring.dur[nr] = -1.0 - (double)status;  // end of stream, through slot nr's barrier like a phase
+    ring_arrive(&ready[nr]);
   }
 }
 
@@ -681,26 +680,15 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
     }
   };
   for (;;) {
-    int dn = 0;
-    if (r >= avail) {  // wait for warp 0: raw phase r ready, or warp 0 finished
-      int got = 0;
-      if (lane == 0) {
-        for (;;) {
-          if (ring_test(&ready[r])) { got = 1; break; }
-          dn = ring.done;
-          if (dn) {
-            __threadfence_block();
-            got = r < ring.published;  // finished after publishing r?
-            if (got) while (!ring_test(&ready[r])) {
-              }
-            break;
-          }
+    if (r >= avail) {  // wait for warp 0: raw phase r, or the end of the stream, in slot r
+      if (lane == 0)
+        while (!ring_test(&ready[r])) {
         }
-      }
-      got = __shfl_sync(0xffffffffu, got, 0);
-      dn = __shfl_sync(0xffffffffu, dn, 0);
-      if (!got) {
-        if (dn > 1) status = dn - 1;
+      __syncwarp();  // lane 0's acquire orders the slot's contents for the whole warp
+      const double dr = ring.dur[r];
+      if (dr < 0.0) {
+        const int st = (int)(-1.0 - dr);
+        if (st != AURORA_OK) status = st;
         break;
       }
       avail = r + 1;
@@ -814,10 +802,6 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
     status_s = AURORA_OK;
     np_s = 0;
     bmax_s = 0.0;
-    if constexpr (TWO) {
-      ring.published = 0;
-      ring.done = 0;
-    }
   }
   if constexpr (TWO) {
     for (int q = tid; q < RING_BARS; q += 64)
@@ -974,14 +958,10 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
       ChunkLane cl;
       chunk_finish(p, cc, cl, lane);  // empty schedule: no runs
     }
-    if (warp == 1 && lane == 0) {
-      status_s = status;
-      np_s = np_;
-    }
-    __syncthreads();
-    status = status_s;
-    np_ = np_s;
+    __syncthreads();  // warp 0's outputs (raw phases, n_raw) are complete before DONE is published
     if (warp == 1) {
+      status = __shfl_sync(0xffffffffu, status, 0);
+      np_ = __shfl_sync(0xffffffffu, np_, 0);
       if (lane == 0) {
         *p.status = status;
         *p.n_phases = status == AURORA_OK ? np_ : 0;
