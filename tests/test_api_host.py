@@ -218,3 +218,21 @@ def test_reference_error_classes_host(moeplan, monkeypatch):
     monkeypatch.undo()
     with pytest.raises(ValueError, match="n <= 32"):  # beyond the device scheduler: a clear error, no fallback
         A.build_schedule(A.TrafficMatrix(np.ones((33, 33))), A.ClusterSpec.uniform(33))
+
+
+def test_measured_rows_in_reference_csv_format(moeplan):
+    """report.csv_text writes the reference's experiment CSV (experiment.py:26-39,
+    314-320) byte for byte: the same rows built as moeplan.experiment.ResultRow
+    and passed to its own csv_text give identical text; measured_rows reads a
+    committed bench line."""
+    import json
+    import os
+    import moeplan.experiment as mexp
+    from paper_2410_17043_b200 import report
+    assert report.CSV_COLUMNS == mexp.CSV_COLUMNS
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    line = json.loads(open(os.path.join(root, "profiles", "r02_bench_c2.json")).read().strip().splitlines()[-1])
+    rows = report.measured_rows(line)
+    assert [r.strategy for r in rows][0] == "aurora" and len(rows) >= 1
+    ref_rows = [mexp.ResultRow(**{c: getattr(r, c) for c in report.CSV_COLUMNS}) for r in rows]
+    assert report.csv_text(rows) == mexp.csv_text(ref_rows)

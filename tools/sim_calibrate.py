@@ -7,9 +7,10 @@ time unit (one token over one link direction at B = 1, i.e. hidden x 2 B /
 (sim.py:130-154) with Aurora's build_schedule and with the SJF / RCS baselines
 (baselines.py:91-109) -- to predict the layer on 8 GPUs (one expert each).
 Runs in the build container, where the reference package is importable
-(PYTHONPATH=/root/reference/pkg/src); never on the GPU box.
+(PYTHONPATH=baseline/_ref or /root/reference/pkg/src); never on the GPU box. Also
+writes the experiment CSV (experiment.py:26-39) with measured and predicted rows.
 
-    PYTHONPATH=/root/reference/pkg/src python tools/sim_calibrate.py [bench.json] [out.json]
+    PYTHONPATH=baseline/_ref python tools/sim_calibrate.py [bench.json] [out.json]
 """
 import json
 import os
@@ -20,8 +21,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def main(src=os.path.join(ROOT, "profiles", "r01_bench_c2.json"),
-         dst=os.path.join(ROOT, "profiles", "r01_sim_calibration.json")):
+def main(src=os.path.join(ROOT, "profiles", "r02_bench_c2.json"),
+         dst=os.path.join(ROOT, "profiles", "r02_sim_calibration.json")):
     from moeplan import baselines as RB
     from moeplan.core import ClusterSpec, LayerProfile, TrafficMatrix
     from moeplan.sim import simulate_exclusive
@@ -65,6 +66,20 @@ def main(src=os.path.join(ROOT, "profiles", "r01_bench_c2.json"),
                       f"{line['ms_per_step'] * 1e3:.0f} us for all 8 ranks on one GPU")
     json.dump(out, open(dst, "w"), indent=1)
     print(out["summary"])
+    # the experiment CSV (experiment.py:26-39): measured loopback rows (this repo's report.py)
+    # followed by the reference simulator's 8-GPU predictions as its own ResultRow objects
+    import moeplan.experiment as mexp
+    sys.path.insert(0, ROOT)
+    from paper_2410_17043_b200.report import measured_rows
+    rows = measured_rows(line)
+    for name, pr in out["predicted_8gpu"].items():
+        rows.append(mexp.ResultRow("exclusive-homo", f"{name}-predicted-8gpu", 0, n, 0.0, cfg["seed"],
+                                   pr["spans_us"]["N"][1] / tau_us - pr["spans_us"]["N"][0] / tau_us,
+                                   pr["spans_us"]["C"][1] / tau_us - pr["spans_us"]["C"][0] / tau_us,
+                                   pr["layer_us"] / tau_us, pr["utilization"]))
+    csv_path = os.path.splitext(dst)[0] + ".csv"
+    open(csv_path, "w").write(mexp.csv_text(rows))
+    print("wrote", os.path.relpath(csv_path, ROOT))
 
 
 if __name__ == "__main__":
