@@ -49,14 +49,15 @@ def parse():
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--ranks", type=int, default=8, help="expert-parallel ranks (GPUs of the modelled cluster)")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c3h", "c4", "c5"],
                     help="c2: Mixtral-8x7B layer (the headline); c3: C2's model colocated with a 16-expert "
                          "top-2 model (hidden 4096, FFN 7168; the config leaves F open) on the same 8 ranks by "
                          "Aurora's colocation plan (single GPU only); c4: C2 on an emulated heterogeneous "
                          "cluster (bandwidths 100/80/50/40 x2, PAPER.md:666; placement by "
                          "assign_exclusive_hetero; copy CTAs per rank follow bandwidth); c5: DeepSeek-style "
                          "64 experts top-6, hidden 5120, FFN 1536 (DeepSeek-V2 expert size; the config "
-                         "leaves F open)")
+                         "leaves F open); c3h: C3 on C4's emulated heterogeneous cluster, placed by "
+                         "colocate_heterogeneous (placement.py:129-157)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -72,12 +73,13 @@ C4_BANDWIDTHS = (1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4)  # PAPER.md:666 ratios 
 
 def workload(args):
     name = {"c2": "C2 Mixtral-8x7B MoE layer", "c3": "C3 Mixtral-8x7B + 16-expert top-2 layers colocated",
+            "c3h": "C3 colocated layers on C4's heterogeneous emulation (colocate_heterogeneous)",
             "c4": "C4 Mixtral-8x7B MoE layer, heterogeneous emulation",
             "c5": "C5 DeepSeek-style 64-expert top-6 MoE layer"}[args.config]
     return {"workload": f"{name} (EP over {args.ranks} ranks)", "hidden": args.hidden, "ffn": args.ffn,
             "experts": args.experts, "top_k": args.topk, "tokens": args.tokens, "ranks": args.ranks,
             "skew": args.skew, "seed": args.seed, "gpus": args.gpus,
-            **({"bandwidths": list(C4_BANDWIDTHS)} if args.config == "c4" else {}),
+            **({"bandwidths": list(C4_BANDWIDTHS)} if args.config in ("c4", "c3h") else {}),
             "l2": "inputs larger than L2 (x >= 128 MiB, expert weights >= 2.6 GiB read every step)"}
 
 
@@ -417,6 +419,49 @@ def baseline_schedules(layer, x, sp, stream, reps=3):
 GEMM_CAPTURE = "profiles/r02_ncu_gemm.json"
 
 
+def placement_effect(layer, cfg, plan, bws, x, stream, steps):
+    """C4: the Theorem-3 placement (assign_exclusive_hetero,
+    placement.py:46-60: the k-th most loaded expert on the k-th fastest rank) against
+    the identity placement on the same emulated cluster (per-rank copy CTAs and GEMM
+    CTA pairs in proportion to the ranks' bandwidth / compute scale). Steps alternate
+    between the two layers (same power state); per-rank GEMM work is reported too."""
+    import numpy as np
+    import torch
+    from paper_2410_17043_b200 import DeploymentPlan
+    from paper_2410_17043_b200.layer import AuroraMoELayer
+    ident = AuroraMoELayer(cfg, DeploymentPlan.identity(cfg.ranks), bandwidths=bws, compute_scales=bws)
+    layers = {"theorem3": layer, "identity": ident}
+    for L in layers.values():
+        for _ in range(2):
+            L(x)
+    torch.cuda.synchronize()
+    times = {k: [] for k in layers}
+    for _ in range(3):
+        for name, L in layers.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                L(x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            L.check_status()
+            times[name].append(e0.elapsed_time(e1) / steps)
+    out = {}
+    for name, L in layers.items():
+        rows = L.counts.cpu().numpy().sum(axis=0).astype(float)   # rows each rank's expert processes
+        part = np.diff(L.gemm_part.cpu().numpy())                  # CTA pairs per rank
+        tiles = np.ceil(rows / 256)                                # m-tiles (256 rows) per rank
+        out[name] = {"assignment": list(L.plan.assignment_a), "ms_per_step": sorted(times[name])[1],
+                     "ms_per_step_runs": times[name], "rows_per_rank": rows.tolist(),
+                     "gemm_pairs_per_rank": part.tolist(),
+                     "gemm_critical_rank": int(np.argmax(tiles / part)),
+                     "gemm_work_ratio_max_over_mean": float((tiles / part).max() / (tiles.sum() / part.sum()))}
+    out["speedup_theorem3_vs_identity"] = out["identity"]["ms_per_step"] / out["theorem3"]["ms_per_step"]
+    del ident
+    torch.cuda.empty_cache()
+    return out
+
+
 def gemm_traffic(args):
     """DRAM bytes (read + write) of the expert GEMM launches of one C2 step,
     from the committed ncu --set full capture; None for other workloads."""
@@ -475,7 +520,19 @@ def run_c3(args):
     del cal_a, cal_b, cal_s
     torch.cuda.empty_cache()
     cplan = plan_colocation(counts_a, slot_counts, slots)
-    pair = ColocatedLayers(cfg_a, cfg_b, cplan)
+    hetero = args.config == "c3h"
+    kw, homo_pair, bws = {}, None, None
+    if hetero:  # C4's cluster: per-rank copy CTAs and GEMM CTA pairs follow bandwidth / compute scale
+        from paper_2410_17043_b200 import ClusterSpec, GpuSpec
+        from paper_2410_17043_b200.colocation import expert_work, plan_colocation_hetero
+        bws = C4_BANDWIDTHS[:n]
+        kw = {"bandwidths": bws, "compute_scales": bws}
+        cluster = ClusterSpec(tuple(GpuSpec(b, b) for b in bws))
+        homo_plan = cplan
+        cplan = plan_colocation_hetero(counts_a, slot_counts, slots, cluster, expert_work(4096, 14336),
+                                       expert_work(4096, 7168))
+        homo_pair = ColocatedLayers(cfg_a, cfg_b, homo_plan, **kw)
+    pair = ColocatedLayers(cfg_a, cfg_b, cplan, **kw)
     for _ in range(args.warmup):
         pair(xa, xb)
     torch.cuda.synchronize()
@@ -562,6 +619,32 @@ def run_c3(args):
                                 "model b's (copy-engine streams, double-buffered device inputs / outputs)"},
             "clocks": clocks.summary(0),
             "timeline_ms": {"a": pair.a.timeline(xa), "b": pair.b.timeline(xb)}}
+    if hetero:
+        # the same two models on the same emulated cluster, pairs placed by the homogeneous plan
+        # (pair p on GPU p) vs colocate_heterogeneous's stage 2; alternated for equal power state
+        res = {"colocate_heterogeneous": [], "homogeneous_plan": []}
+        for p_ in (pair, homo_pair):
+            for _ in range(2):
+                p_(xa, xb)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            for name, p_ in (("colocate_heterogeneous", pair), ("homogeneous_plan", homo_pair)):
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(st)
+                for _ in range(args.steps):
+                    p_(xa, xb)
+                f1.record(st)
+                torch.cuda.synchronize()
+                p_.check_status()
+                res[name].append(f0.elapsed_time(f1) / args.steps)
+        med = {k: sorted(v)[1] for k, v in res.items()}
+        line["placement"] = {
+            "colocate_heterogeneous": {"ms_per_step": med["colocate_heterogeneous"], "runs": res["colocate_heterogeneous"],
+                                       "gpu_of_a": list(cplan.gpu_of_a), "gpu_of_b": list(cplan.gpu_of_b)},
+            "homogeneous_plan": {"ms_per_step": med["homogeneous_plan"], "runs": res["homogeneous_plan"],
+                                 "gpu_of_a": list(homo_pair.cplan.gpu_of_a), "gpu_of_b": list(homo_pair.cplan.gpu_of_b)},
+            "speedup": med["homogeneous_plan"] / med["colocate_heterogeneous"],
+            "work_model": "LayerProfile work in the reference's time unit from measured rates (colocation.expert_work)"}
     print(json.dumps(line))
     return 0
 
@@ -570,7 +653,7 @@ def main():
     args = apply_preset(parse())
     if args.impl == "reference":
         return reference_arm(args)
-    if args.config == "c3":
+    if args.config in ("c3", "c3h"):
         return run_c3(args)
     import numpy as np
     import torch
@@ -616,7 +699,10 @@ def main():
         plan = assign_exclusive_hetero(loads, ClusterSpec(tuple(GpuSpec(b, b) for b in bws)))
         del calib
         torch.cuda.empty_cache()
-    layer = AuroraMoELayer(cfg, plan, rank_base=rank * n_local, n_local=n_local, bandwidths=bws)
+    # C4: each rank also gets a compute share in proportion to its GpuSpec compute_scale (= its
+    # bandwidth ratio): the expert GEMMs' CTA pairs are partitioned among the ranks
+    layer = AuroraMoELayer(cfg, plan, rank_base=rank * n_local, n_local=n_local, bandwidths=bws,
+                           compute_scales=bws)
     if world > 1:
         from paper_2410_17043_b200 import dist as adist
         adist.connect_peers(layer)
@@ -915,6 +1001,8 @@ def main():
         "clocks": clocks.summary(local_rank),
         "timeline_ms": layer.timeline(x),
     }
+    if args.config == "c4" and world == 1:
+        line["placement"] = placement_effect(layer, cfg, plan, bws, x, stream, args.steps)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         weights = cpu_weights(args)
         tps, sec, cores = run_cpu(args, 256, 3, weights=weights)

@@ -302,7 +302,8 @@ int aurora_aggregate(const void* ret_buf, int64_t ret_rank_stride_rows, const in
  *   y = (silu(x W1^T) * (x W3^T)) W2^T, fp32 accumulate. */
 int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                       void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
-                      int64_t cap, int H, int F, int32_t* tile_ctr, int num_sms, void* stream);
+                      int64_t cap, int H, int F, const int32_t* cluster_part, int32_t* tile_ctr,
+                      int num_sms, void* stream);
 
 /* aurora_expert_ffn_combine: the same FFN (one expert per rank: group g is
  * expert rank rank_base + g, all received rows) with the combine fused into
@@ -322,7 +323,8 @@ int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2
                               void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
                               void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                               const int32_t* roff, int n, int rank_base, int32_t* const* ctrs,
-                              int32_t* ticket, int sys, int32_t* tile_ctr, int num_sms, void* stream);
+                              int32_t* ticket, int sys, const int32_t* cluster_part, int32_t* tile_ctr,
+                              int num_sms, void* stream);
 
 /* aurora_expert_ffn_packed_scatter: the packed FFN of the grouped dispatch with the
  * pre-reduction of single-expert rows folded into GEMM2's epilogue. ginfo [a_rows]
@@ -338,14 +340,16 @@ int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const v
                                      int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
                                      void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                                      const int32_t* roff, int n, int rank_base, void* ybuf, int64_t ycap,
-                                     int to_ret, int sys, int32_t* tile_ctr, int num_sms, void* stream);
+                                     int to_ret, int sys, const int32_t* cluster_part, int32_t* tile_ctr,
+                                     int num_sms, void* stream);
 
 /* Same FFN with the groups packed back to back (a rank hosting several
  * experts): group g's rows are a_buf rows [g_off[g], g_off[g] + g_rows[g]);
  * a_rows = rows allocated in a_buf / h_buf / y_buf. */
 int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                              void* y_buf, const int32_t* g_off, const int32_t* g_rows, int G,
-                             int64_t a_rows, int H, int F, int32_t* tile_ctr, int num_sms, void* stream);
+                             int64_t a_rows, int H, int F, const int32_t* cluster_part, int part_groups,
+                             int32_t* tile_ctr, int num_sms, void* stream);
 
 /* Several experts per rank (E > n). After the dispatch, receiver rows of the
  * local ranks (rank r_local: rows r_local*cap + [0, rtot[rank_base+r_local]))
@@ -380,7 +384,14 @@ int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void*
 /* skip_single (both): rows whose (token, rank) has exactly one local expert were
  * finished by aurora_expert_ffn_packed_scatter; only the others are reduced. */
 
-/* tile_ctr (every expert FFN / grouped GEMM entry point): two int32 owned by the caller,
+/* cluster_part (expert FFN entry points; NULL = off): emulated per-rank compute for heterogeneous
+ * clusters (configs C4, C3 on C4's cluster) -- R + 1 ints for R ranks, clusters (CTA pairs,
+ * num_sms / 2 of them) [cluster_part[r], cluster_part[r + 1]) serve rank r's groups only (its
+ * experts: groups r * Gp .. r * Gp + Gp - 1, Gp = 1, experts_per_rank or part_groups), round robin
+ * over their tiles, so a rank's GEMM time follows its share of the GPU like experts on a GPU of that
+ * speed (ClusterSpec compute_scale, reference core.py:135-191; placement.py:46-60 / 129-157 decide
+ * which experts land where). cluster_part[R] must equal num_sms / 2.
+ * tile_ctr (every expert FFN / grouped GEMM entry point): two int32 owned by the caller,
  * zero before first use and re-armed by each launch's last cluster -- the dynamic tile
  * order's {next tile, clusters done} pair. One per stream whose GEMM launches may run
  * concurrently with another's (a layer keeps one per stream it launches on); NULL

@@ -36,23 +36,24 @@ _SIGNATURES = {
     "aurora_engine_ctas": [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp, _c_i64, _vp, _vp],
-    "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _c_int, _vp],
+    "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _vp, _c_int, _vp],
     "aurora_grouped_gemm": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "aurora_expert_ffn_combine": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _vp, _vp,
-                                  _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp],
+                                  _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp],
     "aurora_exchange_counts": [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp, _vp],
     "aurora_expert_hist": [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp],
     "aurora_pack_grouped": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                             _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
     "aurora_combine_wait": [_vp, _c_int, _c_int, _c_int, _c_int, _c_i64, _vp, _vp],
-    "aurora_expert_ffn_packed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _c_int, _vp],
+    "aurora_expert_ffn_packed": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _c_int, _vp,
+                                 _c_int, _vp],
     "aurora_expert_sort": [_vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp,
                            _vp, _c_int, _vp],
     "aurora_gather_rows": [_vp, _vp, _vp, _vp, _c_i64, _c_int, _vp],
     "aurora_expert_reduce": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "aurora_expert_ffn_packed_scatter": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp,
                                          _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_i64, _c_int, _c_int,
-                                         _vp, _c_int, _vp],
+                                         _vp, _vp, _c_int, _vp],
     "aurora_expert_reduce_combine": [_vp, _vp, _vp, _c_i64, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp,
                                      _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],

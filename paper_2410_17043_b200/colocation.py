@@ -22,9 +22,10 @@ import numpy as np
 
 from .commsched import bmax_heterogeneous
 from .core import DeploymentPlan, LayerProfile, TrafficMatrix, combine_colocated
-from .placement import colocate_homogeneous
+from .placement import colocate_heterogeneous, colocate_homogeneous
 
-__all__ = ["lina_slots", "ColocationPlan", "plan_colocation", "combined_bmax", "ColocatedLayers"]
+__all__ = ["lina_slots", "ColocationPlan", "plan_colocation", "plan_colocation_hetero", "combined_bmax",
+           "ColocatedLayers", "expert_work"]
 
 
 def lina_slots(expert_loads) -> tuple:
@@ -65,6 +66,32 @@ def plan_colocation(counts_a, slot_counts_b, slots) -> ColocationPlan:
     gpu_of_b = [0] * (2 * len(slots))
     for s, (e1, e2) in enumerate(slots):
         gpu_of_b[e1] = gpu_of_b[e2] = plan.assignment_b[s]
+    return ColocationPlan(plan, tuple(slots), tuple(plan.assignment_a), tuple(gpu_of_b))
+
+
+def expert_work(hidden: int, ffn: int, gemm_tflops: float = 1480.0, gate_agg_us: float = 13.4) -> dict:
+    """LayerProfile work parameters (core.py:194-221) in the reference's time unit -- one
+    token over one link direction, hidden x 2 B / 900 GB/s -- from measured device rates:
+    an expert row costs 2 * 3 * hidden * ffn FLOPs at the expert GEMMs' measured rate
+    (profiles/r02_bench_c2.json: 1.48 PFLOP/s), gate + aggregation ~13 us per rank
+    (router + pack + aggregate of one rank's 2048 tokens)."""
+    tau_us = hidden * 2 / 900e9 * 1e6
+    row_us = 6.0 * hidden * ffn / (gemm_tflops * 1e12) * 1e6
+    return {"gate_work": gate_agg_us / 2 / tau_us, "agg_work": gate_agg_us / 2 / tau_us,
+            "ffn_work_per_token": row_us / tau_us, "ffn_base_work": 0.0}
+
+
+def plan_colocation_hetero(counts_a, slot_counts_b, slots, cluster, work_a: dict, work_b: dict) -> ColocationPlan:
+    """Aurora's heterogeneous colocation (placement.py:129-157): the homogeneous pairing,
+    then pairs onto GPUs by bottleneck matching on colocated_pair_cost (sim.py:331-356),
+    which weighs each pair's expert work by the GPU's compute_scale and its tokens by the
+    GPU's bandwidth. ``work_*``: LayerProfile work fields of each model (expert_work)."""
+    pa = LayerProfile(d_first=TrafficMatrix(np.asarray(counts_a, dtype=float)), **work_a)
+    pb = LayerProfile(d_first=TrafficMatrix(np.asarray(slot_counts_b, dtype=float)), **work_b)
+    plan = colocate_heterogeneous(pa, pb, cluster)
+    gpu_of_b = [0] * (2 * len(slots))
+    for s_, (e1, e2) in enumerate(slots):
+        gpu_of_b[e1] = gpu_of_b[e2] = plan.assignment_b[s_]
     return ColocationPlan(plan, tuple(slots), tuple(plan.assignment_a), tuple(gpu_of_b))
 
 

@@ -27,7 +27,7 @@
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
-                              const AuroraScatterArgs* scatter);
+                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp);
 
 namespace {
 
@@ -360,14 +360,16 @@ bool use_pair_kernel() {
 int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start,
                    const int32_t* m_rows, int G,
                    int64_t cap, int64_t map_rows, int N, int K, int epilogue, int32_t* tile_ctr, int num_sms,
-                   cudaStream_t stream, const AuroraScatterArgs* scatter = nullptr) {
+                   cudaStream_t stream, const AuroraScatterArgs* scatter = nullptr,
+                   const int32_t* cluster_part = nullptr, int part_gp = 1) {
   // cap > 0: group g owns rows [g*cap, (g+1)*cap); cap == 0: groups packed,
   // m_start[g] absolute, map_rows = rows of the A buffer
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (use_pair_kernel())
     return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, tile_ctr, num_sms,
-                                     stream, scatter);
+                                     stream, scatter, cluster_part, part_gp);
+  if (cluster_part) return AURORA_EINVAL;  // partitioned (emulated per-rank compute): pair kernel only
   if (scatter) return AURORA_EINVAL;  // the fused combine lives in the CTA-pair kernel
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
@@ -409,14 +411,15 @@ extern "C" int aurora_grouped_gemm(const void* a, const void* b, void* c, const 
 extern "C" int aurora_expert_ffn(const void* a_buf, const void* w13, const void* w2, void* h_buf,
                                  void* y_buf, const int32_t* m_start, const int32_t* m_rows, int G,
                                  int64_t cap, int H,
-                                 int F, int32_t* tile_ctr, int num_sms, void* stream) {
+                                 int F, const int32_t* cluster_part, int32_t* tile_ctr, int num_sms,
+                                 void* stream) {
   // h = silu(x W1^T) * (x W3^T): N = 2F interleaved, K = H
   int rc = launch_grouped(a_buf, w13, h_buf, m_start, m_rows, G, cap, 0, 2 * F, H, 1, tile_ctr, num_sms,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, nullptr, cluster_part);
   if (rc != AURORA_OK) return rc;
   // y = h W2^T: N = H, K = F
   return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, nullptr, cluster_part);
 }
 
 extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2,
@@ -425,14 +428,15 @@ extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, con
                                          const int32_t* counts, const int32_t* soff,
                                          const int32_t* roff, int n, int rank_base,
                                          int32_t* const* ctrs, int32_t* ticket, int sys,
-                                         int32_t* tile_ctr, int num_sms, void* stream) {
+                                         const int32_t* cluster_part, int32_t* tile_ctr, int num_sms,
+                                         void* stream) {
   if (!ret_bufs || !counts || !soff || !roff || !ctrs || !ticket) return AURORA_EINVAL;
   int rc = launch_grouped(a_buf, w13, h_buf, nullptr, m_rows, G, cap, 0, 2 * F, H, 1, tile_ctr, num_sms,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, nullptr, cluster_part);
   if (rc != AURORA_OK) return rc;
   const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
   return launch_grouped(h_buf, w2, y_buf, nullptr, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, &sc);
+                        (cudaStream_t)stream, &sc, cluster_part);
 }
 
 extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const void* w2, void* h_buf,
@@ -440,10 +444,11 @@ extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w
                                                 int64_t a_rows, int H, int F, const void* ginfo, int experts_per_rank,
                                                 void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                                                 const int32_t* roff, int n, int rank_base, void* ybuf,
-                                                int64_t ycap, int to_ret, int sys, int32_t* tile_ctr, int num_sms, void* stream) {
+                                                int64_t ycap, int to_ret, int sys, const int32_t* cluster_part,
+                                                int32_t* tile_ctr, int num_sms, void* stream) {
   if (!ginfo || !ret_bufs || !counts || !soff || !roff || !ybuf || experts_per_rank < 1) return AURORA_EINVAL;
   int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, tile_ctr, num_sms,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, nullptr, cluster_part, experts_per_rank);
   if (rc != AURORA_OK) return rc;
   AuroraScatterArgs sc{ret_bufs, counts, soff, roff, nullptr, nullptr, n, rank_base, sys ? 1 : 0};
   sc.ginfo = ginfo;
@@ -452,16 +457,17 @@ extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w
   sc.ycap = ycap;
   sc.to_ret = to_ret ? 1 : 0;
   return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, &sc);
+                        (cudaStream_t)stream, &sc, cluster_part, experts_per_rank);
 }
 
 extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
                                         void* h_buf, void* y_buf, const int32_t* g_off,
                                         const int32_t* g_rows, int G, int64_t a_rows, int H, int F,
-                                        int32_t* tile_ctr, int num_sms, void* stream) {
+                                        const int32_t* cluster_part, int part_groups, int32_t* tile_ctr,
+                                        int num_sms, void* stream) {
   int rc = launch_grouped(a_buf, w13, h_buf, g_off, g_rows, G, 0, a_rows, 2 * F, H, 1, tile_ctr, num_sms,
-                          (cudaStream_t)stream);
+                          (cudaStream_t)stream, nullptr, cluster_part, part_groups);
   if (rc != AURORA_OK) return rc;
   return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, nullptr, cluster_part, part_groups);
 }

@@ -65,6 +65,8 @@ struct Scatter {
 
 struct TileIter2 {
   int n_tiles_n, total;
+  int pg, plc, pnc, plo, phi;  // partitioned mode: this cluster's partition, index among its
+                               // clusters, their count, its tile range [plo, phi)
   int prefix[MAX_GROUPS + 1];
   int mt[MAX_GROUPS];
   int ms[MAX_GROUPS];
@@ -98,7 +100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
                             int epilogue, int group_m, const Scatter sc,
                             int32_t* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_c,
-                            int tma_out) {
+                            int tma_out, const int32_t* __restrict__ part, int part_gp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -133,6 +135,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     it.prefix[G] = acc;
     it.total = acc;
+    // partitioned mode (emulated per-rank compute): clusters [part[q], part[q+1]) serve partition q
+    // only -- groups [q * part_gp, (q + 1) * part_gp), one rank's experts -- round robin over its tiles
+    it.pg = -1;
+    if (part) {
+      for (int q = 0; q < G / part_gp; q++)
+        if (part[q] <= cluster_id && cluster_id < part[q + 1]) {
+          it.pg = q;
+          it.plc = cluster_id - part[q];
+          it.pnc = part[q + 1] - part[q];
+          it.plo = it.prefix[q * part_gp];
+          it.phi = it.prefix[(q + 1) * part_gp];
+        }
+    }
     const int sc_ranks = sc.ginfo ? G / sc.G : G;   // local ranks the table covers
     for (int q = 0; q < (sc.n ? sc_ranks * sc.n : 0); q++) {  // (local rank, sender) -> row block
       const int g = q / sc.n, src = q - g * sc.n, r = sc.rank_base + g;
@@ -166,11 +181,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc::fence_after();
   const uint32_t tmem_base = *tmem_base_s;
   const int k_blocks = K / BK;
-  const bool dyn = tile_ctr != nullptr;
+  const bool dyn = tile_ctr != nullptr && part == nullptr;
   // i-th tile of this cluster (-1: done). Static: round robin over clusters.
   // Dynamic: ring slot i % TRING, published by the leader's producer.
   auto next_tile = [&](int i, bool arrive) -> int {
     if (!dyn) {
+      if (part) {  // round robin over the partition's own clusters
+        if (it.pg < 0) return -1;
+        const int t = it.plo + it.plc + i * it.pnc;
+        return t < it.phi ? t : -1;
+      }
       const int t = cluster_id + i * n_clusters;
       return t < it.total ? t : -1;
     }
@@ -466,7 +486,7 @@ bool make_map_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
-                              const AuroraScatterArgs* scatter) {
+                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp) {
   Scatter sc{};
   if (scatter) {
     const bool packed = scatter->ginfo != nullptr;
@@ -493,6 +513,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
     sc.sys = scatter->sys;
   }
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
+  if (cluster_part && (part_gp < 1 || G % part_gp)) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
@@ -523,7 +544,14 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   // the kernel's last cluster): one per stream of launches that may run concurrently. NULL = round robin.
   static const bool dyn_sched = !getenv("AURORA_GEMM_STATIC") || atoi(getenv("AURORA_GEMM_STATIC")) == 0;
   if (!dyn_sched) tile_ctr = nullptr;
-  const int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BMP * K * 2)));
+  int group_m = (int)max(1LL, min(64LL, (32LL << 20) / ((long long)BMP * K * 2)));
+  // long K (GEMM2, K = F): blocks of 8 m-tiles -- the weight slab of an n-tile serves 8 consecutive
+  // tiles; measured C2 GEMM2 DRAM reads 5.8 GB (4) / 5.0 (6) / 5.0 (8) / 5.3 (12) / 6.6 GB (16)
+  // at equal duration (tools/gemm2_gm_sweep.sh), and ~1.5 % faster sustained steps with 8
+  if (K > 8192) group_m = max(group_m, 8);
+  // experiment hook: AURORA_GEMM_GM_LONGK=g sets the m-block of long-K launches (K > 8192, GEMM2)
+  static const int gm_longk = getenv("AURORA_GEMM_GM_LONGK") ? atoi(getenv("AURORA_GEMM_GM_LONGK")) : 0;
+  if (gm_longk > 0 && K > 8192) group_m = gm_longk;
   if (num_sms <= 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -531,7 +559,8 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   }
   const int grid = num_sms & ~1;
   grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out);
+      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out,
+      cluster_part, part_gp > 0 ? part_gp : 1);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

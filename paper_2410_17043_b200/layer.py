@@ -90,7 +90,8 @@ class AuroraMoELayer:
 
     def __init__(self, cfg: MoEConfig, plan: Optional[DeploymentPlan] = None, *, rank_base: int = 0,
                  n_local: Optional[int] = None, bandwidths=None, device=None, ctas_per_rank: Optional[int] = None,
-                 weights: Optional[dict] = None, spin_limit: int = 1 << 26, gpu_of_expert=None):
+                 weights: Optional[dict] = None, spin_limit: int = 1 << 26, gpu_of_expert=None,
+                 compute_scales=None):
         cfg.validate()
         self.cfg = cfg
         self.L = _lib.load()
@@ -153,6 +154,16 @@ class AuroraMoELayer:
         self.local_of_expert = torch.tensor([self.experts_of_rank(g).index(e) for e, g in enumerate(gpu_of)], **i32)
         self.bw = None if bandwidths is None else torch.tensor(np.asarray(bandwidths, float), dtype=torch.float64,
                                                                device=dev)
+        # emulated per-rank compute (C4: ClusterSpec.compute_scale, reference core.py:135-191): the
+        # expert GEMMs' CTA pairs are split among the local ranks in proportion, each rank's tiles run
+        # on its own share only (aurora_expert_ffn*'s cluster_part)
+        self.compute_scales = None if compute_scales is None else [float(c) for c in compute_scales]
+        self.gemm_part = None
+        if self.compute_scales is not None:
+            if len(self.compute_scales) != n or min(self.compute_scales) <= 0:
+                raise ValueError("compute_scales: one positive value per rank")
+            part = self.cluster_partition([self.compute_scales[r] for r in self.local_ranks], sms // 2)
+            self.gemm_part = torch.tensor(part, dtype=torch.int32, device=dev)
 
         # ---- routing / permutation state
         self.topk_idx = torch.empty(self.T_local, k, **i32)
@@ -318,6 +329,21 @@ class AuroraMoELayer:
             w13.append(interleave_gate_up(w1, w3)[0])
             w2.append((torch.randn(H, F, generator=ge, device=dev) / math.sqrt(F)).to(torch.bfloat16))
         return {"w_gate": w_gate, "bias": bias, "w13": torch.stack(w13), "w2": torch.stack(w2)}
+
+    @staticmethod
+    def cluster_partition(scales, clusters: int) -> list:
+        """Prefix of CTA-pair counts per rank proportional to ``scales`` (largest
+        remainder, at least one each): rank r's GEMM tiles run on clusters
+        [part[r], part[r + 1])."""
+        w = np.asarray(scales, dtype=float)
+        if clusters < len(w):
+            raise ValueError("fewer GEMM clusters than ranks")
+        quota = w / w.sum() * (clusters - len(w))
+        base = np.floor(quota).astype(int) + 1
+        rest = clusters - int(base.sum())
+        order = np.argsort(-(quota - np.floor(quota)), kind="stable")
+        base[order[:rest]] += 1
+        return [0] + np.cumsum(base).tolist()
 
     def _ptr_table(self, ptrs) -> torch.Tensor:
         return torch.tensor([int(p) for p in ptrs], dtype=torch.int64, device=self.dev)
@@ -505,9 +531,13 @@ class AuroraMoELayer:
             m_start, m_rows = self.rloc[rb:].data_ptr(), self.rrem[rb:].data_ptr()
         _lib.check(self.L.aurora_expert_ffn(self.recv.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                             self.hbuf.data_ptr(), self.ybuf.data_ptr(), m_start or None, m_rows,
-                                            self.n_local, self.cap, cfg.hidden, cfg.ffn, self._tctr(stream),
-                                            self.num_sms, stream),
+                                            self.n_local, self.cap, cfg.hidden, cfg.ffn, self._part(part),
+                                            self._tctr(stream), self.num_sms, stream),
                    "aurora_expert_ffn")
+
+    def _part(self, part: str = "all"):
+        """The emulated-compute cluster partition (whole-buffer launches only)."""
+        return self.gemm_part.data_ptr() if (self.gemm_part is not None and part == "all") else None
 
     def _tctr(self, stream: int) -> int:
         """The GEMM tile-counter pair of the stream a launch goes to."""
@@ -540,7 +570,7 @@ class AuroraMoELayer:
             self.ybuf.data_ptr(), self.rtot[self.rank_base:].data_ptr(), self.n_local, self.cap, cfg.hidden,
             cfg.ffn, self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
             self.n, self.rank_base, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), sys_scope,
-            self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_combine")
+            self._part(), self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_combine")
 
     def combine_wait(self, stream: int) -> None:
         """Receiving side of the fused combine: every expert rank's rows for this
@@ -561,7 +591,7 @@ class AuroraMoELayer:
             _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                                   self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                                   self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
-                                                  self._tctr(stream), self.num_sms, stream),
+                                                  self._part(), self.G, self._tctr(stream), self.num_sms, stream),
                        "aurora_expert_ffn_packed")
             inv = None
         elif self.grouped:  # rows already sit in their groups (g_off / g_rows from the grouped pack);
@@ -571,7 +601,8 @@ class AuroraMoELayer:
                 self.y_g.data_ptr(), self.g_off.data_ptr(), self.g_rows.data_ptr(), E_loc, self.max_entries, H,
                 cfg.ffn, self.ginfo.data_ptr(), self.G, self.t_dst_c.data_ptr(), self.counts.data_ptr(),
                 self.soff.data_ptr(), self.roff.data_ptr(), self.n, self.rank_base, self.ybuf.data_ptr(), self.cap,
-                1 if fused else 0, 1 if self.n_local != self.n else 0, self._tctr(stream), self.num_sms, stream),
+                1 if fused else 0, 1 if self.n_local != self.n else 0, self._part(), self._tctr(stream),
+                self.num_sms, stream),
                 "aurora_expert_ffn_packed_scatter")
             inv, skip = None, 1
         else:
@@ -607,7 +638,8 @@ class AuroraMoELayer:
         _lib.check(L.aurora_expert_ffn_packed(self.a_g.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
                                               self.h_g.data_ptr(), self.y_g.data_ptr(), self.g_off.data_ptr(),
                                               self.g_rows.data_ptr(), E_loc, self.max_entries, H, cfg.ffn,
-                                              self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_packed")
+                                              self._part(), self.G, self._tctr(stream), self.num_sms, stream),
+                   "aurora_expert_ffn_packed")
 
     def combine(self, stream: int) -> None:
         # local rows stay in the expert output; the aggregation reads them there

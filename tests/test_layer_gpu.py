@@ -272,6 +272,43 @@ def test_layer_c4_full_size(torch):
     _verify(torch, layer, x, out, bandwidths=bw, sample=_sample(cfg.tokens))
 
 
+def test_layer_compute_partition(torch):
+    """Emulated per-rank compute (C4): with compute_scales the expert GEMMs' CTA
+    pairs are split among the ranks in proportion (cluster_part) and each rank's
+    tiles run on its own share -- same output bits as the shared grid, fused and
+    engine combine, repeatedly (the static partition never touches the tile
+    counters)."""
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=512, ffn=512, experts=8, top_k=2, tokens=4096, ranks=8, skew=1.5, seed=3)
+    scales = [1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4]
+    ref_layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = ref_layer(x).clone()
+    layer = AuroraMoELayer(cfg, compute_scales=scales)
+    part = layer.gemm_part.cpu().tolist()
+    assert part[0] == 0 and part[-1] == layer.num_sms // 2 and all(b > a for a, b in zip(part, part[1:]))
+    assert part[1] - part[0] > part[-1] - part[-2]  # the fast rank has more CTA pairs than the slow one
+    for fused in (True, False, True):
+        layer.fused_combine = fused
+        out = layer(x)
+        torch.cuda.synchronize()
+        layer.check_status()
+        assert torch.equal(out, ref), fused
+    assert AuroraMoELayer.cluster_partition([1, 1, 1, 1], 74)[-1] == 74
+    # several experts per rank (the packed grouped GEMMs, a rank's clusters serve all its experts)
+    cfg5 = MoEConfig(hidden=512, ffn=256, experts=32, top_k=4, tokens=4096, ranks=8, skew=1.0, seed=5)
+    ref5 = AuroraMoELayer(cfg5)
+    x5 = torch.randn(cfg5.tokens, cfg5.hidden, device="cuda").to(torch.bfloat16)
+    r5 = ref5(x5).clone()
+    l5 = AuroraMoELayer(cfg5, compute_scales=scales)
+    for scatter in (True, False):
+        l5.packed_scatter = scatter
+        o5 = l5(x5)
+        torch.cuda.synchronize()
+        l5.check_status()
+        assert torch.equal(o5, r5), scatter
+
+
 def test_layer_heterogeneous_cluster(torch):
     """C4 (heterogeneous emulation), small: placement by assign_exclusive_hetero
     (placement.py:46-60) from a calibration pass, schedule on the fp64

@@ -167,3 +167,63 @@ def test_counts_path_int_domain_and_chunk_tables(A):
         assert [[tuple(x) for x in row] for row in rchunks[:nph].tolist()] == rch
         assert n_in.tolist() == rcnt and n_out.tolist() == sseq
         assert int(prog.item()) == nph | (1 << 20)
+
+
+def test_heterogeneous_chunk_rounding_fuzz(A):
+    """The fp64 heterogeneous path in the layer (aurora_schedule_counts with
+    bandwidths): fractional phase durations become whole-token chunks by
+    cumulative rounding; a pair whose rounded total missed its count would need
+    a fix-up after the engine may have consumed the entry (AURORA_EINVAL). Over
+    1500 MoE-like and adversarial matrices with the paper's bandwidth ratios
+     and random ones, the status is always OK, the schedule is
+    bit-exact with the oracle, and every pair's chunks sum to its count."""
+    import torch
+    from oracle.oracle import build_schedule_oracle
+    from paper_2410_17043_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(2024)
+    dev = torch.device("cuda")
+    i32 = dict(dtype=torch.int32, device=dev)
+    fails = 0
+    for it in range(1500):
+        n = int(rng.choice([2, 4, 8, 8, 8, 16]))
+        if it % 3 == 0:
+            bw = np.asarray([(1.0, 0.8, 0.5, 0.4)[q % 4] for q in range(n)])[rng.permutation(n)]
+        elif it % 3 == 1:
+            bw = rng.choice([100.0, 80.0, 50.0, 40.0], n)
+        else:
+            bw = rng.uniform(0.05, 3.0, n)
+        c = _fuzz_matrix(rng, n, it % 2 if it % 7 else 3).astype(np.int64)
+        c = np.minimum(c, (1 << 20)).astype(np.int32)
+        counts = torch.tensor(c, device=dev)
+        bwt = torch.tensor(bw, dtype=torch.float64, device=dev)
+        P = L.aurora_phase_cap(n)
+        pr = torch.empty(P, n, **i32)
+        pd = torch.empty(P, dtype=torch.float64, device=dev)
+        si = torch.zeros(2, **i32)
+        chunks = torch.empty(P, n, 4, **i32)
+        rchunks = torch.empty(P, n, 4, **i32)
+        n_in, n_out, prog = torch.empty(n, **i32), torch.empty(n, **i32), torch.zeros(1, **i32)
+        rc = L.aurora_schedule_counts(counts.data_ptr(), bwt.data_ptr(), n, pr.data_ptr(), pd.data_ptr(),
+                                      si.data_ptr(), chunks.data_ptr(), rchunks.data_ptr(), n_in.data_ptr(),
+                                      n_out.data_ptr(), si[1:].data_ptr(), prog.data_ptr(), 0, 0, 0, 0,
+                                      _lib.stream_ptr())
+        assert rc == 0
+        torch.cuda.synchronize()
+        nph, status = si.tolist()
+        if status != 0:
+            fails += 1
+            continue
+        d = c.astype(float)
+        np.fill_diagonal(d, 0)
+        o = build_schedule_oracle(d, bw)
+        got = [(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(t))
+               for row, t in zip(pr[:nph].tolist(), pd[:nph].tolist())]
+        assert got == o["phases"], (n, it)
+        tot = np.zeros((n, n))
+        for row in chunks[:nph].cpu().numpy():
+            for i, (j, first, cnt, _) in enumerate(row):
+                if j >= 0:
+                    tot[i, j] += cnt
+        assert np.array_equal(tot, d), it
+    assert fails == 0, f"{fails} of 1500 heterogeneous schedules needed a chunk fix-up (EINVAL)"

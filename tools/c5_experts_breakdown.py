@@ -35,7 +35,7 @@ for _ in range(R):
     ev[2].record(st)
     L.aurora_expert_ffn_packed(layer.a_g.data_ptr(), layer.w13.data_ptr(), layer.w2.data_ptr(), layer.h_g.data_ptr(),
                                layer.y_g.data_ptr(), layer.g_off.data_ptr(), layer.g_rows.data_ptr(), E_loc,
-                               layer.max_entries, H, cfg.ffn, layer.tile_ctrs[0].data_ptr(), layer.num_sms, s)
+                               layer.max_entries, H, cfg.ffn, None, layer.G, layer.tile_ctrs[0].data_ptr(), layer.num_sms, s)
     ev[3].record(st)
     L.aurora_expert_reduce(layer.y_g.data_ptr(), layer.inv.data_ptr(), layer.meta_recv.data_ptr(), layer.cap,
                            layer.meta_bytes, layer.rtot.data_ptr(), layer.n_local, layer.rank_base, k, H,

@@ -28,5 +28,18 @@ for name, (G, m, N, K, ep) in cases.items():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(f"{name}: {ms * 1e3:8.1f} us  {2.0 * G * m * N * K / ms / 1e9:7.1f} TFLOP/s", flush=True)
+    # cuBLAS on the same shape (batched, one matmul per group) for reference
+    a3, b3 = a.view(G, m, K), b.view(G, N, K)
+    cub = lambda: torch.bmm(a3, b3.transpose(1, 2))
+    for _ in range(3):
+        cub()
+    e0.record()
+    for _ in range(10):
+        cub()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_cb = e0.elapsed_time(e1) / 10
+    fl = 2.0 * G * m * N * K
+    print(f"{name}: {ms * 1e3:8.1f} us  {fl / ms / 1e9:7.1f} TFLOP/s   cuBLAS bmm {ms_cb * 1e3:8.1f} us "
+          f"{fl / ms_cb / 1e9:7.1f} TFLOP/s", flush=True)
     del a, b, c
