@@ -419,6 +419,61 @@ def baseline_schedules(layer, x, sp, stream, reps=3):
 GEMM_CAPTURE = "profiles/r02_ncu_gemm.json"
 
 
+def n1_effect(layer, x, stream, steps):
+    """N1 (north_star (4)): the arrival-driven expert GEMM -- GEMM1 a programmatic dependent
+    of an LSU dispatch (one copy CTA per SM), each tile starting once its rows have landed --
+    against the default plan (TMA dispatch on every SM, then GEMM1), alternated three times;
+    plus one traced N1 step: when GEMM1's first tiles started relative to the dispatch CTAs."""
+    import numpy as np
+    import torch
+    from paper_2410_17043_b200 import _lib
+    if layer.G != 1 or not layer.combine_in_gemm:
+        return {"unavailable": "one expert per rank with the fused combine only"}
+    L = _lib.load()
+    times = {"default": [], "n1": []}
+    for _ in range(3):
+        for name, on in (("default", False), ("n1", True)):
+            layer.arrival = on
+            for _ in range(2):
+                layer(x)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                layer(x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            layer.check_status()
+            times[name].append(e0.elapsed_time(e1) / steps)
+    layer.arrival = True
+    eng = torch.zeros(4 * 4096, dtype=torch.int64, device=x.device)
+    gt = torch.zeros(2 * 1024, dtype=torch.int64, device=x.device)
+    L.aurora_debug_set_engine_trace(eng.data_ptr())
+    L.aurora_debug_set_gemm_trace(gt.data_ptr())
+    try:
+        layer(x)
+        torch.cuda.synchronize()
+    finally:
+        L.aurora_debug_set_engine_trace(None)
+        L.aurora_debug_set_gemm_trace(None)
+        layer.arrival = False
+    layer.check_status()
+    e = eng.view(-1, 4).cpu().numpy()
+    e = e[e[:, 0] > 0]
+    g = gt.view(-1, 2).cpu().numpy()
+    g = g[g[:, 0] > 0]
+    t0 = float(e[:, 0].min())
+    trace = {"dispatch_ctas": int(len(e)), "dispatch_end_us": float(e[:, 2].max() - t0) / 1e3,
+             "dispatch_local_rows_done_us": float(e[:, 1].max() - t0) / 1e3,
+             "gemm1_ctas": int(len(g)), "gemm1_last_cta_entry_us": float(g[:, 0].max() - t0) / 1e3,
+             "gemm1_first_cta_entry_us": float(g[:, 0].min() - t0) / 1e3,
+             "gemm1_first_tile_us": float(g[g[:, 1] > 0][:, 1].min() - t0) / 1e3 if (g[:, 1] > 0).any() else None,
+             "gemm1_ctas_started_before_dispatch_end": int((g[:, 0] < e[:, 2].max()).sum())}
+    med = {k: float(np.median(v)) for k, v in times.items()}
+    return {"default_ms_per_step": med["default"], "n1_ms_per_step": med["n1"], "runs": times,
+            "speedup": med["default"] / med["n1"], "trace_us_from_dispatch_start": trace,
+            "switch": "AURORA_N1=1", "default_on": False}
+
+
 def placement_effect(layer, cfg, plan, bws, x, stream, steps):
     """C4: the Theorem-3 placement (assign_exclusive_hetero,
     placement.py:46-60: the k-th most loaded expert on the k-th fastest rank) against
@@ -1003,6 +1058,8 @@ def main():
     }
     if args.config == "c4" and world == 1:
         line["placement"] = placement_effect(layer, cfg, plan, bws, x, stream, args.steps)
+    if args.config == "c2" and world == 1:
+        line["arrival_driven_gemm"] = n1_effect(layer, x, stream, args.steps)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         weights = cpu_weights(args)
         tps, sec, cores = run_cpu(args, 256, 3, weights=weights)

@@ -232,11 +232,18 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
                   const void* const* src_bufs, void* const* dst_bufs, int row_bytes,
                   const void* const* src2_bufs, void* const* dst2_bufs, int row2_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
-                  int32_t* status, int split, const double* bw, void* const* ginfo_bufs, void* stream);
+                  int32_t* status, int split, const double* bw, void* const* ginfo_bufs,
+                  int32_t* const* landed, void* stream);
 /* ginfo_bufs (mode bit 8, nullable): per rank the base of its process's [rows] int4
  * array; every grouped store of a row also writes {receiver-layout row, gate weight,
  * single (the row's only local expert), 0} at the row's group position
- * (aurora_expert_ffn_packed_scatter). */
+ * (aurora_expert_ffn_packed_scatter).
+ * landed (nullable; LSU dispatch, mode bit 6, only): per receiver j the address of its row
+ * landed[j][0..n) (peer memory at N > 1); every copy CTA adds the rows it moved for block
+ * (i -> j) after they are visible -- at each run end and after its share of the local rows
+ * (release) -- the arrival signal of aurora_expert_ffn_combine's arrival-driven GEMM1. The
+ * engine triggers griddepcontrol.launch_dependents at entry, so that GEMM may be a
+ * programmatic dependent launch running beside it. */
 /* aurora_engine_ctas: copy CTAs per local rank the engine will actually use
  * (ctas_per_rank clamped so every copy CTA is co-resident), or -AURORA_E* on
  * error. K2 needs n_local x this value to count hand-over thresholds. The
@@ -323,8 +330,15 @@ int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2
                               void* y_buf, const int32_t* m_rows, int G, int64_t cap, int H, int F,
                               void* const* ret_bufs, const int32_t* counts, const int32_t* soff,
                               const int32_t* roff, int n, int rank_base, int32_t* const* ctrs,
-                              int32_t* ticket, int sys, const int32_t* cluster_part, int32_t* tile_ctr,
-                              int num_sms, void* stream);
+                              int32_t* ticket, int sys, const int32_t* cluster_part, int32_t* landed,
+                              int arrival_pdl, int32_t* tile_ctr, int num_sms, void* stream);
+/* landed (nullable): arrival-driven GEMM1 (N1). landed[g * n + i] = rows of block (sender i ->
+ * local rank rank_base + g) the dispatch has made visible (aurora_engine's landed credits); a
+ * GEMM1 tile starts once every block under its rows is complete, the m-tiles holding only local
+ * rows first. GEMM1's last cluster re-arms landed to zero. arrival_pdl: GEMM1 is launched as a
+ * programmatic dependent of the preceding dispatch launch, so its tiles run beside the copy CTAs
+ * (an LSU dispatch leaves each SM's shared memory to the GEMM). Needs tile_ctr and no
+ * cluster_part. */
 
 /* aurora_expert_ffn_packed_scatter: the packed FFN of the grouped dispatch with the
  * pre-reduction of single-expert rows folded into GEMM2's epilogue. ginfo [a_rows]
@@ -427,6 +441,8 @@ int aurora_debug_set_schedule_profile(long long* prof);
  * per copy CTA {start, local rows done, end, -} at trace[4 * cta]. */
 int aurora_debug_set_schedule_trace(long long* trace);
 int aurora_debug_set_engine_trace(long long* trace);
+/* per expert-GEMM CTA {entry, first tile's loads issued} (%globaltimer ns) at trace[2 * cta] */
+int aurora_debug_set_gemm_trace(long long* trace);
 /* aurora_debug_set_early_rows: rows before the end of a CTA's share of a run at
  * which the TMA engine sends the run's pace signal (engine mode bit 7; default 2). */
 int aurora_debug_set_early_rows(int rows);

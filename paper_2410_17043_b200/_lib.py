@@ -32,14 +32,15 @@ _SIGNATURES = {
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
-                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp, _vp],
+                      _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp, _vp,
+                      _vp],
     "aurora_engine_ctas": [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp, _c_i64, _vp, _vp],
     "aurora_expert_ffn": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _vp, _c_int, _vp],
     "aurora_grouped_gemm": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "aurora_expert_ffn_combine": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _c_i64, _c_int, _c_int, _vp, _vp, _vp,
-                                  _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp],
+                                  _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp],
     "aurora_exchange_counts": [_vp, _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp, _vp],
     "aurora_expert_hist": [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp],
     "aurora_pack_grouped": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -60,6 +61,7 @@ _SIGNATURES = {
     "aurora_debug_set_schedule_profile": [_vp],
     "aurora_debug_set_schedule_trace": [_vp],
     "aurora_debug_set_engine_trace": [_vp],
+    "aurora_debug_set_gemm_trace": [_vp],
     "aurora_debug_set_early_rows": [_c_int],
     "aurora_ipc_handle_bytes": [],
     "aurora_ipc_get": [_vp, _vp, _vp],

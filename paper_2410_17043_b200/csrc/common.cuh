@@ -91,6 +91,15 @@ struct AuroraScatterArgs {
   int to_ret;
 };
 
+// Arrival-driven GEMM1 (aurora_expert_ffn_combine with landed): tiles wait for their rows
+struct AuroraArrivalArgs {
+  int32_t* landed;        // [n_local][n]: rows of block (sender i -> local receiver g) visible
+  const int32_t* counts;  // [n][n]
+  const int32_t* roff;    // [n][n]
+  int n, rank_base, sys;
+  int pdl;                // launch as a programmatic dependent of the preceding dispatch
+};
+
 #define AUR_CHECK_LAUNCH()                          \
   do {                                              \
     cudaError_t _e = cudaGetLastError();            \

@@ -56,6 +56,10 @@ struct EngineParams {
   int32_t* status;
   int meta_k;            // grouped dispatch (mode bit 8): expert records per meta row
   int4* const* ginfo;    // grouped dispatch: per-rank {recv row, weight, single, 0} arrays (nullable)
+  // arrival-driven expert GEMM (LSU dispatch only; nullable): landed[j][i] = rows of block
+  // (sender i -> receiver j) stored and visible, credited per CTA at every run end (and after the
+  // local rows); the GEMM starts a tile once every block under it is complete
+  int32_t* const* landed;
 };
 
 // This CTA's rank (local index), its index among the rank's CTAs and the
@@ -125,22 +129,35 @@ __device__ __forceinline__ void copy_rows(int row_bytes, const char* src_base,
   }
 }
 
-__device__ __forceinline__ void signal(int32_t* ctr, bool sys) {
+// landed: optional arrival credit (rows of this CTA's run now visible at the receiver)
+__device__ __forceinline__ void signal(int32_t* ctr, bool sys, int32_t* landed = nullptr, int rows = 0) {
   __syncthreads();  // every thread's stores of this slice are issued
   if (threadIdx.x == 0) {
     if (sys) {
       __threadfence_system();  // cumulative: orders the CTA's stores (observed via bar.sync)
+      if (landed && rows) red_release_sys_add(landed, rows);
       red_release_sys_add(ctr, 1);      // pace
       red_release_sys_add(ctr + 1, 1);  // done last: once the receiver sees every done, every pace is in
     } else {
       __threadfence();
+      if (landed && rows) red_release_gpu_add(landed, rows);
       red_release_gpu_add(ctr, 1);
       red_release_gpu_add(ctr + 1, 1);
     }
   }
 }
 
+// diagnostics: per copy CTA {start, local rows done, end} in %globaltimer ns
+__device__ long long* g_engine_trace = nullptr;
+__device__ __forceinline__ long long eng_ns0() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
+  // a programmatically dependent launch (the arrival-driven expert GEMM) may start beside this grid
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ int cs[AUR_MAXN];
   int r_local, c, C;
   cta_assign(p, cs, r_local, c, C);
@@ -156,6 +173,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
   const int4* table = dispatch ? p.chunks : p.rchunks;
   __shared__ int abort_s, avail_s, done_s;
   if (threadIdx.x == 0) abort_s = 0;
+  if (threadIdx.x == 0 && g_engine_trace) g_engine_trace[blockIdx.x * 4] = eng_ns0();
   __syncthreads();
 
   // local (diagonal) rows never cross the network (TrafficMatrix zeroes them,
@@ -172,7 +190,15 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     } else {
       copy_rows<false>(p.row_bytes, src, nullptr, p.roff[g * n + g], p.dst_bufs[g], p.soff[g * n + g], r0, r1);
     }
+    if (dispatch && p.landed && r1 > r0) {  // the local block's rows of this CTA are in place
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        red_release_gpu_add(p.landed[g] + g, r1 - r0);
+      }
+    }
   }
+  if (threadIdx.x == 0 && g_engine_trace) g_engine_trace[blockIdx.x * 4 + 1] = eng_ns0();
   if (!do_remote) return;
 
   // wait until phase `need` is final (or the schedule is complete)
@@ -200,6 +226,7 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
     done = done_s;
   };
 
+  int run_rows = 0;  // rows this CTA moved in the open run (arrival credit)
   for (int k = 0;; k++) {
     if (k >= avail) {
       if (done) break;
@@ -245,9 +272,14 @@ __global__ void __launch_bounds__(THREADS, 2) engine_kernel(EngineParams p) {
       const int4 nx = __ldcg(&table[(k + 1) * n + g]);
       run_end = !(nx.x == peer && nx.w < 0);
     }
-    if (run_end) signal(p.ctrs[peer], sys);
+    run_rows += r1 - r0;
+    if (run_end) {
+      signal(p.ctrs[peer], sys, (dispatch && p.landed) ? p.landed[peer] + g : nullptr, run_rows);
+      run_rows = 0;
+    }
   }
 
+  if (threadIdx.x == 0 && g_engine_trace) g_engine_trace[blockIdx.x * 4 + 2] = eng_ns0();
   // completion: CTA 0 of each rank waits for all of its arrivals, then rearms its counter
   if (c == 0 && threadIdx.x == 0) {
     const int expect = dispatch ? __ldcg(&p.n_in[g]) : __ldcg(&p.n_out[g]);
@@ -366,8 +398,7 @@ __device__ bool entry_at(const EngineParams& p, const int4* table, int g, int k,
 
 constexpr int RING = 128;
 
-// diagnostics: per copy CTA {start, local rows done, end} in %globaltimer ns
-__device__ long long* g_engine_trace = nullptr;
+
 __device__ int g_early_rows = 2;  // rows before a run's end at which its pace signal goes out
 __device__ __forceinline__ long long eng_ns() {
   long long t;
@@ -392,6 +423,7 @@ struct TmaShared {
 };
 
 __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p, int S, int slot_bytes) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) unsigned char slots[];
   __shared__ TmaShared sh;
   // per-call buffer offsets behind the row slots (n x n each): every per-entry lookup is a shared read
@@ -751,6 +783,12 @@ static int engine_ctas(int n, int n_local, int ctas_per_rank, int row_bytes, int
   if (!lsu && cudaFuncSetAttribute(engine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
                   cudaSuccess)
     return -1;
+  // the LSU engine needs almost no shared memory, but it shares SMs with the arrival-driven
+  // expert GEMM (N1): an SM's L1 / shared split is fixed while CTAs are resident, so ask for the
+  // largest shared carveout or the GEMM's CTAs could not land beside it
+  if (lsu && cudaFuncSetAttribute(engine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+    return -1;
   const cudaError_t oe = lsu ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_kernel, THREADS, 0)
                              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, engine_tma_kernel,
                                                                              TMA_THREADS, dyn);
@@ -780,7 +818,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, int split, const double* bw, void* const* ginfo_bufs,
-                             void* stream) {
+                             int32_t* const* landed, void* stream) {
   if (split < 0 || split > 2) return AURORA_EINVAL;
   if (mode < 0 || mode > 511 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       ((mode & 256) && ((mode & 65) || !src2_bufs || !dst2_bufs || row2_bytes < 8)) ||
@@ -827,6 +865,8 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.max_phases = max_phases;
   p.spin_limit = spin_limit;
   p.status = status;
+  p.landed = landed;
+  if (landed && (!lsu || (mode & 1))) return AURORA_EINVAL;  // arrival credits: LSU dispatch only
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_local * ctas_per_rank);
   cfg.blockDim = dim3(lsu ? THREADS : TMA_THREADS);

@@ -27,7 +27,8 @@
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
-                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp);
+                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp,
+                              const AuroraArrivalArgs* arrival);
 
 namespace {
 
@@ -361,15 +362,16 @@ int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start
                    const int32_t* m_rows, int G,
                    int64_t cap, int64_t map_rows, int N, int K, int epilogue, int32_t* tile_ctr, int num_sms,
                    cudaStream_t stream, const AuroraScatterArgs* scatter = nullptr,
-                   const int32_t* cluster_part = nullptr, int part_gp = 1) {
+                   const int32_t* cluster_part = nullptr, int part_gp = 1,
+                   const AuroraArrivalArgs* arrival = nullptr) {
   // cap > 0: group g owns rows [g*cap, (g+1)*cap); cap == 0: groups packed,
   // m_start[g] absolute, map_rows = rows of the A buffer
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (use_pair_kernel())
     return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, tile_ctr, num_sms,
-                                     stream, scatter, cluster_part, part_gp);
-  if (cluster_part) return AURORA_EINVAL;  // partitioned (emulated per-rank compute): pair kernel only
+                                     stream, scatter, cluster_part, part_gp, arrival);
+  if (cluster_part || arrival) return AURORA_EINVAL;  // partitioned (emulated per-rank compute): pair kernel only
   if (scatter) return AURORA_EINVAL;  // the fused combine lives in the CTA-pair kernel
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
       (epilogue != 0 && epilogue != 1) || !a || !b || !c || !m_rows)
@@ -428,11 +430,13 @@ extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, con
                                          const int32_t* counts, const int32_t* soff,
                                          const int32_t* roff, int n, int rank_base,
                                          int32_t* const* ctrs, int32_t* ticket, int sys,
-                                         const int32_t* cluster_part, int32_t* tile_ctr, int num_sms,
-                                         void* stream) {
+                                         const int32_t* cluster_part, int32_t* landed, int arrival_pdl,
+                                         int32_t* tile_ctr, int num_sms, void* stream) {
   if (!ret_bufs || !counts || !soff || !roff || !ctrs || !ticket) return AURORA_EINVAL;
+  // landed != NULL: GEMM1 is arrival-driven -- a tile starts once the dispatch has landed its rows
+  const AuroraArrivalArgs arr{landed, counts, roff, n, rank_base, sys ? 1 : 0, arrival_pdl ? 1 : 0};
   int rc = launch_grouped(a_buf, w13, h_buf, nullptr, m_rows, G, cap, 0, 2 * F, H, 1, tile_ctr, num_sms,
-                          (cudaStream_t)stream, nullptr, cluster_part);
+                          (cudaStream_t)stream, nullptr, cluster_part, 1, landed ? &arr : nullptr);
   if (rc != AURORA_OK) return rc;
   const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
   return launch_grouped(h_buf, w2, y_buf, nullptr, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,

@@ -64,7 +64,11 @@ struct Scatter {
 };
 
 struct TileIter2 {
-  int n_tiles_n, total;
+  int n_tiles_n, total, nseg;
+  // tile order = segments (group, first m-tile, m-tiles) back to back; one per group, or with
+  // arrival-driven tiles two per group: the m-tiles holding only local rows first (all groups),
+  // then the rest
+  int seg_g[2 * MAX_GROUPS], seg_m0[2 * MAX_GROUPS], seg_mt[2 * MAX_GROUPS + 1], seg_prefix[2 * MAX_GROUPS + 1];
   int pg, plc, pnc, plo, phi;  // partitioned mode: this cluster's partition, index among its
                                // clusters, their count, its tile range [plo, phi)
   int prefix[MAX_GROUPS + 1];
@@ -75,20 +79,55 @@ struct TileIter2 {
 
 __device__ __forceinline__ void tile_coords2(const TileIter2& it, int G, int gm, int t, int& g,
                                              int& mt, int& nt) {
-  // group of tile t: the last g with prefix[g] <= t (binary search: up to 64 groups)
-  int lo = 0, hi = G - 1;
+  // segment of tile t: the last q with seg_prefix[q] <= t (binary search: up to 128 segments)
+  int lo = 0, hi = it.nseg - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (it.prefix[mid] <= t) lo = mid;
+    if (it.seg_prefix[mid] <= t) lo = mid;
     else hi = mid - 1;
   }
-  g = lo;
-  const int local = t - it.prefix[g];
+  g = it.seg_g[lo];
+  const int local = t - it.seg_prefix[lo];
   const int per_block = gm * it.n_tiles_n;
   const int sb = local / per_block, rem = local - sb * per_block;
-  const int rows = min(gm, it.mt[g] - sb * gm);
-  mt = sb * gm + rem % rows;
+  const int rows = min(gm, it.seg_mt[lo] - sb * gm);
+  mt = it.seg_m0[lo] + sb * gm + rem % rows;
   nt = rem / rows;
+}
+
+// diagnostics (aurora_debug_set_gemm_trace): per CTA {entry, first tile's loads issued} in
+// %globaltimer ns -- shows the arrival-driven GEMM1 running beside the dispatch
+__device__ long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ long long gemm_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Arrival-driven GEMM1 (N1): the receive buffer of local group g (rank rank_base + g) holds the
+// rank's local rows first, then each sender's block at roff[i][j]; landed[g * n + i] counts the
+// rows of block (i -> j) the dispatch has made visible. A tile waits until every block under its
+// rows is complete.
+struct Arrival {
+  int32_t* landed;        // [n_local][n] (this process's receivers), re-armed by the last cluster
+  const int32_t* counts;  // [n][n]
+  const int32_t* roff;    // [n][n]
+  int n, rank_base, sys;
+};
+
+__device__ __forceinline__ void wait_rows_landed(const Arrival& ar, int g, int r_lo, int r_hi) {
+  const int j = ar.rank_base + g;
+  for (int i = 0; i < ar.n; i++) {
+    const int c = ar.counts[i * ar.n + j];
+    const int b0 = ar.roff[i * ar.n + j];
+    if (c == 0 || b0 >= r_hi || b0 + c <= r_lo) continue;
+    const int32_t* f = ar.landed + g * ar.n + i;
+    int spins = 0;
+    while ((ar.sys ? ld_acquire_sys(f) : ld_acquire_gpu(f)) < c)
+      if (++spins > 8) __nanosleep(64);
+  }
+  // the rows were written through the generic proxy; the tile loads are TMA (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
@@ -100,8 +139,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
                             int epilogue, int group_m, const Scatter sc,
                             int32_t* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_c,
-                            int tma_out, const int32_t* __restrict__ part, int part_gp) {
+                            int tma_out, const int32_t* __restrict__ part, int part_gp, const Arrival ar) {
   extern __shared__ uint8_t smem_raw[];
+  // first launch after arming wins (GEMM1; GEMM2's CTAs find the slots taken)
+  if (threadIdx.x == 0 && g_gemm_trace)
+    atomicCAS(reinterpret_cast<unsigned long long*>(g_gemm_trace + blockIdx.x * 2), 0ull,
+              (unsigned long long)gemm_ns());
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
@@ -135,6 +178,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     it.prefix[G] = acc;
     it.total = acc;
+    int ns = 0, sacc = 0;
+    auto add_seg = [&](int g, int m0, int mtn) {
+      if (mtn <= 0) return;
+      it.seg_g[ns] = g;
+      it.seg_m0[ns] = m0;
+      it.seg_mt[ns] = mtn;
+      it.seg_prefix[ns] = sacc;
+      sacc += mtn * it.n_tiles_n;
+      ns++;
+    };
+    if (ar.landed) {  // local-only m-tiles of every group first: they need no network row
+      for (int g = 0; g < G; g++) add_seg(g, 0, min(it.mt[g], ar.counts[(ar.rank_base + g) * (ar.n + 1)] / BMP));
+      for (int g = 0; g < G; g++) {
+        const int l = min(it.mt[g], ar.counts[(ar.rank_base + g) * (ar.n + 1)] / BMP);
+        add_seg(g, l, it.mt[g] - l);
+      }
+    } else {
+      for (int g = 0; g < G; g++) add_seg(g, 0, it.mt[g]);
+    }
+    if (ns == 0) {  // no tiles: keep the search well-defined
+      it.seg_g[0] = 0;
+      it.seg_m0[0] = it.seg_mt[0] = it.seg_prefix[0] = 0;
+      ns = 1;
+    }
+    it.seg_prefix[ns] = sacc;
+    it.nseg = ns;
     // partitioned mode (emulated per-rank compute): clusters [part[q], part[q+1]) serve partition q
     // only -- groups [q * part_gp, (q + 1) * part_gp), one rank's experts -- round robin over its tiles
     it.pg = -1;
@@ -236,6 +305,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (t < 0) break;
         int g, mt, nt;
         tile_coords2(it, G, group_m, t, g, mt, nt);
+        if (ar.landed) {  // N1: this CTA's 128 rows of the tile must have arrived
+          const int r_lo = mt * BMP + (int)rank * HALF;
+          if (r_lo < it.rows[g]) wait_rows_landed(ar, g, r_lo, min(r_lo + HALF, it.rows[g]));
+        }
+        if (i == 0 && g_gemm_trace)
+          atomicCAS(reinterpret_cast<unsigned long long*>(g_gemm_trace + blockIdx.x * 2 + 1), 0ull,
+                    (unsigned long long)gemm_ns());
         const int a_row = (int)(g * cap) + it.ms[g] + mt * BMP + (int)rank * HALF;
         const int b_row = g * N + nt * BN + (int)rank * HALF;
         for (int kb = 0; kb < k_blocks; kb++) {
@@ -413,6 +489,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (atomicAdd(tile_ctr + 1, 1) == n_clusters - 1) {
       tile_ctr[0] = 0;
       tile_ctr[1] = 0;
+      if (ar.landed)  // every tile has passed its arrival wait: re-arm for the next dispatch
+        for (int q = 0; q < G * ar.n; q++) ar.landed[q] = 0;
       __threadfence();
     }
   }
@@ -486,7 +564,8 @@ bool make_map_out(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32_t* m_start,
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
-                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp) {
+                              const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp,
+                              const AuroraArrivalArgs* arrival) {
   Scatter sc{};
   if (scatter) {
     const bool packed = scatter->ginfo != nullptr;
@@ -558,9 +637,35 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = num_sms & ~1;
-  grouped_gemm_2sm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(
-      ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G, (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out,
-      cluster_part, part_gp > 0 ? part_gp : 1);
+  Arrival ar{};
+  if (arrival) {
+    // arrival-driven tiles need the dynamic order (its last cluster re-arms `landed`), whole
+    // receive buffers (m_start 0) and one expert per rank
+    if (!tile_ctr || cluster_part || m_start || scatter || !arrival->landed || !arrival->counts ||
+        !arrival->roff || arrival->n < 1 || arrival->rank_base < 0 || arrival->rank_base + G > arrival->n)
+      return AURORA_EINVAL;
+    ar = Arrival{arrival->landed, arrival->counts, arrival->roff, arrival->n, arrival->rank_base, arrival->sys};
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (arrival && arrival->pdl) {  // programmatic dependent of the dispatch: runs beside it
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel, ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G,
+                         (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out, cluster_part,
+                         part_gp > 0 ? part_gp : 1, ar) != cudaSuccess)
+    return AURORA_ECUDA;
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
+}
+
+extern "C" int aurora_debug_set_gemm_trace(long long* trace) {
+  return cudaMemcpyToSymbol(g_gemm_trace, &trace, sizeof(trace)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }

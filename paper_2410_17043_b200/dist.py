@@ -14,7 +14,8 @@ from typing import Callable, Dict, List
 from . import _lib
 
 BUFFERS = ("recv", "ret", "ctr_d", "ctr_c", "counts2", "xflag")
-OPTIONAL = ("meta_recv", "a_g", "cnt_e2", "ginfo")  # present when ranks host several experts
+OPTIONAL = ("meta_recv", "a_g", "cnt_e2", "ginfo",  # present when ranks host several experts
+            "landed")  # one expert per rank: arrival credits of the arrival-driven expert GEMM
 
 
 def _names(layer) -> tuple:
@@ -27,7 +28,8 @@ def _strides(layer) -> Dict[str, int]:
     # counts2 / xflag: one per process (every rank of a process maps to its base)
     return {"recv": layer.cap * H * 2, "ret": layer.ret_stride * H * 2, "ctr_d": 8, "ctr_c": 8,
             "counts2": 0, "xflag": 0,
-            "meta_recv": layer.cap * layer.meta_bytes, "a_g": 0, "cnt_e2": 0, "ginfo": 0}
+            "meta_recv": layer.cap * layer.meta_bytes, "a_g": 0, "cnt_e2": 0, "ginfo": 0,
+            "landed": layer.n * 4}
 
 
 def local_export(layer) -> dict:

@@ -296,6 +296,12 @@ class AuroraMoELayer:
             self.overlap = False  # the local/network GEMM split assumes one expert per rank
         else:
             self.meta_send = self.meta_recv = None
+        # arrival-driven expert GEMM (N1, one expert per rank): landed[g][i] = rows of block
+        # (sender i -> local rank g) the dispatch has made visible; GEMM1 runs beside the dispatch
+        # (an LSU copy engine, one CTA per SM, leaves the SMs' shared memory to the GEMM) and
+        # starts each tile once its rows have landed. AURORA_N1=1 turns it on.
+        self.landed = torch.zeros(self.n_local, n, **i32) if self.G == 1 else None
+        self.arrival = os.environ.get("AURORA_N1", "0") == "1"
         self.x = None
         self._tables_for(None)
 
@@ -363,6 +369,11 @@ class AuroraMoELayer:
             recv_p, ret_p, ctr_d, ctr_c = peers["recv"], peers["ret"], peers["ctr_d"], peers["ctr_c"]
             self.t_counts2 = self._ptr_table(peers["counts2"])
             self.t_xflag = self._ptr_table(peers["xflag"])
+        if self.landed is not None:  # receiver j's row of arrival credits
+            self.t_landed = self._ptr_table(peers["landed"] if peers is not None else
+                                            [self.landed.data_ptr() + (j - self.rank_base) * self.n * 4
+                                             if self.rank_base <= j < self.rank_base + self.n_local else 0
+                                             for j in range(self.n)])
         self.t_dst_d = self._ptr_table(recv_p)
         self.t_dst_c = self._ptr_table(ret_p)
         self.t_ctr_d = self._ptr_table(ctr_d)
@@ -440,8 +451,11 @@ class AuroraMoELayer:
     def engine_ctas(self, combine: bool, C: Optional[int] = None) -> int:
         """Copy CTAs per local rank the engine launches (clamped to co-residency)."""
         row2 = self.meta_bytes if (self.G > 1 and not combine) else 0
+        lsu = self.engine_lsu
+        if not combine and C is None:
+            lsu, C = self.dispatch_engine()
         c = self.L.aurora_engine_ctas(self.n, self.n_local, C or self.C, self.cfg.hidden * 2, row2,
-                                      1 if self.engine_lsu else 0)
+                                      1 if lsu else 0)
         if c < 1:
             _lib.check(-c, "aurora_engine_ctas")
         return c
@@ -492,6 +506,8 @@ class AuroraMoELayer:
     def _engine(self, mode: int, stream: int) -> None:
         cfg = self.cfg
         combine = mode & 1
+        lsu, C = (self.engine_lsu, self.C) if combine else self.dispatch_engine()
+        landed = self.arrival_on and not combine
         src = self.t_src_c if combine else self.t_src_d
         dst = self.t_dst_c if combine else (self.t_dst_g if self.grouped else self.t_dst_d)
         ctr = self.t_ctr_c if combine else self.t_ctr_d
@@ -499,14 +515,15 @@ class AuroraMoELayer:
         plane2 = self.G > 1 and not combine
         grouped = 256 if (self.grouped and not combine) else 0
         _lib.check(self.L.aurora_engine(
-            mode | sys_scope | self.engine_lsu | self.early_pace | grouped, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
+            mode | sys_scope | lsu | self.early_pace | grouped, self.n, self.n_local, self.rank_base, self.counts.data_ptr(), self.chunks.data_ptr(),
             self.rchunks.data_ptr(), self.progress.data_ptr(), self.n_in.data_ptr(), self.n_out.data_ptr(),
             self.soff.data_ptr(), self.roff.data_ptr(), self.send_list.data_ptr(), self.send_list.shape[1],
             src.data_ptr(), dst.data_ptr(), cfg.hidden * 2,
             self.t_src2.data_ptr() if plane2 else None, self.t_dst2.data_ptr() if plane2 else None,
             self.meta_bytes if plane2 else 0,
-            ctr.data_ptr(), self.C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
-            None if self.bw is None else self.bw.data_ptr(), None, stream),
+            ctr.data_ptr(), C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
+            None if self.bw is None else self.bw.data_ptr(), None,
+            self.t_landed.data_ptr() if landed else None, stream),
             "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
@@ -544,6 +561,19 @@ class AuroraMoELayer:
         return self.tile_ctrs[1 if stream == int(self.side.cuda_stream) else 0].data_ptr()
 
     @property
+    def arrival_on(self) -> bool:
+        """N1 in effect: one expert per rank, combine fused into GEMM2, K2 streamed to the dispatch."""
+        return (self.arrival and self.G == 1 and self.combine_in_gemm and self.stream_schedule
+                and not self.overlap)
+
+    def dispatch_engine(self):
+        """(LSU mode bit, copy CTAs per rank) of the dispatch: with N1 an LSU engine with one
+        CTA per SM, which leaves the SMs' shared memory to the GEMM running beside it."""
+        if self.arrival_on:
+            return 64, max(1, (self.num_sms - 2) // self.n_local)
+        return self.engine_lsu, self.C
+
+    @property
     def grouped(self) -> bool:
         """Rows are dispatched straight into the packed per-expert groups (needs the TMA engine)."""
         return self.G > 1 and self.grouped_dispatch and not self.engine_lsu
@@ -570,7 +600,8 @@ class AuroraMoELayer:
             self.ybuf.data_ptr(), self.rtot[self.rank_base:].data_ptr(), self.n_local, self.cap, cfg.hidden,
             cfg.ffn, self.t_dst_c.data_ptr(), self.counts.data_ptr(), self.soff.data_ptr(), self.roff.data_ptr(),
             self.n, self.rank_base, self.t_ctr_c.data_ptr(), self.gemm_ticket.data_ptr(), sys_scope,
-            self._part(), self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_combine")
+            self._part(), self.landed.data_ptr() if self.arrival_on else None, 1 if self.arrival_on else 0,
+            self._tctr(stream), self.num_sms, stream), "aurora_expert_ffn_combine")
 
     def combine_wait(self, stream: int) -> None:
         """Receiving side of the fused combine: every expert rank's rows for this
@@ -694,7 +725,8 @@ class AuroraMoELayer:
                 self.progress.zero_()  # stream-ordered before both K2 and the engine read it
                 self.schedule(s)
                 self.dispatch(s, overlap_schedule=True)
-                mark("dispatched", main)
+                if not self.arrival_on:  # N1: GEMM1 must directly follow the dispatch (PDL)
+                    mark("dispatched", main)
                 if self.combine_in_gemm:
                     self.experts_combine(s)
                 else:

@@ -80,7 +80,7 @@ def test_expert_ffn_matches_fp32(env):
     m_rows = [cap, 100]
     m = torch.tensor(m_rows, dtype=torch.int32, device="cuda")
     rc = L.aurora_expert_ffn(x.data_ptr(), w13.contiguous().data_ptr(), w2.data_ptr(), h.data_ptr(), y.data_ptr(),
-                             None, m.data_ptr(), G, cap, H, F, _ctr(torch), 0, _lib.stream_ptr())
+                             None, m.data_ptr(), G, cap, H, F, None, _ctr(torch), 0, _lib.stream_ptr())
     assert rc == 0
     torch.cuda.synchronize()
     for gi in range(G):
