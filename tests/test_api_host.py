@@ -236,3 +236,41 @@ def test_measured_rows_in_reference_csv_format(moeplan):
     assert [r.strategy for r in rows][0] == "aurora" and len(rows) >= 1
     ref_rows = [mexp.ResultRow(**{c: getattr(r, c) for c in report.CSV_COLUMNS}) for r in rows]
     assert report.csv_text(rows) == mexp.csv_text(ref_rows)
+
+
+def test_colocation_hetero_plan_matches_reference(moeplan):
+    """plan_colocation_hetero builds LayerProfiles with the measured-rate work model and
+    places pairs by colocate_heterogeneous: the same DeploymentPlan as the reference's own
+    colocate_heterogeneous (placement.py:129-157) on the same profiles and cluster."""
+    import numpy as np
+    from paper_2410_17043_b200.colocation import expert_work, plan_colocation_hetero
+    from paper_2410_17043_b200 import ClusterSpec, GpuSpec
+    rng = np.random.default_rng(11)
+    bws = (1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4)
+    for it in range(20):
+        ca = rng.integers(0, 3000, (8, 8)).astype(float)
+        cb = rng.integers(0, 1500, (8, 8)).astype(float)
+        wa, wb = expert_work(4096, 14336), expert_work(4096, 7168)
+        slots = [(2 * i, 2 * i + 1) for i in range(8)]
+        cp = plan_colocation_hetero(ca, cb, slots, ClusterSpec(tuple(GpuSpec(b, b) for b in bws)), wa, wb)
+        ref = moeplan.colocate_heterogeneous(
+            moeplan.LayerProfile(d_first=moeplan.TrafficMatrix(ca), **wa),
+            moeplan.LayerProfile(d_first=moeplan.TrafficMatrix(cb), **wb),
+            moeplan.ClusterSpec(tuple(moeplan.GpuSpec(b, b) for b in bws)))
+        assert tuple(cp.plan.assignment_a) == tuple(ref.assignment_a)
+        assert tuple(cp.plan.assignment_b) == tuple(ref.assignment_b)
+        assert sorted(cp.gpu_of_b) == [g for g in range(8) for _ in range(2)]
+
+
+def test_cluster_partition_host():
+    """The emulated-compute split of the GEMM's CTA pairs: proportional (largest
+    remainder), at least one pair per rank, covering every pair exactly once."""
+    import pytest
+    from paper_2410_17043_b200.layer import AuroraMoELayer
+    part = AuroraMoELayer.cluster_partition([1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4], 74)
+    sizes = [b - a for a, b in zip(part, part[1:])]
+    assert part[0] == 0 and part[-1] == 74 and min(sizes) >= 1
+    assert sizes == sorted(sizes, reverse=True) and sizes[0] > sizes[-1]
+    assert AuroraMoELayer.cluster_partition([1e-6, 1.0], 2) == [0, 1, 2]
+    with pytest.raises(ValueError):
+        AuroraMoELayer.cluster_partition([1.0] * 9, 8)
