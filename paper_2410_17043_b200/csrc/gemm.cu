@@ -28,7 +28,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
                               const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp,
-                              const AuroraArrivalArgs* arrival);
+                              const AuroraArrivalArgs* arrival, int after_gemm);
 
 namespace {
 
@@ -363,14 +363,14 @@ int launch_grouped(const void* a, const void* b, void* c, const int32_t* m_start
                    int64_t cap, int64_t map_rows, int N, int K, int epilogue, int32_t* tile_ctr, int num_sms,
                    cudaStream_t stream, const AuroraScatterArgs* scatter = nullptr,
                    const int32_t* cluster_part = nullptr, int part_gp = 1,
-                   const AuroraArrivalArgs* arrival = nullptr) {
+                   const AuroraArrivalArgs* arrival = nullptr, int after_gemm = 0) {
   // cap > 0: group g owns rows [g*cap, (g+1)*cap); cap == 0: groups packed,
   // m_start[g] absolute, map_rows = rows of the A buffer
   if (cap < 0 || (cap == 0 && (map_rows <= 0 || !m_start))) return AURORA_EINVAL;
   if (map_rows <= 0) map_rows = (int64_t)G * cap;
   if (use_pair_kernel())
     return aurora_launch_grouped_2sm(a, b, c, m_start, m_rows, G, cap, map_rows, N, K, epilogue, tile_ctr, num_sms,
-                                     stream, scatter, cluster_part, part_gp, arrival);
+                                     stream, scatter, cluster_part, part_gp, arrival, after_gemm);
   if (cluster_part || arrival) return AURORA_EINVAL;  // partitioned (emulated per-rank compute): pair kernel only
   if (scatter) return AURORA_EINVAL;  // the fused combine lives in the CTA-pair kernel
   if (G < 1 || G > MAX_GROUPS || N % BN || K % BK || N <= 0 || K <= 0 ||
@@ -421,7 +421,7 @@ extern "C" int aurora_expert_ffn(const void* a_buf, const void* w13, const void*
   if (rc != AURORA_OK) return rc;
   // y = h W2^T: N = H, K = F
   return launch_grouped(h_buf, w2, y_buf, m_start, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, nullptr, cluster_part);
+                        (cudaStream_t)stream, nullptr, cluster_part, 1, nullptr, 1);
 }
 
 extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, const void* w2,
@@ -440,7 +440,7 @@ extern "C" int aurora_expert_ffn_combine(const void* a_buf, const void* w13, con
   if (rc != AURORA_OK) return rc;
   const AuroraScatterArgs sc{ret_bufs, counts, soff, roff, ctrs, ticket, n, rank_base, sys ? 1 : 0};
   return launch_grouped(h_buf, w2, y_buf, nullptr, m_rows, G, cap, 0, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, &sc, cluster_part);
+                        (cudaStream_t)stream, &sc, cluster_part, 1, nullptr, 1);
 }
 
 extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w13, const void* w2, void* h_buf,
@@ -461,7 +461,7 @@ extern "C" int aurora_expert_ffn_packed_scatter(const void* a_buf, const void* w
   sc.ycap = ycap;
   sc.to_ret = to_ret ? 1 : 0;
   return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, &sc, cluster_part, experts_per_rank);
+                        (cudaStream_t)stream, &sc, cluster_part, experts_per_rank, nullptr, 1);
 }
 
 extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, const void* w2,
@@ -473,5 +473,5 @@ extern "C" int aurora_expert_ffn_packed(const void* a_buf, const void* w13, cons
                           (cudaStream_t)stream, nullptr, cluster_part, part_groups);
   if (rc != AURORA_OK) return rc;
   return launch_grouped(h_buf, w2, y_buf, g_off, g_rows, G, 0, a_rows, H, F, 0, tile_ctr, num_sms,
-                        (cudaStream_t)stream, nullptr, cluster_part, part_groups);
+                        (cudaStream_t)stream, nullptr, cluster_part, part_groups, nullptr, 1);
 }

@@ -139,7 +139,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             const int32_t* __restrict__ m_rows, int G, long long cap, int N, int K,
                             int epilogue, int group_m, const Scatter sc,
                             int32_t* __restrict__ tile_ctr, const __grid_constant__ CUtensorMap map_c,
-                            int tma_out, const int32_t* __restrict__ part, int part_gp, const Arrival ar) {
+                            int tma_out, const int32_t* __restrict__ part, int part_gp, const Arrival ar,
+                            int pdl_wait) {
+  // the next GEMM of the same FFN (a programmatic dependent launch) may start its prologue as CTAs exit
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ uint8_t smem_raw[];
   // first launch after arming wins (GEMM1; GEMM2's CTAs find the slots taken)
   if (threadIdx.x == 0 && g_gemm_trace)
@@ -249,6 +252,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc::cluster_sync();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_base_s;
+  // GEMM2 launched as a programmatic dependent of GEMM1: barriers, TMEM and the tile tables are set
+  // up while GEMM1's last tiles run; wait for GEMM1's grid (its h and the re-armed tile counter)
+  if (pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int k_blocks = K / BK;
   const bool dyn = tile_ctr != nullptr && part == nullptr;
   // i-th tile of this cluster (-1: done). Static: round robin over clusters.
@@ -565,7 +571,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
                               const int32_t* m_rows, int G, int64_t cap, int64_t map_rows, int N,
                               int K, int epilogue, int32_t* tile_ctr, int num_sms, cudaStream_t stream,
                               const AuroraScatterArgs* scatter, const int32_t* cluster_part, int part_gp,
-                              const AuroraArrivalArgs* arrival) {
+                              const AuroraArrivalArgs* arrival, int after_gemm) {
   Scatter sc{};
   if (scatter) {
     const bool packed = scatter->ginfo != nullptr;
@@ -652,7 +658,11 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  if (arrival && arrival->pdl) {  // programmatic dependent of the dispatch: runs beside it
+  // programmatic dependent launch: of the dispatch (N1: runs beside it, gated by `landed`), or of
+  // the FFN's previous GEMM (after_gemm: prologue overlaps its tail, then griddepcontrol.wait)
+  static const bool gemm_pdl = !getenv("AURORA_GEMM_PDL") || atoi(getenv("AURORA_GEMM_PDL")) != 0;
+  if (!gemm_pdl) after_gemm = 0;
+  if ((arrival && arrival->pdl) || after_gemm) {
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
@@ -660,7 +670,7 @@ int aurora_launch_grouped_2sm(const void* a, const void* b, void* c, const int32
   }
   if (cudaLaunchKernelEx(&cfg, grouped_gemm_2sm_kernel, ma, mb, (__nv_bfloat16*)c, m_start, m_rows, G,
                          (long long)cap, N, K, epilogue, group_m, sc, tile_ctr, mc, tma_out, cluster_part,
-                         part_gp > 0 ? part_gp : 1, ar) != cudaSuccess)
+                         part_gp > 0 ? part_gp : 1, ar, after_gemm ? 1 : 0) != cudaSuccess)
     return AURORA_ECUDA;
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
