@@ -404,7 +404,8 @@ int aurora_expert_reduce_combine(const void* yg, const int32_t* inv, const void*
  * experts: groups r * Gp .. r * Gp + Gp - 1, Gp = 1, experts_per_rank or part_groups), round robin
  * over their tiles, so a rank's GEMM time follows its share of the GPU like experts on a GPU of that
  * speed (ClusterSpec compute_scale, reference core.py:135-191; placement.py:46-60 / 129-157 decide
- * which experts land where). cluster_part[R] must equal num_sms / 2.
+ * which experts land where). cluster_part[R] <= num_sms / 2: pairs past it stay idle (a process
+ * emulating slower GPUs than the fastest one).
  * tile_ctr (every expert FFN / grouped GEMM entry point): two int32 owned by the caller,
  * zero before first use and re-armed by each launch's last cluster -- the dynamic tile
  * order's {next tile, clusters done} pair. One per stream whose GEMM launches may run

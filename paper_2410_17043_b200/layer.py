@@ -156,13 +156,20 @@ class AuroraMoELayer:
                                                                device=dev)
         # emulated per-rank compute (C4: ClusterSpec.compute_scale, reference core.py:135-191): the
         # expert GEMMs' CTA pairs are split among the local ranks in proportion, each rank's tiles run
-        # on its own share only (aurora_expert_ffn*'s cluster_part)
+        # on its own share only (aurora_expert_ffn*'s cluster_part); pairs past the last share idle
         self.compute_scales = None if compute_scales is None else [float(c) for c in compute_scales]
         self.gemm_part = None
         if self.compute_scales is not None:
             if len(self.compute_scales) != n or min(self.compute_scales) <= 0:
                 raise ValueError("compute_scales: one positive value per rank")
-            part = self.cluster_partition([self.compute_scales[r] for r in self.local_ranks], sms // 2)
+            # relative speeds must hold across processes too (one rank per GPU at N = 8): the process
+            # whose ranks have the largest scale sum uses every CTA pair, the others leave pairs idle
+            if n % self.n_local:
+                raise ValueError("compute_scales: ranks must split evenly over the processes")
+            sums = [sum(self.compute_scales[p:p + self.n_local]) for p in range(0, n, self.n_local)]
+            mine = sum(self.compute_scales[r] for r in self.local_ranks)
+            usable = max(self.n_local, min(sms // 2, int(round(sms // 2 * mine / max(sums)))))
+            part = self.cluster_partition([self.compute_scales[r] for r in self.local_ranks], usable)
             self.gemm_part = torch.tensor(part, dtype=torch.int32, device=dev)
 
         # ---- routing / permutation state

@@ -341,6 +341,10 @@ def test_layer_compute_partition(torch):
         layer.check_status()
         assert torch.equal(out, ref), fused
     assert AuroraMoELayer.cluster_partition([1, 1, 1, 1], 74)[-1] == 74
+    # one process of two (ranks 4-7: the slow half): only its share of the CTA pairs, idle pairs exit
+    half = AuroraMoELayer(cfg, rank_base=4, n_local=4, compute_scales=scales)
+    hp = half.gemm_part.cpu().tolist()
+    assert hp[-1] == round(layer.num_sms // 2 * 1.8 / 3.6)
     # several experts per rank (the packed grouped GEMMs, a rank's clusters serve all its experts)
     cfg5 = MoEConfig(hidden=512, ffn=256, experts=32, top_k=4, tokens=4096, ranks=8, skew=1.0, seed=5)
     ref5 = AuroraMoELayer(cfg5)
