@@ -571,7 +571,7 @@ class AuroraMoELayer:
     def arrival_on(self) -> bool:
         """N1 in effect: one expert per rank, combine fused into GEMM2, K2 streamed to the dispatch."""
         return (self.arrival and self.G == 1 and self.combine_in_gemm and self.stream_schedule
-                and not self.overlap)
+                and not self.overlap and self.gemm_part is None)
 
     def dispatch_engine(self):
         """(LSU mode bit, copy CTAs per rank) of the dispatch: with N1 an LSU engine with one

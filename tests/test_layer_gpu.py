@@ -660,3 +660,17 @@ def test_layer_cuda_graph_replay(torch, experts, top_k):
             layer.check_status()
             assert torch.equal(y, ref), rep
     assert int(layer.ctr_d.abs().sum()) == 0 and int(layer.ctr_c.abs().sum()) == 0
+
+
+def test_random_configs_all_variants_identical(torch):
+    """Race hunt (tools/stress.py): random small configs (2-16 ranks, 1-4 experts per
+    rank, top-1..6, skews 0-3, emulated compute on some), each through every variant
+    that must give the same bits -- default, engine combine, serial K2, unpaced, N1,
+    LSU engine, ungrouped / unscattered E > n paths -- twice, counters re-armed."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "stress", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "stress.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    m.main(40, 7)
