@@ -309,6 +309,7 @@ class AuroraMoELayer:
         # starts each tile once its rows have landed. AURORA_N1=1 turns it on.
         self.landed = torch.zeros(self.n_local, n, **i32) if self.G == 1 else None
         self.arrival = os.environ.get("AURORA_N1", "0") == "1"
+        self.nvtx = os.environ.get("AURORA_NVTX", "0") == "1"
         self.x = None
         self._tables_for(None)
 
@@ -717,10 +718,17 @@ class AuroraMoELayer:
         main = torch.cuda.current_stream(self.dev)
         s = int(main.cuda_stream)
         tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
+        nvtx = self.nvtx
+
         def mark(k, st):
             if tr and k in tr:
                 tr[k].record(st)
                 self._marked.add(k)
+            if nvtx:  # host-side ranges around each stage's launches (AURORA_NVTX=1; nsys / ncu --nvtx)
+                if k != "start":
+                    torch.cuda.nvtx.range_pop()
+                if k != "end":
+                    torch.cuda.nvtx.range_push(self.NVTX_STAGES.get(k, "aurora: after " + k))
         self._marked = set()
         mark("start", main)
         self.route(x, s)
@@ -790,6 +798,11 @@ class AuroraMoELayer:
 
     TRACE_POINTS = ("start", "packed", "local_copied", "local_gemm_done", "scheduled", "dispatched", "joined",
                     "experts_done", "combined", "end")
+    # NVTX range opened at each trace point (the stage that starts there)
+    NVTX_STAGES = {"start": "aurora: route + pack", "packed": "aurora: schedule + dispatch",
+                   "local_copied": "aurora: local experts", "scheduled": "aurora: remote dispatch",
+                   "dispatched": "aurora: experts", "joined": "aurora: remote experts",
+                   "experts_done": "aurora: combine", "combined": "aurora: aggregate"}
 
     def timeline(self, x: torch.Tensor) -> dict:
         """One traced forward: ms from start to each point (diagnostics)."""

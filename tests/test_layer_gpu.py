@@ -184,6 +184,30 @@ def test_layer_serial_and_overlapped_agree(torch):
         assert torch.equal(serial, out), (overlap, c_ov)
 
 
+def test_layer_nvtx_ranges_balanced(torch):
+    """AURORA_NVTX ranges around the stages stay balanced (push / pop per trace point)
+    for the default, serial-schedule and N1 plans; the output is unchanged."""
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=256, ffn=256, experts=8, top_k=2, tokens=2048, ranks=8, skew=1.0, seed=3)
+    layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = layer(x).clone()
+    layer.nvtx = True
+    for attrs in ({}, {"stream_schedule": False}, {"arrival": True}):
+        for a, v in attrs.items():
+            setattr(layer, a, v)
+        depth0 = torch.cuda.nvtx.range_push("probe")
+        out = layer(x)
+        depth1 = torch.cuda.nvtx.range_push("probe")
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        assert depth1 == depth0, attrs  # same nesting depth before and after the forward
+        assert torch.equal(out, ref)
+        for a in attrs:
+            setattr(layer, a, {"stream_schedule": True, "arrival": False}[a])
+
+
 def test_layer_repeated_calls_rearm_counters(torch):
     from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
     cfg = MoEConfig(hidden=256, ffn=256, experts=8, top_k=2, tokens=2048, ranks=8, skew=0.5, seed=2)
