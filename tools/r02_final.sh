@@ -1,0 +1,17 @@
+#!/bin/bash
+# End-of-round evidence (gpurun_out/final/): GPU tests + smoke, every bench config, the reference arm,
+# the C2 launch list and one ncu --set full capture of both GEMM launches.
+mkdir -p gpurun_out/final
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/final/gputest.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
+for c in c2 c3 c3h c4 c5; do
+  timeout 900 python bench.py --config $c > gpurun_out/final/bench_$c.json 2> gpurun_out/final/bench_$c.err
+done
+timeout 900 python bench.py --impl reference > gpurun_out/final/bench_reference.json 2> gpurun_out/final/bench_reference.err
+K='regex:route|pack|schedule|engine|gemm|aggregate|combine|expert|hist|gather|prepare'
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c 200 --csv \
+  --log-file gpurun_out/final/launches_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:grouped_gemm_2sm_kernel -s 2 -c 2 \
+  -o gpurun_out/final/gemm python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/final/ncu_gemm.json gpurun_out/final/gemm.ncu-rep > /dev/null 2>&1
+tail -2 gpurun_out/final/gputest.log; tail -1 gpurun_out/final/smoke.log
