@@ -588,6 +588,8 @@ def run_c3(args):
                                        expert_work(4096, 7168))
         homo_pair = ColocatedLayers(cfg_a, cfg_b, homo_plan, **kw)
     pair = ColocatedLayers(cfg_a, cfg_b, cplan, **kw)
+    if homo_pair is not None:
+        homo_pair.interleave = pair.interleave
     for _ in range(args.warmup):
         pair(xa, xb)
     torch.cuda.synchronize()
@@ -606,9 +608,29 @@ def run_c3(args):
         time.sleep(0.2)
     pair.check_status()
     ms = e0.elapsed_time(e1) / args.steps
+    # Table-1 interleaving vs the serial order (model a's layer, then model b's), alternated
+    # three times so both see the same power state; the headline uses the layer's default
+    il_default = pair.interleave
+    il_runs = {"interleaved": [], "serial": []}
+    for _ in range(3):
+        for name, il in (("interleaved", True), ("serial", False)):
+            pair.interleave = il
+            pair(xa, xb)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(st)
+            for _ in range(args.steps):
+                pair(xa, xb)
+            f1.record(st)
+            torch.cuda.synchronize()
+            pair.check_status()
+            il_runs[name].append(f0.elapsed_time(f1) / args.steps)
+    pair.interleave = True
+    il_timeline = pair.timeline(xa, xb)
+    pair.interleave = il_default
+    il_med = {k: sorted(v)[1] for k, v in il_runs.items()}
     # end to end: both inputs in from pinned host memory, both outputs back, every step
-    # pipelined like the C2 line: copy-engine streams move model b's input in under model a's
-    # layer, model a's output out under model b's, double-buffered device inputs / outputs
+    # pipelined like the C2 line: copy-engine streams move the next step's inputs in and the
+    # previous step's outputs out under the layers, double-buffered device inputs / outputs
     NB = 2
     xah = [xa.cpu().pin_memory() for _ in range(NB)]
     xbh = [xb.cpu().pin_memory() for _ in range(NB)]
@@ -636,10 +658,9 @@ def run_c3(args):
         if i >= NB:  # the output buffers were drained to the host
             st.wait_event(ev["out_b"][bb])
         st.wait_event(ev["in_a"][bb])
-        pair.a(xad[bb], out=oad[bb])
-        ev["done_a"][bb].record(st)
         st.wait_event(ev["in_b"][bb])
-        pair.b(xbd[bb], out=obd[bb])
+        pair(xad[bb], xbd[bb], out_a=oad[bb], out_b=obd[bb])
+        ev["done_a"][bb].record(st)
         ev["done_b"][bb].record(st)
         d2h_s.wait_event(ev["done_a"][bb])
         with torch.cuda.stream(d2h_s):
@@ -670,9 +691,16 @@ def run_c3(args):
                     "h2d_bytes_per_step": int((xah[0].numel() + xbh[0].numel()) * 2),
                     "d2h_bytes_per_step": int((oah[0].numel() + obh[0].numel()) * 2), "ms_per_step": e2e_ms,
                     "path": "both layers' public forward on pinned host buffers",
-                    "pipeline": "H2D of model b's input under model a's layer, D2H of model a's output under "
-                                "model b's (copy-engine streams, double-buffered device inputs / outputs)"},
+                    "pipeline": "H2D of step i+1's inputs and D2H of step i-1's outputs under step i "
+                                "(copy-engine streams, double-buffered device inputs / outputs)"},
             "clocks": clocks.summary(0),
+            "interleave": {"default_on": il_default, "switch": "AURORA_C3_INTERLEAVE=0 for the serial order",
+                           "interleaved_ms_per_step": il_med["interleaved"], "serial_ms_per_step": il_med["serial"],
+                           "speedup": il_med["serial"] / il_med["interleaved"], "runs": il_runs,
+                           "timeline_ms": il_timeline,
+                           "what": "Table 1 (PAPER.md:473-497) on one GPU: model b on a second stream, its gate "
+                                   "beside model a's gate / dispatch, its dispatch right after model a's, its FFN "
+                                   "behind model a's FFN, model a's aggregation beside it; combines fused"},
             "timeline_ms": {"a": pair.a.timeline(xa), "b": pair.b.timeline(xb)}}
     if hetero:
         # the same two models on the same emulated cluster, pairs placed by the homogeneous plan

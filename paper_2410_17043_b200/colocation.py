@@ -16,7 +16,9 @@ share a GPU run as that GPU's tcgen05 grouped GEMMs.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 
@@ -107,18 +109,75 @@ class ColocatedLayers:
     """Model a (one expert per rank) and model b (two experts per rank) on the
     same ranks, placed by a :class:`ColocationPlan`."""
 
-    def __init__(self, cfg_a, cfg_b, cplan: ColocationPlan, **kw):
+    def __init__(self, cfg_a, cfg_b, cplan: ColocationPlan, *, interleave: Optional[bool] = None, **kw):
+        import torch
+
         from .layer import AuroraMoELayer
         if cfg_a.ranks != cfg_b.ranks or cfg_b.experts != 2 * cfg_a.ranks or cfg_a.experts != cfg_a.ranks:
             raise ValueError("expects model a with one expert per rank and model b with two")
         self.cplan = cplan
         self.a = AuroraMoELayer(cfg_a, DeploymentPlan(cplan.gpu_of_a), **kw)
         self.b = AuroraMoELayer(cfg_b, None, gpu_of_expert=cplan.gpu_of_b, **kw)
+        if interleave is None:
+            interleave = os.environ.get("AURORA_C3_INTERLEAVE", "1") != "0"
+        self.interleave = interleave
+        self.side = torch.cuda.Stream(device=self.a.dev)
+        self._ev = {k: torch.cuda.Event() for k in ("start", "n_a", "n_b", "b_done")}
 
     def forward(self, x_a, x_b, out_a=None, out_b=None):
-        return self.a(x_a, out=out_a), self.b(x_b, out=out_b)
+        """One layer of each model. Serial (``interleave=False``): model a's whole
+        layer, then model b's. Interleaved (default): the one-GPU form of the paper's
+        Table 1 (the reference simulates it in
+        sim.simulate_colocated, sim.py:192-257). Model b runs on a second stream:
+        its gate G_b and its schedule (K2) beside model a's gate, K2 and dispatch
+        N_a; its dispatch N_b right after N_a, so both all-to-alls form one dispatch
+        window (the two copy engines never overlap: each waits on all of its own
+        CTAs); then F_a, and F_b behind it with model a's aggregation A_a beside F_b.
+        The combines C_a / C_b run inside the FFNs' last kernels (fused combine).
+        Where one GPU differs from Table 1: N_b cannot hide under F_a here, because
+        the dispatch is executed by SMs that the persistent GEMM holds."""
+        import torch
+        if not self.interleave:
+            return self.a(x_a, out=out_a), self.b(x_b, out=out_b)
+        for m in (self.a, self.b):
+            if not m.combine_in_gemm or m.arrival_on or m.overlap:
+                raise ValueError("interleaving needs the fused combine, no N1 and no AURORA_OVERLAP on both models")
+        self.a._check_out(out_a, x_a)
+        self.b._check_out(out_b, x_b)
+        main = torch.cuda.current_stream(self.a.dev)
+        ev = self._ev
+        ev["start"].record(main)
+        self.side.wait_event(ev["start"])
+        self.a.front(x_a)                                       # G_a
+        with torch.cuda.stream(self.side):
+            self.b.front(x_b)                                   # G_b beside G_a
+        self.a.send(dispatched=ev["n_a"])                       # K2_a + N_a
+        with torch.cuda.stream(self.side):
+            self.b.send(dispatch_after=ev["n_a"], dispatched=ev["n_b"])  # K2_b beside N_a, then N_b
+        ya = self.a.finish(out_a, experts_after=ev["n_b"])     # F_a (+C_a), A_a
+        with torch.cuda.stream(self.side):
+            yb = self.b.finish(out_b)                           # F_b (+C_b), A_b
+        ev["b_done"].record(self.side)
+        main.wait_event(ev["b_done"])
+        return ya, yb
 
     __call__ = forward
+
+    def timeline(self, x_a, x_b) -> dict:
+        """One traced forward of both models: ms from model a's start to each
+        stage point of each model (the measured counterpart of the Table-1 spans)."""
+        import torch
+        pts = self.a.TRACE_POINTS
+        self.a.trace = {k: torch.cuda.Event(enable_timing=True) for k in pts}
+        self.b.trace = {k: torch.cuda.Event(enable_timing=True) for k in pts}
+        try:
+            self.forward(x_a, x_b)
+            torch.cuda.synchronize(self.a.dev)
+            t0 = self.a.trace["start"]
+            return {name: {k: round(t0.elapsed_time(e), 4) for k, e in m.trace.items() if k in m._marked}
+                    for name, m in (("a", self.a), ("b", self.b))}
+        finally:
+            self.a.trace = self.b.trace = None
 
     def check_status(self) -> None:
         self.a.check_status()

@@ -695,10 +695,18 @@ class AuroraMoELayer:
                                            self.roff.data_ptr(), stream), "aurora_aggregate")
 
     # ------------------------------------------------------------ forward
-    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, *,
+                dispatch_after: Optional[torch.cuda.Event] = None,
+                dispatched: Optional[torch.cuda.Event] = None) -> torch.Tensor:
         r"""x: [tokens of the local ranks, hidden] bf16 on this GPU -> same shape,
         written to ``out`` when given (e.g. one of several pipelined output
         buffers), else to the layer's own ``self.out``.
+
+        ``dispatch_after`` / ``dispatched``: events for running two layers on two
+        streams (colocated models, :class:`~.colocation.ColocatedLayers`): the
+        stream waits for ``dispatch_after`` before K2 + the dispatch, and records
+        ``dispatched`` once the dispatch is launched, so the two layers' copy
+        engines never run at the same time.
 
         Stream plan (no host synchronisation anywhere):
           route -> (counts exchange) -> pack -> K2 schedule ---------------------------+
@@ -708,93 +716,149 @@ class AuroraMoELayer:
         AURORA_OVERLAP=schedule|full instead runs the local rows' expert GEMM on a
         side stream beside K2 and the network dispatch (measured slower).
         """
-        if x.dtype != torch.bfloat16 or x.shape != (self.T_local, self.cfg.hidden) or not x.is_contiguous():
-            raise ValueError(f"x must be contiguous bf16 [{self.T_local}, {self.cfg.hidden}]")
+        self._check_out(out, x)
+        self.front(x)
+        return self.back(out, dispatch_after=dispatch_after, dispatched=dispatched)
+
+    def _check_out(self, out: Optional[torch.Tensor], x: Optional[torch.Tensor] = None) -> None:
+        x = self.x if x is None else x
         if out is not None and (out.dtype != torch.bfloat16 or out.shape != x.shape or not out.is_contiguous()
                                 or out.device != x.device):
             raise ValueError("out must be a contiguous bf16 tensor shaped like x on the same device")
+
+    def _mark(self, k: str, st) -> None:
+        tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
+        if tr and k in tr:
+            tr[k].record(st)
+            self._marked.add(k)
+        if self.nvtx:  # host-side ranges around each stage's launches (AURORA_NVTX=1; nsys / ncu --nvtx)
+            if k != "start":
+                torch.cuda.nvtx.range_pop()
+            if k != "end":
+                torch.cuda.nvtx.range_push(self.NVTX_STAGES.get(k, "aurora: after " + k))
+
+    def front(self, x: torch.Tensor) -> None:
+        """The forward up to the permutation (router, counts exchange, pack) on the
+        current stream; :meth:`back` continues it. ``forward`` = front + back."""
+        if x.dtype != torch.bfloat16 or x.shape != (self.T_local, self.cfg.hidden) or not x.is_contiguous():
+            raise ValueError(f"x must be contiguous bf16 [{self.T_local}, {self.cfg.hidden}]")
         if self.x is None or x.data_ptr() != self.x.data_ptr():
             self._use_input(x)
         main = torch.cuda.current_stream(self.dev)
         s = int(main.cuda_stream)
-        tr = self.trace  # optional {point: cuda.Event} timeline (diagnostics)
-        nvtx = self.nvtx
-
-        def mark(k, st):
-            if tr and k in tr:
-                tr[k].record(st)
-                self._marked.add(k)
-            if nvtx:  # host-side ranges around each stage's launches (AURORA_NVTX=1; nsys / ncu --nvtx)
-                if k != "start":
-                    torch.cuda.nvtx.range_pop()
-                if k != "end":
-                    torch.cuda.nvtx.range_push(self.NVTX_STAGES.get(k, "aurora: after " + k))
         self._marked = set()
-        mark("start", main)
+        self._mark("start", main)
         self.route(x, s)
         self.exchange_counts(s)
         self.pack(s)
-        mark("packed", main)
-        if not self.overlap:
-            if self.stream_schedule:
-                self.progress.zero_()  # stream-ordered before both K2 and the engine read it
-                self.schedule(s)
-                self.dispatch(s, overlap_schedule=True)
-                if not self.arrival_on:  # N1: GEMM1 must directly follow the dispatch (PDL)
-                    mark("dispatched", main)
-                if self.combine_in_gemm:
-                    self.experts_combine(s)
-                else:
-                    self.experts(s)
-            else:
-                self.schedule(s)
-                self.dispatch(s)
-                if self.combine_in_gemm:
-                    self.experts_combine(s)
-                else:
-                    self.experts(s)
+        self._mark("packed", main)
+
+    def back(self, out: Optional[torch.Tensor] = None, *, dispatch_after: Optional[torch.cuda.Event] = None,
+             dispatched: Optional[torch.cuda.Event] = None) -> torch.Tensor:
+        """The forward from K2 on (schedule, dispatch, experts, combine, aggregate) on
+        the current stream, after :meth:`front` of the same batch: :meth:`send` then
+        :meth:`finish` (or the AURORA_OVERLAP split)."""
+        if self.overlap:
+            if dispatch_after is not None or dispatched is not None:
+                raise ValueError("dispatch events exclude AURORA_OVERLAP (a second dispatch on the side stream)")
+            return self._back_overlap(out)
+        self.send(dispatch_after=dispatch_after, dispatched=dispatched)
+        return self.finish(out)
+
+    def send(self, *, dispatch_after: Optional[torch.cuda.Event] = None,
+             dispatched: Optional[torch.cuda.Event] = None) -> None:
+        """K2 and the dispatch on the current stream. ``dispatch_after``: the dispatch
+        waits for this event (K2 still runs before it, so it overlaps what the event
+        guards); ``dispatched`` is recorded when the dispatch has finished."""
+        if self.overlap:
+            raise ValueError("AURORA_OVERLAP layers run back() as a whole")
+        if (dispatch_after is not None or dispatched is not None) and self.arrival_on:
+            raise ValueError("dispatch events exclude N1 (GEMM1 launched right behind the dispatch)")
+        main = torch.cuda.current_stream(self.dev)
+        s = int(main.cuda_stream)
+        if self.stream_schedule and dispatch_after is None:
+            self.progress.zero_()  # stream-ordered before both K2 and the engine read it
+            self.schedule(s)
+            self.dispatch(s, overlap_schedule=True)
         else:
-            self._ev_pack.record(main)
-            self.side.wait_event(self._ev_pack)
-            ss = int(self.side.cuda_stream)
-            self.dispatch(ss, "local")
-            mark("local_copied", self.side)
-            self.experts(ss, "local")
-            mark("local_gemm_done", self.side)
-            self._ev_local.record(self.side)
-            # the remote dispatch may run with fewer copy CTAs beside the local GEMM
-            # (AURORA_C_OVERLAP): K2 counts its hand-over thresholds for the CTAs the
-            # dispatch will actually launch
-            c_disp = (self.C_overlap or self.C) if self.overlap != "schedule" else self.C
-            self.schedule(s, dispatch_ctas=c_disp)
-            mark("scheduled", main)
-            if self.overlap == "schedule":
-                # only the (latency-bound) scheduler hides under the local GEMM;
-                # the bandwidth-bound dispatch runs after it
-                main.wait_event(self._ev_local)
-                mark("joined", main)
-                self.dispatch(s, "remote")
-                mark("dispatched", main)
-            else:
-                c_full = self.C
-                self.C = c_disp
-                try:
-                    self.dispatch(s, "remote")
-                finally:
-                    self.C = c_full
-                mark("dispatched", main)
-                main.wait_event(self._ev_local)
-                mark("joined", main)
-            self.experts(s, "remote")
-        mark("experts_done", main)
+            self.schedule(s)
+            if dispatch_after is not None:
+                main.wait_event(dispatch_after)
+            self.dispatch(s)
+        if dispatched is not None:
+            dispatched.record(main)
+        if not self.arrival_on:  # N1: GEMM1 must directly follow the dispatch (PDL)
+            self._mark("dispatched", main)
+
+    def finish(self, out: Optional[torch.Tensor] = None, *,
+               experts_after: Optional[torch.cuda.Event] = None) -> torch.Tensor:
+        """Experts (+ fused combine), combine, aggregation on the current stream, after
+        :meth:`send`. ``experts_after``: the expert GEMMs wait for this event."""
+        self._check_out(out)
+        main = torch.cuda.current_stream(self.dev)
+        s = int(main.cuda_stream)
+        if experts_after is not None:
+            if self.arrival_on:
+                raise ValueError("experts_after excludes N1 (GEMM1 launched right behind the dispatch)")
+            main.wait_event(experts_after)
+        if self.combine_in_gemm:
+            self.experts_combine(s)
+        else:
+            self.experts(s)
+        return self._tail(out, main)
+
+    def _tail(self, out, main) -> torch.Tensor:
+        s = int(main.cuda_stream)
+        self._mark("experts_done", main)
         if self.combine_in_gemm:
             self.combine_wait(s)
         else:
             self.combine(s)
-        mark("combined", main)
+        self._mark("combined", main)
         self.aggregate(s, out)
-        mark("end", main)
+        self._mark("end", main)
         return self.out if out is None else out
+
+    def _back_overlap(self, out) -> torch.Tensor:
+        """AURORA_OVERLAP=schedule|full: the local rows' dispatch + expert GEMM on the
+        side stream beside K2 and the network dispatch (measured slower)."""
+        self._check_out(out)
+        main = torch.cuda.current_stream(self.dev)
+        s = int(main.cuda_stream)
+        mark = self._mark
+        self._ev_pack.record(main)
+        self.side.wait_event(self._ev_pack)
+        ss = int(self.side.cuda_stream)
+        self.dispatch(ss, "local")
+        mark("local_copied", self.side)
+        self.experts(ss, "local")
+        mark("local_gemm_done", self.side)
+        self._ev_local.record(self.side)
+        # the remote dispatch may run with fewer copy CTAs beside the local GEMM
+        # (AURORA_C_OVERLAP): K2 counts its hand-over thresholds for the CTAs the
+        # dispatch will actually launch
+        c_disp = (self.C_overlap or self.C) if self.overlap != "schedule" else self.C
+        self.schedule(s, dispatch_ctas=c_disp)
+        mark("scheduled", main)
+        if self.overlap == "schedule":
+            # only the (latency-bound) scheduler hides under the local GEMM;
+            # the bandwidth-bound dispatch runs after it
+            main.wait_event(self._ev_local)
+            mark("joined", main)
+            self.dispatch(s, "remote")
+            mark("dispatched", main)
+        else:
+            c_full = self.C
+            self.C = c_disp
+            try:
+                self.dispatch(s, "remote")
+            finally:
+                self.C = c_full
+            mark("dispatched", main)
+            main.wait_event(self._ev_local)
+            mark("joined", main)
+        self.experts(s, "remote")
+        return self._tail(out, main)
 
     TRACE_POINTS = ("start", "packed", "local_copied", "local_gemm_done", "scheduled", "dispatched", "joined",
                     "experts_done", "combined", "end")

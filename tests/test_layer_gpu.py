@@ -488,6 +488,18 @@ def test_colocated_models(torch):
     assert pair.a.G == 1 and pair.b.G == 2
     assert tuple(pair.b.gpu_of) == cp.gpu_of_b
     assert combined_bmax(cal_a.counts.cpu().numpy(), slot_counts, cp.plan) > 0
+    # Table-1 interleaving (model b on a second stream) and the serial order: same bits
+    ref_a, ref_b = out_a.clone(), out_b.clone()
+    for il in (False, True, False, True):
+        pair.interleave = il
+        for _ in range(3):
+            ya, yb = pair(xa, xb)
+        torch.cuda.synchronize()
+        pair.check_status()
+        assert torch.equal(ya, ref_a) and torch.equal(yb, ref_b), il
+    tl = pair.timeline(xa, xb)
+    assert tl["b"]["dispatched"] >= tl["a"]["dispatched"]  # N_b waits for N_a (one copy engine at a time)
+    assert tl["a"]["end"] > 0 and tl["b"]["end"] > 0
 
 
 def test_engine_runs_baseline_schedules(torch):
