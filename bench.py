@@ -880,52 +880,9 @@ def main():
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(ms.item()) / args.steps
 
-    # ---- sustained rate (diagnostic beside the headline): the 1 kW power limiter settles
-    # over ~100 ms, so 60 more back-to-back steps report the rate after it has (last 40)
-    sus = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    sus[0].record(stream)
-    for i_ in range(60):
-        layer(x)
-        if i_ == 19:
-            sus[1].record(stream)
-    sus[2].record(stream)
-    torch.cuda.synchronize()
-    layer.check_status()
-    sustained = {"first_20_ms_per_step": sus[0].elapsed_time(sus[1]) / 20,
-                 "last_40_ms_per_step": sus[1].elapsed_time(sus[2]) / 40}
-
-    # ---- per-stage breakdown (serial pass, not the headline number)
-    # (with the combine fused into GEMM2, the fused and the engine step alternate so
-    # both see the same power / clock state)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
-    evf = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
-    fused = layer.combine_in_gemm
-    for s_ in range(args.steps):
-        staged_step(evs[s_])
-        if fused:
-            staged_step(evf[s_], fused=True)
-    torch.cuda.synchronize()
-    layer.check_status()
-    stage_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
-    fused_ms = ({st: sum(e[i].elapsed_time(e[i + 1]) for e in evf) / args.steps for i, st in enumerate(stages)}
-                if fused else None)
-    serial_ms = sum(stage_ms.values())
-    # ablation (SURVEY 8(f)3): the same engine with the schedule's pacing switched off
-    layer.unpaced = 16
-    for s_ in range(args.steps):
-        staged_step(evs[s_])
-    torch.cuda.synchronize()
-    layer.check_status()
-    layer.unpaced = 0
-    unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
-    baseline_sched = baseline_schedules(layer, x, sp, stream) if world == 1 else {}
-    sched_dispatch_us = a2a_overlapped(args.steps)
-    try:  # a diagnostic beside the headline: never let it take the bench line down
-        library_a2a = library_alltoall(layer, x, args, world, rank, stream)
-    except Exception as e:  # noqa: BLE001
-        library_a2a = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
-
-    # ---- end to end through the public API with host buffers (pinned), copies timed.
+    # ---- end to end through the public API with host buffers (pinned), copies timed,
+    # right after the headline steps (same power regime as `value`; the diagnostics below
+    # run the GPU for many more steps).
     # Serving-style pipeline: the copy engines move step i+1's input in and step
     # i-1's output out while the SMs run step i (double-buffered device input and
     # output, one stream per copy direction, events order the reuse of buffers).
@@ -973,6 +930,52 @@ def main():
     e2e_ms = float(e2e_ms.item())
     layer.check_status()
     assert torch.equal(outh[(args.steps - 1) % NB], od[(args.steps - 1) % NB].cpu())
+
+    # ---- sustained rate (diagnostic beside the headline): the 1 kW power limiter settles
+    # over ~100 ms, so 60 more back-to-back steps report the rate after it has (last 40)
+    sus = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    sus[0].record(stream)
+    for i_ in range(60):
+        layer(x)
+        if i_ == 19:
+            sus[1].record(stream)
+    sus[2].record(stream)
+    torch.cuda.synchronize()
+    layer.check_status()
+    sustained = {"first_20_ms_per_step": sus[0].elapsed_time(sus[1]) / 20,
+                 "last_40_ms_per_step": sus[1].elapsed_time(sus[2]) / 40}
+
+    # ---- per-stage breakdown (serial pass, not the headline number)
+    # (with the combine fused into GEMM2, the fused and the engine step alternate so
+    # both see the same power / clock state)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    evf = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    fused = layer.combine_in_gemm
+    for s_ in range(args.steps):
+        staged_step(evs[s_])
+        if fused:
+            staged_step(evf[s_], fused=True)
+    torch.cuda.synchronize()
+    layer.check_status()
+    stage_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
+    fused_ms = ({st: sum(e[i].elapsed_time(e[i + 1]) for e in evf) / args.steps for i, st in enumerate(stages)}
+                if fused else None)
+    serial_ms = sum(stage_ms.values())
+    # ablation (SURVEY 8(f)3): the same engine with the schedule's pacing switched off
+    layer.unpaced = 16
+    for s_ in range(args.steps):
+        staged_step(evs[s_])
+    torch.cuda.synchronize()
+    layer.check_status()
+    layer.unpaced = 0
+    unpaced_ms = {st: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i, st in enumerate(stages)}
+    baseline_sched = baseline_schedules(layer, x, sp, stream) if world == 1 else {}
+    sched_dispatch_us = a2a_overlapped(args.steps)
+    try:  # a diagnostic beside the headline: never let it take the bench line down
+        library_a2a = library_alltoall(layer, x, args, world, rank, stream)
+    except Exception as e:  # noqa: BLE001
+        library_a2a = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+
 
     # ---- roofline of the dominant kernel (the tcgen05 expert GEMMs) and the all-to-all bound
     counts = layer.counts.cpu().numpy().astype(np.int64)
