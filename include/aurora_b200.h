@@ -233,7 +233,7 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
                   const void* const* src2_bufs, void* const* dst2_bufs, int row2_bytes,
                   int32_t* const* ctrs, int ctas_per_rank, int max_phases, int64_t spin_limit,
                   int32_t* status, int split, const double* bw, void* const* ginfo_bufs,
-                  int32_t* const* landed, void* stream);
+                  int32_t* const* landed, const double* phase_dur, float unit_ns, void* stream);
 /* ginfo_bufs (mode bit 8, nullable): per rank the base of its process's [rows] int4
  * array; every grouped store of a row also writes {receiver-layout row, gate weight,
  * single (the row's only local expert), 0} at the row's group position
@@ -243,7 +243,13 @@ int aurora_engine(int mode, int n, int n_local, int rank_base, const int32_t* co
  * (i -> j) after they are visible -- at each run end and after its share of the local rows
  * (release) -- the arrival signal of aurora_expert_ffn_combine's arrival-driven GEMM1. The
  * engine triggers griddepcontrol.launch_dependents at entry, so that GEMM may be a
- * programmatic dependent launch running beside it. */
+ * programmatic dependent launch running beside it.
+ * phase_dur / unit_ns (TMA engine; phase_dur NULL or unit_ns 0 = off): deadline pacing. A run
+ * also starts once the schedule's own clock reaches its phase -- the copy CTA's first remote
+ * entry + (phase_dur[0] + ... + phase_dur[k-1]) * unit_ns ns -- whichever comes first with the
+ * hand-over, so a late flag no longer delays the chain. phase_dur = aurora_schedule_counts'
+ * output (the combine replays the same phases); unit_ns = ns per schedule time unit of a pair
+ * (row bytes / link bytes per ns). Pacing only: rows and completion are unchanged. */
 /* aurora_engine_ctas: copy CTAs per local rank the engine will actually use
  * (ctas_per_rank clamped so every copy CTA is co-resident), or -AURORA_E* on
  * error. K2 needs n_local x this value to count hand-over thresholds. The

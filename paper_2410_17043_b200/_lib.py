@@ -33,7 +33,7 @@ _SIGNATURES = {
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,
                       _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_i64, _vp, _c_int, _vp, _vp, _vp,
-                      _vp],
+                      _vp, ctypes.c_float, _vp],
     "aurora_engine_ctas": [_c_int, _c_int, _c_int, _c_int, _c_int, _c_int],
     "aurora_aggregate": [_vp, _c_i64, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                          _c_int, _vp, _vp, _c_i64, _vp, _vp],

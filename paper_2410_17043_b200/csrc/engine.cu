@@ -60,6 +60,11 @@ struct EngineParams {
   // (sender i -> receiver j) stored and visible, credited per CTA at every run end (and after the
   // local rows); the GEMM starts a tile once every block under it is complete
   int32_t* const* landed;
+  // deadline pacing (TMA engine; phase_dur nullable = off): a run also starts once the schedule's
+  // own clock reaches its phase -- t0 (the copy CTA's first remote entry) + start(k) * unit_ns,
+  // start(k) = the durations of phases 0..k-1 -- whichever comes first with the hand-over
+  const double* phase_dur;
+  float unit_ns;
 };
 
 // This CTA's rank (local index), its index among the rank's CTAs and the
@@ -92,6 +97,20 @@ __device__ void cta_assign(const EngineParams& p, int* cs /* smem [AUR_MAXN] */,
 __device__ __forceinline__ bool wait_ge(const int32_t* ctr, int target, long long limit, bool sys) {
   long long spins = 0;
   while ((sys ? ld_acquire_sys(ctr) : ld_acquire_gpu(ctr)) < target) {
+    if (limit && ++spins > limit) return false;
+    if (spins > 64) __nanosleep(20);
+  }
+  return true;
+}
+
+// wait until *ctr >= target or the %globaltimer reaches `due` (deadline pacing), bounded
+__device__ __forceinline__ bool wait_ge_or_until(const int32_t* ctr, int target, long long due, long long limit,
+                                                 bool sys) {
+  long long spins = 0;
+  while ((sys ? ld_acquire_sys(ctr) : ld_acquire_gpu(ctr)) < target) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t >= due) return true;
     if (limit && ++spins > limit) return false;
     if (spins > 64) __nanosleep(20);
   }
@@ -400,6 +419,7 @@ constexpr int RING = 128;
 
 
 __device__ int g_early_rows = 2;  // rows before a run's end at which its pace signal goes out
+
 __device__ __forceinline__ long long eng_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -410,6 +430,8 @@ struct TmaShared {
   uint64_t full[16], empty[16];
   int4 win[32];     // producer's window of global entries
   int4 ring[RING];  // entries handed to the consumer (producer -> consumer, in order)
+  float ring_t[RING];  // deadline pacing: schedule time (units) at which entry k's phase starts
+  float wdur[32];      // deadline pacing: durations of the producer's window of phases
   volatile int known, known_done, cons_k;
   int32_t idx[32];
   // per-call metadata staged once: every per-entry lookup is a shared-memory read
@@ -487,18 +509,29 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     const char* src = p.src_bufs[r_local];
     const char* src2 = rb2 ? p.src2_bufs[r_local] : nullptr;
     const int32_t* list = p.send_list + (size_t)r_local * p.send_list_stride;
+    const double* ddur = p.phase_dur;
+    double tcum = 0.0;  // deadline pacing: schedule time at the start of phase k
     for (int k = do_local ? -1 : 0; do_remote || k < 0; k++) {
       int peer, first, ntok;
       if (k < 0) {
         peer = g, first = 0, ntok = sh.nloc;
       } else {
         int4 e;
+        const int wb = w.base + w.cnt;
         if (!entry_at(p, table, g, k, w, e, abort)) break;
+        if (ddur && w.base + w.cnt != wb) {  // a new window: its phases' durations
+          if (lane < w.cnt) sh.wdur[lane] = (float)__ldcg(&ddur[w.base + lane]);
+          __syncwarp();
+        }
         // hand the entry to the consumer (it never reads the global table itself)
         if (lane == 0) {
           while (k - sh.cons_k >= RING - 1 && !*abort) {
           }
           sh.ring[k & (RING - 1)] = e;
+          if (ddur) {
+            sh.ring_t[k & (RING - 1)] = (float)tcum;
+            tcum += sh.wdur[k - w.base];
+          }
           __threadfence_block();
           sh.known = k + 1;
         }
@@ -556,6 +589,8 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
     // run left to issue -- about the flag's round trip -- so the next sender's
     // first stores follow this run's last ones instead of waiting a hand-over
     const int EARLY = (p.mode & 128) ? g_early_rows : 0;  // mode bit 7
+    const float unit_ns = p.phase_dur ? p.unit_ns : 0.0f;
+    long long t0 = 0;  // deadline pacing: this CTA's clock origin (its first remote entry)
     auto pace = [&](int peer_) {
       if (sys) red_relaxed_sys_add(sh.ctr[peer_], 1);
       else red_relaxed_gpu_add(sh.ctr[peer_], 1);
@@ -576,6 +611,7 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
       } else {
         int4 e = make_int4(-1, 0, 0, 0);
         if (lane == 0) {
+          if (k == 0 && unit_ns > 0.0f) t0 = eng_ns();
           while (k >= sh.known && !sh.known_done && !*abort) {
           }
           sh.cons_k = k;
@@ -601,9 +637,19 @@ __global__ void __launch_bounds__(TMA_THREADS) engine_tma_kernel(EngineParams p,
         peer = e.x, first = e.y, ntok = e.z;
         if (!cont) {  // run start: every earlier run into `peer` must have landed
           prev_peer = peer;
-          if (paced && lane == 0 && !wait_ge(sh.ctr[peer], e.w, p.spin_limit, sys)) {
-            atomicExch(p.status, AURORA_ETIMEOUT);
-            *abort = 1;
+          if (paced && lane == 0) {
+            bool ok;
+            if (unit_ns > 0.0f) {  // ... or the schedule's clock has reached this phase
+              if (!t0) t0 = eng_ns();
+              const long long due = t0 + (long long)(sh.ring_t[k & (RING - 1)] * unit_ns);
+              ok = wait_ge_or_until(sh.ctr[peer], e.w, due, p.spin_limit, sys);
+            } else {
+              ok = wait_ge(sh.ctr[peer], e.w, p.spin_limit, sys);
+            }
+            if (!ok) {
+              atomicExch(p.status, AURORA_ETIMEOUT);
+              *abort = 1;
+            }
           }
           __syncwarp();
           if (*abort) break;
@@ -818,7 +864,7 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
                              void* const* dst2_bufs, int row2_bytes, int32_t* const* ctrs,
                              int ctas_per_rank, int max_phases, int64_t spin_limit,
                              int32_t* status, int split, const double* bw, void* const* ginfo_bufs,
-                             int32_t* const* landed, void* stream) {
+                             int32_t* const* landed, const double* phase_dur, float unit_ns, void* stream) {
   if (split < 0 || split > 2) return AURORA_EINVAL;
   if (mode < 0 || mode > 511 || (mode & 12) == 12 || n < 1 || n > AUR_MAXN || n_local < 1 ||
       ((mode & 256) && ((mode & 65) || !src2_bufs || !dst2_bufs || row2_bytes < 8)) ||
@@ -866,6 +912,9 @@ extern "C" int aurora_engine(int mode, int n, int n_local, int rank_base, const 
   p.spin_limit = spin_limit;
   p.status = status;
   p.landed = landed;
+  if (unit_ns < 0.0f || !(unit_ns == unit_ns)) return AURORA_EINVAL;
+  p.phase_dur = unit_ns > 0.0f ? phase_dur : nullptr;
+  p.unit_ns = unit_ns;
   if (landed && (!lsu || (mode & 1))) return AURORA_EINVAL;  // arrival credits: LSU dispatch only
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(n_local * ctas_per_rank);

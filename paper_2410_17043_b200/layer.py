@@ -249,6 +249,10 @@ class AuroraMoELayer:
         self.engine_lsu = 64 if os.environ.get("AURORA_ENGINE", "tma") == "lsu" else 0
         # TMA engine: release a receiver when a run has ~a flag round trip of rows left (mode bit 7)
         self.early_pace = 128 if os.environ.get("AURORA_EARLY_PACE", "1") != "0" else 0
+        # deadline pacing: a run also starts when the schedule's clock (phase durations at this
+        # link rate, GB/s per pair) reaches its phase, so a late hand-over flag no longer delays
+        # the chain; 0 = flags only (AURORA_DEADLINE_GBPS)
+        self.deadline_gbps = float(os.environ.get("AURORA_DEADLINE_GBPS", "0"))
         # how a process's copy CTAs are split among the ranks it drives (csrc/apportion.cuh):
         # by bandwidth when the cluster is heterogeneous (C4: a rank's copy rate follows its
         # bandwidth), else by volume (one rank per GPU: identity; loopback: the hot rank gets the
@@ -531,7 +535,9 @@ class AuroraMoELayer:
             self.meta_bytes if plane2 else 0,
             ctr.data_ptr(), C, self.P, self.spin_limit, self.engine_status.data_ptr(), self.split,
             None if self.bw is None else self.bw.data_ptr(), None,
-            self.t_landed.data_ptr() if landed else None, stream),
+            self.t_landed.data_ptr() if landed else None,
+            self.phase_dur.data_ptr() if self.deadline_gbps > 0 else None,
+            cfg.hidden * 2 / self.deadline_gbps if self.deadline_gbps > 0 else 0.0, stream),
             "aurora_engine")
 
     def dispatch(self, stream: int, part: str = "all", overlap_schedule: bool = False) -> None:
@@ -938,6 +944,9 @@ class AuroraMoELayer:
         self.rchunks[:P].copy_(torch.from_numpy(rch))
         self.n_in.copy_(torch.from_numpy(n_in))
         self.n_out.copy_(torch.from_numpy(n_out))
+        if P:  # deadline pacing reads the phase durations
+            self.phase_dur[:len(sched.phases)].copy_(torch.tensor([ph.duration for ph in sched.phases],
+                                                                  dtype=torch.float64))
         self.sched_i[0] = len(sched.phases)
         self.progress.fill_(len(sched.phases) | PROGRESS_DONE)
 

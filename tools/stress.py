@@ -1,7 +1,7 @@
 """Randomised stress of the layer's execution variants (race hunting): random small
 configs, each run through every variant that must give identical bits -- default,
 engine combine, serial K2, unpaced, LSU engine, N1 (arrival-driven GEMM1), emulated
-compute partition -- repeated, with the counters checked re-armed after each config.
+compute partition, deadline pacing -- repeated, with the counters checked re-armed after each config.
 
     python tools/stress.py [iterations] [seed]
 """
@@ -27,6 +27,7 @@ def variants(layer):
         yield "no_packed_scatter", {"packed_scatter": False}
         yield "ungrouped", {"grouped_dispatch": False}
     yield "lsu", {"engine_lsu": 64}
+    yield "deadline", {"deadline_gbps": 700.0}
 
 
 def main(iters=60, seed=0):
