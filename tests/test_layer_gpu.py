@@ -702,7 +702,8 @@ def test_random_configs_all_variants_identical(torch):
     """Race hunt (tools/stress.py): random small configs (2-16 ranks, 1-4 experts per
     rank, top-1..6, skews 0-3, emulated compute on some), each through every variant
     that must give the same bits -- default, engine combine, serial K2, unpaced, N1,
-    LSU engine, ungrouped / unscattered E > n paths -- twice, counters re-armed."""
+    LSU engine, ungrouped / unscattered E > n paths, deadline pacing -- twice, counters
+    re-armed."""
     import importlib.util
     import os
     spec = importlib.util.spec_from_file_location(
@@ -710,3 +711,42 @@ def test_random_configs_all_variants_identical(torch):
     m = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(m)
     m.main(40, 7)
+
+
+def test_deadline_pacing_same_rows(torch):
+    """Deadline pacing (a run may start at its phase's scheduled time as well as on its
+    hand-over flag) changes when rows move, never which: the dispatch and the engine
+    combine give the default's bits at a realistic rate, at a rate so high that every
+    deadline has passed (the engine in phase order, unpaced in effect) and on host-loaded
+    baseline tables (load_schedule fills the phase durations)."""
+    import paper_2410_17043_b200 as A
+    from paper_2410_17043_b200 import baselines as B
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=1024, ffn=256, experts=8, top_k=2, tokens=4096, ranks=8, skew=1.5, seed=21)
+    layer = AuroraMoELayer(cfg)
+    x = torch.randn(cfg.tokens, cfg.hidden, device="cuda").to(torch.bfloat16)
+    ref = layer(x).clone()
+    for fused in (True, False):
+        layer.fused_combine = fused
+        for gbps in (700.0, 1e9):
+            layer.deadline_gbps = gbps
+            for _ in range(2):
+                out = layer(x)
+                torch.cuda.synchronize()
+                layer.check_status()
+                assert torch.equal(out, ref), (fused, gbps)
+    d = layer.counts.cpu().numpy().astype(float)
+    np.fill_diagonal(d, 0)
+    sched = B.schedule_rcs(A.TrafficMatrix(d), A.ClusterSpec.uniform(8), 3)
+    layer.deadline_gbps = 700.0
+    s = torch.cuda.current_stream().cuda_stream
+    layer.route(x, s)
+    layer.pack(s)
+    layer.load_schedule(sched)
+    layer.dispatch(s)
+    layer.experts(s)
+    layer.combine(s)
+    layer.aggregate(s)
+    torch.cuda.synchronize()
+    layer.check_status()
+    assert torch.equal(layer.out, ref)
