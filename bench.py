@@ -612,7 +612,7 @@ def run_c3(args):
     # three times so both see the same power state; the headline uses the layer's default
     il_default = pair.interleave
     il_runs = {"interleaved": [], "serial": []}
-    for _ in range(3):
+    for _ in range(3 if not hetero else 0):
         for name, il in (("interleaved", True), ("serial", False)):
             pair.interleave = il
             pair(xa, xb)
@@ -624,10 +624,11 @@ def run_c3(args):
             torch.cuda.synchronize()
             pair.check_status()
             il_runs[name].append(f0.elapsed_time(f1) / args.steps)
-    pair.interleave = True
-    il_timeline = pair.timeline(xa, xb)
-    pair.interleave = il_default
-    il_med = {k: sorted(v)[1] for k, v in il_runs.items()}
+    if not hetero:
+        pair.interleave = True
+        il_timeline = pair.timeline(xa, xb)
+        pair.interleave = il_default
+        il_med = {k: sorted(v)[1] for k, v in il_runs.items()}
     # end to end: both inputs in from pinned host memory, both outputs back, every step
     # pipelined like the C2 line: copy-engine streams move the next step's inputs in and the
     # previous step's outputs out under the layers, double-buffered device inputs / outputs
@@ -694,13 +695,17 @@ def run_c3(args):
                     "pipeline": "H2D of step i+1's inputs and D2H of step i-1's outputs under step i "
                                 "(copy-engine streams, double-buffered device inputs / outputs)"},
             "clocks": clocks.summary(0),
-            "interleave": {"default_on": il_default, "switch": "AURORA_C3_INTERLEAVE=0 for the serial order",
-                           "interleaved_ms_per_step": il_med["interleaved"], "serial_ms_per_step": il_med["serial"],
-                           "speedup": il_med["serial"] / il_med["interleaved"], "runs": il_runs,
-                           "timeline_ms": il_timeline,
-                           "what": "Table 1 (PAPER.md:473-497) on one GPU: model b on a second stream, its gate "
-                                   "beside model a's gate / dispatch, its dispatch right after model a's, its FFN "
-                                   "behind model a's FFN, model a's aggregation beside it; combines fused"},
+            "interleave": ({"default_on": il_default, "switch": "AURORA_C3_INTERLEAVE=0 for the serial order",
+                            "interleaved_ms_per_step": il_med["interleaved"], "serial_ms_per_step": il_med["serial"],
+                            "speedup": il_med["serial"] / il_med["interleaved"], "runs": il_runs,
+                            "timeline_ms": il_timeline,
+                            "what": "Table 1 (PAPER.md:473-497) on one GPU: model b on a second stream, its gate "
+                                    "and K2 beside model a's gate / dispatch, its dispatch right after model a's, "
+                                    "its FFN behind model a's FFN, model a's aggregation beside it; combines fused"}
+                           if not hetero else
+                           {"default_on": False, "note": "off under the per-rank compute emulation: the two models' "
+                                                         "FFNs would overlap on different SMs, giving every emulated "
+                                                         "GPU twice its CTA pairs"}),
             "timeline_ms": {"a": pair.a.timeline(xa), "b": pair.b.timeline(xb)}}
     if hetero:
         # the same two models on the same emulated cluster, pairs placed by the homogeneous plan

@@ -118,8 +118,13 @@ class ColocatedLayers:
         self.cplan = cplan
         self.a = AuroraMoELayer(cfg_a, DeploymentPlan(cplan.gpu_of_a), **kw)
         self.b = AuroraMoELayer(cfg_b, None, gpu_of_expert=cplan.gpu_of_b, **kw)
+        emulated = self.a.gemm_part is not None or self.b.gemm_part is not None
         if interleave is None:
-            interleave = os.environ.get("AURORA_C3_INTERLEAVE", "1") != "0"
+            # not under the per-rank compute emulation (compute_scales): the two models' FFNs
+            # would overlap on different SMs, handing every emulated GPU twice its CTA pairs
+            interleave = os.environ.get("AURORA_C3_INTERLEAVE", "1") != "0" and not emulated
+        elif interleave and emulated:
+            raise ValueError("interleaving would break the per-rank compute emulation (compute_scales)")
         self.interleave = interleave
         self.side = torch.cuda.Stream(device=self.a.dev)
         self._ev = {k: torch.cuda.Event() for k in ("start", "n_a", "n_b", "b_done")}
