@@ -18,6 +18,7 @@
 // table (per phase, per sender: receiver, first token, token count, position
 // in the receiver's arrival order) plus the send/receive buffer layout, so
 // the MoE layer never synchronises with the host between router and engine.
+#include <type_traits>
 #include "common.cuh"
 
 namespace {
@@ -204,6 +205,7 @@ __device__ bool perfect_matching(MatchState& s, int n) {
 
 #include "fastmatch.cuh"
 #include "fastmatch8b.cuh"
+#include "fastmatch8d.cuh"
 #include "fastmatch16.cuh"
 #include "apportion.cuh"
 
@@ -239,11 +241,18 @@ struct Dom<int> {
 
 template <int NB, typename V>
 __device__ __forceinline__ V row_pick(const V (&a)[NB], int j) {
-  V r = a[0];
+  if constexpr (NB == 8) {  // select tree: depth 3 instead of a chain of 7
+    const V a01 = (j & 1) ? a[1] : a[0], a23 = (j & 1) ? a[3] : a[2];
+    const V a45 = (j & 1) ? a[5] : a[4], a67 = (j & 1) ? a[7] : a[6];
+    const V a03 = (j & 2) ? a23 : a01, a47 = (j & 2) ? a67 : a45;
+    return (j & 4) ? a47 : a03;
+  } else {
+    V r = a[0];
 #pragma unroll
-  for (int q = 1; q < NB; q++)
-    if (q == j) r = a[q];
-  return r;
+    for (int q = 1; q < NB; q++)
+      if (q == j) r = a[q];
+    return r;
+  }
 }
 template <int NB, typename V>
 __device__ __forceinline__ void row_put(V (&a)[NB], int j, V v) {
@@ -633,6 +642,92 @@ __device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V>
   }
 }
 
+// Integer domain, n <= 8 (the in-layer path): the same decomposition with
+// incremental state. Every entry stays >= 0 and real <= remaining holds
+// throughout (both drop by the phase duration on the matched cells, real is
+// clipped at 0), so the snap and np.minimum of commsched.py:254-255 are
+// no-ops and support / preferred change only on the n matched cells: they
+// live as bytes of two 64-bit words (byte i = row i) on every lane and lose
+// the bits of the cells a phase drains. The matching runs on every lane with
+// identical, warp-uniform inputs -- no divergence and no broadcast of its
+// result; lane i keeps row i of remaining / real in registers.
+// (Measured alternative, slower: the cells in shared memory and the whole step
+// warp-uniform, 80 vs 74 us per launch at C2.)
+__device__ int g_sched_generic = 0;  // diagnostics: 1 = the generic per-step masks (aurora_debug_set_schedule_variant)
+
+__device__ void decompose_warp_i8(const SchedParams& p, Row<8, int> rem0, Row<8, int> real0, RawRing<8>& ring,
+                                  uint64_t* ready) {
+  const int lane = threadIdx.x & 31, n = p.n;
+  const bool on = lane < n;
+  const int R_MAX = n * n - 2 * n + 2;
+  int rem[8], real[8];
+  uint32_t sup = 0, pref = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    rem[j] = rem0.v[j];
+    real[j] = real0.v[j];
+    if (rem[j] > 0) sup |= 1u << j;
+    if (real[j] > 0) pref |= 1u << j;
+  }
+  const uint32_t sh = 8u * (lane & 3);
+  const uint32_t p0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? pref << sh : 0u);
+  const uint32_t p1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? pref << sh : 0u);
+  const uint32_t s0 = __reduce_or_sync(0xffffffffu, (on && lane < 4) ? sup << sh : 0u);
+  const uint32_t s1 = __reduce_or_sync(0xffffffffu, (on && lane >= 4) ? sup << sh : 0u);
+  uint64_t P = ((uint64_t)p1 << 32) | p0, S = ((uint64_t)s1 << 32) | s0;
+  int nr = 0, status = AURORA_OK;
+  long long cy[3] = {0, 0, 0};
+  while (S != 0) {  // remaining.any()
+    if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
+    const long long t1 = clock64();
+    FastMatch8d f;
+    f.P = P;
+    f.S = S;
+    if (!f.run(n)) { status = AURORA_ENOMATCH; break; }
+    const long long t2 = clock64();
+    const int pj = on ? (int)f.ml((uint32_t)lane, n) : 0;
+    const int v = on ? row_pick<8, int>(rem, pj) : 0x7fffffff;
+    const int dur = (int)__reduce_min_sync(0xffffffffu, (unsigned)v);
+    bool zr = false, zp = false;
+    if (on) {
+      const int r = v - dur;
+      row_put<8, int>(rem, pj, r);
+      int q = row_pick<8, int>(real, pj) - dur;
+      q = q < 0 ? 0 : q;
+      row_put<8, int>(real, pj, q);
+      zr = r == 0;
+      zp = q == 0;
+      ring.perm[nr * 8 + lane] = (signed char)pj;
+      if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
+    }
+    // drained cells leave support / preferred: lane i's bit pj of byte i
+    const uint32_t bit = (1u << pj) << (8u * (lane & 3)), lo = on && lane < 4, hi = on && lane >= 4;
+    const uint32_t crl = __reduce_or_sync(0xffffffffu, zr && lo ? bit : 0u);
+    const uint32_t crh = __reduce_or_sync(0xffffffffu, zr && hi ? bit : 0u);
+    const uint32_t cpl = __reduce_or_sync(0xffffffffu, zp && lo ? bit : 0u);
+    const uint32_t cph = __reduce_or_sync(0xffffffffu, zp && hi ? bit : 0u);
+    S &= ~(((uint64_t)crh << 32) | crl);
+    P &= ~(((uint64_t)cph << 32) | cpl);
+    if (lane == 0) {
+      ring.dur[nr] = (double)dur;
+      if (p.raw_dur) p.raw_dur[nr] = (double)dur;
+    }
+    __syncwarp();
+    if (lane == 0) ring_arrive(&ready[nr]);
+    nr++;
+    const long long t3 = clock64();
+    cy[1] += t2 - t1;
+    cy[2] += t3 - t2;
+  }
+  if (lane == 0) {
+    if (p.n_raw) *p.n_raw = nr;
+    if (p.prof)
+      for (int q = 0; q < 3; q++) p.prof[q] = cy[q];
+    ring.dur[nr] = -1.0 - (double)status;  // end of stream, through slot nr's barrier like a phase
+    ring_arrive(&ready[nr]);
+  }
+}
+
 template <int NB, typename V>
 __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom<V> dom, RawRing<NB>& ring,
                            uint64_t* ready,
@@ -757,7 +852,12 @@ __device__ void schedule_two_warps(const SchedParams& p, const double* R, const 
         q0.v[j] = (lane < n && j < n) ? (V)Q[lane * ld + j] : (V)0;
       }
     }
-    decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
+    if constexpr (NB == 8 && std::is_same<V, int>::value) {
+      if (!g_sched_generic) decompose_warp_i8(p, r0, q0, ring, ready);
+      else decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
+    } else {
+      decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
+    }
   } else {
     strip_warp<NB, V>(p, Tt, ld, dom, ring, ready, cc, bw_i, stream, np_, status);
   }
@@ -1072,6 +1172,10 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
 // prof[8] (NULL switches it off).
 extern "C" int aurora_debug_set_schedule_trace(long long* trace) {
   return cudaMemcpyToSymbol(g_sched_trace, &trace, sizeof(trace)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
+}
+
+extern "C" int aurora_debug_set_schedule_variant(int generic) {
+  return cudaMemcpyToSymbol(g_sched_generic, &generic, sizeof(int)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }
 
 extern "C" int aurora_debug_set_schedule_profile(long long* prof) {

@@ -6,6 +6,7 @@
 
 #include "../../paper_2410_17043_b200/csrc/fastmatch.cuh"
 #include "../../paper_2410_17043_b200/csrc/fastmatch8b.cuh"
+#include "../../paper_2410_17043_b200/csrc/fastmatch8d.cuh"
 #include "../../paper_2410_17043_b200/csrc/fastmatch16.cuh"
 
 extern "C" int oracle_perfect_matching_masks(int n, const uint32_t* sup, const uint32_t* pref, int* perm);
@@ -87,6 +88,19 @@ static int check8(std::mt19937& rng, int iters) {
     if (sameb && okb)
       for (int u = 0; u < n; u++) sameb &= (int)((fb.ML >> (8 * u)) & 15) == ref[u];
     if (!sameb && bad++ < 5) std::printf("mismatch FastMatch8b n=%d ok=%d/%d\n", n, (int)okb, ok_ref);
+    // the K2 in-layer matcher (no candidate stacks)
+    FastMatch8d fd;
+    fd.P = fb.P;
+    fd.S = 0;
+    for (int u = 0; u < n; u++) fd.S |= (uint64_t)sup[u] << (8 * u);
+    const bool okd = fd.run(n);
+    bool samed = okd == (bool)ok_ref;
+    if (samed && okd)
+      for (int u = 0; u < n; u++) {
+        samed &= (int)fd.ml((uint32_t)u, n) == ref[u];
+        if (!fd.kuhned) samed &= (int)((fd.MLB >> (8 * u)) & 0xFF) == (1 << ref[u]);
+      }
+    if (!samed && bad++ < 5) std::printf("mismatch FastMatch8d n=%d ok=%d/%d\n", n, (int)okd, ok_ref);
   }
   return bad;
 }
@@ -128,7 +142,7 @@ static int check16(std::mt19937& rng, int iters) {
 
 int main() {
   std::mt19937 rng(12345);
-  int bad = check<8>(rng, 200000) + check<16>(rng, 100000) + check8(rng, 300000) + check16(rng, 300000);
+  int bad = check<8>(rng, 200000) + check<16>(rng, 100000) + check8(rng, 600000) + check16(rng, 300000);
   std::printf("fastmatch mismatches: %d\n", bad);
   return bad != 0;
 }

@@ -1,4 +1,4 @@
-"""The K2 fast-path matchers (csrc/fastmatch.cuh, fastmatch8b.cuh, fastmatch16.cuh; host+device) are bit-exact with
+"""The K2 fast-path matchers (csrc/fastmatch.cuh, fastmatch8b.cuh, fastmatch8d.cuh, fastmatch16.cuh; host+device) are bit-exact with
 the oracle's perfect_matching / hopcroft_karp restatement (matching.py:20-112)
 on 300k random bitmask graphs -- checked on the host, no GPU needed."""
 import os
