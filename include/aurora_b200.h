@@ -443,6 +443,10 @@ int aurora_debug_schedule_cycles(const double* d, int n, long long* prof, int32_
  * cycles to the device array prof[8] = {snap+masks, matching, update, strip,
  * decompose, prologue, whole kernel, chunk pass}; NULL turns it off. */
 int aurora_debug_set_schedule_profile(long long* prof);
+/* Diagnostics: the in-layer K2 path (int32 counts, uniform cluster, n <= 8)
+ * decomposes with FastMatch8d and incremental support / preferred words (0,
+ * the default) or with FastMatch8b and per-step masks (1). Same results. */
+int aurora_debug_set_schedule_variant(int generic);
 /* Diagnostics timelines (%globaltimer ns; NULL switches off): K2 records the
  * time each phase is published at trace[count & 511]; the TMA engine records
  * per copy CTA {start, local rows done, end, -} at trace[4 * cta]. */

@@ -59,6 +59,7 @@ _SIGNATURES = {
                                      _vp, _vp, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int, _vp],
     "aurora_debug_schedule_cycles": [_vp, _c_int, _vp, _vp, _vp, _vp],
     "aurora_debug_set_schedule_profile": [_vp],
+    "aurora_debug_set_schedule_variant": [_c_int],
     "aurora_debug_set_schedule_trace": [_vp],
     "aurora_debug_set_engine_trace": [_vp],
     "aurora_debug_set_gemm_trace": [_vp],

@@ -227,3 +227,52 @@ def test_heterogeneous_chunk_rounding_fuzz(A):
                     tot[i, j] += cnt
         assert np.array_equal(tot, d), it
     assert fails == 0, f"{fails} of 1500 heterogeneous schedules needed a chunk fix-up (EINVAL)"
+
+
+def test_int8_decomposition_variants_vs_oracle(A):
+    """The in-layer n <= 8 integer decomposition (FastMatch8d, incremental
+    support / preferred words) and the per-step-mask path (FastMatch8b,
+    aurora_debug_set_schedule_variant(1)) give the oracle's schedule on 600
+    MoE-like / sparse-with-ties / wide-range count matrices."""
+    import torch
+    from oracle.oracle import build_schedule_oracle
+    from paper_2410_17043_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(4242)
+    dev = torch.device("cuda")
+    i32 = dict(dtype=torch.int32, device=dev)
+    try:
+        for it in range(600):
+            n = int(rng.integers(1, 9))
+            kind = it % 3
+            if kind == 2:
+                c = rng.integers(0, 1 << 24, (n, n)) * (rng.random((n, n)) < 0.7)
+            else:
+                c = _fuzz_matrix(rng, n, kind)
+            c = c.astype(np.int32)
+            d = c.astype(float)
+            np.fill_diagonal(d, 0)
+            o = build_schedule_oracle(d)["phases"]
+            counts = torch.tensor(c, **i32)
+            P = L.aurora_phase_cap(n)
+            for variant in (0, 1):
+                assert L.aurora_debug_set_schedule_variant(variant) == 0
+                pr = torch.empty(P, n, **i32)
+                pd = torch.empty(P, dtype=torch.float64, device=dev)
+                si = torch.zeros(2, **i32)
+                ch = torch.empty(P, n, 4, **i32)
+                rch = torch.empty(P, n, 4, **i32)
+                nin = torch.empty(n, **i32)
+                nout = torch.empty(n, **i32)
+                assert L.aurora_schedule_counts(counts.data_ptr(), None, n, pr.data_ptr(), pd.data_ptr(),
+                                                si.data_ptr(), ch.data_ptr(), rch.data_ptr(), nin.data_ptr(),
+                                                nout.data_ptr(), si[1:].data_ptr(), None, 0, 0, 0, 0,
+                                                _lib.stream_ptr()) == 0
+                torch.cuda.synchronize()
+                nph, status = si.tolist()
+                assert status == 0
+                got = [(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(t))
+                       for row, t in zip(pr[:nph].tolist(), pd[:nph].tolist())]
+                assert got == o, (it, n, variant)
+    finally:
+        L.aurora_debug_set_schedule_variant(0)
