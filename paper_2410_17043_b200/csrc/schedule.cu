@@ -422,6 +422,17 @@ __device__ __forceinline__ bool ring_test(uint64_t* bar) {
   return ok != 0;
 }
 
+// blocking wait: the warp sleeps in the barrier unit instead of polling (a polling warp's
+// test_wait traffic shares the MIO pipe with warp 0's shuffles and reductions)
+__device__ __forceinline__ void ring_wait(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], 0;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
 template <int NB>
 struct RawRing {
   static constexpr int R = NB * NB - 2 * NB + 2;
@@ -776,9 +787,7 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   };
   for (;;) {
     if (r >= avail) {  // wait for warp 0: raw phase r, or the end of the stream, in slot r
-      if (lane == 0)
-        while (!ring_test(&ready[r])) {
-        }
+      if (lane == 0) ring_wait(&ready[r]);
       __syncwarp();  // lane 0's acquire orders the slot's contents for the whole warp
       const double dr = ring.dur[r];
       if (dr < 0.0) {
@@ -1034,6 +1043,7 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
 
   if constexpr (TWO) {
     ChunkCtx cc{cd_s, cc_s, cum_s, tok_s, lastc_s, rcnt_s, rtmp_s, want_s, p.bw ? bw_s : nullptr, MAXN, MAXN};
+    // (measured: doing this during warp 0's prologue instead is 2 us slower per launch)
     if (warp == 1 && p.chunks) {
       split_ctas();
       chunk_init(cc, n, lane);

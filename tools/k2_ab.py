@@ -10,6 +10,7 @@ from paper_2410_17043_b200 import _lib
 from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
 
 L = _lib.load()
+VARIANTS = tuple(int(v) for v in os.environ.get("K2_VARIANTS", "1,0,1,0").split(","))
 names = ["w0:snap+mask", "w0:match", "w0:update+publish", "w1:strip busy", "w1:close/publish", "prologue", "kernel", "w1:total"]
 for skew in (0.0, 1.0, 2.0):
     cfg = MoEConfig(hidden=256, ffn=256, experts=8, top_k=2, tokens=16384, ranks=8, skew=skew, seed=0)
@@ -19,7 +20,7 @@ for skew in (0.0, 1.0, 2.0):
     torch.cuda.synchronize()
     s = _lib.stream_ptr()
     res = {}
-    for var in (1, 0, 1, 0):
+    for var in VARIANTS:
         L.aurora_debug_set_schedule_variant(var)
         prof = torch.zeros(8, dtype=torch.int64, device="cuda")
         L.aurora_debug_set_schedule_profile(prof.data_ptr())
@@ -42,6 +43,6 @@ for skew in (0.0, 1.0, 2.0):
         pv[4] = f"{pv[4] >> 32}/{pv[4] & 0xffffffff}"
         print(f"skew {skew} variant {var}: {res[var][1]:.1f} us/launch, {len(key)} phases;",
               " ".join(f"{k}={v}" for k, v in zip(names, pv)), flush=True)
-    assert res[0][0] == res[1][0], "variants disagree"
+    assert all(res[v][0] == res[VARIANTS[0]][0] for v in res), "variants disagree"
     L.aurora_debug_set_schedule_variant(0)
 print("identical phases across variants")
