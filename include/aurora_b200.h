@@ -443,9 +443,12 @@ int aurora_debug_schedule_cycles(const double* d, int n, long long* prof, int32_
  * cycles to the device array prof[8] = {snap+masks, matching, update, strip,
  * decompose, prologue, whole kernel, chunk pass}; NULL turns it off. */
 int aurora_debug_set_schedule_profile(long long* prof);
-/* Diagnostics: the in-layer K2 path (int32 counts, uniform cluster, n <= 8)
- * decomposes with FastMatch8d and incremental support / preferred words (0,
- * the default) or with FastMatch8b and per-step masks (1). Same results. */
+/* Diagnostics: the in-layer K2 path (int32 counts, uniform cluster, n <= 8):
+ * 0 (default) cell-lane decomposition and strip (FastMatch8d, two cells of
+ * the matrix per lane, support / preferred / active sets as ballots); 1
+ * FastMatch8b with per-step masks; 2 cell-lane decomposition with the
+ * row-lane strip; 3 row-lane incremental decomposition (lane i = row i) with
+ * the row-lane strip. Same results. */
 int aurora_debug_set_schedule_variant(int generic);
 /* Diagnostics timelines (%globaltimer ns; NULL switches off): K2 records the
  * time each phase is published at trace[count & 511]; the TMA engine records

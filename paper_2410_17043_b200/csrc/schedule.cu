@@ -439,6 +439,7 @@ struct RawRing {
   // dur[r] < 0 ends the stream: warp 0 finished after r raw phases with status -1 - dur[r].
   // Every hand-off, the final one included, goes through the mbarrier of its slot.
   double dur[R + 1];
+  unsigned long long mask[R];  // cell-lane path: bit 8i + j set iff sender i is matched to j
   signed char perm[R * NB];
 };
 
@@ -664,7 +665,10 @@ __device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V>
 // result; lane i keeps row i of remaining / real in registers.
 // (Measured alternative, slower: the cells in shared memory and the whole step
 // warp-uniform, 80 vs 74 us per launch at C2.)
-__device__ int g_sched_generic = 0;  // diagnostics: 1 = the generic per-step masks (aurora_debug_set_schedule_variant)
+// K2 variant (aurora_debug_set_schedule_variant): 0 = default, 1 = the generic per-step
+// masks, 2 = cell-lane decomposition (below) with the row-lane strip, 3 = row-lane
+// decomposition (decompose_warp_i8) -- 0 is the cell-lane decomposition and strip.
+__device__ int g_sched_generic = 0;
 
 __device__ void decompose_warp_i8(const SchedParams& p, Row<8, int> rem0, Row<8, int> real0, RawRing<8>& ring,
                                   uint64_t* ready) {
@@ -720,6 +724,81 @@ __device__ void decompose_warp_i8(const SchedParams& p, Row<8, int> rem0, Row<8,
     S &= ~(((uint64_t)crh << 32) | crl);
     P &= ~(((uint64_t)cph << 32) | cpl);
     if (lane == 0) {
+      ring.dur[nr] = (double)dur;
+      if (p.raw_dur) p.raw_dur[nr] = (double)dur;
+    }
+    __syncwarp();
+    if (lane == 0) ring_arrive(&ready[nr]);
+    nr++;
+    const long long t3 = clock64();
+    cy[1] += t2 - t1;
+    cy[2] += t3 - t2;
+  }
+  if (lane == 0) {
+    if (p.n_raw) *p.n_raw = nr;
+    if (p.prof)
+      for (int q = 0; q < 3; q++) p.prof[q] = cy[q];
+    ring.dur[nr] = -1.0 - (double)status;  // end of stream, through slot nr's barrier like a phase
+    ring_arrive(&ready[nr]);
+  }
+}
+
+
+// Cell-lane layout (n <= 8, integer domain; the in-layer path): lane l holds the
+// cells (l >> 3, l & 7) and (4 + (l >> 3), l & 7) of a matrix, so the bit of a
+// cell in a 64-bit support word (byte i = row i) is the lane's own index in the
+// lo / hi ballot. A decomposition step then needs no per-lane column select:
+// the matched cells come from one byte permute of the matching's right->left
+// table, the phase duration is one min reduction, and support / preferred are
+// re-read by four ballots (commsched.py:249-278; a cell leaves the support
+// exactly when it reaches 0, since every entry stays >= 0 and real <= remaining).
+__device__ __forceinline__ uint64_t ballot64(bool a, bool b) {
+  return ((uint64_t)__ballot_sync(0xffffffffu, b) << 32) | __ballot_sync(0xffffffffu, a);
+}
+
+__device__ void decompose_warp_cells(const SchedParams& p, Row<8, int> rem0, Row<8, int> real0,
+                                     RawRing<8>& ring, uint64_t* ready) {
+  const int lane = threadIdx.x & 31, n = p.n;
+  const int R_MAX = n * n - 2 * n + 2;
+  const int j = lane & 7, ia = lane >> 3;  // cells (ia, j) and (ia + 4, j)
+  int ra = 0, rb = 0, qa = 0, qb = 0;
+#pragma unroll
+  for (int c = 0; c < 8; c++) {  // rows (lane i = row i) -> cells
+    const int x0 = __shfl_sync(0xffffffffu, rem0.v[c], ia), x1 = __shfl_sync(0xffffffffu, rem0.v[c], ia + 4);
+    const int y0 = __shfl_sync(0xffffffffu, real0.v[c], ia), y1 = __shfl_sync(0xffffffffu, real0.v[c], ia + 4);
+    if (c == j) { ra = x0; rb = x1; qa = y0; qb = y1; }
+  }
+  const bool jv = j < n;
+  if (!jv || ia >= n) ra = qa = 0;
+  if (!jv || ia + 4 >= n) rb = qb = 0;
+  uint64_t S = ballot64(ra > 0, rb > 0), P = ballot64(qa > 0, qb > 0);
+  const bool keep_perm = p.raw_perm != nullptr || g_sched_generic == 2;  // row-lane strip reads ring.perm
+  int nr = 0, status = AURORA_OK;
+  long long cy[3] = {0, 0, 0};
+  while (S != 0) {  // remaining.any()
+    if (nr >= R_MAX) { status = AURORA_EOVERFLOW; break; }
+    const long long t1 = clock64();
+    FastMatch8d f;
+    f.P = P;
+    f.S = S;
+    if (!f.run(n)) { status = AURORA_ENOMATCH; break; }
+    const long long t2 = clock64();
+    const uint32_t owner = FastMatch8d::perm(f.MR, (uint32_t)j) & 0xFFu;  // left vertex matched to column j
+    const bool ma = jv && owner == (uint32_t)ia, mb = jv && owner == (uint32_t)ia + 4u;
+    const int va = ma ? ra : 0x7fffffff, vb = mb ? rb : 0x7fffffff;
+    const int dur = (int)__reduce_min_sync(0xffffffffu, (unsigned)(va < vb ? va : vb));
+    if (ma) { ra -= dur; qa = qa > dur ? qa - dur : 0; }
+    if (mb) { rb -= dur; qb = qb > dur ? qb - dur : 0; }
+    S = ballot64(ra > 0, rb > 0);
+    P = ballot64(qa > 0, qb > 0);
+    const uint64_t M = ballot64(ma, mb);
+    if (keep_perm && lane < n) {
+      const int pj = (int)f.ml((uint32_t)lane, n);
+      ring.perm[nr * 8 + lane] = (signed char)pj;
+      if (p.raw_perm) p.raw_perm[nr * n + lane] = pj;
+    }
+    if (lane == 0) {
+      ring.mask[nr] = M;
       ring.dur[nr] = (double)dur;
       if (p.raw_dur) p.raw_dur[nr] = (double)dur;
     }
@@ -843,6 +922,103 @@ __device__ void strip_warp(const SchedParams& p, const double* t_in, int ld, Dom
   if (p.chunks && status == AURORA_OK && chunk_finish(p, cc, cl, lane) && stream) status = AURORA_EINVAL;
 }
 
+// strip + _coalesce (commsched.py:306-322) on the cell-lane layout: `lr` (the real
+// demand still undelivered) as two cells per lane, a raw phase as its matched-cell
+// mask. The active cells of a sub-phase are one pair of ballots; two phases are
+// _coalesce-identical exactly when their active-cell masks are equal (a cell is a
+// (sender, receiver) pair), so no per-lane receiver is needed until a phase closes.
+__device__ void strip_warp_cells(const SchedParams& p, RawRing<8>& ring, uint64_t* ready, const ChunkCtx& cc,
+                                 double bw_i, bool stream, int& np_out, int& status) {
+  const int lane = threadIdx.x & 31, n = p.n;
+  const bool on = lane < n;
+  const int P_MAX = 2 * n * n - 3 * n + 2;
+  const int j = lane & 7, ia = lane >> 3, ib = ia + 4;
+  int la = (j < n && ia < n && ia != j) ? p.d32[ia * n + j] : 0;  // t.entries, zero diagonal
+  int lb = (j < n && ib < n && ib != j) ? p.d32[ib * n + j] : 0;
+  ChunkLane cl;
+  int np_ = 0, r = 0, avail = 0, cur_dur = 0;
+  uint64_t lastA = 0;
+  bool closing_ok = true;
+  const long long t_begin = clock64();
+  long long busy = 0, c_chunk = 0, c_pub = 0;
+  int closed = 0, published = 0;
+  auto close_phase = [&]() {
+    const int k = np_ - 1;
+    const long long q0 = clock64();
+    const uint32_t row = on ? (uint32_t)(lastA >> (8 * lane)) & 0xFFu : 0u;
+    const int recv = row ? __ffs((int)row) - 1 : -1;
+    if (on) p.phase_recv[k * n + lane] = recv;
+    if (lane == 0) p.phase_dur[k] = (double)cur_dur;
+    if (p.chunks) chunk_step(p, cc, cl, k, on ? recv : -1, (double)cur_dur, bw_i, lane);
+    closed = k + 1;
+    c_chunk += clock64() - q0;
+  };
+  auto maybe_publish = [&](int next_r) {  // as strip_warp
+    if (!stream || closed == published) return;
+    int nxt = 0;
+    if (lane == 0) nxt = ring_test(&ready[next_r]) ? 1 : 0;
+    nxt = __shfl_sync(0xffffffffu, nxt, 0);
+    if (!nxt || closed - published >= 4) {
+      const long long q1 = clock64();
+      publish(p.progress, closed, lane);
+      published = closed;
+      c_pub += clock64() - q1;
+    }
+  };
+  for (;;) {
+    if (r >= avail) {
+      if (lane == 0) ring_wait(&ready[r]);
+      __syncwarp();
+      const double dr = ring.dur[r];
+      if (dr < 0.0) {
+        const int st = (int)(-1.0 - dr);
+        if (st != AURORA_OK) status = st;
+        break;
+      }
+      avail = r + 1;
+    }
+    const long long b0 = clock64();
+    const uint64_t M = ring.mask[r];
+    int left = (int)ring.dur[r];
+    r++;
+    const bool ma = (M >> lane) & 1u, mb = (M >> (lane + 32)) & 1u;
+    while (left > 0) {
+      const bool aa = ma && la > 0, ab = mb && lb > 0;
+      const uint64_t A = ballot64(aa, ab);
+      int step = left;  // idle Phase((), left) when nothing is active (commsched.py:312-316)
+      if (A != 0) {
+        const int va = aa ? la : 0x7fffffff, vb = ab ? lb : 0x7fffffff;
+        const int m = (int)__reduce_min_sync(0xffffffffu, (unsigned)(va < vb ? va : vb));
+        step = m < left ? m : left;
+      }
+      if (np_ > 0 && A == lastA) {
+        cur_dur += step;
+      } else {
+        if (np_ > 0) close_phase();
+        if (np_ >= P_MAX) { status = AURORA_EOVERFLOW; closing_ok = false; break; }
+        np_++;
+        cur_dur = step;
+        lastA = A;
+      }
+      if (A == 0) break;
+      if (aa) la -= step;
+      if (ab) lb -= step;
+      left -= step;
+    }
+    busy += clock64() - b0;
+    if (status != AURORA_OK) break;
+    maybe_publish(r);
+  }
+  if (status == AURORA_OK && np_ > 0 && closing_ok) close_phase();
+  if (p.prof && lane == 0) {
+    p.prof[3] = busy;
+    p.prof[4] = (c_chunk << 32) | (c_pub & 0xffffffffll);
+    p.prof[7] = clock64() - t_begin;
+  }
+  np_out = status == AURORA_OK ? np_ : 0;
+  if (p.chunks && status == AURORA_OK && chunk_finish(p, cc, cl, lane) && stream) status = AURORA_EINVAL;
+}
+
 template <int NB, typename V>
 __device__ void schedule_two_warps(const SchedParams& p, const double* R, const double* Q, const double* Tt,
                                    int ld, MatchState& ms, Dom<V> dom, RawRing<NB>& ring, uint64_t* ready,
@@ -862,12 +1038,20 @@ __device__ void schedule_two_warps(const SchedParams& p, const double* R, const 
       }
     }
     if constexpr (NB == 8 && std::is_same<V, int>::value) {
-      if (!g_sched_generic) decompose_warp_i8(p, r0, q0, ring, ready);
+      const int var = g_sched_generic;
+      if (var == 0 || var == 2) decompose_warp_cells(p, r0, q0, ring, ready);
+      else if (var == 3) decompose_warp_i8(p, r0, q0, ring, ready);
       else decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
     } else {
       decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
     }
   } else {
+    if constexpr (NB == 8 && std::is_same<V, int>::value) {
+      if (g_sched_generic == 0) {
+        strip_warp_cells(p, ring, ready, cc, bw_i, stream, np_, status);
+        return;
+      }
+    }
     strip_warp<NB, V>(p, Tt, ld, dom, ring, ready, cc, bw_i, stream, np_, status);
   }
 }

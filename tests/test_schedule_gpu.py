@@ -230,10 +230,12 @@ def test_heterogeneous_chunk_rounding_fuzz(A):
 
 
 def test_int8_decomposition_variants_vs_oracle(A):
-    """The in-layer n <= 8 integer decomposition (FastMatch8d, incremental
-    support / preferred words) and the per-step-mask path (FastMatch8b,
-    aurora_debug_set_schedule_variant(1)) give the oracle's schedule on 600
-    MoE-like / sparse-with-ties / wide-range count matrices."""
+    """Every K2 variant of the in-layer n <= 8 integer path gives the oracle's
+    schedule, and all give the same engine chunk tables, on 600 MoE-like /
+    sparse-with-ties / wide-range count matrices (aurora_debug_set_schedule_variant:
+    0 = cell-lane decomposition + cell-lane strip (default), 1 = per-step masks
+    with FastMatch8b, 2 = cell-lane decomposition + row-lane strip, 3 = row-lane
+    incremental decomposition + row-lane strip)."""
     import torch
     from oracle.oracle import build_schedule_oracle
     from paper_2410_17043_b200 import _lib
@@ -255,7 +257,8 @@ def test_int8_decomposition_variants_vs_oracle(A):
             o = build_schedule_oracle(d)["phases"]
             counts = torch.tensor(c, **i32)
             P = L.aurora_phase_cap(n)
-            for variant in (0, 1):
+            tables = None
+            for variant in (0, 1, 2, 3):
                 assert L.aurora_debug_set_schedule_variant(variant) == 0
                 pr = torch.empty(P, n, **i32)
                 pd = torch.empty(P, dtype=torch.float64, device=dev)
@@ -274,5 +277,9 @@ def test_int8_decomposition_variants_vs_oracle(A):
                 got = [(tuple((i, int(j)) for i, j in enumerate(row) if j >= 0), float(t))
                        for row, t in zip(pr[:nph].tolist(), pd[:nph].tolist())]
                 assert got == o, (it, n, variant)
+                t = [v[:nph].cpu() if v.dim() > 1 else v.cpu() for v in (ch, rch, nin, nout)]
+                if tables is None:
+                    tables = t
+                assert all(torch.equal(a, b) for a, b in zip(t, tables)), (it, n, variant)
     finally:
         L.aurora_debug_set_schedule_variant(0)

@@ -1,6 +1,7 @@
 """K2 in-layer A/B: launch time and section cycles of the scheduler variants
-(aurora_debug_set_schedule_variant: 0 = incremental n <= 8 integer path,
-1 = per-step masks), identical outputs checked. Layer shapes are small: K2
+(aurora_debug_set_schedule_variant: 0 = cell-lane decomposition + strip (default),
+1 = per-step masks, 2 = cell-lane decomposition + row-lane strip, 3 = row-lane
+incremental decomposition + strip), identical outputs checked. Layer shapes are small: K2
 only sees the traffic matrix, which depends on routing (tokens, ranks, skew)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,7 +11,7 @@ from paper_2410_17043_b200 import _lib
 from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
 
 L = _lib.load()
-VARIANTS = tuple(int(v) for v in os.environ.get("K2_VARIANTS", "1,0,1,0").split(","))
+VARIANTS = tuple(int(v) for v in os.environ.get("K2_VARIANTS", "3,0,3,0").split(","))
 names = ["w0:snap+mask", "w0:match", "w0:update+publish", "w1:strip busy", "w1:close/publish", "prologue", "kernel", "w1:total"]
 for skew in (0.0, 1.0, 2.0):
     cfg = MoEConfig(hidden=256, ffn=256, experts=8, top_k=2, tokens=16384, ranks=8, skew=skew, seed=0)

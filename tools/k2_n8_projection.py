@@ -27,7 +27,7 @@ for skew in (0.0, 1.0, 2.0):
     torch.cuda.synchronize()
     st = torch.zeros(512, dtype=torch.int64, device="cuda")
     case = {"skew": skew}
-    for variant in (1, 0):
+    for variant in (3, 0):
         L.aurora_debug_set_schedule_variant(variant)
         lags, k2s = [], []
         for it in range(4):
