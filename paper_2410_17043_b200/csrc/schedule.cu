@@ -669,6 +669,7 @@ __device__ void decompose_warp(const SchedParams& p, Row<NB, V> rem0, Row<NB, V>
 // masks, 2 = cell-lane decomposition (below) with the row-lane strip, 3 = row-lane
 // decomposition (decompose_warp_i8) -- 0 is the cell-lane decomposition and strip.
 __device__ int g_sched_generic = 0;
+int g_host_variant = 0;  // host mirror of g_sched_generic (variant 0 launches the compact I8 kernel)
 
 __device__ void decompose_warp_i8(const SchedParams& p, Row<8, int> rem0, Row<8, int> real0, RawRing<8>& ring,
                                   uint64_t* ready) {
@@ -1019,7 +1020,7 @@ __device__ void strip_warp_cells(const SchedParams& p, RawRing<8>& ring, uint64_
   if (p.chunks && status == AURORA_OK && chunk_finish(p, cc, cl, lane) && stream) status = AURORA_EINVAL;
 }
 
-template <int NB, typename V>
+template <int NB, typename V, bool CELLS_ONLY = false>
 __device__ void schedule_two_warps(const SchedParams& p, const double* R, const double* Q, const double* Tt,
                                    int ld, MatchState& ms, Dom<V> dom, RawRing<NB>& ring, uint64_t* ready,
                                    const ChunkCtx& cc, double bw_i, bool stream, int& np_, int& status,
@@ -1037,7 +1038,9 @@ __device__ void schedule_two_warps(const SchedParams& p, const double* R, const 
         q0.v[j] = (lane < n && j < n) ? (V)Q[lane * ld + j] : (V)0;
       }
     }
-    if constexpr (NB == 8 && std::is_same<V, int>::value) {
+    if constexpr (CELLS_ONLY) {
+      decompose_warp_cells(p, r0, q0, ring, ready);
+    } else if constexpr (NB == 8 && std::is_same<V, int>::value) {
       const int var = g_sched_generic;
       if (var == 0 || var == 2) decompose_warp_cells(p, r0, q0, ring, ready);
       else if (var == 3) decompose_warp_i8(p, r0, q0, ring, ready);
@@ -1046,7 +1049,10 @@ __device__ void schedule_two_warps(const SchedParams& p, const double* R, const 
       decompose_warp<NB, V>(p, r0, q0, ms.pref, ms.sup, ms.ml, dom, ring, ready);
     }
   } else {
-    if constexpr (NB == 8 && std::is_same<V, int>::value) {
+    if constexpr (CELLS_ONLY) {
+      strip_warp_cells(p, ring, ready, cc, bw_i, stream, np_, status);
+      return;
+    } else if constexpr (NB == 8 && std::is_same<V, int>::value) {
       if (g_sched_generic == 0) {
         strip_warp_cells(p, ring, ready, cc, bw_i, stream, np_, status);
         return;
@@ -1059,8 +1065,11 @@ __device__ void schedule_two_warps(const SchedParams& p, const double* R, const 
 __device__ long long* g_sched_prof = nullptr;
 
 // MAXN = 16: two warps (n <= 16, the shapes the layer uses). MAXN = 32: one
-// warp, generic matcher, chunk pass after the decomposition.
-template <int MAXN>
+// warp, generic matcher, chunk pass after the decomposition. I8: the in-layer
+// path only (int32 counts, uniform cluster, n <= 8, the default variant) -- the
+// same code with every other path compiled out, so the hot code is compact
+// (fewer instruction-cache lines to fetch cold, right after the expert GEMM).
+template <int MAXN, bool I8 = false>
 __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kernel(SchedParams p) {
   constexpr bool TWO = MAXN <= 16;
   __shared__ double t_s[MAXN][MAXN + 1];     // time matrix; later "remaining" of strip
@@ -1129,19 +1138,21 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
 
   double b_max = 0.0, eps = 0.0, row = -INF, col = -INF;
   // integer fast path: int32 counts on a uniform cluster, n <= 16
-  const bool int_fast = TWO && p.d32 && !p.bw;
+  const bool int_fast = I8 || (TWO && p.d32 && !p.bw);
   Row<8, int> rem8, real8;
   Row<16, int> rem16, real16;
   if (warp == 0 && int_fast) {
     bool bad = false;
-    const int bm = n <= 8 ? int_prologue<8>(p, lane, rem8, real8, bad) : int_prologue<16>(p, lane, rem16, real16, bad);
+    int bm;
+    if constexpr (I8) bm = int_prologue<8>(p, lane, rem8, real8, bad);
+    else bm = n <= 8 ? int_prologue<8>(p, lane, rem8, real8, bad) : int_prologue<16>(p, lane, rem16, real16, bad);
     if (lane == 0) {
       bmax_s = (double)bm;
       if (p.b_max) *p.b_max = (double)bm;
       status_s = bad ? AURORA_EINVAL : (bm > 0 ? AURORA_OK : -1);
       if (p.prof) p.prof[5] = clock64() - k_start;
     }
-  } else if (warp == 0) {
+  } else if (!I8 && warp == 0) {
     // ---- time_normalize (commsched.py:181-190) + TimeMatrix checks (211-219)
     bool bad = false;
     if (on) {
@@ -1239,7 +1250,10 @@ __global__ void __launch_bounds__(MAXN <= 16 ? 64 : 32, 1) aurora_schedule_kerne
       const double* Q = &real_s[0][0];
       const double* Tt = &t_s[0][0];
       RawRing<MAXN>& rg = ring;
-      if (n <= 8) {
+      if constexpr (I8) {
+        auto& r8 = reinterpret_cast<RawRing<8>&>(rg);
+        schedule_two_warps<8, int, true>(p, R, Q, nullptr, MAXN + 1, ms, Dom<int>{}, r8, ready_s, cc, bw_i, stream, np_, status, &rem8, &real8);
+      } else if (n <= 8) {
         auto& r8 = reinterpret_cast<RawRing<8>&>(rg);  // fits: R_8 * 8 < R_16 * 16
         if (int_dom) schedule_two_warps<8, int>(p, R, Q, nullptr, MAXN + 1, ms, Dom<int>{}, r8, ready_s, cc, bw_i, stream, np_, status, &rem8, &real8);
         else schedule_two_warps<8, double>(p, R, Q, Tt, MAXN + 1, ms, Dom<double>{eps}, r8, ready_s, cc, bw_i, stream, np_, status);
@@ -1369,6 +1383,7 @@ extern "C" int aurora_debug_set_schedule_trace(long long* trace) {
 }
 
 extern "C" int aurora_debug_set_schedule_variant(int generic) {
+  g_host_variant = generic;
   return cudaMemcpyToSymbol(g_sched_generic, &generic, sizeof(int)) == cudaSuccess ? AURORA_OK : AURORA_ECUDA;
 }
 
@@ -1387,7 +1402,12 @@ void launch_schedule(const SchedParams& p, cudaStream_t s) {
     constexpr int kReserve = 150 * 1024;
     static bool attr = cudaFuncSetAttribute(aurora_schedule_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             kReserve) == cudaSuccess;
-    aurora_schedule_kernel<16><<<1, 64, attr ? kReserve : 0, s>>>(p);
+    static bool attr8 = cudaFuncSetAttribute(aurora_schedule_kernel<16, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kReserve) == cudaSuccess;
+    if (p.d32 && !p.bw && p.n <= 8 && g_host_variant == 0)
+      aurora_schedule_kernel<16, true><<<1, 64, attr8 ? kReserve : 0, s>>>(p);
+    else
+      aurora_schedule_kernel<16><<<1, 64, attr ? kReserve : 0, s>>>(p);
   }
   else
     aurora_schedule_kernel<32><<<1, 32, 0, s>>>(p);
