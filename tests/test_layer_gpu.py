@@ -502,6 +502,64 @@ def test_colocated_models(torch):
     assert tl["a"]["end"] > 0 and tl["b"]["end"] > 0
 
 
+@pytest.mark.parametrize("hetero", [False, True])
+def test_colocated_models_full_size(torch, hetero):
+    """C3 (and C3 on C4's emulated cluster) at the bench shapes, built the way
+    bench.py --config c3 / c3h builds them: Mixtral-shape model a (8 experts
+    top-2, FFN 14336) and the 16-expert top-2 model b (FFN 7168) on 8 ranks,
+    16384 tokens each; calibration routing -> Lina slots of model b ->
+    colocate_homogeneous (placement.py:109-126), or colocate_heterogeneous
+    (placement.py:129-157) with per-rank copy / compute shares. Every bit-exact
+    check of _verify for both layers (routing, logits, traffic matrices,
+    permutations, schedules on the time-normalised matrices, chunk tables,
+    dispatched rows) and sampled outputs vs the bf16-emulating oracle."""
+    from paper_2410_17043_b200 import ClusterSpec, GpuSpec, _lib
+    from paper_2410_17043_b200.colocation import (ColocatedLayers, expert_work, lina_slots, plan_colocation,
+                                                  plan_colocation_hetero)
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    n, T = 8, 16384
+    cfg_a = MoEConfig(hidden=4096, ffn=14336, experts=n, top_k=2, tokens=T, ranks=n, skew=1.0, seed=0)
+    cfg_b = MoEConfig(hidden=4096, ffn=7168, experts=2 * n, top_k=2, tokens=T, ranks=n, skew=1.5, seed=1)
+    g = torch.Generator(device="cuda").manual_seed(101)
+    xa = torch.randn(T, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    xb = torch.randn(T, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    sp = _lib.stream_ptr()
+    cal_a = AuroraMoELayer(cfg_a)
+    cal_a.route(xa, sp)
+    cal_b = AuroraMoELayer(cfg_b)
+    cal_b.route(xb, sp)
+    torch.cuda.synchronize()
+    counts_a = cal_a.counts.cpu().numpy()
+    slots = lina_slots(np.bincount(cal_b.topk_idx.cpu().numpy().ravel(), minlength=2 * n))
+    slot_of = [0] * (2 * n)
+    for s_, (e1, e2) in enumerate(slots):
+        slot_of[e1] = slot_of[e2] = s_
+    cal_s = AuroraMoELayer(cfg_b, gpu_of_expert=slot_of, weights={"w_gate": cal_b.w_gate, "bias": cal_b.bias,
+                                                                   "w13": cal_b.w13, "w2": cal_b.w2})
+    cal_s.route(xb, sp)
+    torch.cuda.synchronize()
+    slot_counts = cal_s.counts.cpu().numpy()
+    del cal_a, cal_b, cal_s
+    torch.cuda.empty_cache()
+    kw, bws = {}, None
+    if hetero:
+        bws = [1.0, 1.0, 0.8, 0.8, 0.5, 0.5, 0.4, 0.4]
+        kw = {"bandwidths": bws, "compute_scales": bws}
+        cluster = ClusterSpec(tuple(GpuSpec(b, b) for b in bws))
+        cp = plan_colocation_hetero(counts_a, slot_counts, slots, cluster, expert_work(4096, 14336),
+                                    expert_work(4096, 7168))
+    else:
+        cp = plan_colocation(counts_a, slot_counts, slots)
+    pair = ColocatedLayers(cfg_a, cfg_b, cp, **kw)
+    out_a, out_b = pair(xa, xb)
+    out_a, out_b = out_a.clone(), out_b.clone()
+    torch.cuda.synchronize()
+    pair.check_status()
+    assert tuple(pair.b.gpu_of) == tuple(cp.gpu_of_b)
+    for layer, x, out in ((pair.a, xa, out_a), (pair.b, xb, out_b)):
+        _verify(torch, layer, x, out, bandwidths=bws, sample=_sample(T, 128, 4))
+
+
 def test_engine_runs_baseline_schedules(torch):
     """SJF / RCS schedules (baselines.py) executed by the same engine deliver
     the same rows: identical layer output to the Aurora-scheduled run."""
