@@ -29,6 +29,10 @@ _SIGNATURES = {
                      _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_route_gate_floats": [_c_int, _c_int],
     "aurora_route_prepare_gate": [_vp, _c_int, _c_int, _vp, _vp],
+    "aurora_route_tc_bytes": [_c_int, _c_int],
+    "aurora_route_prepare_gate_tc": [_vp, _c_int, _c_int, _vp, _vp],
+    "aurora_route_tc": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_int,
+                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "aurora_pack": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                     _vp, _vp, _vp, _vp, _vp],
     "aurora_engine": [_c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_int,

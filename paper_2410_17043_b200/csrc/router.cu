@@ -392,6 +392,269 @@ __global__ void __launch_bounds__(WARPS * 32) route_tail_kernel(
                    slot_dst, blk_cnt, counts, sel_s, sv_s);
 }
 
+// ============================================================================
+// Tensor-core router (E > 8): the gate's dense contraction on tcgen05, the
+// logits that decide anything recomputed exactly.
+//
+// 1. La = x W_pad^T on the CTA-pair grouped GEMM (gemm2sm.cu; W_pad = the gate
+//    padded to 256 rows, bf16 out): an approximation of every logit.
+// 2. route_exact_kernel, per token: the m = min(k + 2, E) experts with the
+//    largest approximate logits a_e = La_e + bias_e are the candidates; their
+//    logits are recomputed in the DEFINED order (same per-lane fmaf chains and
+//    xor tree as route_tma_kernel / oracle_router_logits: same bits). Every
+//    other expert's logit is bounded above by
+//        ub_e = a_e + 2^-8 |La_e| + 2^-20 (|a_e| + 1) + C * S_t,
+//        S_t  = sum_h |x_th| max_e |w_eh|   (>= sum_h |x_th w_eh|),
+//    covering the bf16 rounding of La, the tensor-core accumulation and the
+//    defined order's own rounding: worst cases (K/16 + 32) 2^-23 S_t (one
+//    ulp per accumulation step, truncating) and (K/32 + 5) 2^-24 S_t, together
+//    < 2^-14.5 S_t at K = 5120; C = 2^-13, a 2.8x margin over the worst case
+//    (measured errors are ~100x below it). When the k-th largest exact
+//    candidate logit exceeds max ub over the non-candidates, the exact top-k
+//    is among the candidates, so the top-k (the lowest index on ties), the
+//    softmax weights, the traffic matrix and the permutation are those of the
+//    exact logits; otherwise the token's logits are all recomputed exactly
+//    (counted in n_fallback). logits[t][e] is then exact for every candidate
+//    (and for every expert of a fallback token) and a_e for the others, which
+//    lie strictly below the k-th selected value -- route_tail_kernel's top-k
+//    over the row is the exact one.
+// ============================================================================
+constexpr int RX_W = 16, RX_TPW = 4, RX_TOK = RX_W * RX_TPW, RX_NS = 3;
+constexpr int RX_XB = RX_TOK * 512;             // x chunk: 64 tokens x 256 h bf16
+constexpr int RX_WB = MAXE * 512;               // gate chunk: E x 256 h bf16 (chunk-contiguous layout)
+constexpr int RX_STAGE = RX_XB + RX_WB + 1024;  // + max_e |w_eh| for the chunk (256 fp32)
+
+__device__ __forceinline__ uint32_t f2key(float f) {  // order-preserving float -> uint
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ float warp_sum_tree(float v) {  // xor tree 16, 8, 4, 2, 1: every lane ends with it
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// MC candidates per token (k + 2, rounded up to even: FFMA2 pairs); slots past min(k + 2, E) repeat
+// the last candidate and are ignored
+template <int MC>
+__global__ void __launch_bounds__(RX_W * 32, 1) route_exact_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ w_gate, const __nv_bfloat16* __restrict__ wchunk,
+    const float* __restrict__ wmax, const __nv_bfloat16* __restrict__ la, const float* __restrict__ bias,
+    int T, int H, int E, int k, float* __restrict__ logits, int32_t* __restrict__ n_fallback) {
+  extern __shared__ __align__(1024) uint8_t rx_raw[];
+  uint8_t* xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rx_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[RX_NS], empty[RX_NS];
+  __shared__ int fb_s[RX_TOK];
+  __shared__ int nfb_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t xs_u = tc::smem_u32(xs);
+  const int t0 = blockIdx.x * RX_TOK, chunks = H / 256;
+  const int m = min(min(k + 2, E), MC);
+  const uint32_t wbytes = (uint32_t)E * 512;
+  if (tid == 0) nfb_s = 0;
+  init_ring<RX_NS, RX_W>(full, empty);
+  __syncthreads();
+  auto fill = [&](int c, int st) {
+    uint8_t* d = xs + st * RX_STAGE;
+    tc::mbar_expect_tx(&full[st], RX_XB + wbytes + 1024);
+    tma_load_2d(d, &xmap, &full[st], 256 * c, t0);
+    bulk_load(d + RX_XB, wchunk + (size_t)c * E * 256, wbytes, &full[st]);
+    bulk_load(d + RX_XB + RX_WB, wmax + 256 * c, 1024, &full[st]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < RX_NS && c < chunks; c++) fill(c, c);
+
+  // ---- candidates: the m largest approximate logits (lane holds experts lane, lane + 32)
+  uint32_t cpk[RX_TPW][(MC + 3) / 4];
+  float thr[RX_TPW];
+#pragma unroll
+  for (int tt = 0; tt < RX_TPW; tt++) {
+    const int t = t0 + warp * RX_TPW + tt;
+    float a[2] = {-INFINITY, -INFINITY}, ub[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int e = lane + 32 * h;
+      if (t < T && e < E) {
+        const float l = __bfloat162float(la[(size_t)t * 256 + e]);
+        a[h] = l + bias[e];
+        ub[h] = a[h] + ldexpf(fabsf(l), -8) + ldexpf(fabsf(a[h]) + 1.0f, -20);
+      }
+    }
+    uint32_t taken = 0, elast = 0;
+#pragma unroll
+    for (int q = 0; q < (MC + 3) / 4; q++) cpk[tt][q] = 0;
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      if (j >= m) {  // padding slot: the last candidate again (its result is ignored)
+        cpk[tt][j >> 2] |= elast << (8 * (j & 3));
+        continue;
+      }
+      const bool ok0 = !(taken & 1u) && lane < E, ok1 = !(taken & 2u) && lane + 32 < E;
+      const uint32_t k0 = ok0 ? f2key(a[0]) : 0u, k1 = ok1 ? f2key(a[1]) : 0u;
+      const bool pick1 = k1 > k0;  // ties: the lower index (lane < lane + 32)
+      const uint32_t kb = pick1 ? k1 : k0;
+      const uint32_t kmax = __reduce_max_sync(0xffffffffu, kb);
+      const uint32_t e = __reduce_min_sync(0xffffffffu, (kb == kmax && (ok0 || ok1)) ? (uint32_t)(lane + (pick1 ? 32 : 0)) : 255u);
+      if ((int)e == lane) taken |= 1u;
+      if ((int)e == lane + 32) taken |= 2u;
+      cpk[tt][j >> 2] |= e << (8 * (j & 3));
+      elast = e;
+    }
+    const uint32_t u0 = (!(taken & 1u) && lane < E) ? f2key(ub[0]) : 0u;
+    const uint32_t u1 = (!(taken & 2u) && lane + 32 < E) ? f2key(ub[1]) : 0u;
+    const uint32_t um = __reduce_max_sync(0xffffffffu, u0 > u1 ? u0 : u1);
+    thr[tt] = um ? key2f(um) : -INFINITY;
+  }
+
+  // ---- exact candidate logits: per lane the defined chains over h = 256 c + 8 lane + jj, two
+  // candidates per fp32x2 FMA (FFMA2: two independent RN fmas, the same bits as two fmaf)
+  float2 acc[RX_TPW][MC / 2];
+  float sab[RX_TPW];
+#pragma unroll
+  for (int tt = 0; tt < RX_TPW; tt++) {
+    sab[tt] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < MC / 2; j++) acc[tt][j] = make_float2(0.0f, 0.0f);
+  }
+  for (int c = 0; c < chunks; c++) {
+    const int s = c % RX_NS;
+    tc::mbar_wait(&full[s], (uint32_t)(c / RX_NS) & 1u);
+    const uint32_t st = xs_u + s * RX_STAGE;
+    const uint32_t wst = st + RX_XB + 16 * lane;
+    float mh[8];
+    {
+      const int4 m0 = lds128(st + RX_XB + RX_WB + 32 * lane), m1 = lds128(st + RX_XB + RX_WB + 32 * lane + 16);
+      mh[0] = __int_as_float(m0.x); mh[1] = __int_as_float(m0.y); mh[2] = __int_as_float(m0.z); mh[3] = __int_as_float(m0.w);
+      mh[4] = __int_as_float(m1.x); mh[5] = __int_as_float(m1.y); mh[6] = __int_as_float(m1.z); mh[7] = __int_as_float(m1.w);
+    }
+#pragma unroll
+    for (int tt = 0; tt < RX_TPW; tt++) {
+      float xf[8];
+      bf16x8_to_f32(lds128(st + (warp * RX_TPW + tt) * 512 + 16 * lane), xf);
+#pragma unroll
+      for (int jj = 0; jj < 8; jj++) sab[tt] = fmaf(fabsf(xf[jj]), mh[jj], sab[tt]);
+#pragma unroll
+      for (int jp = 0; jp < MC / 2; jp++) {
+        const uint32_t e0 = (cpk[tt][(2 * jp) >> 2] >> (8 * ((2 * jp) & 3))) & 0xFFu;
+        const uint32_t e1 = (cpk[tt][(2 * jp + 1) >> 2] >> (8 * ((2 * jp + 1) & 3))) & 0xFFu;
+        float w0[8], w1[8];
+        bf16x8_to_f32(lds128(wst + e0 * 512), w0);
+        bf16x8_to_f32(lds128(wst + e1 * 512), w1);
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++)
+          acc[tt][jp] = __ffma2_rn(make_float2(xf[jj], xf[jj]), make_float2(w0[jj], w1[jj]), acc[tt][jp]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty[s]);
+    if (tid == 0 && c + RX_NS < chunks) {
+      tc::mbar_wait(&empty[s], (uint32_t)(c / RX_NS) & 1u);
+      fill(c + RX_NS, s);
+    }
+  }
+
+  // ---- exact logits, the certificate, the row of logits
+  constexpr float C_TC = 1.0f / 8192.0f;
+#pragma unroll
+  for (int tt = 0; tt < RX_TPW; tt++) {
+    const int tl = warp * RX_TPW + tt, t = t0 + tl;
+    const float S = warp_sum_tree(sab[tt]) * 1.001f;
+    float ex[MC];
+    uint32_t ce[MC];
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      ce[j] = (cpk[tt][j >> 2] >> (8 * (j & 3))) & 0xFFu;
+      const float v = warp_sum_tree((j & 1) ? acc[tt][j >> 1].y : acc[tt][j >> 1].x);  // every lane: the tree
+      ex[j] = j < m ? v + bias[ce[j]] : -INFINITY;
+    }
+    // k-th largest exact candidate logit
+    uint32_t used = 0;
+    float kth = INFINITY;
+    for (int q = 0; q < k; q++) {
+      int bj = -1;
+      float bv = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < MC; j++)
+        if (j < m && !((used >> j) & 1u) && (bj < 0 || ex[j] > bv)) { bj = j; bv = ex[j]; }
+      used |= 1u << bj;
+      kth = bv;
+    }
+    const bool certified = m >= E || kth > thr[tt] + C_TC * S;
+    if (t < T) {
+      if (certified) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int e = lane + 32 * h;
+          if (e < E) {
+            float v = __bfloat162float(la[(size_t)t * 256 + e]) + bias[e];
+#pragma unroll
+            for (int j = 0; j < MC; j++)
+              if (j < m && ce[j] == (uint32_t)e) v = ex[j];
+            logits[(size_t)t * E + e] = v;
+          }
+        }
+      } else if (lane == 0) {
+        fb_s[atomicAdd(&nfb_s, 1)] = t;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- fallback (not certified): every logit of the token in the defined order, from global
+  // memory; the CTA's 16 warps share the experts (warp w: e = w, w + 16, w + 32, w + 48)
+  const int nfb = nfb_s;
+  for (int q = 0; q < nfb; q++) {
+    const int t = fb_s[q];
+    float a[MAXE / RX_W];
+#pragma unroll
+    for (int r = 0; r < MAXE / RX_W; r++) a[r] = 0.0f;
+#pragma unroll 4
+    for (int c = 0; c < chunks; c++) {
+      float xf[8];
+      bf16x8_to_f32(__ldg(reinterpret_cast<const int4*>(x + (size_t)t * H + 256 * c + 8 * lane)), xf);
+#pragma unroll
+      for (int r = 0; r < MAXE / RX_W; r++) {
+        const int e = warp + RX_W * r;
+        if (e < E) {
+          float wf[8];
+          bf16x8_to_f32(__ldg(reinterpret_cast<const int4*>(w_gate + (size_t)e * H + 256 * c + 8 * lane)), wf);
+#pragma unroll
+          for (int jj = 0; jj < 8; jj++) a[r] = fmaf(xf[jj], wf[jj], a[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < MAXE / RX_W; r++) {
+      const int e = warp + RX_W * r;
+      const float v = warp_sum_tree(a[r]);
+      if (e < E && lane == 0) logits[(size_t)t * E + e] = v + bias[e];
+    }
+  }
+  if (tid == 0 && nfb && n_fallback) atomicAdd(n_fallback, nfb);
+}
+
+// gate in the exact kernel's layout: wchunk[c][e][256] = w[e][256 c ..], wmax[h] = max_e |w[e][h]|,
+// wpad[256][H] = w rows (rows >= E zero)
+__global__ void prepare_gate_tc_kernel(const __nv_bfloat16* __restrict__ w, int E, int H,
+                                       __nv_bfloat16* __restrict__ wchunk, float* __restrict__ wmax,
+                                       __nv_bfloat16* __restrict__ wpad) {
+  const long long total = 256LL * H;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < total; o += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(o / H), h = (int)(o % H);
+    const __nv_bfloat16 v = e < E ? w[(size_t)e * H + h] : __float2bfloat16(0.0f);
+    wpad[o] = v;
+    if (e < E) wchunk[((size_t)(h / 256) * E + e) * 256 + (h % 256)] = v;
+    if (e == 0) {
+      float mx = 0.0f;
+      for (int q = 0; q < E; q++) mx = fmaxf(mx, fabsf(__bfloat162float(w[(size_t)q * H + h])));
+      wmax[h] = mx;
+    }
+  }
+}
+
 typedef CUresult (*EncodeTiledFnR)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -706,6 +969,60 @@ extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, cons
       slot_dst, blk_cnt, counts, T, k, n, rank_base, tokens_per_rank, send_list, pos, soff, roff,
       rtot, rloc, rrem, topk_idx, topk_w, local_of_expert, (uint8_t*)meta, ((k * 8 + 15) / 16) * 16,
       GroupedArgs{});
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_route_tc_bytes(int E, int H) {  // bytes of the tensor-core router's gate copies
+  if (E < 9 || E > MAXE || H <= 0 || H % 256) return -AURORA_EINVAL;
+  return 256 * H * 2 + E * H * 2 + H * 4;
+}
+
+extern "C" int aurora_route_prepare_gate_tc(const void* w_gate, int E, int H, void* gate_tc, void* stream) {
+  if (!w_gate || !gate_tc || E < 9 || E > MAXE || H <= 0 || H % 256) return AURORA_EINVAL;
+  uint8_t* b = (uint8_t*)gate_tc;
+  __nv_bfloat16* wpad = (__nv_bfloat16*)b;
+  __nv_bfloat16* wchunk = (__nv_bfloat16*)(b + (size_t)256 * H * 2);
+  float* wmax = (float*)(b + (size_t)256 * H * 2 + (size_t)E * H * 2);
+  prepare_gate_tc_kernel<<<256, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)w_gate, E, H, wchunk, wmax, wpad);
+  AUR_CHECK_LAUNCH();
+  return AURORA_OK;
+}
+
+extern "C" int aurora_route_tc(const void* x, const void* w_gate, const void* gate_tc, const float* bias, int T,
+                               int H, int E, int k, const int32_t* gpu_of_expert, int n, int rank_base,
+                               int tokens_per_rank, int32_t* topk_idx, float* topk_w, int32_t* slot_dst,
+                               int32_t* blk_cnt, int32_t* counts, float* logits, void* la_buf,
+                               const int32_t* t_rows, int32_t* tile_ctr, int32_t* n_fallback, void* stream) {
+  if (T <= 0 || H % 256 || H > 8192 || k < 1 || k > MAXK || k > E || E < 9 || E > MAXE || n < 1 || n > AUR_MAXN ||
+      tokens_per_rank % TILE || T % tokens_per_rank || !x || !w_gate || !gate_tc || !bias || !logits || !la_buf ||
+      !t_rows)
+    return AURORA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint8_t* b = (const uint8_t*)gate_tc;
+  const __nv_bfloat16* wpad = (const __nv_bfloat16*)b;
+  const __nv_bfloat16* wchunk = (const __nv_bfloat16*)(b + (size_t)256 * H * 2);
+  const float* wmax = (const float*)(b + (size_t)256 * H * 2 + (size_t)E * H * 2);
+  // 1. approximate logits on the tensor cores: one group of T rows, N = 256 (the padded gate), K = H
+  int rc = aurora_grouped_gemm(x, wpad, la_buf, nullptr, t_rows, 1, (int64_t)T, 256, H, 0, tile_ctr, 0, stream);
+  if (rc != AURORA_OK) return rc;
+  // 2. exact candidates + certificate (fallback: the whole row)
+  CUtensorMap xmap;
+  if (!make_x_map(&xmap, x, (uint64_t)T, (uint64_t)H, RX_TOK)) return AURORA_ECUDA;
+  constexpr int rdyn = RX_NS * RX_STAGE + 1024;
+  static bool attr = cudaFuncSetAttribute(route_exact_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          rdyn) == cudaSuccess &&
+                     cudaFuncSetAttribute(route_exact_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          rdyn) == cudaSuccess;
+  if (!attr) return AURORA_ECUDA;
+  auto kern = k + 2 <= 8 ? route_exact_kernel<8> : route_exact_kernel<10>;
+  kern<<<(T + RX_TOK - 1) / RX_TOK, RX_W * 32, rdyn, s>>>(
+      xmap, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w_gate, wchunk, wmax, (const __nv_bfloat16*)la_buf, bias,
+      T, H, E, k, logits, n_fallback);
+  // 3. top-k, weights, destinations, histograms over the (certified) logits
+  route_tail_kernel<<<(T + TILE - 1) / TILE, WARPS * 32, 0, s>>>(logits, T, E, k, gpu_of_expert, n, rank_base,
+                                                                  tokens_per_rank, topk_idx, topk_w, slot_dst,
+                                                                  blk_cnt, counts);
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }

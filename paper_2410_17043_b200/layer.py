@@ -189,6 +189,19 @@ class AuroraMoELayer:
         # E > 8: router logits workspace (the (tile, 8-expert pass) units run on a balanced grid)
         self.logits = (torch.empty(self.T_local, cfg.experts, dtype=torch.float32, device=dev)
                        if cfg.experts > 8 else None)
+        # E > 8: the gate's contraction on the tensor cores, the deciding logits recomputed exactly
+        # (aurora_route_tc; AURORA_ROUTER=fma selects the FMA router)
+        self.router_tc = (self.logits is not None and os.environ.get("AURORA_ROUTER", "tc") != "fma"
+                          and cfg.hidden <= 8192)
+        if self.router_tc:
+            nb = self.L.aurora_route_tc_bytes(cfg.experts, cfg.hidden)
+            self.gate_tc = torch.empty(nb, dtype=torch.uint8, device=dev)
+            _lib.check(self.L.aurora_route_prepare_gate_tc(self.w_gate.data_ptr(), cfg.experts, cfg.hidden,
+                                                           self.gate_tc.data_ptr(), _lib.stream_ptr()),
+                       "aurora_route_prepare_gate_tc")
+            self.la_buf = torch.empty(self.T_local, 256, dtype=torch.bfloat16, device=dev)
+            self.t_rows = torch.tensor([self.T_local], dtype=torch.int32, device=dev)
+            self.n_fallback = torch.zeros(1, dtype=torch.int32, device=dev)  # uncertified tokens, cumulative
 
         # ---- schedule tables (written by K2 on the device)
         P = self.L.aurora_phase_cap(n)
@@ -428,12 +441,24 @@ class AuroraMoELayer:
         self.counts = self.counts2[self._xstep & 1]
         # only this process's rows: a peer may already have stored its rows for this step
         self.counts[self.rank_base:self.rank_base + self.n_local].zero_()
-        _lib.check(self.L.aurora_route(x.data_ptr(), self.gate_prep.data_ptr(), self.bias.data_ptr(), self.T_local,
-                                       cfg.hidden, cfg.experts, cfg.top_k, self.gpu_of_expert.data_ptr(), self.n,
-                                       self.rank_base, cfg.tokens_per_rank, self.topk_idx.data_ptr(),
-                                       self.topk_w.data_ptr(), self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
-                                       self.counts.data_ptr(), None if self.logits is None else self.logits.data_ptr(),
-                                       stream), "aurora_route")
+        if self.router_tc:
+            _lib.check(self.L.aurora_route_tc(x.data_ptr(), self.w_gate.data_ptr(), self.gate_tc.data_ptr(),
+                                              self.bias.data_ptr(), self.T_local, cfg.hidden, cfg.experts,
+                                              cfg.top_k, self.gpu_of_expert.data_ptr(), self.n, self.rank_base,
+                                              cfg.tokens_per_rank, self.topk_idx.data_ptr(), self.topk_w.data_ptr(),
+                                              self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
+                                              self.counts.data_ptr(), self.logits.data_ptr(), self.la_buf.data_ptr(),
+                                              self.t_rows.data_ptr(), None, self.n_fallback.data_ptr(), stream),
+                       "aurora_route_tc")
+        else:
+            _lib.check(self.L.aurora_route(x.data_ptr(), self.gate_prep.data_ptr(), self.bias.data_ptr(),
+                                           self.T_local, cfg.hidden, cfg.experts, cfg.top_k,
+                                           self.gpu_of_expert.data_ptr(), self.n, self.rank_base,
+                                           cfg.tokens_per_rank, self.topk_idx.data_ptr(), self.topk_w.data_ptr(),
+                                           self.slot_dst.data_ptr(), self.blk_cnt.data_ptr(),
+                                           self.counts.data_ptr(),
+                                           None if self.logits is None else self.logits.data_ptr(),
+                                           stream), "aurora_route")
         if self.grouped:
             self.cnt_e = self.cnt_e2[self._xstep & 1]
             self.cnt_e[self.rank_base:self.rank_base + self.n_local].zero_()
@@ -889,7 +914,7 @@ class AuroraMoELayer:
 
     def kernels_per_step(self) -> int:
         """Launches of this library's kernels in one forward (bench's gpu_launches)."""
-        n = 2 if self.logits is not None else 1          # router (+ top-k tail when E > 8)
+        n = 1 if self.logits is None else (3 if self.router_tc else 2)  # router (+ GEMM, exact pass / tail)
         n += 1 if self.grouped else 0                      # per-expert histogram
         n += 3                                             # pack, K2, dispatch engine
         if self.overlap:

@@ -82,6 +82,24 @@ def _check_output(torch, layer, x, out, sample=None):
     return float(rel_bf.max()), float(rel32.max())
 
 
+def _check_logits(layer, ref_logits, idx):
+    """FMA router: every logit has the oracle's bits. Tensor-core router
+    (aurora_route_tc): the selected experts' logits have the oracle's bits, and
+    every logit that differs from the oracle's is an approximation strictly
+    below the token's k-th selected logit (and close to the exact value)."""
+    got = layer.logits.cpu().numpy()
+    ref = np.asarray(ref_logits, np.float32)
+    if not getattr(layer, "router_tc", False):
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+        return
+    sel = np.take_along_axis(got, idx, axis=1)
+    assert np.array_equal(sel.view(np.uint32), np.take_along_axis(ref, idx, axis=1).view(np.uint32))
+    diff = got.view(np.uint32) != ref.view(np.uint32)
+    kth = np.broadcast_to(sel.min(axis=1, keepdims=True), got.shape)
+    assert (got[diff] < kth[diff]).all()
+    assert (np.abs(got - ref) <= 2.0 ** -6 * np.abs(ref) + 0.1).all()
+
+
 def _verify(torch, layer, x, out, bandwidths=None, sample=None):
     """Every bit-exact check against the oracle, then the numeric output
     check. Routing (expert choice, logits when E > 8, gate weights), the
@@ -95,8 +113,8 @@ def _verify(torch, layer, x, out, bandwidths=None, sample=None):
     n, k = cfg.ranks, cfg.top_k
     logits, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), k)
     assert np.array_equal(layer.topk_idx.cpu().numpy(), idx)
-    if layer.logits is not None:  # E > 8: the balanced split router leaves its logits: same bits as the oracle
-        assert np.array_equal(layer.logits.cpu().numpy().view(np.uint32), np.asarray(logits, np.float32).view(np.uint32))
+    if layer.logits is not None:  # E > 8: the router leaves its logits
+        _check_logits(layer, logits, idx)
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-5)
     counts, lists, pos = pack_oracle(idx, layer.gpu_of, n)
     assert np.array_equal(layer.counts.cpu().numpy(), counts)
@@ -730,6 +748,56 @@ def test_router_ties_pick_lower_index(torch, experts, top_k):
     assert np.array_equal(got, idx)
     assert (got[:, 0] % 2 == 0).all()  # the first choice is always the lower twin
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-6)
+
+
+@pytest.mark.parametrize("experts,top_k,hidden,skew", [(16, 2, 512, 1.0), (32, 4, 1024, 0.0), (64, 6, 5120, 1.0),
+                                                        (64, 6, 5120, 2.0), (64, 8, 2048, 0.5), (24, 6, 768, 1.0)])
+def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew):
+    """aurora_route_tc (tensor-core approximate logits + exact candidates +
+    certificate) gives the FMA router's output bit for bit: top-k, softmax
+    weights, destinations, block histograms, traffic matrix, and the selected
+    logits. Also on adversarial inputs: x scaled by 2^12 and 2^-12, and gate
+    rows duplicated with a 1-ulp perturbation (near-ties below the certificate's
+    bound, so those tokens take the exact fallback)."""
+    import os
+    from oracle.oracle import bf16_bits, router_oracle
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=hidden, ffn=256, experts=experts, top_k=top_k, tokens=4096, ranks=8, skew=skew, seed=31)
+    gpu_of = [e * 8 // experts for e in range(experts)]
+    w = AuroraMoELayer.synthetic_weights(cfg, torch.device("cuda"),
+                                         [e for r in range(8) for e in range(experts) if gpu_of[e] == r])
+    wg = w["w_gate"]
+    for e in range(1, experts, 4):  # near-twins: the bf16 neighbour of one entry
+        row = wg[e - 1].clone()
+        row.view(torch.int16)[3] += 1  # the next bf16 value (away from zero)
+        wg[e] = row
+        w["bias"][e] = w["bias"][e - 1]
+    layers = {}
+    for mode in ("tc", "fma"):
+        os.environ["AURORA_ROUTER"] = mode
+        try:
+            layers[mode] = AuroraMoELayer(cfg, gpu_of_expert=gpu_of, weights=w)
+        finally:
+            os.environ.pop("AURORA_ROUTER", None)
+    assert layers["tc"].router_tc and not layers["fma"].router_tc
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x0 = torch.randn(cfg.tokens, cfg.hidden, device="cuda", generator=g)
+    for scale in (1.0, 4096.0, 1.0 / 4096.0):
+        x = (x0 * scale).to(torch.bfloat16)
+        outs = {}
+        for mode, layer in layers.items():
+            layer.route(x, int(torch.cuda.current_stream().cuda_stream))
+            torch.cuda.synchronize()
+            outs[mode] = [t.clone() for t in (layer.topk_idx, layer.topk_w, layer.slot_dst, layer.blk_cnt,
+                                               layer.counts)]
+        for a, b in zip(outs["tc"], outs["fma"]):
+            assert torch.equal(a, b), scale
+        ref, idx, _ = router_oracle(bf16_bits(x), bf16_bits(layers["tc"].w_gate), layers["tc"].bias.cpu().numpy(),
+                                    top_k)
+        assert np.array_equal(layers["tc"].topk_idx.cpu().numpy(), idx)
+        _check_logits(layers["tc"], ref, idx)
+    nfb = int(layers["tc"].n_fallback.item())
+    assert nfb < 3 * cfg.tokens  # most tokens certified even with the near-twins
 
 
 @pytest.mark.parametrize("experts,top_k", [(8, 2), (32, 4)])
