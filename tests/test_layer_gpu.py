@@ -750,22 +750,26 @@ def test_router_ties_pick_lower_index(torch, experts, top_k):
     assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-6)
 
 
-@pytest.mark.parametrize("experts,top_k,hidden,skew", [(16, 2, 512, 1.0), (32, 4, 1024, 0.0), (64, 6, 5120, 1.0),
-                                                        (64, 6, 5120, 2.0), (64, 8, 2048, 0.5), (24, 6, 768, 1.0)])
-def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew):
+@pytest.mark.parametrize("experts,top_k,hidden,skew,tokens,ranks", [
+    (16, 2, 512, 1.0, 4096, 8), (32, 4, 1024, 0.0, 4096, 8), (64, 6, 5120, 1.0, 4096, 8),
+    (64, 6, 5120, 2.0, 4096, 8), (64, 8, 2048, 0.5, 4096, 8), (24, 6, 768, 1.0, 4096, 8),
+    (16, 3, 512, 1.0, 384, 2), (64, 6, 1024, 1.0, 320, 1)])
+def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew, tokens, ranks):
     """aurora_route_tc (tensor-core approximate logits + exact candidates +
     certificate) gives the FMA router's output bit for bit: top-k, softmax
     weights, destinations, block histograms, traffic matrix, and the selected
     logits. Also on adversarial inputs: x scaled by 2^12 and 2^-12, and gate
     rows duplicated with a 1-ulp perturbation (near-ties below the certificate's
-    bound, so those tokens take the exact fallback)."""
+    bound, so those tokens take the exact fallback). Token counts that leave a
+    partial 256-row GEMM tile (384, 320) and a partial 64-token tile (320)."""
     import os
     from oracle.oracle import bf16_bits, router_oracle
     from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
-    cfg = MoEConfig(hidden=hidden, ffn=256, experts=experts, top_k=top_k, tokens=4096, ranks=8, skew=skew, seed=31)
-    gpu_of = [e * 8 // experts for e in range(experts)]
+    cfg = MoEConfig(hidden=hidden, ffn=256, experts=experts, top_k=top_k, tokens=tokens, ranks=ranks, skew=skew,
+                    seed=31)
+    gpu_of = [e * ranks // experts for e in range(experts)]
     w = AuroraMoELayer.synthetic_weights(cfg, torch.device("cuda"),
-                                         [e for r in range(8) for e in range(experts) if gpu_of[e] == r])
+                                         [e for r in range(ranks) for e in range(experts) if gpu_of[e] == r])
     wg = w["w_gate"]
     for e in range(1, experts, 4):  # near-twins: the bf16 neighbour of one entry
         row = wg[e - 1].clone()
