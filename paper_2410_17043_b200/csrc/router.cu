@@ -431,14 +431,31 @@ __device__ __forceinline__ uint32_t f2key(float f) {  // order-preserving float 
 __device__ __forceinline__ float key2f(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
+// fp32 += bf16 x bf16 with one rounding (fma.rn.f32.bf16 -> FHFMA.BF16, reading either half of a
+// packed register directly): the product of two bf16 is exact in fp32, so this is fmaf on the
+// widened values -- the same bits, without the widening instructions
+__device__ __forceinline__ float fma_bf16_lo(uint32_t a, uint32_t b, float c) {
+  unsigned short al, ah, bl, bh;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(al), "h"(bl));
+  return c;
+}
+__device__ __forceinline__ float fma_bf16_hi(uint32_t a, uint32_t b, float c) {
+  unsigned short al, ah, bl, bh;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(ah), "h"(bh));
+  return c;
+}
 __device__ __forceinline__ float warp_sum_tree(float v) {  // xor tree 16, 8, 4, 2, 1: every lane ends with it
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// MC candidates per token (k + 2, rounded up to even: FFMA2 pairs); slots past min(k + 2, E) repeat
-// the last candidate and are ignored
+// MC candidates per token (>= k + 2); slots past min(k + 2, E) repeat the last candidate and are
+// ignored
 template <int MC>
 __global__ void __launch_bounds__(RX_W * 32, 1) route_exact_kernel(
     const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ x,
@@ -510,15 +527,14 @@ __global__ void __launch_bounds__(RX_W * 32, 1) route_exact_kernel(
     thr[tt] = um ? key2f(um) : -INFINITY;
   }
 
-  // ---- exact candidate logits: per lane the defined chains over h = 256 c + 8 lane + jj, two
-  // candidates per fp32x2 FMA (FFMA2: two independent RN fmas, the same bits as two fmaf)
-  float2 acc[RX_TPW][MC / 2];
-  float sab[RX_TPW];
+  // ---- exact candidate logits: per lane the defined chains over h = 256 c + 8 lane + jj,
+  // jj = 2q (low half of word q), 2q + 1 (high half): one FHFMA.BF16 per term
+  float acc[RX_TPW][MC], sab[RX_TPW];
 #pragma unroll
   for (int tt = 0; tt < RX_TPW; tt++) {
     sab[tt] = 0.0f;
 #pragma unroll
-    for (int j = 0; j < MC / 2; j++) acc[tt][j] = make_float2(0.0f, 0.0f);
+    for (int j = 0; j < MC; j++) acc[tt][j] = 0.0f;
   }
   for (int c = 0; c < chunks; c++) {
     const int s = c % RX_NS;
@@ -533,20 +549,26 @@ __global__ void __launch_bounds__(RX_W * 32, 1) route_exact_kernel(
     }
 #pragma unroll
     for (int tt = 0; tt < RX_TPW; tt++) {
-      float xf[8];
-      bf16x8_to_f32(lds128(st + (warp * RX_TPW + tt) * 512 + 16 * lane), xf);
+      const int4 xv = lds128(st + (warp * RX_TPW + tt) * 512 + 16 * lane);
+      const uint32_t xw[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+      {
+        float xf[8];
+        bf16x8_to_f32(xv, xf);
 #pragma unroll
-      for (int jj = 0; jj < 8; jj++) sab[tt] = fmaf(fabsf(xf[jj]), mh[jj], sab[tt]);
+        for (int jj = 0; jj < 8; jj++) sab[tt] = fmaf(fabsf(xf[jj]), mh[jj], sab[tt]);
+      }
 #pragma unroll
-      for (int jp = 0; jp < MC / 2; jp++) {
-        const uint32_t e0 = (cpk[tt][(2 * jp) >> 2] >> (8 * ((2 * jp) & 3))) & 0xFFu;
-        const uint32_t e1 = (cpk[tt][(2 * jp + 1) >> 2] >> (8 * ((2 * jp + 1) & 3))) & 0xFFu;
-        float w0[8], w1[8];
-        bf16x8_to_f32(lds128(wst + e0 * 512), w0);
-        bf16x8_to_f32(lds128(wst + e1 * 512), w1);
+      for (int j = 0; j < MC; j++) {
+        const uint32_t e = (cpk[tt][j >> 2] >> (8 * (j & 3))) & 0xFFu;
+        const int4 wv = lds128(wst + e * 512);
+        const uint32_t ww[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
+        float a = acc[tt][j];
 #pragma unroll
-        for (int jj = 0; jj < 8; jj++)
-          acc[tt][jp] = __ffma2_rn(make_float2(xf[jj], xf[jj]), make_float2(w0[jj], w1[jj]), acc[tt][jp]);
+        for (int q = 0; q < 4; q++) {
+          a = fma_bf16_lo(xw[q], ww[q], a);
+          a = fma_bf16_hi(xw[q], ww[q], a);
+        }
+        acc[tt][j] = a;
       }
     }
     __syncwarp();
@@ -568,7 +590,7 @@ __global__ void __launch_bounds__(RX_W * 32, 1) route_exact_kernel(
 #pragma unroll
     for (int j = 0; j < MC; j++) {
       ce[j] = (cpk[tt][j >> 2] >> (8 * (j & 3))) & 0xFFu;
-      const float v = warp_sum_tree((j & 1) ? acc[tt][j >> 1].y : acc[tt][j >> 1].x);  // every lane: the tree
+      const float v = warp_sum_tree(acc[tt][j]);  // every lane: the tree's value
       ex[j] = j < m ? v + bias[ce[j]] : -INFINITY;
     }
     // k-th largest exact candidate logit

@@ -758,7 +758,8 @@ def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew, token
     """aurora_route_tc (tensor-core approximate logits + exact candidates +
     certificate) gives the FMA router's output bit for bit: top-k, softmax
     weights, destinations, block histograms, traffic matrix, and the selected
-    logits. Also on adversarial inputs: x scaled by 2^12 and 2^-12, and gate
+    logits. Also on adversarial inputs: x scaled by 2^12, 2^-12 and 2^-118 (subnormal
+    products: the exact pass's bf16 FMAs keep subnormals like fmaf), and gate
     rows duplicated with a 1-ulp perturbation (near-ties below the certificate's
     bound, so those tokens take the exact fallback). Token counts that leave a
     partial 256-row GEMM tile (384, 320) and a partial 64-token tile (320)."""
@@ -786,7 +787,7 @@ def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew, token
     assert layers["tc"].router_tc and not layers["fma"].router_tc
     g = torch.Generator(device="cuda").manual_seed(5)
     x0 = torch.randn(cfg.tokens, cfg.hidden, device="cuda", generator=g)
-    for scale in (1.0, 4096.0, 1.0 / 4096.0):
+    for scale in (1.0, 4096.0, 1.0 / 4096.0, 2.0 ** -118):  # the last: subnormal products and sums
         x = (x0 * scale).to(torch.bfloat16)
         outs = {}
         for mode, layer in layers.items():
