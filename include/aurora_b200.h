@@ -124,10 +124,12 @@ int aurora_route(const void* x, const float* gate_prep, const float* bias, int T
                  int k, const int32_t* gpu_of_expert, int n, int rank_base, int tokens_per_rank,
                  int32_t* topk_idx, float* topk_w, int32_t* slot_dst, int32_t* blk_cnt,
                  int32_t* counts, float* logits, void* stream);
-/* aurora_route_gate_floats: floats of the prepared gate (ceil(E/8) * 8 * H), or -AURORA_E*.
+/* aurora_route_gate_floats: floats of the prepared gate (ceil(E/8) * 8 * H, + 4 * H when
+ *   E <= 8), or -AURORA_E*.
  * aurora_route_prepare_gate: w_gate[E][H] bf16 -> gate_prep: widened to fp32 (exact) in the
  *   router's shared-memory order (per 8-expert pass and 256-h chunk, lane-major expert pairs;
- *   experts past E zero). Once per layer (the gate is a weight). */
+ *   experts past E zero); for E <= 8 followed by the bf16 rows [8][H] (zero past E) that the
+ *   E <= 8 router reads with TMA. Once per layer (the gate is a weight). */
 int aurora_route_gate_floats(int E, int H);
 /* aurora_route_tc: the same router output (bit-exact top-k, weights, slot_dst, blk_cnt,
  *   counts) for 8 < E <= 64 with the gate's contraction on the tensor cores: approximate

@@ -46,6 +46,23 @@ __device__ __forceinline__ int4 lds128(uint32_t addr) {
   return v;
 }
 
+// fp32 += bf16 x bf16 with one rounding (fma.rn.f32.bf16 -> FHFMA.BF16, reading either half of a
+// packed register directly): the product of two bf16 is exact in fp32, so this is fmaf on the
+// widened values -- the same bits, without the widening instructions
+__device__ __forceinline__ float fma_bf16_lo(uint32_t a, uint32_t b, float c) {
+  unsigned short al, ah, bl, bh;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(al), "h"(bl));
+  return c;
+}
+__device__ __forceinline__ float fma_bf16_hi(uint32_t a, uint32_t b, float c) {
+  unsigned short al, ah, bl, bh;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
+  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(ah), "h"(bh));
+  return c;
+}
 // top-k + softmax + destinations (thread per token, first 64 threads) and the
 // tile's destination histogram (warp-aggregated), shared by both router kernels
 // presel (sel_s / sv_s non-null): the selection was made by warp_topk, read it from shared memory
@@ -279,6 +296,97 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
              slot_dst, blk_cnt, counts);
 }
 
+// E <= 8: one CTA per 64-token tile, 16 warps x 4 tokens, the gate read as bf16 rows (a TMA box of
+// 8 experts x 256 h per chunk, from the bf16 copy aurora_route_prepare_gate keeps after the fp32
+// block) and every term one FHFMA.BF16 on the packed halves of x and the gate (= fmaf on the
+// widened values): no widening instructions, half the gate's shared-memory bytes, and twice the
+// warps of route_tma_kernel (whose fp32 gate fragments hold 64 registers per thread). Same per-lane
+// chains and xor tree (a reduce-scatter: lane q ends with (token q / 8, expert q % 8)): same bits.
+constexpr int BW = 16, BTPW = 4, BS = 4;
+constexpr int BXB = TILE * 512, BWB = 8 * 512, BCH = BXB + BWB;
+__global__ void __launch_bounds__(BW * 32, 1) route_bf16_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
+    const float* __restrict__ bias, int T, int H, int E, int k, const int32_t* __restrict__ gpu_of_expert, int n,
+    int rank_base, int tokens_per_rank, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+    int32_t* __restrict__ slot_dst, int32_t* __restrict__ blk_cnt, int32_t* __restrict__ counts) {
+  extern __shared__ __align__(1024) uint8_t bs_raw[];
+  uint8_t* xs = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(bs_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ float logit_s[TILE][MAXE + 1];
+  __shared__ int hist_s[AUR_MAXN];
+  __shared__ __align__(8) uint64_t full[BS], empty[BS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t xs_u = tc::smem_u32(xs);
+  const int t0 = blockIdx.x * TILE, chunks = H / 256;
+  if (tid < AUR_MAXN) hist_s[tid] = 0;
+  init_ring<BS, BW>(full, empty);
+  __syncthreads();
+  auto fill = [&](int c, int st) {
+    tc::mbar_expect_tx(&full[st], BCH);
+    tma_load_2d(xs + st * BCH, &xmap, &full[st], 256 * c, t0);
+    tma_load_2d(xs + st * BCH + BXB, &wmap, &full[st], 256 * c, 0);
+  };
+  if (tid == 0)
+    for (int c = 0; c < BS && c < chunks; c++) fill(c, c);
+  float acc[BTPW][8];
+#pragma unroll
+  for (int tt = 0; tt < BTPW; tt++)
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc[tt][e] = 0.0f;
+  for (int c = 0; c < chunks; c++) {
+    const int s = c % BS;
+    tc::mbar_wait(&full[s], (uint32_t)(c / BS) & 1u);
+    const uint32_t st = xs_u + s * BCH;
+    uint32_t w[8][4];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int4 v = lds128(st + BXB + e * 512 + 16 * lane);
+      w[e][0] = (uint32_t)v.x; w[e][1] = (uint32_t)v.y; w[e][2] = (uint32_t)v.z; w[e][3] = (uint32_t)v.w;
+    }
+#pragma unroll
+    for (int tt = 0; tt < BTPW; tt++) {
+      const int4 xv = lds128(st + (warp * BTPW + tt) * 512 + 16 * lane);
+      const uint32_t xw[4] = {(uint32_t)xv.x, (uint32_t)xv.y, (uint32_t)xv.z, (uint32_t)xv.w};
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        float a = acc[tt][e];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          a = fma_bf16_lo(xw[q], w[e][q], a);
+          a = fma_bf16_hi(xw[q], w[e][q], a);
+        }
+        acc[tt][e] = a;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty[s]);
+    if (tid == 0 && c + BS < chunks) {
+      tc::mbar_wait(&empty[s], (uint32_t)(c / BS) & 1u);
+      fill(c + BS, s);
+    }
+  }
+  // reduce-scatter over the lanes: lane q ends with pair q = (token q / 8, expert q % 8)
+  float v[32];
+#pragma unroll
+  for (int qq = 0; qq < 32; qq++) v[qq] = acc[qq >> 3][qq & 7];
+#pragma unroll
+  for (int o = 16, sz = 32; o >= 1; o >>= 1, sz >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int qq = 0; qq < sz / 2; qq++) {
+      const float mine = upper ? v[qq + sz / 2] : v[qq];
+      const float send = upper ? v[qq] : v[qq + sz / 2];
+      v[qq] = mine + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  {
+    const int tq = lane >> 3, eq = lane & 7;
+    if (eq < E) logit_s[warp * BTPW + tq][eq] = v[0] + bias[eq];
+  }
+  __syncthreads();
+  route_tail(logit_s, hist_s, t0, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank, topk_idx, topk_w,
+             slot_dst, blk_cnt, counts);
+}
+
 // E > 8: the (64-token tile, 8-expert pass) units of the gate are spread over a
 // persistent grid (C5: 256 tiles x 8 passes = 2048 units over 148 CTAs, so the
 // FMA-bound work balances across the SMs instead of running 256 whole tiles in
@@ -430,23 +538,6 @@ __device__ __forceinline__ uint32_t f2key(float f) {  // order-preserving float 
 }
 __device__ __forceinline__ float key2f(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-// fp32 += bf16 x bf16 with one rounding (fma.rn.f32.bf16 -> FHFMA.BF16, reading either half of a
-// packed register directly): the product of two bf16 is exact in fp32, so this is fmaf on the
-// widened values -- the same bits, without the widening instructions
-__device__ __forceinline__ float fma_bf16_lo(uint32_t a, uint32_t b, float c) {
-  unsigned short al, ah, bl, bh;
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
-  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(al), "h"(bl));
-  return c;
-}
-__device__ __forceinline__ float fma_bf16_hi(uint32_t a, uint32_t b, float c) {
-  unsigned short al, ah, bl, bh;
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(al), "=h"(ah) : "r"(a));
-  asm("mov.b32 {%0, %1}, %2;" : "=h"(bl), "=h"(bh) : "r"(b));
-  asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(ah), "h"(bh));
-  return c;
 }
 __device__ __forceinline__ float warp_sum_tree(float v) {  // xor tree 16, 8, 4, 2, 1: every lane ends with it
 #pragma unroll
@@ -872,12 +963,22 @@ __global__ void __launch_bounds__(TILE) pack_kernel(
 
 extern "C" int aurora_route_gate_floats(int E, int H) {
   if (E < 1 || E > MAXE || H <= 0 || H % 256) return -AURORA_EINVAL;
-  return ((E + REP - 1) / REP) * H * REP;
+  // E <= 8: + the bf16 rows [8][H] (zero past E) route_bf16_kernel reads, after the fp32 block
+  return ((E + REP - 1) / REP) * H * REP + (E <= REP ? 4 * H : 0);
+}
+
+__global__ void prepare_gate_bf16_kernel(const __nv_bfloat16* __restrict__ w, int E, int H,
+                                         __nv_bfloat16* __restrict__ wb) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < 8 * H; o += gridDim.x * blockDim.x)
+    wb[o] = o / H < E ? w[o] : __float2bfloat16(0.0f);
 }
 
 extern "C" int aurora_route_prepare_gate(const void* w_gate, int E, int H, float* gate_prep, void* stream) {
   if (!w_gate || !gate_prep || E < 1 || E > MAXE || H <= 0 || H % 256) return AURORA_EINVAL;
   prepare_gate_kernel<<<256, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)w_gate, E, H, gate_prep);
+  if (E <= REP)
+    prepare_gate_bf16_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)w_gate, E, H, reinterpret_cast<__nv_bfloat16*>(gate_prep + (size_t)H * REP));
   AUR_CHECK_LAUNCH();
   return AURORA_OK;
 }
@@ -917,6 +1018,18 @@ extern "C" int aurora_route(const void* x, const float* gate_prep, const float* 
                                                                                    logits);
     route_tail_kernel<<<blocks, WARPS * 32, 0, s>>>(logits, T, E, k, gpu_of_expert, n, rank_base, tokens_per_rank,
                                                      topk_idx, topk_w, slot_dst, blk_cnt, counts);
+    AUR_CHECK_LAUNCH();
+    return AURORA_OK;
+  }
+  if (E <= REP) {  // bf16 gate rows after the fp32 block (aurora_route_prepare_gate)
+    constexpr int bdyn = BS * BCH + 1024;
+    static bool battr = cudaFuncSetAttribute(route_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bdyn) ==
+                        cudaSuccess;
+    if (!battr) return AURORA_ECUDA;
+    CUtensorMap wmap;
+    if (!make_x_map(&wmap, gate_prep + (size_t)H * REP, 8, (uint64_t)H, 8)) return AURORA_ECUDA;
+    route_bf16_kernel<<<blocks, BW * 32, bdyn, s>>>(xmap, wmap, bias, T, H, E, k, gpu_of_expert, n, rank_base,
+                                                    tokens_per_rank, topk_idx, topk_w, slot_dst, blk_cnt, counts);
     AUR_CHECK_LAUNCH();
     return AURORA_OK;
   }
