@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) route_tma_kernel(
 // widened values): no widening instructions, half the gate's shared-memory bytes, and twice the
 // warps of route_tma_kernel (whose fp32 gate fragments hold 64 registers per thread). Same per-lane
 // chains and xor tree (a reduce-scatter: lane q ends with (token q / 8, expert q % 8)): same bits.
-constexpr int BW = 16, BTPW = 4, BS = 4;
+constexpr int BW = 16, BTPW = 4, BS = 5;
 constexpr int BXB = TILE * 512, BWB = 8 * 512, BCH = BXB + BWB;
 __global__ void __launch_bounds__(BW * 32, 1) route_bf16_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
