@@ -134,7 +134,8 @@ int aurora_route_gate_floats(int E, int H);
 /* aurora_route_tc: the same router output (bit-exact top-k, weights, slot_dst, blk_cnt,
  *   counts) for 8 < E <= 64 with the gate's contraction on the tensor cores: approximate
  *   logits La = x W^T by the CTA-pair grouped GEMM into la_buf ([T][256] bf16 workspace;
- *   t_rows: device int32 {T}; tile_ctr as for aurora_grouped_gemm, nullable), then per token
+ *   t_rows: one device int32 of workspace, set to T here; tile_ctr as for aurora_grouped_gemm,
+ *   nullable), then per token
  *   the min(k + 2, E) largest approximate logits recomputed in the defined order and a
  *   certificate that no other expert can reach the k-th (bound: 2^-8 |La| + 2^-20 (|a| + 1)
  *   + 2^-13 sum_h |x_h| max_e |w_eh|); uncertified tokens get every logit exactly
@@ -149,7 +150,7 @@ int aurora_route_prepare_gate_tc(const void* w_gate, int E, int H, void* gate_tc
 int aurora_route_tc(const void* x, const void* w_gate, const void* gate_tc, const float* bias, int T, int H,
                     int E, int k, const int32_t* gpu_of_expert, int n, int rank_base, int tokens_per_rank,
                     int32_t* topk_idx, float* topk_w, int32_t* slot_dst, int32_t* blk_cnt, int32_t* counts,
-                    float* logits, void* la_buf, const int32_t* t_rows, int32_t* tile_ctr, int32_t* n_fallback,
+                    float* logits, void* la_buf, int32_t* t_rows, int32_t* tile_ctr, int32_t* n_fallback,
                     void* stream);
 int aurora_route_prepare_gate(const void* w_gate, int E, int H, float* gate_prep, void* stream);
 

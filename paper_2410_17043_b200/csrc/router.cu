@@ -1108,6 +1108,8 @@ extern "C" int aurora_pack(const int32_t* slot_dst, const int32_t* blk_cnt, cons
   return AURORA_OK;
 }
 
+__global__ void set_rows_kernel(int32_t* rows, int T) { *rows = T; }
+
 extern "C" int aurora_route_tc_bytes(int E, int H) {  // bytes of the tensor-core router's gate copies
   if (E < 9 || E > MAXE || H <= 0 || H % 256) return -AURORA_EINVAL;
   return 256 * H * 2 + E * H * 2 + H * 4;
@@ -1128,7 +1130,7 @@ extern "C" int aurora_route_tc(const void* x, const void* w_gate, const void* ga
                                int H, int E, int k, const int32_t* gpu_of_expert, int n, int rank_base,
                                int tokens_per_rank, int32_t* topk_idx, float* topk_w, int32_t* slot_dst,
                                int32_t* blk_cnt, int32_t* counts, float* logits, void* la_buf,
-                               const int32_t* t_rows, int32_t* tile_ctr, int32_t* n_fallback, void* stream) {
+                               int32_t* t_rows, int32_t* tile_ctr, int32_t* n_fallback, void* stream) {
   if (T <= 0 || H % 256 || H > 8192 || k < 1 || k > MAXK || k > E || E < 9 || E > MAXE || n < 1 || n > AUR_MAXN ||
       tokens_per_rank % TILE || T % tokens_per_rank || !x || !w_gate || !gate_tc || !bias || !logits || !la_buf ||
       !t_rows)
@@ -1139,6 +1141,9 @@ extern "C" int aurora_route_tc(const void* x, const void* w_gate, const void* ga
   const __nv_bfloat16* wchunk = (const __nv_bfloat16*)(b + (size_t)256 * H * 2);
   const float* wmax = (const float*)(b + (size_t)256 * H * 2 + (size_t)E * H * 2);
   // 1. approximate logits on the tensor cores: one group of T rows, N = 256 (the padded gate), K = H
+  //    (the GEMM reads its row count on the device: written here, so a stale value cannot feed the
+  //    certificate approximations of another batch)
+  set_rows_kernel<<<1, 1, 0, s>>>(t_rows, T);
   int rc = aurora_grouped_gemm(x, wpad, la_buf, nullptr, t_rows, 1, (int64_t)T, 256, H, 0, tile_ctr, 0, stream);
   if (rc != AURORA_OK) return rc;
   // 2. exact candidates + certificate (fallback: the whole row)

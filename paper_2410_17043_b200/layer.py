@@ -200,7 +200,7 @@ class AuroraMoELayer:
                                                            self.gate_tc.data_ptr(), _lib.stream_ptr()),
                        "aurora_route_prepare_gate_tc")
             self.la_buf = torch.empty(self.T_local, 256, dtype=torch.bfloat16, device=dev)
-            self.t_rows = torch.tensor([self.T_local], dtype=torch.int32, device=dev)
+            self.t_rows = torch.zeros(1, dtype=torch.int32, device=dev)  # GEMM row count (set by the call)
             self.n_fallback = torch.zeros(1, dtype=torch.int32, device=dev)  # uncertified tokens, cumulative
 
         # ---- schedule tables (written by K2 on the device)
@@ -914,7 +914,7 @@ class AuroraMoELayer:
 
     def kernels_per_step(self) -> int:
         """Launches of this library's kernels in one forward (bench's gpu_launches)."""
-        n = 1 if self.logits is None else (3 if self.router_tc else 2)  # router (+ GEMM, exact pass / tail)
+        n = 1 if self.logits is None else (4 if self.router_tc else 2)  # router (+ rows, GEMM, exact pass / tail)
         n += 1 if self.grouped else 0                      # per-expert histogram
         n += 3                                             # pack, K2, dispatch engine
         if self.overlap:
