@@ -801,6 +801,20 @@ def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew, token
                                     top_k)
         assert np.array_equal(layers["tc"].topk_idx.cpu().numpy(), idx)
         _check_logits(layers["tc"], ref, idx)
+        # the certificate's bound on every (token, expert): |a_e - L_e| against
+        # 2^-8 |La_e| + 2^-20 (|a_e| + 1) + 2^-13 S_t, a_e = La_e + bias_e (fp32), L_e the defined logit
+        lt = layers["tc"]
+        la = lt.la_buf[:, :experts].float().cpu().numpy().astype(np.float64)
+        a = (lt.la_buf[:, :experts].float() + lt.bias).cpu().numpy().astype(np.float64)
+        xa = np.abs(x.float().cpu().numpy().astype(np.float64))
+        S = xa @ np.abs(lt.w_gate.float().cpu().numpy().astype(np.float64)).max(axis=0)
+        err = np.abs(a - np.asarray(ref, np.float64))
+        rest = 2.0 ** -20 * (np.abs(a) + 1) + 2.0 ** -13 * S[:, None]
+        assert (err <= 2.0 ** -8 * np.abs(la) + rest).all(), scale  # the bound holds
+        # beyond the worst-case bf16 rounding of La (which the bf16 term is exactly), the tensor-core
+        # and defined-order accumulation use under half of their allowance
+        beyond = np.maximum(err - 2.0 ** -8 * np.abs(la), 0.0) / rest
+        assert beyond.max() < 0.5, (scale, float(beyond.max()))
     nfb = int(layers["tc"].n_fallback.item())
     assert nfb < 3 * cfg.tokens  # most tokens certified even with the near-twins
 
