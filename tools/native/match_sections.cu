@@ -12,6 +12,7 @@
 #ifdef HAVE_8E
 #include "fm8e.cuh"
 #endif
+#include "fm8f.cuh"
 template <class M>
 __global__ void bench(const uint32_t* g, int ng, int reps, uint64_t* out, long long* cyc) {
   const int lane = threadIdx.x;
@@ -64,5 +65,14 @@ int main(int argc, char** argv) {
   for (int i = 0; i < ng; i++) bad += r0[i] != r1[i];
   printf("8e %.0f cyc/match, mismatches %d\n", ce, bad);
 #endif
+  {
+    double cf = run<FastMatch8f>(dg, ng, o1, cy, hc);
+    std::vector<uint64_t> r0(ng), r1(ng);
+    cudaMemcpy(r0.data(), o0, ng * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r1.data(), o1, ng * 8, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int i = 0; i < ng; i++) bad += r0[i] != r1[i];
+    printf("8f (lane-parallel bfs) %.0f cyc/match, mismatches %d\n", cf, bad);
+  }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
