@@ -819,6 +819,32 @@ def test_router_tc_matches_fma_router(torch, experts, top_k, hidden, skew, token
     assert nfb < 3 * cfg.tokens  # most tokens certified even with the near-twins
 
 
+@pytest.mark.parametrize("experts,top_k,hidden,ranks", [(1, 1, 256, 1), (2, 1, 512, 2), (3, 2, 768, 1),
+                                                         (5, 3, 1024, 1), (7, 7, 256, 7), (8, 8, 512, 8),
+                                                         (8, 1, 4096, 8), (4, 2, 2048, 4)])
+def test_router_small_e_vs_oracle(torch, experts, top_k, hidden, ranks):
+    """The E <= 8 router (bf16 gate rows by TMA, FHFMA.BF16 terms) at every expert count and k:
+    top-k, softmax weights, destinations and the traffic matrix bit-exact with the oracle, on
+    Gaussian and on 2^-118-scaled (subnormal-product) inputs."""
+    from oracle.oracle import bf16_bits, pack_oracle, router_oracle
+    from paper_2410_17043_b200.layer import AuroraMoELayer, MoEConfig
+    cfg = MoEConfig(hidden=hidden, ffn=256, experts=experts, top_k=top_k, tokens=64 * 4 * ranks, ranks=ranks,
+                    skew=0.7, seed=41)
+    gpu_of = [e * ranks // experts for e in range(experts)]
+    layer = AuroraMoELayer(cfg, gpu_of_expert=gpu_of)
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x0 = torch.randn(cfg.tokens, hidden, device="cuda", generator=g)
+    for scale in (1.0, 2.0 ** -118):
+        x = (x0 * scale).to(torch.bfloat16)
+        layer.route(x, int(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        _, idx, wts = router_oracle(bf16_bits(x), bf16_bits(layer.w_gate), layer.bias.cpu().numpy(), top_k)
+        assert np.array_equal(layer.topk_idx.cpu().numpy(), idx), scale
+        assert np.allclose(layer.topk_w.cpu().numpy(), wts, atol=1e-6), scale
+        counts, _, _ = pack_oracle(idx, gpu_of, ranks)
+        assert np.array_equal(layer.counts.cpu().numpy(), counts), scale
+
+
 @pytest.mark.parametrize("experts,top_k", [(8, 2), (32, 4)])
 def test_layer_cuda_graph_replay(torch, experts, top_k):
     """The whole forward captured as one CUDA graph: replays with new inputs
